@@ -1,0 +1,176 @@
+"""ctypes wrapper of the fp64 CPU oracle (oracle.c).
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, ``__graft_entry__.smoke()`` and the
+``cpu_baseline`` / ``--impl reference`` legs of bench.py.  The product package
+(paper_2506_01979_b200) never imports this module.
+
+Inputs are numpy arrays holding the exact bytes the GPU path consumes:
+logits as uint16 (raw bf16) or float32, shaped [B][K][G+1][V] (or with a larger row
+stride), tokens int32 [B][K][G+1], uniforms float32.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "liboracle.so")
+_SRC = os.path.join(_HERE, "oracle.c")
+
+OR_BF16, OR_F32 = 0, 1
+ST_GAMMA_CLAMPED, ST_BRANCH_CLAMPED, ST_BAD_TOKEN, ST_NONFINITE, ST_ZERO_RESID = 1, 2, 4, 8, 16
+TIE_ACC_MASK, TIE_ACC_DEC, TIE_SAMPLE, TIE_ILLCOND, TIE_CONF, TIE_EQ7 = 1, 2, 4, 8, 16, 32
+CONF_TOP1, CONF_TOKEN, CONF_ENTROPY = 0, 1, 2
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle.c with gcc (plain -O2, OpenMP across sequences only)."""
+    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < max(
+        os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "oracle.h"))
+    ):
+        subprocess.check_call(
+            ["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-Wall", "-o", _SO, _SRC, "-lm"]
+        )
+    return _SO
+
+
+class _Dims(ctypes.Structure):
+    _fields_ = [
+        ("B", ctypes.c_int32), ("K", ctypes.c_int32), ("G", ctypes.c_int32), ("V", ctypes.c_int32),
+        ("row_stride", ctypes.c_int64), ("seq_stride", ctypes.c_int64),
+        ("dtype", ctypes.c_int32), ("pad_", ctypes.c_int32),
+    ]
+
+
+_P = ctypes.c_void_p
+_VERIFY_FIELDS = [
+    ("lse_p", np.float64, "row"), ("lse_q", np.float64, "row"),
+    ("top1_q", np.float64, "row"), ("entropy_q", np.float64, "row"),
+    ("top1_id_q", np.int32, "row"),
+    ("p_tok", np.float64, "row"), ("q_tok", np.float64, "row"),
+    ("acc_mask", np.uint32, "bk"), ("n_acc", np.int32, "bk"),
+    ("sel_k", np.int32, "b"), ("commit_len", np.int32, "b"),
+    ("out_tok", np.int32, "out"),
+    ("y_tok", np.int32, "b"), ("y_kind", np.int32, "b"),
+    ("offsets", np.int32, "b1"), ("packed_tok", np.int32, "packed"),
+    ("path_rolled", np.int32, "b"), ("branch_discarded", np.int32, "b"),
+    ("keep_mask", np.uint32, "bk"), ("resid_mass", np.float64, "b"),
+    ("status", np.int32, "b"), ("ties", np.uint32, "b"),
+    ("margin_acc", np.float64, "b"), ("margin_sample", np.float64, "b"),
+]
+_CONF_FIELDS = [
+    ("top1_prob", np.float64, "row"), ("top1_id", np.int32, "row"),
+    ("entropy", np.float64, "row"), ("tok_prob", np.float64, "row"),
+    ("stat", np.float64, "row"), ("stop", np.int32, "bk"), ("k_next", np.int32, "bk"),
+    ("gamma_next", np.int32, "bk"), ("ties", np.uint32, "bk"),
+]
+
+
+class _VerifyOut(ctypes.Structure):
+    _fields_ = [(n, _P) for n, _, _ in _VERIFY_FIELDS]
+
+
+class _ConfOut(ctypes.Structure):
+    _fields_ = [(n, _P) for n, _, _ in _CONF_FIELDS]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = ctypes.CDLL(build())
+        _lib.oracle_verify.restype = ctypes.c_int
+        _lib.oracle_verify_f64u.restype = ctypes.c_int
+        _lib.oracle_confidence.restype = ctypes.c_int
+        _lib.oracle_row_softmax.restype = ctypes.c_double
+        _lib.oracle_adaptive_k.restype = ctypes.c_int
+        _lib.oracle_adaptive_k.argtypes = [ctypes.c_double, ctypes.c_int]
+    return _lib
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _dims(L: np.ndarray, B, K, G, V):
+    if L.dtype == np.uint16:
+        dt = OR_BF16
+    elif L.dtype == np.float32:
+        dt = OR_F32
+    else:
+        raise TypeError("logits must be uint16 (raw bf16) or float32")
+    assert L.flags.c_contiguous and L.shape[:3] == (B, K, G + 1)
+    return _Dims(B, K, G, V, L.shape[3], 0, dt, 0)
+
+
+def _shape(kind, B, K, G, rowlen):
+    return {"row": (B, K, rowlen), "bk": (B, K), "b": (B,), "b1": (B + 1,),
+            "out": (B, G + 2), "packed": (B * (G + 2),)}[kind]
+
+
+def verify(PL, QL, tok, u, us, gamma=None, branch_pos=None, rule=0, nthreads=0, V=None,
+           f64_uniforms=False):
+    """One verify-and-branch round on the oracle.  Returns a dict of numpy arrays."""
+    B, K, R1, stride = PL.shape
+    G = R1 - 1
+    V = stride if V is None else V
+    d = _dims(PL, B, K, G, V)
+    d.row_stride = stride
+    assert QL.shape == PL.shape and QL.dtype == PL.dtype
+    tok = np.ascontiguousarray(tok, dtype=np.int32)
+    out = {n: np.empty(_shape(kind, B, K, G, R1), dtype=dt) for n, dt, kind in _VERIFY_FIELDS}
+    o = _VerifyOut(*[_ptr(out[n]) for n, _, _ in _VERIFY_FIELDS])
+    g = None if gamma is None else np.ascontiguousarray(gamma, dtype=np.int32)
+    s = None if branch_pos is None else np.ascontiguousarray(branch_pos, dtype=np.int32)
+    if f64_uniforms:
+        uu = np.ascontiguousarray(u, dtype=np.float64)
+        uss = np.ascontiguousarray(us, dtype=np.float64)
+        fn = lib().oracle_verify_f64u
+    else:
+        uu = np.ascontiguousarray(u, dtype=np.float32)
+        uss = np.ascontiguousarray(us, dtype=np.float32)
+        fn = lib().oracle_verify
+    rc = fn(ctypes.byref(d), _ptr(PL), _ptr(QL), _ptr(tok), _ptr(uu), _ptr(uss), _ptr(g), _ptr(s),
+            ctypes.c_int(rule), ctypes.c_int(nthreads), ctypes.byref(o))
+    if rc != 0:
+        raise ValueError("oracle_verify rejected its arguments")
+    out["packed_tok"] = out["packed_tok"][: out["offsets"][-1]]
+    return out
+
+
+def confidence(QL, tok=None, mode=CONF_TOP1, eps=0.2, lam=1.0, k_max=6, nthreads=0, V=None):
+    """Draft confidence over rows 0..G-1 of every (b,k) group (SURVEY §8.0 Confidence)."""
+    B, K, R1, stride = QL.shape
+    G = R1 - 1
+    V = stride if V is None else V
+    d = _dims(QL, B, K, G, V)
+    d.row_stride = stride
+    out = {n: np.empty(_shape(kind, B, K, G, G), dtype=dt) for n, dt, kind in _CONF_FIELDS}
+    o = _ConfOut(*[_ptr(out[n]) for n, _, _ in _CONF_FIELDS])
+    t = None if tok is None else np.ascontiguousarray(tok, dtype=np.int32)
+    rc = lib().oracle_confidence(ctypes.byref(d), _ptr(QL), _ptr(t), ctypes.c_int(mode),
+                                 ctypes.c_double(eps), ctypes.c_double(lam), ctypes.c_int(k_max),
+                                 ctypes.c_int(nthreads), ctypes.byref(o))
+    if rc != 0:
+        raise ValueError("oracle_confidence rejected its arguments")
+    return out
+
+
+def row_softmax(L, b, slot, i, V=None):
+    """fp64 softmax of one physical row: (P[V], lse)."""
+    B, K, R1, stride = L.shape
+    V = stride if V is None else V
+    d = _dims(L, B, K, R1 - 1, V)
+    d.row_stride = stride
+    P = np.empty(V, dtype=np.float64)
+    lse = lib().oracle_row_softmax(ctypes.byref(d), _ptr(L), b, slot, i, _ptr(P))
+    return P, lse
+
+
+def adaptive_k(c: float, k_max: int) -> int:
+    return lib().oracle_adaptive_k(c, k_max)
