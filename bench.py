@@ -1,0 +1,403 @@
+#!/usr/bin/env python
+"""Benchmark of the SpecBranch verify-and-branch step on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl ours|reference]
+
+One step = one pass of the whole hot path over one batch of synthetic input
+([draft confidence ->] sb_verify_branches -> sb_select_branch, through the C ABI).
+Default workload: BASELINE config C4 (Qwen V=151936, 2048 sequences per GPU, K=4,
+gamma=8, bf16) — the configuration the metric's "1/2/4/8 GPUs" is quoted on.
+Sequences shard across ranks with no data-path collective (weak scaling: each rank
+owns 2048 sequences).  Rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "verified draft tokens/sec and logit HBM GB/s (% of B200 peak) at 1/2/4/8 GPUs"
+
+
+def peaks():
+    try:
+        pk = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[j] for r in self.rows for j in range(4) if len(r) > 3 + j and r[3 + j] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def verified_tokens(gamma, bpos, K):
+    """sum_b [s_b + K (L_b - s_b)]."""
+    t = 0
+    for g, s in zip(gamma, bpos):
+        L = g if s < g else g + 1
+        t += s + K * (L - s)
+    return t
+
+
+def bytes_model(gamma, bpos, y_kind, K, V, es, G, conf_rows=0):
+    """Algorithmic bytes of one step: a1 row pairs, a4 sampled
+    rows (2 for a residual, 1 for a bonus; a bonus row needs 2 passes), a6 draft rows,
+    plus 12 B per path token (token + uniform + output)."""
+    units = sum(L + (K - 1) * (L - 1 - s) for g, s in zip(gamma, bpos) for L in [g if s < g else g + 1])
+    a1 = units * 2 * V * es
+    a4 = sum(2 if k == 1 else (1 if k == 2 else 0) for k in y_kind) * V * es
+    a6 = conf_rows * V * es
+    small = verified_tokens(gamma, bpos, K) * 12
+    return a1, a4, a6, small, units
+
+
+def run_ours(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+
+    from paper_2506_01979_b200 import api, synth
+    from paper_2506_01979_b200.build import build
+
+    build()
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    cfg = synth.config(args.config)
+    Bl = cfg.B * cfg.rounds
+    b0, b1 = rank * Bl, (rank + 1) * Bl
+    t0 = time.time()
+    inp = synth.generate(cfg, device=dev, b0=b0, b1=b1)
+    gen_s = time.time() - t0
+    d = api.dims_for(inp["PL"], V=inp["V"])
+    buf = api.StepBuffers.alloc(d, dev)
+    adaptive = cfg.layout == "adaptive"
+    stream = torch.cuda.current_stream()
+    es = 2 if cfg.dtype == "bf16" else 4
+
+    def step():
+        return api.verify_step(d, inp, buf, adaptive=adaptive, stream=stream)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    gamma = (buf.c_gamma.view(-1) if adaptive else inp["gamma"]).cpu().tolist()
+    bpos = inp["branch_pos"].cpu().tolist()
+    ykind = buf.y_kind.cpu().tolist()
+    a1, a4, a6, small, units = bytes_model(gamma, bpos, ykind, cfg.K, cfg.V, es, cfg.G,
+                                           conf_rows=(Bl * cfg.G if adaptive else 0))
+    toks = verified_tokens(gamma, bpos, cfg.K)
+    committed = int(buf.commit_len.sum())
+
+    # ---- timed region: K steps, per-call events on the launching stream
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local_rank) as clk:
+        start.record(stream)
+        for k in range(args.steps):
+            e = ev[k]
+            e[0].record(stream)
+            if adaptive:
+                api.sb_draft_confidence(api.conf_dims(d), inp["QL"], None, api.SB_CONF_TOP1, 0.2, 1.0, 6,
+                                        buf.c_top1, buf.c_id, buf.c_ent, None, buf.c_stat, buf.c_stop,
+                                        buf.c_knext, buf.c_gamma, buf.conf_workspace, stream)
+                g = buf.c_gamma.view(-1)
+            else:
+                g = inp["gamma"]
+            e[1].record(stream)
+            api.sb_verify_branches(d, inp["PL"], inp["QL"], inp["tok"], inp["u"], g, inp["branch_pos"],
+                                   buf.lse_p, buf.lse_q, buf.p_tok, buf.q_tok, buf.acc_mask, buf.n_acc,
+                                   buf.top1_q, buf.top1_id_q, buf.entropy_q, buf.status, buf.workspace,
+                                   stream)
+            e[2].record(stream)
+            api.sb_select_branch(d, inp["PL"], inp["QL"], inp["tok"], inp["u"], inp["us"], g,
+                                 inp["branch_pos"], buf.n_acc, 0, buf.sel_k, buf.commit_len, buf.out_tok,
+                                 buf.y_tok, buf.y_kind, buf.offsets, buf.packed_tok, buf.path_rolled,
+                                 buf.branch_discarded, buf.keep_mask, buf.resid_mass, buf.status,
+                                 buf.workspace, stream)
+            e[3].record(stream)
+        end.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    ms = start.elapsed_time(end)
+    t_conf = sum(e[0].elapsed_time(e[1]) for e in ev) / args.steps
+    t_ver = sum(e[1].elapsed_time(e[2]) for e in ev) / args.steps
+    t_sel = sum(e[2].elapsed_time(e[3]) for e in ev) / args.steps
+    ms_step = ms / args.steps
+    if world > 1:
+        t = torch.tensor([ms_step, float(toks), float(committed), float(a1 + a4 + a6 + small)], device=dev,
+                         dtype=torch.float64)
+        mx = t.clone()
+        torch.distributed.all_reduce(mx[:1], op=torch.distributed.ReduceOp.MAX)
+        torch.distributed.all_reduce(t[1:], op=torch.distributed.ReduceOp.SUM)
+        ms_step_all, toks_all, comm_all, bytes_all = float(mx[0]), float(t[1]), float(t[2]), float(t[3])
+    else:
+        ms_step_all, toks_all, comm_all, bytes_all = ms_step, toks, committed, a1 + a4 + a6 + small
+
+    # ---- e2e through the public API with host buffers (pinned), H2D + D2H inside
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, inp, d, buf, adaptive, stream, dev, world)
+    if rank != 0:
+        return None
+    peak, peak_src = peaks()
+    ver_gbs = (a1 + small) / (t_ver * 1e-3) / 1e9
+    step_gbs = bytes_all / (ms_step_all * 1e-3) / 1e9
+    value = toks_all / (ms_step_all * 1e-3)
+    line = {
+        "metric": METRIC, "value": round(value, 1), "unit": "verified draft tokens/s",
+        "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
+        "ms_per_step": round(ms_step_all, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic (seeded, DESIGN.md §Input recipe)",
+        "config": {"workload": f"{cfg.name.upper()}: {cfg.note}", "V": cfg.V, "K": cfg.K, "G": cfg.G,
+                   "per_rank_batch": Bl, "global_batch": Bl * world, "layout": cfg.layout,
+                   "parallelism": f"sequence-sharded x{world} (no data-path collective)",
+                   "l2": "inputs larger than L2 (%.1f GB per step vs 126 MB)" % (bytes_all / 1e9 / world)},
+        "logit_GBps": round(step_gbs, 1), "logit_frac_of_peak": round(step_gbs / world / peak, 4),
+        "committed_tokens_per_s": round(comm_all / (ms_step_all * 1e-3), 1),
+        "breakdown_ms": {"draft_confidence": round(t_conf, 4), "verify": round(t_ver, 4),
+                         "select": round(t_sel, 4)},
+        "roofline": {"bound": "hbm", "kernel": "sb_verify_branches (k_plan + k_rows)",
+                     "achieved": round(ver_gbs, 1), "peak": peak, "peak_source": peak_src, "unit": "GB/s",
+                     "frac": round(ver_gbs / peak, 4), "traffic": traffic_from_profiles(cfg.name),
+                     "algorithmic_bytes_per_launch": a1 + small, "row_pairs_per_launch": units},
+        "gpu_launches": args.steps * ((1 if adaptive else 0) + 2 + 1),
+        "clocks": clk.summary(),
+        "generation_s": round(gen_s, 1),
+    }
+    if e2e is not None:
+        line["e2e"] = e2e
+    if not args.no_cpu_baseline and world == 1:
+        line["cpu_baseline"] = cpu_baseline(cfg, inp, adaptive, buf, budget_s=args.cpu_budget)
+    return line
+
+
+def traffic_from_profiles(name):
+    p = os.path.join(ROOT, "profiles", f"traffic_{name}.json")
+    try:
+        return json.load(open(p))["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
+def run_e2e(args, inp, d, buf, adaptive, stream, dev, world):
+    import torch
+
+    from paper_2506_01979_b200 import api
+
+    keys = ("PL", "QL", "tok", "u", "us", "gamma", "branch_pos")
+    host = {k: torch.empty(inp[k].shape, dtype=inp[k].dtype, pin_memory=True) for k in keys}
+    for k in keys:
+        host[k].copy_(inp[k])
+    dv = {k: inp[k] for k in keys}
+    dv["V"] = inp["V"]
+    h2d = sum(host[k].numel() * host[k].element_size() for k in keys)
+    outs = ("commit_len", "out_tok", "y_tok", "sel_k", "offsets")
+    hout = {k: torch.empty(getattr(buf, k).shape, dtype=torch.int32, pin_memory=True) for k in outs}
+    d2h = sum(v.numel() * 4 for v in hout.values())
+    steps = max(1, min(args.steps, args.e2e_steps))
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record(stream)
+    for _ in range(steps):
+        for k in keys:
+            dv[k].copy_(host[k], non_blocking=True)
+        api.verify_step(d, dv, buf, adaptive=adaptive, stream=stream)
+        for k in outs:
+            hout[k].copy_(getattr(buf, k), non_blocking=True)
+    e.record(stream)
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e) / steps
+    gamma = (buf.c_gamma.view(-1) if adaptive else inp["gamma"]).cpu().tolist()
+    toks = verified_tokens(gamma, inp["branch_pos"].cpu().tolist(), d.K)
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t[0])
+        toks *= world
+    return {"value": round(toks / (ms * 1e-3), 1), "unit": "verified draft tokens/s",
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "ms_per_step": round(ms, 3),
+            "steps": steps, "path": "pinned host -> H2D -> verify_step (C ABI) -> D2H of the commit"}
+
+
+def cpu_baseline(cfg, inp, adaptive, buf, budget_s=15.0):
+    """The fp64 oracle as it stands, on this host's cores, over a bounded sample."""
+    import numpy as np
+    import torch
+
+    import oracle
+    from paper_2506_01979_b200 import synth
+
+    nthreads = os.cpu_count() or 1
+    B = inp["PL"].shape[0]
+    gamma_all = (buf.c_gamma.view(-1) if adaptive else inp["gamma"]).cpu().numpy()
+
+    def run(idx):
+        it = torch.as_tensor(idx, device=inp["PL"].device)
+        sub = synth.to_numpy_inputs({k: (v.index_select(0, it) if torch.is_tensor(v) else v) for k, v in inp.items()})
+        t0 = time.time()
+        if adaptive:
+            c = oracle.confidence(np.ascontiguousarray(sub["QL"][:, :1]), V=sub["V"], nthreads=nthreads)
+            g = c["gamma_next"][:, 0]
+        else:
+            g = sub["gamma"]
+        oracle.verify(sub["PL"], sub["QL"], sub["tok"], sub["u"], sub["us"], g, sub["branch_pos"],
+                      nthreads=nthreads, V=sub["V"])
+        return time.time() - t0, verified_tokens(g.tolist(), sub["branch_pos"].tolist(), cfg.K)
+
+    n = min(B, nthreads)
+    dt, tk = run(np.arange(n))
+    if dt < budget_s and n < B:
+        n2 = int(min(B, max(n, n * budget_s / max(dt, 1e-3))))
+        n2 = max(n, (n2 // nthreads) * nthreads)
+        if n2 > n:
+            dt, tk = run(np.arange(n2))
+            n = n2
+    return {"value": round(tk / dt, 1), "unit": "verified draft tokens/s", "cores": nthreads,
+            "kind": "oracle", "sample": f"{n} of {B} sequences of {cfg.name.upper()} (first {n}), {dt:.1f} s, "
+                                        f"OpenMP over sequences, fp64 plain loops"}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the oracle (the only reference this tier has), on host cores."""
+    if rank != 0:
+        return None
+    import numpy as np
+    import torch
+
+    import oracle
+    from paper_2506_01979_b200 import synth
+
+    cfg = synth.config(args.config)
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    nthreads = os.cpu_count() or 1
+    per_step = max(nthreads, int(args.ref_seqs))
+    adaptive = cfg.layout == "adaptive"
+    total_steps = args.warmup + args.steps
+    inp = synth.generate(cfg, device=dev, b0=0, b1=per_step * min(total_steps, 2))
+    sub_all = synth.to_numpy_inputs(inp)
+    times, toks = [], 0
+    for k in range(total_steps):
+        lo = (k % 2) * per_step
+        sub = {kk: (v[lo:lo + per_step] if isinstance(v, np.ndarray) else v) for kk, v in sub_all.items()}
+        t0 = time.time()
+        if adaptive:
+            c = oracle.confidence(np.ascontiguousarray(sub["QL"][:, :1]), V=sub["V"], nthreads=nthreads)
+            g = c["gamma_next"][:, 0]
+        else:
+            g = sub["gamma"]
+        oracle.verify(sub["PL"], sub["QL"], sub["tok"], sub["u"], sub["us"], g, sub["branch_pos"],
+                      nthreads=nthreads, V=sub["V"])
+        dt = time.time() - t0
+        if k >= args.warmup:
+            times.append(dt)
+            toks += verified_tokens(g.tolist(), sub["branch_pos"].tolist(), cfg.K)
+    tot = sum(times)
+    value = toks / tot
+    return {
+        "impl": "reference", "metric": METRIC, "value": round(value, 1), "unit": "verified draft tokens/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * tot / len(times), 2), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, DESIGN.md §Input recipe)",
+        "config": {"workload": f"{cfg.name.upper()}: {cfg.note}", "V": cfg.V, "K": cfg.K, "G": cfg.G,
+                   "per_rank_batch": cfg.B * cfg.rounds, "layout": cfg.layout,
+                   "step_sample": f"{per_step} sequences per step"},
+        "cpu_baseline": {"value": round(value, 1), "unit": "verified draft tokens/s", "cores": nthreads,
+                         "kind": "oracle", "sample": f"{per_step} sequences of {cfg.name.upper()} per step"},
+        "e2e": {"value": round(value, 1), "unit": "verified draft tokens/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--ref-seqs", type=int, default=32)
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        line = run_reference(args, rank, world)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        return
+    if world > 1:
+        import torch
+
+        torch.cuda.set_device(local_rank)
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    line = run_ours(args, rank, world, local_rank)
+    if line is not None:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch
+
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

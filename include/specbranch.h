@@ -1,0 +1,193 @@
+/*
+ * specbranch.h — C ABI of the B200 (sm_100a) verify-and-branch step of SpecBranch
+ * (arXiv 2506.01979).  Library: paper_2506_01979_b200/libspecbranch.so.
+ *
+ * Citations: P<n> = PAPER.md line n (the paper), S<n> = SPEC.md line n, SURVEY §8.0 =
+ * the contract restated from those passages.  DESIGN.md lists every reading taken
+ * where the paper is silent or ambiguous.
+ *
+ * Problem statement the arguments follow (Alg. 1 inputs P480-492, §3 P94, Eq. 7 P218,
+ * Eq. 9 P239): target logits p and draft logits q for B sequences x K branches x
+ * (G+1) rows, the draft tokens (including the K branch tokens at the branch row), the
+ * per-position uniforms r_i ~ U(0,1) (P531), the draft length gamma_b, the branch row
+ * s_b, and the confidence threshold eps / k_max of Eq. 6-7.
+ *
+ * Conventions common to every entry point
+ *   - All array pointers are DEVICE pointers, caller-owned (e.g. torch tensors), and
+ *     must stay valid until the stream work completes.  The library allocates nothing
+ *     and never synchronises the host; every call is stream-ordered on `stream`.
+ *   - Layouts (row-major, 0-based):
+ *       logits  [B][K][G+1][row_stride]  element (b,slot,i,v) at
+ *               b*seq_stride + (slot*(G+1) + i)*row_stride + v   (bf16 or fp32)
+ *       tok     int32 [B][K][G+1]   token of branch slot k at row i (ts map below)
+ *       u       fp32  [B][K][G+1]   uniforms in [0,1) at the same slots as tok
+ *       "row arrays"  [B][K][G+1] indexed by the physical logit row (b, ls(k,i), i)
+ *       "path arrays" [B][K][G+1] indexed by the token slot      (b, ts(k,i), i)
+ *     Slot maps (Eq. 7-8 P218-222, Alg. 1 P538):
+ *       ls(k,i) = (i <= s_b) ? 0 : k     rows up to the branch row share slot 0
+ *       ts(k,i) = (i <  s_b) ? 0 : k     each branch owns its token/uniform from s_b on
+ *     Path length L_b = gamma_b if s_b < gamma_b (bonus row gamma_b), else gamma_b + 1
+ *     (Algorithm-1 form: the branch token sits at the target's p_{gamma+1}, P538).
+ *   - Entries of row / path arrays that are not on any tested path are written NaN
+ *     (float) or -1 (int).  Rows >= L_b are never read.
+ *   - Host-checkable argument errors return SB_ERR_INVALID_ARG before any launch.
+ *     Data errors found on the device never fail the call: they are clamped or
+ *     skipped and reported per sequence in status[b] (SB_ST_* bits).
+ *   - workspace: device buffer of sb_workspace_bytes(d) bytes, 256-byte aligned, that
+ *     must be ZERO-FILLED before its first use; every call leaves it re-usable.  The
+ *     same workspace must be passed to sb_select_branch after sb_verify_branches (it
+ *     carries the per-row softmax state between them) and must not be shared by calls
+ *     in flight on different streams.
+ *   - Functions are stateless apart from `workspace` and thread-safe across streams.
+ */
+#ifndef SPECBRANCH_H
+#define SPECBRANCH_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* sb_stream_t; /* identical to cudaStream_t; NULL = default */
+
+typedef enum {
+  SB_OK = 0,
+  SB_ERR_INVALID_ARG = 1, /* bad dims, null required pointer, misaligned workspace   */
+  SB_ERR_UNSUPPORTED = 2, /* valid request this build does not implement            */
+  SB_ERR_CUDA = 3,        /* a CUDA launch or runtime call failed                   */
+  SB_ERR_NCCL = 4,        /* reserved for the vocabulary-sharded exchange           */
+  SB_ERR_WORKSPACE = 5    /* workspace_bytes < sb_workspace_bytes(d)                */
+} sb_status;
+
+typedef enum { SB_BF16 = 0, SB_F32 = 1 } sb_dtype;
+typedef enum { SB_SELECT_EQ9 = 0, SB_SELECT_ALG1 = 1 } sb_select_rule;
+typedef enum { SB_CONF_TOP1 = 0, SB_CONF_TOKEN = 1, SB_CONF_ENTROPY = 2 } sb_conf_mode;
+
+/* per-sequence status bits (status[b]) */
+#define SB_ST_GAMMA_CLAMPED 1u  /* gamma_b outside [0,G]: clamped                        */
+#define SB_ST_BRANCH_CLAMPED 2u /* s_b outside [0,gamma_b]: clamped                      */
+#define SB_ST_BAD_TOKEN 4u      /* a path token outside [0,V): that test counts rejected */
+#define SB_ST_NONFINITE 8u      /* a row read holds NaN/+inf or is all -inf              */
+#define SB_ST_ZERO_RESID 16u    /* residual mass R == 0 after a rejection: sampled from p */
+
+typedef struct {
+  int32_t B;          /* sequences, >= 1                                              */
+  int32_t K;          /* branch slots, 1..32                                          */
+  int32_t G;          /* gamma_max, 0..31 (rows per slot = G+1)                       */
+  int32_t V;          /* vocabulary columns, >= 2                                     */
+  int32_t v_offset;   /* vocabulary shard offset; unsharded: 0                        */
+  int32_t v_total;    /* full vocabulary; unsharded: V                                */
+  int64_t row_stride; /* elements between rows, >= V                                  */
+  int64_t seq_stride; /* elements between sequences; 0 -> K*(G+1)*row_stride         */
+  int32_t dtype;      /* sb_dtype of the logits                                       */
+  int32_t reserved;   /* must be 0                                                    */
+} sb_dims;
+
+/* Library version string, and a static message for a status code. */
+const char* sb_version(void);
+const char* sb_status_string(sb_status s);
+
+/* Device bytes the caller must provide as `workspace` for dims d (0 if d invalid). */
+size_t sb_workspace_bytes(const sb_dims* d);
+
+/*
+ * sb_verify_branches — row statistics, acceptance test and first rejection.
+ *   (§3 P94 beta = min(1, p/q) and Match; Alg. 1 P523-534; branch tests P538)
+ *
+ * For every physical row pair (p row, q row) on a tested path — slot 0 rows
+ * 0..min(s_b, L_b-1), plus rows s_b+1..L_b-1 of every slot — computes in one streaming
+ * pass: lse = m + ln sum exp(l - m) of both rows, and for the q row the top-1
+ * probability, its smallest id and the entropy H = -sum q ln q in nats (§4.2 P170).
+ * Then for every path token x through the row: P[x], Q[x] and the acceptance bit
+ * acc = (u * Q[x] <= P[x])   (accept iff r <= p/q, P534/P538; Q[x] = 0 accepts, S127),
+ * and per branch k the accepted prefix n_k = min({i < L_b : !acc(k,i)} U {L_b}).
+ *
+ * Inputs : p_logits, q_logits  logits (layout above);
+ *          tok, u              path tokens / uniforms [B][K][G+1];
+ *          gamma               [B] draft lengths, NULL -> G for all;
+ *          branch_pos          [B] branch rows s_b, NULL -> 0 for all.
+ * Outputs: lse_p, lse_q        row arrays (natural log);
+ *          top1_q, top1_id_q, entropy_q  row arrays (q rows), each nullable;
+ *          p_tok, q_tok        path arrays, P_i[x], Q_i[x];
+ *          acc_mask            [B][K] uint32, bit i = acc(k,i) for i < L_b;
+ *          n_acc               [B][K] accepted prefix lengths;
+ *          status              [B] SB_ST_* bits (overwritten).
+ * comm must be NULL (vocabulary sharding: see DESIGN.md; SB_ERR_UNSUPPORTED otherwise).
+ */
+sb_status sb_verify_branches(const sb_dims* d, const void* p_logits, const void* q_logits,
+                             const int32_t* tok, const float* u, const int32_t* gamma,
+                             const int32_t* branch_pos, float* lse_p, float* lse_q,
+                             float* p_tok, float* q_tok, uint32_t* acc_mask, int32_t* n_acc,
+                             float* top1_q, int32_t* top1_id_q, float* entropy_q,
+                             int32_t* status, void* comm, void* workspace,
+                             size_t workspace_bytes, sb_stream_t stream);
+
+/*
+ * sb_select_branch — branch-point verification, correction/bonus sample, commit.
+ *   (Eq. 9 P236-241; Alg. 1 P536-557; residual P94/P547/P554; rollback P655; RB P317/P734)
+ *
+ * Per sequence b with A = {k : n_k > s_b}:
+ *   SB_SELECT_EQ9  k* = argmax_{k in A} p_logits[b][0][s_b][tok[b][k][s_b]] (raw target
+ *                  logits = argmax p within the row, "maximum logits" P241); ties ->
+ *                  smaller token id, then smaller k;
+ *   SB_SELECT_ALG1 k* = argmax_{k in A} u[b][k][s_b], ties -> smaller k (P540).
+ *   A empty: k* = -1; commit tok[b][0][0..j-1], j = min(n_0, s_b), and y drawn from
+ *            norm(max(0, P_j - Q_j)) of slot 0 (P547, P554, P655).
+ *   else n = n_{k*}: commit k*'s path tokens 0..n-1, then
+ *            n <  L_b            -> y ~ norm(max(0, P_n - Q_n)) at row n of slot ls(k*,n);
+ *            n == L_b, s_b<gamma -> y ~ P_{gamma_b} of slot k* (bonus, P94);
+ *            n == L_b, s_b==gamma-> no y (branch token accepted, P237).
+ *   Sampling: inverse CDF over ascending token id with the one uniform us[b]:
+ *   j* = min{j : F(j) > us*R}, F(j) = sum_{v<=j} r(v); if rounding leaves us*R >= F(V-1)
+ *   the last v with r(v) > 0.  R == 0 after a rejection samples from P instead
+ *   (SB_ST_ZERO_RESID; SPEC "no residual mass", S134-140).
+ *
+ * Inputs : p_logits, q_logits, tok, u as for sb_verify_branches; us [B] in [0,1);
+ *          gamma, branch_pos as before; n_acc from sb_verify_branches; rule.
+ * Outputs: sel_k [B] (k* or -1); commit_len [B]; out_tok [B][G+2] committed tokens
+ *          (-1 padded); y_tok [B] (-1 none); y_kind [B] (0 none, 1 residual, 2 bonus);
+ *          offsets [B+1] exclusive scan of commit_len; packed_tok [B*(G+2)] nullable,
+ *          the commits concatenated at offsets; path_rolled [B] = L_b - n (RB
+ *          numerator, P317); branch_discarded [B] = (K-1)(L_b - s_b) (excluded from RB,
+ *          P734); keep_mask [B][K] bit i of slot k set iff the draft token at (k,i) is
+ *          committed (the KV rows to keep, P241); resid_mass [B] nullable, the mass R of
+ *          the sampled vector (1 for a bonus, 0 for none); status [B] (bits OR-ed in).
+ */
+sb_status sb_select_branch(const sb_dims* d, const void* p_logits, const void* q_logits,
+                           const int32_t* tok, const float* u, const float* us,
+                           const int32_t* gamma, const int32_t* branch_pos,
+                           const int32_t* n_acc, sb_select_rule rule, int32_t* sel_k,
+                           int32_t* commit_len, int32_t* out_tok, int32_t* y_tok,
+                           int32_t* y_kind, int32_t* offsets, int32_t* packed_tok,
+                           int32_t* path_rolled, int32_t* branch_discarded,
+                           uint32_t* keep_mask, float* resid_mass, int32_t* status,
+                           void* comm, void* workspace, size_t workspace_bytes,
+                           sb_stream_t stream);
+
+/*
+ * sb_draft_confidence — the implicit draft-confidence statistic and adaptive gamma.
+ *   (§4.2 P170; Eq. 6 P194-202; Eq. 7 P218; Alg. 1 P517; App. E.6 P954/P965)
+ *
+ * Over rows i = 0..G-1 of every (b,k) group of q_logits:
+ *   top1_prob = max_x q(x), top1_id (smallest), entropy H (nats), tok_prob = q(x_i)
+ *   of tok[b][k][i] (TOKEN mode; nullable otherwise), and
+ *   stat_i = top1_prob (TOP1) | tok_prob (TOKEN) | 1 - sqrt(lambda * H) (ENTROPY);
+ *   stop = min({i : stat_i <= eps} U {G})   (Eq. 6 keeps q(x) > eps);
+ *   k_next = max(1, floor(k_max (1 - c))) with c the top-1 (TOKEN: token) probability
+ *   at the stop row (Eq. 7), -1 when stop == G;  gamma_next = max(1, stop).
+ * Output arrays [B][K][G] (rows) and [B][K] (groups); all but stop nullable.
+ * To score only slot 0 of a [B][K'][G+1] tensor pass K = 1 and seq_stride of K'.
+ */
+sb_status sb_draft_confidence(const sb_dims* d, const void* q_logits, const int32_t* tok,
+                              sb_conf_mode mode, float eps, float lambda, int32_t k_max,
+                              float* top1_prob, int32_t* top1_id, float* entropy,
+                              float* tok_prob, float* stat, int32_t* stop, int32_t* k_next,
+                              int32_t* gamma_next, void* comm, void* workspace,
+                              size_t workspace_bytes, sb_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPECBRANCH_H */

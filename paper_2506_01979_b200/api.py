@@ -1,0 +1,196 @@
+"""Python binding of the C ABI (include/specbranch.h) — same names, torch tensors in.
+
+Argument marshalling only: tensors are checked for device / dtype / contiguity and
+passed as raw device pointers; every step of the verify-and-branch path runs in
+libspecbranch.so.  PyTorch provides device memory and streams, nothing else.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib as L
+from ._lib import (SB_BF16, SB_CONF_ENTROPY, SB_CONF_TOKEN, SB_CONF_TOP1, SB_F32,  # noqa: F401
+                   SB_SELECT_ALG1, SB_SELECT_EQ9)
+
+
+def dims_for(logits: torch.Tensor, V: int | None = None, K: int | None = None,
+             seq_stride: int = 0) -> L.sb_dims:
+    """sb_dims of a [B][K][G+1][row_stride] logits tensor (row_stride >= V)."""
+    if logits.dim() != 4:
+        raise ValueError("logits must be [B][K][G+1][row_stride]")
+    B, K0, R1, rs = logits.shape
+    if logits.stride(3) != 1 or logits.stride(2) != rs or logits.stride(1) != R1 * rs:
+        raise ValueError("logits rows must be contiguous with row_stride = shape[3]")
+    dt = {torch.bfloat16: SB_BF16, torch.float32: SB_F32}.get(logits.dtype)
+    if dt is None:
+        raise TypeError("logits must be bfloat16 or float32")
+    V = rs if V is None else V
+    K = K0 if K is None else K
+    ss = seq_stride or (logits.stride(0) if logits.stride(0) != K * R1 * rs else 0)
+    return L.sb_dims(B, K, R1 - 1, V, 0, V, rs, ss, dt, 0)
+
+
+def _ptr(t: torch.Tensor | None, dtype=None, what=""):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError(f"{what}: expected a CUDA tensor")
+    if dtype is not None and t.dtype not in (dtype if isinstance(dtype, tuple) else (dtype,)):
+        raise TypeError(f"{what}: expected {dtype}, got {t.dtype}")
+    if not t.is_contiguous() and what not in ("p_logits", "q_logits"):
+        raise ValueError(f"{what}: expected a contiguous tensor")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def sb_workspace_bytes(d: L.sb_dims) -> int:
+    return int(L.lib().sb_workspace_bytes(ctypes.byref(d)))
+
+
+def make_workspace(d: L.sb_dims, device) -> torch.Tensor:
+    """Zero-filled device workspace (the ABI requires zero before first use)."""
+    n = sb_workspace_bytes(d)
+    if n == 0:
+        raise ValueError("invalid sb_dims")
+    return torch.zeros(n, dtype=torch.uint8, device=device)
+
+
+I32, F32 = torch.int32, torch.float32
+LOG = (torch.bfloat16, torch.float32)
+
+
+def sb_verify_branches(d, p_logits, q_logits, tok, u, gamma, branch_pos, lse_p, lse_q, p_tok,
+                       q_tok, acc_mask, n_acc, top1_q, top1_id_q, entropy_q, status, workspace,
+                       stream=None):
+    rc = L.lib().sb_verify_branches(
+        ctypes.byref(d), _ptr(p_logits, LOG, "p_logits"), _ptr(q_logits, LOG, "q_logits"),
+        _ptr(tok, I32, "tok"), _ptr(u, F32, "u"), _ptr(gamma, I32, "gamma"),
+        _ptr(branch_pos, I32, "branch_pos"), _ptr(lse_p, F32, "lse_p"), _ptr(lse_q, F32, "lse_q"),
+        _ptr(p_tok, F32, "p_tok"), _ptr(q_tok, F32, "q_tok"), _ptr(acc_mask, I32, "acc_mask"),
+        _ptr(n_acc, I32, "n_acc"), _ptr(top1_q, F32, "top1_q"), _ptr(top1_id_q, I32, "top1_id_q"),
+        _ptr(entropy_q, F32, "entropy_q"), _ptr(status, I32, "status"), None,
+        _ptr(workspace, torch.uint8, "workspace"), workspace.numel(), _stream(stream))
+    L.check(rc, "sb_verify_branches")
+
+
+def sb_select_branch(d, p_logits, q_logits, tok, u, us, gamma, branch_pos, n_acc, rule, sel_k,
+                     commit_len, out_tok, y_tok, y_kind, offsets, packed_tok, path_rolled,
+                     branch_discarded, keep_mask, resid_mass, status, workspace, stream=None):
+    rc = L.lib().sb_select_branch(
+        ctypes.byref(d), _ptr(p_logits, LOG, "p_logits"), _ptr(q_logits, LOG, "q_logits"),
+        _ptr(tok, I32, "tok"), _ptr(u, F32, "u"), _ptr(us, F32, "us"), _ptr(gamma, I32, "gamma"),
+        _ptr(branch_pos, I32, "branch_pos"), _ptr(n_acc, I32, "n_acc"), int(rule),
+        _ptr(sel_k, I32, "sel_k"), _ptr(commit_len, I32, "commit_len"), _ptr(out_tok, I32, "out_tok"),
+        _ptr(y_tok, I32, "y_tok"), _ptr(y_kind, I32, "y_kind"), _ptr(offsets, I32, "offsets"),
+        _ptr(packed_tok, I32, "packed_tok"), _ptr(path_rolled, I32, "path_rolled"),
+        _ptr(branch_discarded, I32, "branch_discarded"), _ptr(keep_mask, I32, "keep_mask"),
+        _ptr(resid_mass, F32, "resid_mass"), _ptr(status, I32, "status"), None,
+        _ptr(workspace, torch.uint8, "workspace"), workspace.numel(), _stream(stream))
+    L.check(rc, "sb_select_branch")
+
+
+def sb_draft_confidence(d, q_logits, tok, mode, eps, lam, k_max, top1_prob, top1_id, entropy,
+                        tok_prob, stat, stop, k_next, gamma_next, workspace, stream=None):
+    rc = L.lib().sb_draft_confidence(
+        ctypes.byref(d), _ptr(q_logits, LOG, "q_logits"), _ptr(tok, I32, "tok"), int(mode),
+        float(eps), float(lam), int(k_max), _ptr(top1_prob, F32, "top1_prob"),
+        _ptr(top1_id, I32, "top1_id"), _ptr(entropy, F32, "entropy"), _ptr(tok_prob, F32, "tok_prob"),
+        _ptr(stat, F32, "stat"), _ptr(stop, I32, "stop"), _ptr(k_next, I32, "k_next"),
+        _ptr(gamma_next, I32, "gamma_next"), None, _ptr(workspace, torch.uint8, "workspace"),
+        workspace.numel(), _stream(stream))
+    L.check(rc, "sb_draft_confidence")
+
+
+# ------------------------------------------------------------------ convenience layer
+@dataclass
+class StepBuffers:
+    """Every output of one verify-and-branch round, preallocated on the device."""
+    lse_p: torch.Tensor
+    lse_q: torch.Tensor
+    p_tok: torch.Tensor
+    q_tok: torch.Tensor
+    acc_mask: torch.Tensor
+    n_acc: torch.Tensor
+    top1_q: torch.Tensor
+    top1_id_q: torch.Tensor
+    entropy_q: torch.Tensor
+    status: torch.Tensor
+    sel_k: torch.Tensor
+    commit_len: torch.Tensor
+    out_tok: torch.Tensor
+    y_tok: torch.Tensor
+    y_kind: torch.Tensor
+    offsets: torch.Tensor
+    packed_tok: torch.Tensor
+    path_rolled: torch.Tensor
+    branch_discarded: torch.Tensor
+    keep_mask: torch.Tensor
+    resid_mass: torch.Tensor
+    # draft confidence (slot-0 rows) for the adaptive-gamma configurations
+    c_top1: torch.Tensor
+    c_id: torch.Tensor
+    c_ent: torch.Tensor
+    c_stat: torch.Tensor
+    c_stop: torch.Tensor
+    c_knext: torch.Tensor
+    c_gamma: torch.Tensor
+    workspace: torch.Tensor
+    conf_workspace: torch.Tensor
+
+    @staticmethod
+    def alloc(d: L.sb_dims, device) -> "StepBuffers":
+        B, K, G = d.B, d.K, d.G
+        R1 = G + 1
+        e = lambda *s, dt=F32: torch.empty(s, dtype=dt, device=device)  # noqa: E731
+        dc = L.sb_dims(B, 1, G, d.V, 0, d.V, d.row_stride,
+                       d.seq_stride or K * R1 * d.row_stride, d.dtype, 0)
+        return StepBuffers(
+            lse_p=e(B, K, R1), lse_q=e(B, K, R1), p_tok=e(B, K, R1), q_tok=e(B, K, R1),
+            acc_mask=e(B, K, dt=I32), n_acc=e(B, K, dt=I32), top1_q=e(B, K, R1),
+            top1_id_q=e(B, K, R1, dt=I32), entropy_q=e(B, K, R1), status=e(B, dt=I32),
+            sel_k=e(B, dt=I32), commit_len=e(B, dt=I32), out_tok=e(B, G + 2, dt=I32),
+            y_tok=e(B, dt=I32), y_kind=e(B, dt=I32), offsets=e(B + 1, dt=I32),
+            packed_tok=e(B * (G + 2), dt=I32), path_rolled=e(B, dt=I32),
+            branch_discarded=e(B, dt=I32), keep_mask=e(B, K, dt=I32), resid_mass=e(B),
+            c_top1=e(B, 1, max(G, 1)), c_id=e(B, 1, max(G, 1), dt=I32), c_ent=e(B, 1, max(G, 1)),
+            c_stat=e(B, 1, max(G, 1)), c_stop=e(B, 1, dt=I32), c_knext=e(B, 1, dt=I32),
+            c_gamma=e(B, 1, dt=I32),
+            workspace=make_workspace(d, device), conf_workspace=make_workspace(dc, device))
+
+
+def conf_dims(d: L.sb_dims) -> L.sb_dims:
+    """Slot-0 view of a [B][K][G+1] draft tensor (the drafted path before branching)."""
+    return L.sb_dims(d.B, 1, d.G, d.V, 0, d.V, d.row_stride,
+                     d.seq_stride or d.K * (d.G + 1) * d.row_stride, d.dtype, 0)
+
+
+def verify_step(d: L.sb_dims, inp: dict, buf: StepBuffers, rule: int = SB_SELECT_EQ9,
+                adaptive: bool = False, eps: float = 0.2, k_max: int = 6, stream=None):
+    """One whole hot-path step: [draft confidence -> adaptive gamma] -> verify -> select.
+
+    inp: PL, QL, tok, u, us, gamma, branch_pos device tensors (synth.generate layout).
+    With adaptive=True gamma_b = max(1, stop_b) of the slot-0 draft rows (Eq. 6, TOP1)
+    replaces inp["gamma"] and s_b = 0.
+    """
+    gamma = inp["gamma"]
+    if adaptive:
+        sb_draft_confidence(conf_dims(d), inp["QL"], None, SB_CONF_TOP1, eps, 1.0, k_max,
+                            buf.c_top1, buf.c_id, buf.c_ent, None, buf.c_stat, buf.c_stop,
+                            buf.c_knext, buf.c_gamma, buf.conf_workspace, stream)
+        gamma = buf.c_gamma.view(-1)
+    sb_verify_branches(d, inp["PL"], inp["QL"], inp["tok"], inp["u"], gamma, inp["branch_pos"],
+                       buf.lse_p, buf.lse_q, buf.p_tok, buf.q_tok, buf.acc_mask, buf.n_acc,
+                       buf.top1_q, buf.top1_id_q, buf.entropy_q, buf.status, buf.workspace, stream)
+    sb_select_branch(d, inp["PL"], inp["QL"], inp["tok"], inp["u"], inp["us"], gamma,
+                     inp["branch_pos"], buf.n_acc, rule, buf.sel_k, buf.commit_len, buf.out_tok,
+                     buf.y_tok, buf.y_kind, buf.offsets, buf.packed_tok, buf.path_rolled,
+                     buf.branch_discarded, buf.keep_mask, buf.resid_mass, buf.status,
+                     buf.workspace, stream)
+    return gamma

@@ -1,0 +1,36 @@
+// sb_api.cu — version, status strings, workspace sizing, device attributes.
+#include <cuda_runtime.h>
+
+#include "sb_host.h"
+
+namespace sb {
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+}  // namespace sb
+
+extern "C" const char* sb_version(void) { return "specbranch-b200 0.1 (sm_100a)"; }
+
+extern "C" const char* sb_status_string(sb_status s) {
+  switch (s) {
+    case SB_OK: return "ok";
+    case SB_ERR_INVALID_ARG: return "invalid argument";
+    case SB_ERR_UNSUPPORTED: return "unsupported";
+    case SB_ERR_CUDA: return "CUDA error";
+    case SB_ERR_NCCL: return "NCCL error";
+    case SB_ERR_WORKSPACE: return "workspace too small";
+  }
+  return "unknown status";
+}
+
+extern "C" size_t sb_workspace_bytes(const sb_dims* d) {
+  if (!sb::dims_valid(d)) return 0;
+  return sb::carve(*d, nullptr).bytes;
+}

@@ -1,0 +1,344 @@
+// sb_common.cuh — shared device helpers of libspecbranch (sm_100a only).
+//
+// Row softmax state in log2 units.  With c = fp32(log2 e) every element contributes
+//   e_v = 2^(l_v * c - ms),   ms = m * c (one fp32 constant per running max m)
+// computed as ex2.approx(fma(l_v, c, -ms)): the product l*c is exact inside the FMA,
+// so the rounding of ms cancels between a row's normaliser Z = sum e_v and any single
+// probability 2^(l_x c - MS) / Z evaluated later in fp64 with the same MS.  The
+// entropy uses S1 = sum e_v * a_v (a_v the exponent), H = ln2 * (log2 Z - S1 / Z).
+// All reductions are fixed-order trees (no float atomics): bit-reproducible.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <math_constants.h>
+#include <stdint.h>
+
+#include "../../include/specbranch.h"
+
+namespace sb {
+
+constexpr float kC = 1.4426950408889634f;  // fp32(log2 e)
+constexpr float kLn2 = 0.69314718055994531f;
+constexpr int kMaxK = 32;
+constexpr int kMaxG = 31;
+
+struct Dims {
+  int B, K, G, V;
+  int64_t rs;  // row stride (elements)
+  int64_t ss;  // sequence stride (elements)
+  int dtype;
+};
+
+__host__ __device__ inline int64_t row_off(const Dims& d, int b, int slot, int i) {
+  return (int64_t)b * d.ss + ((int64_t)slot * (d.G + 1) + i) * d.rs;
+}
+__host__ __device__ inline int64_t ent(const Dims& d, int b, int k, int i) {  // [B][K][G+1]
+  return ((int64_t)b * d.K + k) * (d.G + 1) + i;
+}
+
+// ------------------------------------------------------------------ small PTX helpers
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+__device__ __forceinline__ uint4 ldg_stream(const void* p) {
+  uint4 r;
+  asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ float bf16_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf16_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+
+template <typename T>
+__device__ __forceinline__ float ld_scalar(const T* p);
+template <>
+__device__ __forceinline__ float ld_scalar<float>(const float* p) {
+  return __ldg(p);
+}
+template <>
+__device__ __forceinline__ float ld_scalar<__nv_bfloat16>(const __nv_bfloat16* p) {
+  return __uint_as_float((uint32_t)__ldg(reinterpret_cast<const unsigned short*>(p)) << 16);
+}
+
+// Unpack one 16-byte vector into E fp32 values (exact widening).
+template <typename T>
+struct Vec;
+template <>
+struct Vec<__nv_bfloat16> {
+  static constexpr int E = 8;
+  __device__ __forceinline__ static void unpack(const uint4& v, float* f) {
+    f[0] = bf16_lo(v.x); f[1] = bf16_hi(v.x); f[2] = bf16_lo(v.y); f[3] = bf16_hi(v.y);
+    f[4] = bf16_lo(v.z); f[5] = bf16_hi(v.z); f[6] = bf16_lo(v.w); f[7] = bf16_hi(v.w);
+  }
+  __device__ __forceinline__ static float vmax(const float* f) {
+    return fmax3(fmax3(f[0], f[1], f[2]), fmax3(f[3], f[4], f[5]), fmaxf(f[6], f[7]));
+  }
+};
+template <>
+struct Vec<float> {
+  static constexpr int E = 4;
+  __device__ __forceinline__ static void unpack(const uint4& v, float* f) {
+    f[0] = __uint_as_float(v.x); f[1] = __uint_as_float(v.y);
+    f[2] = __uint_as_float(v.z); f[3] = __uint_as_float(v.w);
+  }
+  __device__ __forceinline__ static float vmax(const float* f) {
+    return fmaxf(fmax3(f[0], f[1], f[2]), f[3]);
+  }
+};
+
+// ------------------------------------------------------------------ online row state
+// Per-thread running state of one row.  NA independent accumulators for ILP and a
+// shorter fp32 summation chain.  kQ adds S1 (entropy) and the top-1 index.
+template <bool kQ, int NA>
+struct RowAcc {
+  float m;       // running max (raw logit units), -inf until the first finite value
+  float ms;      // m * c (fp32), the exponent offset used by every term
+  float z[NA];   // sum of 2^(l c - ms)
+  float s1[kQ ? NA : 1];
+  int idx;       // smallest index attaining m (kQ only)
+
+  __device__ __forceinline__ void init() {
+    m = -CUDART_INF_F;
+    ms = 0.f;
+#pragma unroll
+    for (int j = 0; j < NA; ++j) z[j] = 0.f;
+#pragma unroll
+    for (int j = 0; j < (kQ ? NA : 1); ++j) s1[j] = 0.f;
+    idx = 0x7fffffff;
+  }
+
+  // raise the running max to nm (> m); rare after the first few vectors
+  __device__ __forceinline__ void rescale(float nm) {
+    const float nms = nm * kC;
+    const float sc = (m == -CUDART_INF_F) ? 0.f : ex2(ms - nms);
+    const float dd = ms - nms;
+#pragma unroll
+    for (int j = 0; j < NA; ++j) {
+      if (kQ) s1[j] = sc * (s1[j] + z[j] * dd);
+      z[j] *= sc;
+    }
+    m = nm;
+    ms = nms;
+  }
+
+  // accumulate E values f[] whose first element has index base
+  template <int E>
+  __device__ __forceinline__ void add(const float* f, float vmax, int base) {
+    if (vmax > m) {
+      rescale(vmax);
+      if (kQ) {
+        int first = E;
+#pragma unroll
+        for (int j = E - 1; j >= 0; --j)
+          if (f[j] == vmax) first = j;
+        idx = base + first;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+      const float a = fmaf(f[j], kC, -ms);
+      const float e = ex2(a);
+      z[j % NA] += e;
+      if (kQ) s1[j % NA] = fmaf(e, fmaxf(a, -200.f), s1[j % NA]);
+    }
+  }
+
+  __device__ __forceinline__ void add1(float f, int index) {
+    if (f > m) {
+      rescale(f);
+      if (kQ) idx = index;
+    }
+    const float a = fmaf(f, kC, -ms);
+    const float e = ex2(a);
+    z[0] += e;
+    if (kQ) s1[0] = fmaf(e, fmaxf(a, -200.f), s1[0]);
+  }
+};
+
+// Reduced row state (one per thread after folding accumulators, then across threads).
+struct RowStat {
+  float m, ms, z, s1;
+  int idx;
+};
+
+template <bool kQ, int NA>
+__device__ __forceinline__ RowStat fold(const RowAcc<kQ, NA>& a) {
+  RowStat r;
+  r.m = a.m;
+  r.ms = a.ms;
+  float z = 0.f, s = 0.f;
+#pragma unroll
+  for (int j = 0; j < NA; ++j) z += a.z[j];
+  if (kQ) {
+#pragma unroll
+    for (int j = 0; j < NA; ++j) s += a.s1[j];
+  }
+  r.z = z;
+  r.s1 = s;
+  r.idx = kQ ? a.idx : 0;
+  return r;
+}
+
+// Combine two states (commutative up to rounding; called in a fixed tree order).
+__device__ __forceinline__ RowStat combine(RowStat a, RowStat b) {
+  // make `a` the one with the larger max (ties: smaller index)
+  if (b.m > a.m || (b.m == a.m && b.idx < a.idx)) {
+    RowStat t = a;
+    a = b;
+    b = t;
+  }
+  if (b.m == -CUDART_INF_F || a.m == -CUDART_INF_F) {
+    // nothing finite in b (or anywhere): b contributes 0 (its z is 0 or NaN-marked)
+    if (b.m == -CUDART_INF_F && !(b.z == b.z)) a.z = b.z;  // keep NaN poison
+    return a;
+  }
+  const float dd = b.ms - a.ms;
+  const float sc = ex2(dd);
+  a.s1 = a.s1 + sc * (b.s1 + b.z * dd);
+  a.z = a.z + sc * b.z;
+  return a;
+}
+
+__device__ __forceinline__ RowStat shfl_xor(const RowStat& s, int o) {
+  RowStat r;
+  r.m = __shfl_xor_sync(0xffffffffu, s.m, o);
+  r.ms = __shfl_xor_sync(0xffffffffu, s.ms, o);
+  r.z = __shfl_xor_sync(0xffffffffu, s.z, o);
+  r.s1 = __shfl_xor_sync(0xffffffffu, s.s1, o);
+  r.idx = __shfl_xor_sync(0xffffffffu, s.idx, o);
+  return r;
+}
+
+// Block-wide reduction of RowStat; result valid in every thread.  smem: NT/32 entries.
+template <int NT>
+__device__ __forceinline__ RowStat block_reduce(RowStat s, RowStat* smem) {
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s = combine(s, shfl_xor(s, o));
+  if (lane == 0) smem[w] = s;
+  __syncthreads();
+  RowStat r = smem[0];
+#pragma unroll
+  for (int j = 1; j < NW; ++j) r = combine(r, smem[j]);
+  __syncthreads();  // smem reusable after return
+  return r;
+}
+
+// Stream one row [0, V) into a per-thread accumulator (vector path if vec_ok).
+template <typename T, bool kQ, int NA, int NT, int U>
+__device__ __forceinline__ void stream_row(const T* __restrict__ row, int V, bool vec_ok,
+                                           RowAcc<kQ, NA>& acc) {
+  constexpr int E = Vec<T>::E;
+  const int tid = threadIdx.x;
+  int done = 0;
+  if (vec_ok) {
+    const int nvec = V / E;
+    const uint4* rv = reinterpret_cast<const uint4*>(row);
+    const int full = nvec / (U * NT) * (U * NT);
+    for (int vb = tid; vb < full; vb += U * NT) {
+      uint4 x[U];
+#pragma unroll
+      for (int j = 0; j < U; ++j) x[j] = ldg_stream(rv + vb + j * NT);
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        float f[E];
+        Vec<T>::unpack(x[j], f);
+        acc.template add<E>(f, Vec<T>::vmax(f), (vb + j * NT) * E);
+      }
+    }
+    for (int vb = full + tid; vb < nvec; vb += NT) {
+      float f[E];
+      Vec<T>::unpack(ldg_stream(rv + vb), f);
+      acc.template add<E>(f, Vec<T>::vmax(f), vb * E);
+    }
+    done = nvec * E;
+  }
+  for (int v = done + tid; v < V; v += NT) acc.add1(ld_scalar(row + v), v);
+}
+
+// Two rows (p and q) interleaved so both streams keep loads in flight.
+template <typename T, int NA, int NT, int U>
+__device__ __forceinline__ void stream_pair(const T* __restrict__ prow, const T* __restrict__ qrow,
+                                            int V, bool vec_ok, RowAcc<false, NA>& pa,
+                                            RowAcc<true, NA>& qa) {
+  constexpr int E = Vec<T>::E;
+  const int tid = threadIdx.x;
+  int done = 0;
+  if (vec_ok) {
+    const int nvec = V / E;
+    const uint4* pv = reinterpret_cast<const uint4*>(prow);
+    const uint4* qv = reinterpret_cast<const uint4*>(qrow);
+    const int full = nvec / (U * NT) * (U * NT);
+    for (int vb = tid; vb < full; vb += U * NT) {
+      uint4 xp[U], xq[U];
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        xp[j] = ldg_stream(pv + vb + j * NT);
+        xq[j] = ldg_stream(qv + vb + j * NT);
+      }
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        float f[E];
+        Vec<T>::unpack(xp[j], f);
+        pa.template add<E>(f, Vec<T>::vmax(f), (vb + j * NT) * E);
+        Vec<T>::unpack(xq[j], f);
+        qa.template add<E>(f, Vec<T>::vmax(f), (vb + j * NT) * E);
+      }
+    }
+    for (int vb = full + tid; vb < nvec; vb += NT) {
+      float f[E];
+      Vec<T>::unpack(ldg_stream(pv + vb), f);
+      pa.template add<E>(f, Vec<T>::vmax(f), vb * E);
+      Vec<T>::unpack(ldg_stream(qv + vb), f);
+      qa.template add<E>(f, Vec<T>::vmax(f), vb * E);
+    }
+    done = nvec * E;
+  }
+  for (int v = done + tid; v < V; v += NT) {
+    pa.add1(ld_scalar(prow + v), v);
+    qa.add1(ld_scalar(qrow + v), v);
+  }
+}
+
+// Final per-row quantities from a reduced state.
+struct RowOut {
+  float MS;     // exponent offset (log2 units) of Z
+  float Z;      // sum 2^(l c - MS)
+  bool finite;  // row had a distribution (no NaN / +inf, not all -inf)
+};
+__device__ __forceinline__ RowOut finish(const RowStat& r) {
+  RowOut o;
+  o.MS = r.ms;
+  o.Z = r.z;
+  o.finite = (r.m != -CUDART_INF_F) && (r.m != CUDART_INF_F) && (r.z == r.z) && (r.z > 0.f) &&
+             (r.z != CUDART_INF_F);
+  return o;
+}
+
+// Probability of one token from the row state, in fp64: 2^(l_x c - MS) / Z.
+__device__ __forceinline__ double tok_prob(float lx, float MS, float Z) {
+  const double arg = (double)lx * (double)kC - (double)MS;  // exact product in fp64
+  return exp2(arg) / (double)Z;
+}
+
+// Warp-level inclusive scan (Kogge-Stone), fixed order.
+__device__ __forceinline__ float warp_incl_scan(float x) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const float y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  return x;
+}
+
+}  // namespace sb

@@ -1,0 +1,159 @@
+// sb_confidence.cu — sb_draft_confidence: the implicit draft-confidence statistic
+// (§4.2 P170: max_x q(x) or 1 - sqrt(lambda H); App. E.6 P954/P965), the Eq. 6 stop
+// (keep q(x) > eps, P198; Alg. 1 "Mask" P517) and Eq. 7's adaptive branch count
+// k = max(1, floor(k_max (1 - q(x_b)))) at the stop row (P218).  SURVEY §8.1 row a6.
+//
+// One unit = one q row; persistent CTAs stream it once (same online state as the
+// verify kernel), write the per-row statistics; the CTA finishing a (b,k) group takes
+// the first row whose statistic is <= eps (ballot/ffs over <= 31 rows).
+#include <algorithm>
+
+#include "sb_host.h"
+
+namespace sb {
+
+struct ConfParams {
+  Dims d;
+  const void* QL;
+  const int* tok;
+  int mode;
+  float eps, lambda;
+  int k_max;
+  float *top1_prob, *entropy, *tok_prob, *stat;
+  int* top1_id;
+  int *stop, *k_next, *gamma_next;
+  int* cnt;
+  float* ws_stat;
+  float* ws_c;
+};
+
+template <typename T, int NT, int U>
+__global__ void __launch_bounds__(NT) k_conf(ConfParams p, bool vec_ok) {
+  constexpr int NA = 4;
+  __shared__ RowStat red[NT / 32];
+  __shared__ int s_last;
+  const Dims& d = p.d;
+  const int tid = threadIdx.x, G = d.G;
+  const int total = d.B * d.K * G;
+  const T* QL = static_cast<const T*>(p.QL);
+  for (int unit = blockIdx.x; unit < total; unit += gridDim.x) {
+    const int grp = unit / G, i = unit % G;
+    const int b = grp / d.K, k = grp % d.K;
+    const T* row = QL + row_off(d, b, k, i);
+    RowAcc<true, NA> a;
+    a.init();
+    stream_row<T, true, NA, NT, U>(row, d.V, vec_ok, a);
+    const RowStat s = block_reduce<NT>(fold(a), red);
+    const RowOut o = finish(s);
+    if (tid == 0) {
+      const int64_t e = (int64_t)grp * G + i;
+      double top1 = CUDART_NAN, H = CUDART_NAN, tp = CUDART_NAN, st = CUDART_NAN;
+      int id = -1;
+      if (o.finite) {
+        const double LN2 = 0.69314718055994530942;
+        top1 = tok_prob(s.m, o.MS, o.Z);
+        id = s.idx;
+        H = LN2 * (log2((double)o.Z) - (double)s.s1 / (double)o.Z);
+        if (p.tok) {
+          const int x = __ldg(p.tok + ent(d, b, k, i));
+          if (x >= 0 && x < d.V) tp = tok_prob(ld_scalar(row + x), o.MS, o.Z);
+        }
+        if (p.mode == SB_CONF_TOP1) st = top1;                       // max_x q(x)
+        else if (p.mode == SB_CONF_TOKEN) st = tp;                   // q(x_i)
+        else st = 1.0 - sqrt((double)p.lambda * fmax(H, 0.0));       // 1 - sqrt(lambda H)
+      }
+      if (p.top1_prob) p.top1_prob[e] = (float)top1;
+      if (p.top1_id) p.top1_id[e] = id;
+      if (p.entropy) p.entropy[e] = (float)H;
+      if (p.tok_prob) p.tok_prob[e] = (float)tp;
+      if (p.stat) p.stat[e] = (float)st;
+      p.ws_stat[e] = (float)st;
+      p.ws_c[e] = (float)(p.mode == SB_CONF_TOKEN ? tp : top1);
+      __threadfence();
+      s_last = (atomicAdd(p.cnt + grp, 1) == G - 1);
+    }
+    __syncthreads();
+    if (s_last && tid == 0) {
+      __threadfence();
+      int stop = G;
+      for (int r = 0; r < G; ++r) {
+        const float sv = __ldcg(p.ws_stat + (int64_t)grp * G + r);
+        if ((double)sv <= (double)p.eps) { stop = r; break; }  // Eq. 6: keep q(x) > eps
+      }
+      int kn = -1;
+      if (stop < G) {
+        const double c = (double)__ldcg(p.ws_c + (int64_t)grp * G + stop);
+        const double kk = floor((double)p.k_max * (1.0 - c));  // Eq. 7
+        kn = kk < 1.0 ? 1 : (int)kk;
+      }
+      p.stop[grp] = stop;
+      if (p.k_next) p.k_next[grp] = kn;
+      if (p.gamma_next) p.gamma_next[grp] = stop > 1 ? stop : 1;
+      p.cnt[grp] = 0;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void k_conf_empty(int n, int* stop, int* k_next, int* gamma_next) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g < n) {
+    stop[g] = 0;
+    if (k_next) k_next[g] = -1;
+    if (gamma_next) gamma_next[g] = 1;
+  }
+}
+
+template <typename T, int NT, int U>
+static sb_status launch_conf(const ConfParams& p, bool vok, cudaStream_t s) {
+  static int g = 0;
+  if (g == 0) {
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_conf<T, NT, U>, NT, 0);
+    g = std::max(1, occ) * num_sms();
+  }
+  const int64_t units = (int64_t)p.d.B * p.d.K * p.d.G;
+  const int grid = (int)std::min<int64_t>(g, units);
+  k_conf<T, NT, U><<<grid, NT, 0, s>>>(p, vok);
+  return cuda_status(cudaGetLastError());
+}
+
+}  // namespace sb
+
+using namespace sb;
+
+extern "C" sb_status sb_draft_confidence(const sb_dims* dd, const void* q_logits,
+                                         const int32_t* tok, sb_conf_mode mode, float eps,
+                                         float lambda, int32_t k_max, float* top1_prob,
+                                         int32_t* top1_id, float* entropy, float* tok_prob,
+                                         float* stat, int32_t* stop, int32_t* k_next,
+                                         int32_t* gamma_next, void* comm, void* workspace,
+                                         size_t workspace_bytes, sb_stream_t stream) {
+  if (!dims_valid(dd) || !q_logits || !stop || !workspace) return SB_ERR_INVALID_ARG;
+  if (mode != SB_CONF_TOP1 && mode != SB_CONF_TOKEN && mode != SB_CONF_ENTROPY)
+    return SB_ERR_INVALID_ARG;
+  if (mode == SB_CONF_TOKEN && !tok) return SB_ERR_INVALID_ARG;
+  if (!(eps > 0.f && eps < 1.f) || !(lambda > 0.f) || k_max < 1) return SB_ERR_INVALID_ARG;
+  if (comm) return SB_ERR_UNSUPPORTED;
+  if ((uintptr_t)workspace % 256) return SB_ERR_INVALID_ARG;
+  const Workspace w = carve(*dd, workspace);
+  if (workspace_bytes < w.bytes) return SB_ERR_WORKSPACE;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dd->G == 0) {
+    const int n = dd->B * dd->K;
+    k_conf_empty<<<(n + 255) / 256, 256, 0, s>>>(n, stop, k_next, gamma_next);
+    return cuda_status(cudaGetLastError());
+  }
+  ConfParams p;
+  p.d = to_dims(dd); p.QL = q_logits; p.tok = tok; p.mode = mode; p.eps = eps; p.lambda = lambda;
+  p.k_max = k_max; p.top1_prob = top1_prob; p.entropy = entropy; p.tok_prob = tok_prob;
+  p.stat = stat; p.top1_id = top1_id; p.stop = stop; p.k_next = k_next; p.gamma_next = gamma_next;
+  p.cnt = w.conf_cnt; p.ws_stat = w.conf_stat; p.ws_c = w.conf_c;
+  const bool vok = vec_ok(dd, q_logits);
+  const size_t row_bytes = (size_t)dd->V * elem_size(dd);
+  if (dd->dtype == SB_BF16)
+    return row_bytes <= 131072 ? launch_conf<__nv_bfloat16, 128, 4>(p, vok, s)
+                               : launch_conf<__nv_bfloat16, 256, 4>(p, vok, s);
+  return row_bytes <= 131072 ? launch_conf<float, 128, 4>(p, vok, s)
+                             : launch_conf<float, 256, 4>(p, vok, s);
+}

@@ -1,0 +1,89 @@
+// sb_host.h — host-side helpers shared by the C-ABI entry points (argument checks,
+// workspace carving, launch geometry).  No device code.
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#include "sb_common.cuh"
+
+namespace sb {
+
+struct SeqInfo {
+  int g, s, L, st;  // clamped gamma_b, branch row s_b, path length L_b, clamp bits
+};
+
+// Workspace carve-up (all offsets 256-byte aligned).
+struct Workspace {
+  SeqInfo* info;     // [B]
+  int* unit_off;     // [B+1] exclusive scan of tested row pairs per sequence
+  int* cnt;          // [B]   rows-kernel completion counters (self-resetting)
+  int* sel_cnt;      // [1]   select-kernel completion counter (self-resetting)
+  float4* rowstat;   // [B][K][G+1] (MS_p, Z_p, MS_q, Z_q) per physical row
+  uint8_t* pflag;    // [B][K][G+1] per token slot: bit0 acc, bit1 bad token, bit2 nonfinite
+  int* conf_cnt;     // [B][K] confidence-kernel completion counters (self-resetting)
+  float* conf_stat;  // [B][K][G] statistic per row
+  float* conf_c;     // [B][K][G] Eq. 7 confidence per row
+  size_t bytes;
+};
+
+inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+inline Workspace carve(const sb_dims& d, void* base) {
+  Workspace w{};
+  const size_t B = (size_t)d.B, K = (size_t)d.K, R1 = (size_t)d.G + 1, G = (size_t)d.G;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += align256(bytes);
+    return (char*)base + o;
+  };
+  w.info = (SeqInfo*)take(sizeof(SeqInfo) * B);
+  w.unit_off = (int*)take(sizeof(int) * (B + 1));
+  w.cnt = (int*)take(sizeof(int) * B);
+  w.sel_cnt = (int*)take(sizeof(int) * 4);
+  w.rowstat = (float4*)take(sizeof(float4) * B * K * R1);
+  w.pflag = (uint8_t*)take(B * K * R1);
+  w.conf_cnt = (int*)take(sizeof(int) * B * K);
+  w.conf_stat = (float*)take(sizeof(float) * B * K * (G ? G : 1));
+  w.conf_c = (float*)take(sizeof(float) * B * K * (G ? G : 1));
+  w.bytes = off;
+  return w;
+}
+
+inline bool dims_valid(const sb_dims* d) {
+  if (!d) return false;
+  if (d->B < 1 || d->K < 1 || d->K > kMaxK || d->G < 0 || d->G > kMaxG || d->V < 2) return false;
+  if (d->row_stride < d->V) return false;
+  if (d->dtype != SB_BF16 && d->dtype != SB_F32) return false;
+  if (d->v_offset != 0 || (d->v_total != 0 && d->v_total != d->V)) return false;  // unsharded build
+  if (d->reserved != 0) return false;
+  const int64_t min_ss = (int64_t)d->K * (d->G + 1) * d->row_stride;
+  if (d->seq_stride != 0 && d->seq_stride < min_ss) return false;
+  return true;
+}
+
+inline Dims to_dims(const sb_dims* d) {
+  Dims x;
+  x.B = d->B; x.K = d->K; x.G = d->G; x.V = d->V;
+  x.rs = d->row_stride;
+  x.ss = d->seq_stride ? d->seq_stride : (int64_t)d->K * (d->G + 1) * d->row_stride;
+  x.dtype = d->dtype;
+  return x;
+}
+
+inline size_t elem_size(const sb_dims* d) { return d->dtype == SB_BF16 ? 2 : 4; }
+
+// 16-byte vector loads are legal for every row iff the base pointer and both strides
+// keep 16-byte alignment.
+inline bool vec_ok(const sb_dims* d, const void* p) {
+  const size_t es = elem_size(d);
+  const Dims x = to_dims(d);
+  return ((uintptr_t)p % 16 == 0) && ((size_t)x.rs * es % 16 == 0) && ((size_t)x.ss * es % 16 == 0);
+}
+
+inline sb_status cuda_status(cudaError_t e) { return e == cudaSuccess ? SB_OK : SB_ERR_CUDA; }
+
+int num_sms();  // cached cudaDevAttrMultiProcessorCount of the current device
+
+}  // namespace sb

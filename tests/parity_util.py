@@ -1,0 +1,124 @@
+"""Parity harness: run the CUDA path (through the C ABI) and the fp64 oracle on the same
+bytes and compare element by element.  Test infrastructure (imports oracle/).
+
+Bars (BASELINE.json north_star; SURVEY §8.4 "Pass criteria"):
+  * discrete outputs bit-exact, except sequences the oracle flags as near ties
+    (|u - P/Q| < 1e-6, sample |t - F| < 1e-6, R < 1e-4, |stat - eps| < 1e-6,
+    Eq. 7 argument within 1e-6 of an integer);
+  * continuous outputs |gpu - ref| <= 1e-5 |ref| + 1e-7 (lse: 1e-5 max(1, |ref|)).
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+import oracle
+from paper_2506_01979_b200 import api, synth
+
+REL, ABS = 1e-5, 1e-7
+
+
+def gpu_run(inp: dict, rule=0, adaptive=False, eps=0.2, k_max=6):
+    d = api.dims_for(inp["PL"], V=inp["V"])
+    buf = api.StepBuffers.alloc(d, inp["PL"].device)
+    gamma = api.verify_step(d, inp, buf, rule=rule, adaptive=adaptive, eps=eps, k_max=k_max)
+    torch.cuda.synchronize()
+    out = {k: getattr(buf, k).cpu().numpy() for k in buf.__dataclass_fields__
+           if k not in ("workspace", "conf_workspace")}
+    out["acc_mask"] = out["acc_mask"].view(np.uint32)
+    out["keep_mask"] = out["keep_mask"].view(np.uint32)
+    out["gamma_used"] = gamma.cpu().numpy().astype(np.int32)
+    return out, d, buf
+
+
+def _close(g, r, rel=REL, ab=ABS):
+    g = np.asarray(g, np.float64)
+    r = np.asarray(r, np.float64)
+    nan_ok = np.array_equal(np.isnan(g), np.isnan(r))
+    m = ~np.isnan(r)
+    err = np.abs(g[m] - r[m])
+    ok = bool(np.all(err <= rel * np.abs(r[m]) + ab)) if m.any() else True
+    relerr = float(np.max(err / np.maximum(np.abs(r[m]), 1e-30))) if m.any() else 0.0
+    return nan_ok and ok, relerr
+
+
+def compare(g: dict, o: dict, sel=None, strict=True):
+    """Compare gpu outputs g with oracle outputs o on sequences `sel` (indices into g)."""
+    B = o["status"].shape[0]
+    sel = np.arange(B) if sel is None else np.asarray(sel)
+    gs = {k: (v[sel] if isinstance(v, np.ndarray) and v.ndim >= 1 and v.shape[0] >= len(sel) and k not in ("offsets", "packed_tok") else v)
+          for k, v in g.items()}
+    rep = {"n": B, "fail": []}
+    ties = o["ties"]
+    t_dec = (ties & (oracle.TIE_ACC_DEC)) != 0
+    t_mask = (ties & oracle.TIE_ACC_MASK) != 0
+    t_samp = (ties & (oracle.TIE_SAMPLE | oracle.TIE_ILLCOND)) != 0
+    rep["ties"] = {"acc_mask": int(t_mask.sum()), "decision": int(t_dec.sum()), "sample": int(t_samp.sum())}
+
+    def fail(name, idx):
+        idx = np.atleast_1d(idx)
+        if idx.size:
+            rep["fail"].append((name, idx[:8].tolist()))
+
+    # continuous
+    for k in ("lse_p", "lse_q"):
+        r = o[k]
+        gg = gs[k].astype(np.float64)
+        nan_ok = np.array_equal(np.isnan(gg), np.isnan(r))
+        m = ~np.isnan(r)
+        err = np.abs(gg[m] - r[m]) / np.maximum(1.0, np.abs(r[m]))
+        rep[f"max_err_{k}"] = float(err.max()) if err.size else 0.0
+        if not nan_ok or (err.size and err.max() > REL):
+            fail(k, np.where(np.any((np.isnan(gg) != np.isnan(r)).reshape(len(sel), -1), axis=1))[0])
+            if err.size and err.max() > REL:
+                rep["fail"].append((k + "_tol", float(err.max())))
+    for k in ("top1_q", "entropy_q", "p_tok", "q_tok"):
+        ok, relerr = _close(gs[k], o[k])
+        rep[f"max_rel_{k}"] = relerr
+        if not ok:
+            bad = ~np.isclose(gs[k].astype(np.float64), o[k], rtol=REL, atol=ABS, equal_nan=True)
+            fail(k, np.where(bad.reshape(len(sel), -1).any(axis=1))[0])
+    # discrete
+    ok_id = gs["top1_id_q"] == o["top1_id_q"]
+    fail("top1_id_q", np.where(~ok_id.reshape(len(sel), -1).all(axis=1))[0])
+    fail("status", np.where(gs["status"] != o["status"])[0])
+    am = (gs["acc_mask"] != o["acc_mask"]).any(axis=1) & ~t_mask
+    fail("acc_mask", np.where(am)[0])
+    nd = (gs["n_acc"] != o["n_acc"]).any(axis=1) & ~t_dec
+    fail("n_acc", np.where(nd)[0])
+    for k in ("sel_k", "commit_len", "y_kind", "path_rolled", "branch_discarded"):
+        fail(k, np.where((gs[k] != o[k]) & ~t_dec)[0])
+    fail("keep_mask", np.where((gs["keep_mask"] != o["keep_mask"]).any(axis=1) & ~t_dec)[0])
+    fail("y_tok", np.where((gs["y_tok"] != o["y_tok"]) & ~t_dec & ~t_samp)[0])
+    ot = (gs["out_tok"] != o["out_tok"]).any(axis=1) & ~t_dec & ~t_samp
+    fail("out_tok", np.where(ot)[0])
+    same = (gs["y_kind"] == o["y_kind"]) & ~t_dec & ~t_samp
+    ok, relerr = _close(gs["resid_mass"][same], o["resid_mass"][same], REL, 1e-6)
+    rep["max_rel_resid_mass"] = relerr
+    if not ok:
+        rep["fail"].append(("resid_mass", relerr))
+    rep["exact_seq"] = int((~t_dec & ~t_samp).sum())
+    rep["y_compared"] = int(((gs["y_kind"] != 0) & ~t_dec & ~t_samp).sum())
+    if strict:
+        assert not rep["fail"], rep
+    return rep
+
+
+def internal_consistency(g: dict, G: int):
+    """offsets = exclusive scan of commit_len; packed stream = concatenated commits."""
+    cl = g["commit_len"]
+    assert g["offsets"][0] == 0 and np.array_equal(np.diff(g["offsets"]), cl)
+    for b in range(len(cl)):
+        seg = g["packed_tok"][g["offsets"][b]: g["offsets"][b + 1]]
+        assert np.array_equal(seg, g["out_tok"][b, : cl[b]])
+        assert (g["out_tok"][b, cl[b]:] == -1).all()
+
+
+def oracle_for(inp_np: dict, gamma, rule=0, nthreads=0):
+    return oracle.verify(inp_np["PL"], inp_np["QL"], inp_np["tok"], inp_np["u"], inp_np["us"],
+                         gamma, inp_np["branch_pos"], rule=rule, nthreads=nthreads, V=inp_np["V"])
+
+
+def subset(inp_np: dict, idx):
+    out = {k: (v[idx] if isinstance(v, np.ndarray) else v) for k, v in inp_np.items()}
+    return out
