@@ -1,5 +1,6 @@
 // sb_api.cu — version, status strings, workspace sizing, device attributes.
 #include <cuda_runtime.h>
+#include <stdlib.h>
 
 #include "sb_host.h"
 
@@ -13,6 +14,10 @@ int num_sms() {
     if (n <= 0) n = 148;
   }
   return n;
+}
+bool tma_disabled() {
+  const char* e = getenv("SB_DISABLE_TMA");
+  return e && e[0] == '1';
 }
 }  // namespace sb
 

@@ -20,6 +20,12 @@ namespace sb {
 constexpr float kC = 1.4426950408889634f;  // fp32(log2 e)
 constexpr float kLn2 = 0.69314718055994531f;
 constexpr int kMaxK = 32;
+constexpr float kMsEmpty = -1e30f;  // exponent offset of a state that has seen no finite value
+// Lazy offset: rescale only when max*c - ms exceeds the threshold.  p rows need only
+// Z, so 2^20 of headroom is free; q rows also sum S1 = sum e*a, whose fp32 rounding
+// grows with the offset lag |a| of the largest terms, so they keep the lag <= 6.
+constexpr float kRescaleP = 20.f;
+constexpr float kRescaleQ = 6.f;
 constexpr int kMaxG = 31;
 
 struct Dims {
@@ -107,7 +113,7 @@ struct RowAcc {
 
   __device__ __forceinline__ void init() {
     m = -CUDART_INF_F;
-    ms = 0.f;
+    ms = kMsEmpty;
 #pragma unroll
     for (int j = 0; j < NA; ++j) z[j] = 0.f;
 #pragma unroll
@@ -118,7 +124,7 @@ struct RowAcc {
   // raise the running max to nm (> m); rare after the first few vectors
   __device__ __forceinline__ void rescale(float nm) {
     const float nms = nm * kC;
-    const float sc = (m == -CUDART_INF_F) ? 0.f : ex2(ms - nms);
+    const float sc = ex2(ms - nms);  // 0 from the kMsEmpty sentinel
     const float dd = ms - nms;
 #pragma unroll
     for (int j = 0; j < NA; ++j) {
@@ -163,11 +169,94 @@ struct RowAcc {
   }
 };
 
+// Lazy-offset accumulator for the streaming (TMA) kernels.  Per group of N values:
+// the exact running max m (one FMNMX), the group tag of its first occurrence (Q rows;
+// one FSETP + SEL), and the exponent offset ms raised only when max*c - ms > 20, a
+// warp-uniform rare branch, so the hot path is unpack, FFMA, MUFU.EX2, FADD (+ FMNMX,
+// FFMA for the entropy sum of q rows).
+template <bool kQ, int NA>
+struct LazyAcc {
+  float m;
+  float ms;
+  float z[NA];
+  float s1[kQ ? NA : 1];
+  int tag;
+
+  __device__ __forceinline__ void init() {
+    m = -CUDART_INF_F;
+    ms = kMsEmpty;
+#pragma unroll
+    for (int j = 0; j < NA; ++j) z[j] = 0.f;
+#pragma unroll
+    for (int j = 0; j < (kQ ? NA : 1); ++j) s1[j] = 0.f;
+    tag = -1;
+  }
+  __device__ __forceinline__ void rescale(float nms) {
+    const float dd = ms - nms;
+    const float sc = ex2(dd);
+#pragma unroll
+    for (int j = 0; j < NA; ++j) {
+      if (kQ) s1[j] = sc * fmaf(z[j], dd, s1[j]);
+      z[j] *= sc;
+    }
+    ms = nms;
+  }
+  template <int N>
+  __device__ __forceinline__ void add(const float* f, int t) {
+    float cm = f[0];
+#pragma unroll
+    for (int j = 1; j + 1 < N; j += 2) cm = fmax3(cm, f[j], f[j + 1]);
+    if (N % 2 == 0) cm = fmaxf(cm, f[N - 1]);
+    if (kQ) tag = (cm > m) ? t : tag;
+    m = fmaxf(m, cm);
+    const bool up = cm * kC - ms > (kQ ? kRescaleQ : kRescaleP);
+    if (__any_sync(0xffffffffu, up)) {
+      if (up) rescale(cm * kC);
+    }
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      const float a = fmaf(f[j], kC, -ms);
+      const float e = ex2(a);
+      z[j % NA] += e;
+      if (kQ) s1[j % NA] = fmaf(e, fmaxf(a, -200.f), s1[j % NA]);
+    }
+  }
+};
+
 // Reduced row state (one per thread after folding accumulators, then across threads).
 struct RowStat {
   float m, ms, z, s1;
   int idx;
 };
+
+template <bool kQ, int NA>
+__device__ __forceinline__ RowStat fold_lazy(const LazyAcc<kQ, NA>& a) {
+  RowStat r;
+  r.m = a.m;
+  r.ms = a.ms;
+  float z = 0.f, s = 0.f;
+#pragma unroll
+  for (int j = 0; j < NA; ++j) z += a.z[j];
+  if (kQ) {
+#pragma unroll
+    for (int j = 0; j < NA; ++j) s += a.s1[j];
+  }
+  r.z = z;
+  r.s1 = s;
+  r.idx = 0x7fffffff;
+  return r;
+}
+
+// Identity element of combine().
+__device__ __forceinline__ RowStat rowstat_empty() {
+  RowStat r;
+  r.m = -CUDART_INF_F;
+  r.ms = kMsEmpty;
+  r.z = 0.f;
+  r.s1 = 0.f;
+  r.idx = 0x7fffffff;
+  return r;
+}
 
 template <bool kQ, int NA>
 __device__ __forceinline__ RowStat fold(const RowAcc<kQ, NA>& a) {
@@ -187,24 +276,22 @@ __device__ __forceinline__ RowStat fold(const RowAcc<kQ, NA>& a) {
   return r;
 }
 
-// Combine two states (commutative up to rounding; called in a fixed tree order).
-__device__ __forceinline__ RowStat combine(RowStat a, RowStat b) {
-  // make `a` the one with the larger max (ties: smaller index)
-  if (b.m > a.m || (b.m == a.m && b.idx < a.idx)) {
-    RowStat t = a;
-    a = b;
-    b = t;
-  }
-  if (b.m == -CUDART_INF_F || a.m == -CUDART_INF_F) {
-    // nothing finite in b (or anywhere): b contributes 0 (its z is 0 or NaN-marked)
-    if (b.m == -CUDART_INF_F && !(b.z == b.z)) a.z = b.z;  // keep NaN poison
-    return a;
-  }
-  const float dd = b.ms - a.ms;
-  const float sc = ex2(dd);
-  a.s1 = a.s1 + sc * (b.s1 + b.z * dd);
-  a.z = a.z + sc * b.z;
-  return a;
+// Combine two states (called in a fixed tree order).  The exact max / first index
+// follow the larger value (ties: smaller index); the sums are brought to the larger
+// exponent offset.  Works for any offsets (lazy or exact), for empty states (kMsEmpty,
+// z = 0) and keeps NaN poison (z = NaN) of non-finite rows.
+__device__ __forceinline__ RowStat combine(const RowStat& a, const RowStat& b) {
+  RowStat r;
+  const bool bw = b.m > a.m || (b.m == a.m && b.idx < a.idx);
+  r.m = bw ? b.m : a.m;
+  r.idx = bw ? b.idx : a.idx;
+  const float MS = fmaxf(a.ms, b.ms);
+  const float da = a.ms - MS, db = b.ms - MS;
+  const float sa = ex2(da), sb = ex2(db);
+  r.z = a.z * sa + b.z * sb;
+  r.s1 = sa * fmaf(a.z, da, a.s1) + sb * fmaf(b.z, db, b.s1);
+  r.ms = MS;
+  return r;
 }
 
 __device__ __forceinline__ RowStat shfl_xor(const RowStat& s, int o) {

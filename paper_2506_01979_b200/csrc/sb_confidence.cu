@@ -9,6 +9,7 @@
 #include <algorithm>
 
 #include "sb_host.h"
+#include "sb_ring.cuh"
 
 namespace sb {
 
@@ -27,6 +28,64 @@ struct ConfParams {
   float* ws_c;
 };
 
+// Per-row statistic and the group-completion logic shared by both kernels.
+template <typename T, typename Sync>
+__device__ __forceinline__ void conf_epilogue(const ConfParams& p, int grp, int i, const T* row,
+                                              const RowStat& s, int tid, int* s_last, Sync sync) {
+  const Dims& d = p.d;
+  const int G = d.G;
+  const int b = grp / d.K, k = grp % d.K;
+  const RowOut o = finish(s);
+  if (tid == 0) {
+    const int64_t e = (int64_t)grp * G + i;
+    double top1 = CUDART_NAN, H = CUDART_NAN, tp = CUDART_NAN, st = CUDART_NAN;
+    int id = -1;
+    if (o.finite) {
+      const double LN2 = 0.69314718055994530942;
+      top1 = tok_prob(s.m, o.MS, o.Z);
+      id = s.idx;
+      H = LN2 * (log2((double)o.Z) - (double)s.s1 / (double)o.Z);
+      if (p.tok) {
+        const int x = __ldg(p.tok + ent(d, b, k, i));
+        if (x >= 0 && x < d.V) tp = tok_prob(ld_scalar(row + x), o.MS, o.Z);
+      }
+      if (p.mode == SB_CONF_TOP1) st = top1;                  // max_x q(x)
+      else if (p.mode == SB_CONF_TOKEN) st = tp;              // q(x_i)
+      else st = 1.0 - sqrt((double)p.lambda * fmax(H, 0.0));  // 1 - sqrt(lambda H)
+    }
+    if (p.top1_prob) p.top1_prob[e] = (float)top1;
+    if (p.top1_id) p.top1_id[e] = id;
+    if (p.entropy) p.entropy[e] = (float)H;
+    if (p.tok_prob) p.tok_prob[e] = (float)tp;
+    if (p.stat) p.stat[e] = (float)st;
+    p.ws_stat[e] = (float)st;
+    p.ws_c[e] = (float)(p.mode == SB_CONF_TOKEN ? tp : top1);
+    __threadfence();
+    *s_last = (atomicAdd(p.cnt + grp, 1) == G - 1);
+  }
+  sync();
+  if (*s_last && tid == 0) {
+    __threadfence();
+    int stop = G;
+    for (int r = 0; r < G; ++r) {
+      const float sv = __ldcg(p.ws_stat + (int64_t)grp * G + r);
+      if ((double)sv <= (double)p.eps) { stop = r; break; }  // Eq. 6: keep q(x) > eps
+    }
+    int kn = -1;
+    if (stop < G) {
+      const double c = (double)__ldcg(p.ws_c + (int64_t)grp * G + stop);
+      const double kk = floor((double)p.k_max * (1.0 - c));  // Eq. 7
+      kn = kk < 1.0 ? 1 : (int)kk;
+    }
+    p.stop[grp] = stop;
+    if (p.k_next) p.k_next[grp] = kn;
+    if (p.gamma_next) p.gamma_next[grp] = stop > 1 ? stop : 1;
+    p.cnt[grp] = 0;
+  }
+  sync();
+}
+
+// Register-staged fallback (any alignment / stride).
 template <typename T, int NT, int U>
 __global__ void __launch_bounds__(NT) k_conf(ConfParams p, bool vec_ok) {
   constexpr int NA = 4;
@@ -44,54 +103,176 @@ __global__ void __launch_bounds__(NT) k_conf(ConfParams p, bool vec_ok) {
     a.init();
     stream_row<T, true, NA, NT, U>(row, d.V, vec_ok, a);
     const RowStat s = block_reduce<NT>(fold(a), red);
-    const RowOut o = finish(s);
-    if (tid == 0) {
-      const int64_t e = (int64_t)grp * G + i;
-      double top1 = CUDART_NAN, H = CUDART_NAN, tp = CUDART_NAN, st = CUDART_NAN;
-      int id = -1;
-      if (o.finite) {
-        const double LN2 = 0.69314718055994530942;
-        top1 = tok_prob(s.m, o.MS, o.Z);
-        id = s.idx;
-        H = LN2 * (log2((double)o.Z) - (double)s.s1 / (double)o.Z);
-        if (p.tok) {
-          const int x = __ldg(p.tok + ent(d, b, k, i));
-          if (x >= 0 && x < d.V) tp = tok_prob(ld_scalar(row + x), o.MS, o.Z);
+    conf_epilogue(p, grp, i, row, s, tid, &s_last, [] { __syncthreads(); });
+  }
+}
+
+// TMA ring version (same warp roles as k_rows_tma): producer warp streams 16 KB chunks
+// of each q row, 16 consumer warps fold them, an epilogue warp finishes each row.
+constexpr int cNS = 8;
+constexpr int cCW = 16;
+constexpr int cCT = cCW * 32;
+constexpr int cVPT = 2;
+constexpr int cChunk = cCT * cVPT * 16;
+constexpr int cNP = 4;
+constexpr int cThreads = cCT + 64;
+
+struct ConfSmem {
+  uint64_t full[cNS], empty[cNS];
+  uint64_t pfull[cNP], pempty[cNP];
+  RowStat part[cNP][cCW];
+  int s_last;
+  alignas(128) uint8_t buf[cNS][cChunk];
+};
+
+template <typename T>
+__device__ __forceinline__ RowStat conf_warp_part(const LazyAcc<true, 4>& a, const T* row,
+                                                  int nvec_last, int nchunks) {
+  constexpr int E = Vec<T>::E;
+  const int tid = threadIdx.x;
+  RowStat s = fold_lazy(a);
+  float mw = s.m;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mw = fmaxf(mw, __shfl_xor_sync(0xffffffffu, mw, o));
+  uint4 x[cVPT];
+  bool have[cVPT];
+  const bool need = (a.m == mw) && (mw > -CUDART_INF_F) && (a.tag >= 0);
+  const int c = a.tag;
+  if (need) {
+    const int nvec = (c == nchunks - 1) ? nvec_last : cChunk / 16;
+    const uint4* cv = reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(row) + (size_t)c * cChunk);
+#pragma unroll
+    for (int j = 0; j < cVPT; ++j) {
+      const int v = tid + j * cCT;
+      have[j] = v < nvec;
+      if (have[j]) x[j] = __ldg(cv + v);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s = combine(s, shfl_xor(s, o));
+  s.m = mw;
+  int cand = 0x7fffffff;
+  if (need) {
+#pragma unroll
+    for (int j = cVPT - 1; j >= 0; --j) {
+      if (!have[j]) continue;
+      float f[E];
+      Vec<T>::unpack(x[j], f);
+#pragma unroll
+      for (int e = E - 1; e >= 0; --e)
+        if (f[e] == mw) cand = c * (cChunk / (int)sizeof(T)) + (tid + j * cCT) * E + e;
+    }
+  }
+  s.idx = __reduce_min_sync(0xffffffffu, (unsigned)cand);
+  return s;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(cThreads, 1) k_conf_tma(ConfParams p) {
+  constexpr int E = Vec<T>::E;
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  ConfSmem& S = *reinterpret_cast<ConfSmem*>(smem_raw);
+  const Dims& d = p.d;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, G = d.G;
+  if (tid == 0) {
+    for (int s = 0; s < cNS; ++s) {
+      mbar_init(&S.full[s], 1);
+      mbar_init(&S.empty[s], cCW);
+    }
+    for (int s = 0; s < cNP; ++s) {
+      mbar_init(&S.pfull[s], cCW);
+      mbar_init(&S.pempty[s], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int total = d.B * d.K * G;
+  const T* QL = static_cast<const T*>(p.QL);
+  const uint32_t row_bytes = (uint32_t)d.V * sizeof(T);
+  const int nchunks = (row_bytes + cChunk - 1) / cChunk;
+  const int nvec_last = (int)(row_bytes - (uint32_t)(nchunks - 1) * cChunk) / 16;
+  if (warp == cCW) {
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      RingPos<cNS> rp;
+      for (int unit = blockIdx.x; unit < total; unit += gridDim.x) {
+        const int grp = unit / G, i = unit % G;
+        const char* row =
+            reinterpret_cast<const char*>(QL + row_off(d, grp / d.K, grp % d.K, i));
+        for (int c = 0; c < nchunks; ++c) {
+          const uint32_t bytes = min((uint32_t)cChunk, row_bytes - (uint32_t)c * cChunk);
+          mbar_wait(&S.empty[rp.stage], rp.phase ^ 1u);
+          mbar_expect_tx(&S.full[rp.stage], bytes);
+          bulk_g2s(S.buf[rp.stage], row + (size_t)c * cChunk, bytes, &S.full[rp.stage], pol);
+          rp.advance();
         }
-        if (p.mode == SB_CONF_TOP1) st = top1;                       // max_x q(x)
-        else if (p.mode == SB_CONF_TOKEN) st = tp;                   // q(x_i)
-        else st = 1.0 - sqrt((double)p.lambda * fmax(H, 0.0));       // 1 - sqrt(lambda H)
       }
-      if (p.top1_prob) p.top1_prob[e] = (float)top1;
-      if (p.top1_id) p.top1_id[e] = id;
-      if (p.entropy) p.entropy[e] = (float)H;
-      if (p.tok_prob) p.tok_prob[e] = (float)tp;
-      if (p.stat) p.stat[e] = (float)st;
-      p.ws_stat[e] = (float)st;
-      p.ws_c[e] = (float)(p.mode == SB_CONF_TOKEN ? tp : top1);
-      __threadfence();
-      s_last = (atomicAdd(p.cnt + grp, 1) == G - 1);
     }
-    __syncthreads();
-    if (s_last && tid == 0) {
-      __threadfence();
-      int stop = G;
-      for (int r = 0; r < G; ++r) {
-        const float sv = __ldcg(p.ws_stat + (int64_t)grp * G + r);
-        if ((double)sv <= (double)p.eps) { stop = r; break; }  // Eq. 6: keep q(x) > eps
-      }
-      int kn = -1;
-      if (stop < G) {
-        const double c = (double)__ldcg(p.ws_c + (int64_t)grp * G + stop);
-        const double kk = floor((double)p.k_max * (1.0 - c));  // Eq. 7
-        kn = kk < 1.0 ? 1 : (int)kk;
-      }
-      p.stop[grp] = stop;
-      if (p.k_next) p.k_next[grp] = kn;
-      if (p.gamma_next) p.gamma_next[grp] = stop > 1 ? stop : 1;
-      p.cnt[grp] = 0;
+    return;
+  }
+  if (warp == cCW + 1) {
+    RingPos<cNP> up;
+    for (int unit = blockIdx.x; unit < total; unit += gridDim.x) {
+      const int grp = unit / G, i = unit % G;
+      mbar_wait(&S.pfull[up.stage], up.phase);
+      RowStat r = lane < cCW ? S.part[up.stage][lane] : rowstat_empty();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.pempty[up.stage]);
+      up.advance();
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) r = combine(r, shfl_xor(r, o));
+      const T* row = QL + row_off(d, grp / d.K, grp % d.K, i);
+      conf_epilogue(p, grp, i, row, r, lane, &S.s_last, [] { __syncwarp(); });
     }
-    __syncthreads();
+    return;
+  }
+  RingPos<cNS> rp;
+  RingPos<cNP> up;
+  for (int unit = blockIdx.x; unit < total; unit += gridDim.x) {
+    LazyAcc<true, 4> a;
+    a.init();
+    for (int c = 0; c < nchunks - 1; ++c) {
+      mbar_wait(&S.full[rp.stage], rp.phase);
+      uint4 x[cVPT];
+#pragma unroll
+      for (int j = 0; j < cVPT; ++j) x[j] = lds128(S.buf[rp.stage] + (tid + j * cCT) * 16);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.empty[rp.stage]);
+      rp.advance();
+      float f[cVPT * E];
+#pragma unroll
+      for (int j = 0; j < cVPT; ++j) Vec<T>::unpack(x[j], f + j * E);
+      a.template add<cVPT * E>(f, c);
+    }
+    {
+      const int c = nchunks - 1;
+      mbar_wait(&S.full[rp.stage], rp.phase);
+      float f[cVPT * E];
+#pragma unroll
+      for (int j = 0; j < cVPT; ++j) {
+        const int v = tid + j * cCT;
+        if (v < nvec_last) {
+          Vec<T>::unpack(lds128(S.buf[rp.stage] + v * 16), f + j * E);
+        } else {
+#pragma unroll
+          for (int e = 0; e < E; ++e) f[j * E + e] = -CUDART_INF_F;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.empty[rp.stage]);
+      rp.advance();
+      a.template add<cVPT * E>(f, c);
+    }
+    const int grp = unit / G, i = unit % G;
+    const T* row = QL + row_off(d, grp / d.K, grp % d.K, i);
+    const RowStat s = conf_warp_part<T>(a, row, nvec_last, nchunks);
+    if (lane == 0) {
+      mbar_wait(&S.pempty[up.stage], up.phase ^ 1u);
+      S.part[up.stage][warp] = s;
+      mbar_arrive(&S.pfull[up.stage]);
+    }
+    __syncwarp();
+    up.advance();
   }
 }
 
@@ -115,6 +296,22 @@ static sb_status launch_conf(const ConfParams& p, bool vok, cudaStream_t s) {
   const int64_t units = (int64_t)p.d.B * p.d.K * p.d.G;
   const int grid = (int)std::min<int64_t>(g, units);
   k_conf<T, NT, U><<<grid, NT, 0, s>>>(p, vok);
+  return cuda_status(cudaGetLastError());
+}
+
+template <typename T>
+static sb_status launch_conf_tma(const ConfParams& p, cudaStream_t s) {
+  static bool attr = false;
+  const int smem = (int)sizeof(ConfSmem);
+  if (!attr) {
+    if (cudaFuncSetAttribute(k_conf_tma<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+        cudaSuccess)
+      return SB_ERR_CUDA;
+    attr = true;
+  }
+  const int64_t units = (int64_t)p.d.B * p.d.K * p.d.G;
+  const int grid = (int)std::min<int64_t>(num_sms(), units);
+  k_conf_tma<T><<<grid, cThreads, smem, s>>>(p);
   return cuda_status(cudaGetLastError());
 }
 
@@ -151,6 +348,8 @@ extern "C" sb_status sb_draft_confidence(const sb_dims* dd, const void* q_logits
   p.cnt = w.conf_cnt; p.ws_stat = w.conf_stat; p.ws_c = w.conf_c;
   const bool vok = vec_ok(dd, q_logits);
   const size_t row_bytes = (size_t)dd->V * elem_size(dd);
+  if (vok && row_bytes % 16 == 0 && !tma_disabled())
+    return dd->dtype == SB_BF16 ? launch_conf_tma<__nv_bfloat16>(p, s) : launch_conf_tma<float>(p, s);
   if (dd->dtype == SB_BF16)
     return row_bytes <= 131072 ? launch_conf<__nv_bfloat16, 128, 4>(p, vok, s)
                                : launch_conf<__nv_bfloat16, 256, 4>(p, vok, s);

@@ -84,6 +84,7 @@ inline bool vec_ok(const sb_dims* d, const void* p) {
 
 inline sb_status cuda_status(cudaError_t e) { return e == cudaSuccess ? SB_OK : SB_ERR_CUDA; }
 
-int num_sms();  // cached cudaDevAttrMultiProcessorCount of the current device
+int num_sms();        // cached cudaDevAttrMultiProcessorCount of the current device
+bool tma_disabled();  // SB_DISABLE_TMA=1 forces the register-staged kernels (tests)
 
 }  // namespace sb

@@ -17,6 +17,7 @@
 #include <algorithm>
 
 #include "sb_host.h"
+#include "sb_ring.cuh"
 
 namespace sb {
 
@@ -31,7 +32,7 @@ struct SelParams {
   int rule;
   const SeqInfo* info;
   const float4* rowstat;
-  int* sel_cnt;
+  int* sel_cnt;   // [0] completion, [1] dynamic sequence, [2] stopped-decider counters
   int *sel_k, *commit_len, *out_tok, *y_tok, *y_kind, *offsets, *packed_tok, *path_rolled,
       *branch_discarded, *status;
   uint32_t* keep_mask;
@@ -331,6 +332,502 @@ __global__ void __launch_bounds__(NT) k_select(SelParams p, bool vec_ok) {
   }
 }
 
+// ---------------------------------------------------------------- TMA select
+// Persistent, one CTA per SM, sequences b = blockIdx.x + k*gridDim.x, four warp roles:
+//   decider   (warp 18): Eq. 9 / Alg. 1 selection and the sampling row, one sequence
+//                        ahead per queue slot (lanes = branches, shuffle argmax);
+//   producer  (warp 16): cp.async.bulk of the sampled row (pair) in 16 KB chunks;
+//   consumers (0..15)  : r(v) = max(0, P - Q) (or P) for 16 ids per thread per chunk,
+//                        per-lane sums + warp Kogge-Stone scan -> one sum per
+//                        512-byte segment (32 lanes x 16 B, ascending ids);
+//                        a bonus row first gets a softmax-state pass;
+//   epilogue  (warp 17): fp64 prefix over segment sums, locate us*R, re-read that one
+//                        segment (L2), same arithmetic -> first id past us*R; commit.
+constexpr int sNS = 6;
+constexpr int sCW = 16;
+constexpr int sCT = sCW * 32;
+constexpr int sVPT = 2;
+constexpr int sChunk = sCT * sVPT * 16;  // 16 KB per row per stage
+constexpr int sNQ = 4;                   // sequences in flight
+constexpr int sSegMax = 1024;            // 512-byte segments per row (rows <= 512 KB)
+constexpr int sThreads = sCT + 96;
+
+struct Dec {
+  int b;  // sequence (-1: no more work)
+  int ksel, npath, kind, row, slot;
+  float4 rs;  // softmax state of the sampled row pair (kind 1; from sb_verify_branches)
+};
+
+struct SelSmem {
+  uint64_t full[sNS], empty[sNS];
+  uint64_t dfull[sNQ], dempty[sNQ], sfull[sNQ];
+  Dec dec[sNQ];
+  float rs[sNQ][4];
+  int ok[sNQ];
+  RowStat red[sCW];
+  float seg[sNQ][sSegMax];
+  int s_last;
+  alignas(128) uint8_t buf[sNS][2][sChunk];
+};
+
+// r(v) for the E ids of one 16-byte vector.  Explicit rounding intrinsics keep the
+// arithmetic identical wherever it is inlined (consumers and epilogue must agree).
+template <typename T>
+__device__ __forceinline__ void r_values(const uint4& vp, const uint4& vq, bool resid, float MSp,
+                                         float iZp, float MSq, float iZq, float* r) {
+  constexpr int E = Vec<T>::E;
+  float lp[E], lq[E];
+  Vec<T>::unpack(vp, lp);
+  Vec<T>::unpack(vq, lq);
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const float P = __fmul_rn(ex2(__fmaf_rn(lp[e], kC, -MSp)), iZp);
+    if (resid) {
+      const float Q = __fmul_rn(ex2(__fmaf_rn(lq[e], kC, -MSq)), iZq);
+      r[e] = fmaxf(__fsub_rn(P, Q), 0.f);
+    } else {
+      r[e] = P;
+    }
+  }
+}
+template <int E>
+__device__ __forceinline__ float seq_sum(const float* r) {
+  float s = 0.f;
+#pragma unroll
+  for (int e = 0; e < E; ++e) s = __fadd_rn(s, r[e]);
+  return s;
+}
+__device__ __forceinline__ float warp_scan_rn(float x) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const float y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x = __fadd_rn(x, y);
+  }
+  return x;
+}
+
+// The epilogue warp's own pass over a whole row (rare: zero residual mass fallback).
+template <typename T>
+__device__ void warp_segments(const T* prow, const T* qrow, uint32_t row_bytes, int nseg, bool resid,
+                              float MSp, float iZp, float MSq, float iZq, float* seg) {
+  constexpr int E = Vec<T>::E;
+  const int lane = threadIdx.x & 31;
+  for (int sI = 0; sI < nseg; ++sI) {
+    const uint32_t off = (uint32_t)sI * 512 + lane * 16;
+    uint4 vp = make_uint4(0xff80ff80u, 0xff80ff80u, 0xff80ff80u, 0xff80ff80u), vq = vp;
+    if (sizeof(T) == 4) vp = vq = make_uint4(0xff800000u, 0xff800000u, 0xff800000u, 0xff800000u);
+    if (off < row_bytes) {
+      vp = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(prow) + off));
+      if (resid) vq = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(qrow) + off));
+    }
+    float r[E];
+    r_values<T>(vp, vq, resid, MSp, iZp, MSq, iZq, r);
+    const float incl = warp_scan_rn(seq_sum<E>(r));
+    if (lane == 31) seg[sI] = incl;
+  }
+  __syncwarp();
+}
+
+template <typename T>
+__global__ void __launch_bounds__(sThreads, 1) k_select_tma(SelParams p) {
+  constexpr int E = Vec<T>::E;
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  SelSmem& S = *reinterpret_cast<SelSmem*>(smem_raw);
+  const Dims& d = p.d;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < sNS; ++s) {
+      mbar_init(&S.full[s], 1);
+      mbar_init(&S.empty[s], sCW);
+    }
+    for (int s = 0; s < sNQ; ++s) {
+      mbar_init(&S.dfull[s], 1);
+      mbar_init(&S.dempty[s], 1);
+      mbar_init(&S.sfull[s], sCW);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const T* PL = static_cast<const T*>(p.PL);
+  const T* QL = static_cast<const T*>(p.QL);
+  const uint32_t row_bytes = (uint32_t)d.V * sizeof(T);
+  const int nchunks = (row_bytes + sChunk - 1) / sChunk;
+  const int nvec_last = (int)(row_bytes - (uint32_t)(nchunks - 1) * sChunk) / 16;
+  const int nseg = nchunks * (sChunk / 512);
+
+  if (warp == sCW + 2) {  // ---------------- decider
+    RingPos<sNQ> dq;
+    for (;;) {
+      if (lane == 0) mbar_wait(&S.dempty[dq.stage], dq.phase ^ 1u);
+      __syncwarp();
+      int b = 0;
+      if (lane == 0) b = atomicAdd(p.sel_cnt + 1, 1);  // dynamic: sequences differ in cost
+      b = __shfl_sync(0xffffffffu, b, 0);
+      if (b >= d.B) {
+        if (lane == 0) {
+          S.dec[dq.stage].b = -1;
+          mbar_arrive(&S.dfull[dq.stage]);
+          // the last decider to stop resets the work counter (all increments are done)
+          if (atomicAdd(p.sel_cnt + 2, 1) == (int)gridDim.x - 1) {
+            p.sel_cnt[1] = 0;
+            p.sel_cnt[2] = 0;
+          }
+        }
+        break;
+      }
+      const SeqInfo in = p.info[b];
+      // lane k: is branch k in A = {k : n_k > s_b}, and its key
+      const int k = lane;
+      int nk = 0, xk = 0x7fffffff;
+      float key = -CUDART_INF_F;
+      bool inA = false;
+      if (k < d.K) {
+        nk = __ldg(p.n_acc + (int64_t)b * d.K + k);
+        inA = nk > in.s;
+        if (inA) {
+          xk = __ldg(p.tok + ent(d, b, k, in.s));
+          key = (p.rule == SB_SELECT_ALG1) ? __ldg(p.u + ent(d, b, k, in.s))
+                                           : ld_scalar(PL + row_off(d, b, 0, in.s) + xk);
+        }
+      }
+      // argmax over A: larger key; Eq. 9 ties -> smaller token then smaller k; Alg. 1 ties -> smaller k
+      int bk = inA ? k : 0x7fffffff, btok = inA ? (p.rule == SB_SELECT_ALG1 ? 0 : xk) : 0x7fffffff;
+      float bkey = key;
+      bool bin = inA;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const float okey = __shfl_xor_sync(0xffffffffu, bkey, o);
+        const int otok = __shfl_xor_sync(0xffffffffu, btok, o);
+        const int ok_ = __shfl_xor_sync(0xffffffffu, bk, o);
+        const bool oin = __shfl_xor_sync(0xffffffffu, (int)bin, o);
+        bool take;
+        if (!oin) take = false;
+        else if (!bin) take = true;
+        else take = okey > bkey || (okey == bkey && (otok < btok || (otok == btok && ok_ < bk)));
+        if (take) { bkey = okey; btok = otok; bk = ok_; bin = true; }
+      }
+      const int ksel = bin ? bk : -1;
+      const int n0 = __shfl_sync(0xffffffffu, nk, 0);
+      const int nsel = __shfl_sync(0xffffffffu, nk, ksel < 0 ? 0 : ksel);
+      if (lane == 0) {
+        Dec D;
+        D.b = b;
+        D.ksel = ksel;
+        if (ksel < 0) {
+          D.npath = min(n0, in.s);  // rejection in the shared prefix or at the branch row (P655)
+          D.kind = 1; D.row = D.npath; D.slot = 0;
+        } else {
+          D.npath = nsel;
+          if (nsel < in.L) { D.kind = 1; D.row = nsel; D.slot = (nsel <= in.s) ? 0 : ksel; }
+          else if (in.s < in.g) { D.kind = 2; D.row = in.g; D.slot = ksel; }  // bonus, p_{gamma+1}
+          else { D.kind = 0; D.row = 0; D.slot = 0; }  // branch token accepted (P237)
+        }
+        D.rs = (D.kind == 1) ? p.rowstat[ent(d, b, D.slot, D.row)] : make_float4(0.f, 1.f, 0.f, 1.f);
+        S.dec[dq.stage] = D;
+        mbar_arrive(&S.dfull[dq.stage]);
+      }
+      dq.advance();
+    }
+    return;
+  }
+  if (warp == sCW) {  // ---------------- producer
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      RingPos<sNQ> dq;
+      RingPos<sNS> rp;
+      for (;;) {
+        mbar_wait(&S.dfull[dq.stage], dq.phase);
+        const Dec D = S.dec[dq.stage];
+        dq.advance();
+        if (D.b < 0) break;
+        const int b = D.b;
+        const int npass = D.kind == 1 ? 1 : (D.kind == 2 ? 2 : 0);
+        const char* prow = reinterpret_cast<const char*>(PL + row_off(d, b, D.slot, D.row));
+        const char* qrow = reinterpret_cast<const char*>(QL + row_off(d, b, D.slot, D.row));
+        for (int pass = 0; pass < npass; ++pass)
+          for (int c = 0; c < nchunks; ++c) {
+            const uint32_t bytes = min((uint32_t)sChunk, row_bytes - (uint32_t)c * sChunk);
+            mbar_wait(&S.empty[rp.stage], rp.phase ^ 1u);
+            mbar_expect_tx(&S.full[rp.stage], (D.kind == 1 ? 2 : 1) * bytes);
+            bulk_g2s(S.buf[rp.stage][0], prow + (size_t)c * sChunk, bytes, &S.full[rp.stage], pol);
+            if (D.kind == 1)
+              bulk_g2s(S.buf[rp.stage][1], qrow + (size_t)c * sChunk, bytes, &S.full[rp.stage], pol);
+            rp.advance();
+          }
+      }
+    }
+    return;
+  }
+  if (warp == sCW + 1) {  // ---------------- epilogue
+    RingPos<sNQ> dq;
+    for (;;) {
+      mbar_wait(&S.dfull[dq.stage], dq.phase);
+      const Dec D = S.dec[dq.stage];
+      if (D.b < 0) break;
+      const int b = D.b;
+      mbar_wait(&S.sfull[dq.stage], dq.phase);
+      const SeqInfo in = p.info[b];
+      const int q = dq.stage;
+      int kind = D.kind, y = -1, st = 0;
+      double mass = 0.0;
+      if (kind != 0) {
+        const float MSp = S.rs[q][0], Zp = S.rs[q][1], MSq = S.rs[q][2], Zq = S.rs[q][3];
+        if (!S.ok[q]) {
+          kind = 0;
+          st |= SB_ST_NONFINITE;
+        } else {
+          const T* prow = PL + row_off(d, b, D.slot, D.row);
+          const T* qrow = QL + row_off(d, b, D.slot, D.row);
+          const float iZp = 1.f / Zp, iZq = 1.f / Zq;
+          bool resid = (kind == 1);
+          float* seg = S.seg[q];
+          const int per = (nseg + 31) / 32;
+          double R = 0.0, excl = 0.0, incl = 0.0;
+          for (int attempt = 0; attempt < 2; ++attempt) {
+            double local = 0.0;
+            for (int j = 0; j < per; ++j) {
+              const int sI = lane * per + j;
+              if (sI < nseg) local += (double)seg[sI];
+            }
+            incl = local;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const double yv = __shfl_up_sync(0xffffffffu, incl, o);
+              if (lane >= o) incl += yv;
+            }
+            excl = __shfl_up_sync(0xffffffffu, incl, 1);  // lane ranges [excl, incl) tile [0, R)
+            if (lane == 0) excl = 0.0;
+            R = __shfl_sync(0xffffffffu, incl, 31);
+            if (R > 0.0 || !resid) break;
+            resid = false;  // "no residual mass" (S134-140): sample from P
+            st |= SB_ST_ZERO_RESID;
+            warp_segments<T>(prow, qrow, row_bytes, nseg, false, MSp, iZp, MSq, iZq, seg);
+          }
+          const double t = (double)__ldg(p.us + b) * R;
+          // exactly one lane's [excl, incl) holds t; it rescans its segments in fp64
+          int found = -1, lastpos = -1;
+          double Fprev = 0.0;
+          const bool mine = (excl <= t && incl > t);
+          if (mine) {
+            double F = excl;
+            for (int j = 0; j < per; ++j) {
+              const int sI = lane * per + j;
+              if (sI >= nseg) break;
+              if (seg[sI] > 0.f) lastpos = sI;
+              if (found < 0 && F + (double)seg[sI] > t) { found = sI; Fprev = F; }
+              F += (double)seg[sI];
+            }
+          } else {
+            for (int j = 0; j < per; ++j) {
+              const int sI = lane * per + j;
+              if (sI < nseg && seg[sI] > 0.f) lastpos = sI;
+            }
+          }
+          const unsigned who = __ballot_sync(0xffffffffu, found >= 0);
+          int sStar;
+          double trem;
+          if (who) {
+            const int src = __ffs(who) - 1;
+            sStar = __shfl_sync(0xffffffffu, found, src);
+            trem = t - __shfl_sync(0xffffffffu, Fprev, src);
+          } else {  // rounding: the last segment with mass, and the in-segment fallback
+            const unsigned mw = __ballot_sync(0xffffffffu, mine);
+            const int src = mw ? __ffs(mw) - 1 : -1;
+            const int cand = src >= 0 ? __shfl_sync(0xffffffffu, lastpos, src) : -1;
+            sStar = cand >= 0 ? cand : (int)__reduce_max_sync(0xffffffffu, (unsigned)(lastpos + 1)) - 1;
+            trem = CUDART_INF;
+          }
+          if (sStar >= 0) {
+            // pass B: re-read segment sStar (one 16-byte vector per lane) from L2
+            const uint32_t off = (uint32_t)sStar * 512 + lane * 16;
+            uint4 vp, vq;
+            if (sizeof(T) == 2) vp = vq = make_uint4(0xff80ff80u, 0xff80ff80u, 0xff80ff80u, 0xff80ff80u);
+            else vp = vq = make_uint4(0xff800000u, 0xff800000u, 0xff800000u, 0xff800000u);
+            if (off < row_bytes) {
+              vp = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(prow) + off));
+              if (resid) vq = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(qrow) + off));
+            }
+            float r[E];
+            r_values<T>(vp, vq, resid, MSp, iZp, MSq, iZq, r);
+            const float incl = warp_scan_rn(seq_sum<E>(r));
+            float F = __shfl_up_sync(0xffffffffu, incl, 1);
+            if (lane == 0) F = 0.f;
+            int cand = 0x7fffffff, lastv = -1;
+            const int vbase = (int)(off / sizeof(T));
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+              F = __fadd_rn(F, r[e]);
+              if (cand == 0x7fffffff && (double)F > trem && r[e] > 0.f) cand = vbase + e;
+              if (r[e] > 0.f) lastv = vbase + e;
+            }
+            const int pick = (int)__reduce_min_sync(0xffffffffu, (unsigned)cand);
+            y = (pick != 0x7fffffff) ? pick : (int)__reduce_max_sync(0xffffffffu, (unsigned)(lastv + 1)) - 1;
+          }
+          mass = R;
+        }
+      }
+      // commit (SURVEY §8.0 "Commit")
+      const int ksel = D.ksel, npath = D.npath, kpath = ksel < 0 ? 0 : ksel;
+      int* out = p.out_tok + (int64_t)b * (d.G + 2);
+      for (int qq = lane; qq < d.G + 2; qq += 32) {
+        int v = -1;
+        if (qq < npath) v = __ldg(p.tok + ent(d, b, (qq < in.s) ? 0 : kpath, qq));
+        else if (qq == npath && kind != 0) v = y;
+        out[qq] = v;
+      }
+      if (lane < d.K) {
+        uint32_t km = 0;
+        for (int qq = 0; qq < npath; ++qq)
+          if (((qq < in.s) ? 0 : kpath) == lane) km |= 1u << qq;
+        p.keep_mask[(int64_t)b * d.K + lane] = km;
+      }
+      if (lane == 0) {
+        p.sel_k[b] = ksel;
+        p.commit_len[b] = npath + (kind != 0);
+        p.y_tok[b] = (kind != 0) ? y : -1;
+        p.y_kind[b] = kind;
+        p.path_rolled[b] = in.L - npath;
+        p.branch_discarded[b] = (d.K - 1) * (in.L - in.s);
+        if (p.resid_mass) p.resid_mass[b] = (kind != 0) ? (float)mass : 0.f;
+        if (st) atomicOr(p.status + b, st);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.dempty[dq.stage]);
+      dq.advance();
+      // global completion -> the last sequence's epilogue scans the offsets
+      int last = 0;
+      if (lane == 0) {
+        __threadfence();
+        last = (atomicAdd(p.sel_cnt, 1) == d.B - 1);
+      }
+      last = __shfl_sync(0xffffffffu, last, 0);
+      if (last) {
+        __threadfence();
+        const int per = (d.B + 31) / 32;
+        const int b0 = min(d.B, lane * per), b1 = min(d.B, b0 + per);
+        int loc = 0;
+        for (int qq = b0; qq < b1; ++qq) loc += __ldcg(p.commit_len + qq);
+        int incl = loc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int yv = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += yv;
+        }
+        int run = incl - loc;
+        for (int qq = b0; qq < b1; ++qq) {
+          p.offsets[qq] = run;
+          const int cl = __ldcg(p.commit_len + qq);
+          if (p.packed_tok)
+            for (int c = 0; c < cl; ++c) p.packed_tok[run + c] = __ldcg(p.out_tok + (int64_t)qq * (d.G + 2) + c);
+          run += cl;
+        }
+        if (lane == 31) p.offsets[d.B] = incl;
+        if (lane == 0) p.sel_cnt[0] = 0;  // leave the workspace re-usable
+      }
+    }
+    return;
+  }
+  // ---------------- consumers
+  RingPos<sNQ> dq;
+  RingPos<sNS> rp;
+  for (;;) {
+    mbar_wait(&S.dfull[dq.stage], dq.phase);
+    const Dec D = S.dec[dq.stage];
+    if (D.b < 0) break;
+    const int q = dq.stage;
+    if (D.kind == 2) {  // bonus row: its softmax state first
+      LazyAcc<false, 4> a;
+      a.init();
+      for (int c = 0; c < nchunks; ++c) {
+        const int nvec = (c == nchunks - 1) ? nvec_last : sChunk / 16;
+        mbar_wait(&S.full[rp.stage], rp.phase);
+        float f[sVPT * E];
+#pragma unroll
+        for (int j = 0; j < sVPT; ++j) {
+          const int v = tid + j * sCT;
+          if (v < nvec) {
+            Vec<T>::unpack(lds128(S.buf[rp.stage][0] + v * 16), f + j * E);
+          } else {
+#pragma unroll
+            for (int e = 0; e < E; ++e) f[j * E + e] = -CUDART_INF_F;
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.empty[rp.stage]);
+        rp.advance();
+        a.template add<sVPT * E>(f, c);
+      }
+      RowStat s = fold_lazy(a);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s = combine(s, shfl_xor(s, o));
+      if (lane == 0) S.red[warp] = s;
+      consumer_sync(sCT);
+      if (tid == 0) {
+        RowStat r = S.red[0];
+        for (int j = 1; j < sCW; ++j) r = combine(r, S.red[j]);
+        const RowOut o = finish(r);
+        S.rs[q][0] = o.MS; S.rs[q][1] = o.Z; S.rs[q][2] = 0.f; S.rs[q][3] = 1.f;
+        S.ok[q] = o.finite;
+      }
+      consumer_sync(sCT);
+    } else if (D.kind == 1 && tid == 0) {  // the epilogue reads the same state from S.rs
+      S.rs[q][0] = D.rs.x; S.rs[q][1] = D.rs.y; S.rs[q][2] = D.rs.z; S.rs[q][3] = D.rs.w;
+      S.ok[q] = (D.rs.y == D.rs.y) && (D.rs.w == D.rs.w);
+    }
+    if (D.kind != 0) {
+      const bool resid = (D.kind == 1);
+      const float4 rsv = resid ? D.rs : make_float4(S.rs[q][0], S.rs[q][1], S.rs[q][2], S.rs[q][3]);
+      const bool ok = resid ? ((rsv.y == rsv.y) && (rsv.w == rsv.w)) : (S.ok[q] != 0);
+      const float MSp = rsv.x, iZp = 1.f / rsv.y, MSq = rsv.z, iZq = 1.f / rsv.w;
+      for (int c = 0; c < nchunks; ++c) {
+        const int nvec = (c == nchunks - 1) ? nvec_last : sChunk / 16;
+        mbar_wait(&S.full[rp.stage], rp.phase);
+        uint4 vp[sVPT], vq[sVPT];
+#pragma unroll
+        for (int j = 0; j < sVPT; ++j) {
+          const int v = tid + j * sCT;
+          if (v < nvec) {
+            vp[j] = lds128(S.buf[rp.stage][0] + v * 16);
+            vq[j] = resid ? lds128(S.buf[rp.stage][1] + v * 16) : vp[j];
+          } else {
+            vp[j] = vq[j] = (sizeof(T) == 2) ? make_uint4(0xff80ff80u, 0xff80ff80u, 0xff80ff80u, 0xff80ff80u)
+                                             : make_uint4(0xff800000u, 0xff800000u, 0xff800000u, 0xff800000u);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.empty[rp.stage]);
+        rp.advance();
+#pragma unroll
+        for (int j = 0; j < sVPT; ++j) {
+          float r[E];
+          r_values<T>(vp[j], vq[j], resid, MSp, iZp, MSq, iZq, r);
+          const float incl = warp_scan_rn(ok ? seq_sum<E>(r) : 0.f);
+          if (lane == 31) S.seg[q][c * (sChunk / 512) + j * sCW + warp] = incl;
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&S.sfull[q]);
+    dq.advance();
+  }
+}
+
+template <typename T>
+static sb_status launch_select_tma(const SelParams& p, cudaStream_t s) {
+  static bool attr = false;
+  const int smem = (int)sizeof(SelSmem);
+  if (!attr) {
+    if (cudaFuncSetAttribute(k_select_tma<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+        cudaSuccess)
+      return SB_ERR_CUDA;
+    attr = true;
+  }
+  const int grid = std::min(num_sms(), p.d.B);
+  k_select_tma<T><<<grid, sThreads, smem, s>>>(p);
+  return cuda_status(cudaGetLastError());
+}
+
 template <typename T, int NT>
 static sb_status launch_select(const SelParams& p, bool vok, cudaStream_t s) {
   k_select<T, NT><<<p.d.B, NT, 0, s>>>(p, vok);
@@ -372,6 +869,9 @@ extern "C" sb_status sb_select_branch(const sb_dims* dd, const void* p_logits, c
   p.resid_mass = resid_mass;
   const bool vok = vec_ok(dd, p_logits) && vec_ok(dd, q_logits);
   cudaStream_t s = (cudaStream_t)stream;
+  const size_t row_bytes = (size_t)dd->V * elem_size(dd);
+  if (vok && row_bytes % 16 == 0 && row_bytes <= (size_t)sSegMax * 512 && !tma_disabled())
+    return dd->dtype == SB_BF16 ? launch_select_tma<__nv_bfloat16>(p, s) : launch_select_tma<float>(p, s);
   if (dd->dtype == SB_BF16) {
     if ((dd->V + 256 * 8 - 1) / (256 * 8) > kMaxTiles) return SB_ERR_UNSUPPORTED;
     return launch_select<__nv_bfloat16, 256>(p, vok, s);

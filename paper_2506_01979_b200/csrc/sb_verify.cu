@@ -16,6 +16,7 @@
 #include <cstdio>
 
 #include "sb_host.h"
+#include "sb_ring.cuh"
 
 namespace sb {
 
@@ -87,7 +88,146 @@ __global__ void __launch_bounds__(1024) k_plan(Dims d, const int* __restrict__ g
   if (tid == NT - 1) unit_off[d.B] = run;
 }
 
+// ---------------------------------------------------------------- shared unit logic
+struct Unit {
+  int b, slot, i;
+  SeqInfo in;
+};
+
+// unit -> (sequence, slot, row): upper-bound search over the offsets, then slot 0 rows
+// 0..L-1 followed by rows s+1..L-1 of slots 1..K-1
+__device__ __forceinline__ Unit decode_unit(const RowsParams& p, int unit) {
+  const Dims& d = p.d;
+  int lo = 0, hi = d.B;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (__ldg(p.unit_off + mid) <= unit) lo = mid; else hi = mid;
+  }
+  Unit u;
+  u.b = lo;
+  u.in = p.info[lo];
+  const int j = unit - __ldg(p.unit_off + lo);
+  if (j < u.in.L) {
+    u.slot = 0;
+    u.i = j;
+  } else {
+    const int per = u.in.L - 1 - u.in.s, jj = j - u.in.L;
+    u.slot = 1 + jj / per;
+    u.i = u.in.s + 1 + jj % per;
+  }
+  return u;
+}
+
+// Everything after a row pair's statistics are known: path-token probabilities and the
+// acceptance test, row outputs, and (in the CTA completing the sequence) n_k, status and
+// the sentinels.  `tid` / `nt` index the participating threads; `sync` is their barrier.
+template <typename T, typename Sync>
+__device__ __forceinline__ void unit_epilogue(const RowsParams& p, const Unit& un, const T* prow,
+                                              const T* qrow, const RowStat& ps, const RowStat& qs,
+                                              int tid, int nt, int* s_last, int* s_st, Sync sync) {
+  const Dims& d = p.d;
+  const int b = un.b, slot = un.slot, i = un.i;
+  const SeqInfo& in = un.in;
+  const RowOut po = finish(ps), qo = finish(qs);
+  // path tokens through this row: K branch tokens at the branch row, else one
+  const bool branch_row = (slot == 0 && i == in.s);
+  const int ntok = branch_row ? d.K : 1;
+  if (tid < ntok) {
+    const int ts = branch_row ? tid : slot;
+    const int64_t e = ent(d, b, ts, i);
+    const int x = __ldg(p.tok + e);
+    uint8_t fl = 0;
+    float pt = CUDART_NAN_F, qt = CUDART_NAN_F;
+    if (!(po.finite && qo.finite)) {
+      fl |= 4;
+    } else if (x < 0 || x >= d.V) {
+      fl |= 2;
+    } else {
+      const double Px = tok_prob(ld_scalar(prow + x), po.MS, po.Z);
+      const double Qx = tok_prob(ld_scalar(qrow + x), qo.MS, qo.Z);
+      pt = (float)Px;
+      qt = (float)Qx;
+      // accept iff r <= p/q (P534, P538), as u*Q[x] <= P[x]; Q[x] = 0 accepts (S127)
+      if ((double)__ldg(p.u + e) * Qx <= Px) fl |= 1;
+    }
+    p.p_tok[e] = pt;
+    p.q_tok[e] = qt;
+    p.pflag[e] = fl;
+  }
+  if (tid == 0) {
+    const int64_t e = ent(d, b, slot, i);
+    const double LN2 = 0.69314718055994530942;
+    p.lse_p[e] = po.finite ? (float)(((double)po.MS + log2((double)po.Z)) * LN2) : CUDART_NAN_F;
+    p.lse_q[e] = qo.finite ? (float)(((double)qo.MS + log2((double)qo.Z)) * LN2) : CUDART_NAN_F;
+    const bool conf_ok = po.finite && qo.finite;  // as the oracle: q stats iff both rows finite
+    if (p.top1_q) p.top1_q[e] = conf_ok ? (float)tok_prob(qs.m, qo.MS, qo.Z) : CUDART_NAN_F;
+    if (p.top1_id_q) p.top1_id_q[e] = conf_ok ? qs.idx : -1;
+    if (p.entropy_q) {
+      const double Z = qo.Z;
+      p.entropy_q[e] = conf_ok ? (float)(LN2 * (log2(Z) - (double)qs.s1 / Z)) : CUDART_NAN_F;
+    }
+    p.rowstat[e] = make_float4(po.MS, po.finite ? po.Z : CUDART_NAN_F, qo.MS,
+                               qo.finite ? qo.Z : CUDART_NAN_F);
+  }
+  // completion: the CTA finishing the sequence decides n_k (first zero bit)
+  sync();
+  if (tid == 0) {
+    __threadfence();
+    const int units_b = __ldg(p.unit_off + b + 1) - __ldg(p.unit_off + b);
+    const int prev = atomicAdd(p.cnt + b, 1);
+    *s_last = (prev == units_b - 1);
+    *s_st = in.st;
+  }
+  sync();
+  if (*s_last) {
+    __threadfence();
+    const int R1 = d.G + 1;
+    if (tid < d.K) {
+      const int k = tid;
+      uint32_t mask = 0;
+      int st = 0;
+      for (int r = 0; r < in.L; ++r) {
+        const int ts = (r < in.s) ? 0 : k;
+        const uint8_t fl = __ldcg(p.pflag + ent(d, b, ts, r));
+        if (fl & 1) mask |= 1u << r;
+        if (fl & 2) st |= SB_ST_BAD_TOKEN;
+        if (fl & 4) st |= SB_ST_NONFINITE;
+      }
+      const uint32_t rej = ~mask & (in.L >= 32 ? 0xffffffffu : ((1u << in.L) - 1));
+      p.acc_mask[(int64_t)b * d.K + k] = mask;
+      p.n_acc[(int64_t)b * d.K + k] = rej ? (__ffs(rej) - 1) : in.L;
+      if (st) atomicOr(s_st, st);
+    }
+    // sentinels for entries no tested path touches
+    for (int q = tid; q < d.K * R1; q += nt) {
+      const int k = q / R1, r = q % R1;
+      const int64_t e = ent(d, b, k, r);
+      const bool phys = (k == 0) ? (r < in.L) : (r > in.s && r < in.L);
+      const bool path = (k == 0) ? (r < in.L) : (r >= in.s && r < in.L);
+      if (!phys) {
+        p.lse_p[e] = CUDART_NAN_F;
+        p.lse_q[e] = CUDART_NAN_F;
+        if (p.top1_q) p.top1_q[e] = CUDART_NAN_F;
+        if (p.top1_id_q) p.top1_id_q[e] = -1;
+        if (p.entropy_q) p.entropy_q[e] = CUDART_NAN_F;
+      }
+      if (!path) {
+        p.p_tok[e] = CUDART_NAN_F;
+        p.q_tok[e] = CUDART_NAN_F;
+      }
+    }
+    sync();
+    if (tid == 0) {
+      p.status[b] = *s_st;
+      p.cnt[b] = 0;  // leave the workspace re-usable
+    }
+  }
+  sync();
+}
+
 // ---------------------------------------------------------------- rows
+// Register-staged fallback (any alignment / stride): each thread streams its share of
+// the row pair with 16-byte (or scalar) loads.
 template <typename T, int NT, int U>
 __global__ void __launch_bounds__(NT) k_rows(RowsParams p, bool vec_ok) {
   constexpr int NA = 4;
@@ -99,28 +239,10 @@ __global__ void __launch_bounds__(NT) k_rows(RowsParams p, bool vec_ok) {
   const int total = __ldg(p.unit_off + d.B);
   const T* PL = static_cast<const T*>(p.PL);
   const T* QL = static_cast<const T*>(p.QL);
-
   for (int unit = blockIdx.x; unit < total; unit += gridDim.x) {
-    // unit -> sequence (upper bound search over the offsets), then (slot, row)
-    int lo = 0, hi = d.B;  // find largest b with unit_off[b] <= unit
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (__ldg(p.unit_off + mid) <= unit) lo = mid; else hi = mid;
-    }
-    const int b = lo;
-    const SeqInfo in = p.info[b];
-    const int j = unit - __ldg(p.unit_off + b);
-    int slot, i;
-    if (j < in.L) {
-      slot = 0; i = j;
-    } else {
-      const int per = in.L - 1 - in.s, jj = j - in.L;
-      slot = 1 + jj / per;
-      i = in.s + 1 + jj % per;
-    }
-    const T* prow = PL + row_off(d, b, slot, i);
-    const T* qrow = QL + row_off(d, b, slot, i);
-
+    const Unit un = decode_unit(p, unit);
+    const T* prow = PL + row_off(d, un.b, un.slot, un.i);
+    const T* qrow = QL + row_off(d, un.b, un.slot, un.i);
     RowAcc<false, NA> pa;
     RowAcc<true, NA> qa;
     pa.init();
@@ -128,104 +250,236 @@ __global__ void __launch_bounds__(NT) k_rows(RowsParams p, bool vec_ok) {
     stream_pair<T, NA, NT, U>(prow, qrow, d.V, vec_ok, pa, qa);
     const RowStat ps = block_reduce<NT>(fold(pa), red);
     const RowStat qs = block_reduce<NT>(fold(qa), red);
-    const RowOut po = finish(ps), qo = finish(qs);
+    unit_epilogue(p, un, prow, qrow, ps, qs, tid, NT, &s_last, &s_st, [] { __syncthreads(); });
+  }
+}
 
-    // path tokens through this row: K branch tokens at the branch row, else one
-    const bool branch_row = (slot == 0 && i == in.s);
-    const int ntok = branch_row ? d.K : 1;
-    if (tid < ntok) {
-      const int ts = branch_row ? tid : slot;
-      const int64_t e = ent(d, b, ts, i);
-      const int x = __ldg(p.tok + e);
-      uint8_t fl = 0;
-      float pt = CUDART_NAN_F, qt = CUDART_NAN_F;
-      if (!(po.finite && qo.finite)) {
-        fl |= 4;
-      } else if (x < 0 || x >= d.V) {
-        fl |= 2;
-      } else {
-        const double Px = tok_prob(ld_scalar(prow + x), po.MS, po.Z);
-        const double Qx = tok_prob(ld_scalar(qrow + x), qo.MS, qo.Z);
-        pt = (float)Px;
-        qt = (float)Qx;
-        // accept iff r <= p/q (P534, P538), as u*Q[x] <= P[x]; Q[x] = 0 accepts (S127)
-        if ((double)__ldg(p.u + e) * Qx <= Px) fl |= 1;
-      }
-      p.p_tok[e] = pt;
-      p.q_tok[e] = qt;
-      p.pflag[e] = fl;
-    }
-    if (tid == 0) {
-      const int64_t e = ent(d, b, slot, i);
-      const double LN2 = 0.69314718055994530942;
-      p.lse_p[e] = po.finite ? (float)(((double)po.MS + log2((double)po.Z)) * LN2) : CUDART_NAN_F;
-      p.lse_q[e] = qo.finite ? (float)(((double)qo.MS + log2((double)qo.Z)) * LN2) : CUDART_NAN_F;
-      const bool conf_ok = po.finite && qo.finite;  // as the oracle: q stats iff both rows finite
-      if (p.top1_q)
-        p.top1_q[e] = conf_ok ? (float)tok_prob(qs.m, qo.MS, qo.Z) : CUDART_NAN_F;
-      if (p.top1_id_q) p.top1_id_q[e] = conf_ok ? qs.idx : -1;
-      if (p.entropy_q) {
-        const double Z = qo.Z;
-        p.entropy_q[e] = conf_ok ? (float)(LN2 * (log2(Z) - (double)qs.s1 / Z)) : CUDART_NAN_F;
-      }
-      p.rowstat[e] = make_float4(po.MS, po.finite ? po.Z : CUDART_NAN_F, qo.MS,
-                                 qo.finite ? qo.Z : CUDART_NAN_F);
-    }
+// ---------------------------------------------------------------- rows, TMA ring
+// Warp-specialised persistent kernel, one CTA per SM:
+//   warp kCW      producer  : cp.async.bulk of 16 KB p and q row chunks into a kNS-stage
+//                             shared ring (mbarrier full/empty per stage);
+//   warps 0..15   consumers : fold each chunk into the lazy online state, then per unit
+//                             one warp reduction (+ exact first-argmax) -> a partial in
+//                             shared memory (double-buffered, mbarrier handshake);
+//   warp kCW+1    epilogue  : combines the 16 partials, runs the unit epilogue (token
+//                             tests, row outputs, per-sequence completion), concurrently
+//                             with the consumers streaming the next unit.
+constexpr int kNS = 6;                   // ring stages
+constexpr int kCW = 16;                  // consumer warps
+constexpr int kCT = kCW * 32;            // consumer threads
+constexpr int kVPT = 2;                  // 16-byte vectors per consumer thread per row per stage
+constexpr int kChunk = kCT * kVPT * 16;  // bytes per row per stage (16 KB)
+constexpr int kNP = 2;                   // partial slots (units in flight to the epilogue)
+constexpr int kThreads = kCT + 64;
 
-    // completion: the CTA finishing the sequence decides n_k (ballot/ffs over rows)
-    __syncthreads();
-    if (tid == 0) {
-      __threadfence();
-      const int units_b = __ldg(p.unit_off + b + 1) - __ldg(p.unit_off + b);
-      const int prev = atomicAdd(p.cnt + b, 1);
-      s_last = (prev == units_b - 1);
-      s_st = in.st;
-    }
-    __syncthreads();
-    if (s_last) {
-      __threadfence();
-      const int R1 = d.G + 1;
-      if (tid < d.K) {
-        const int k = tid;
-        uint32_t mask = 0;
-        int st = 0;
-        for (int r = 0; r < in.L; ++r) {
-          const int ts = (r < in.s) ? 0 : k;
-          const uint8_t fl = __ldcg(p.pflag + ent(d, b, ts, r));
-          if (fl & 1) mask |= 1u << r;
-          if (fl & 2) st |= SB_ST_BAD_TOKEN;
-          if (fl & 4) st |= SB_ST_NONFINITE;
-        }
-        const uint32_t rej = ~mask & (in.L >= 32 ? 0xffffffffu : ((1u << in.L) - 1));
-        p.acc_mask[(int64_t)b * d.K + k] = mask;
-        p.n_acc[(int64_t)b * d.K + k] = rej ? (__ffs(rej) - 1) : in.L;
-        if (st) atomicOr(&s_st, st);
-      }
-      // sentinels for entries no tested path touches
-      for (int q = tid; q < d.K * R1; q += NT) {
-        const int k = q / R1, r = q % R1;
-        const int64_t e = ent(d, b, k, r);
-        const bool phys = (k == 0) ? (r < in.L) : (r > in.s && r < in.L);
-        const bool path = (k == 0) ? (r < in.L) : (r >= in.s && r < in.L);
-        if (!phys) {
-          p.lse_p[e] = CUDART_NAN_F;
-          p.lse_q[e] = CUDART_NAN_F;
-          if (p.top1_q) p.top1_q[e] = CUDART_NAN_F;
-          if (p.top1_id_q) p.top1_id_q[e] = -1;
-          if (p.entropy_q) p.entropy_q[e] = CUDART_NAN_F;
-        }
-        if (!path) {
-          p.p_tok[e] = CUDART_NAN_F;
-          p.q_tok[e] = CUDART_NAN_F;
-        }
-      }
-      __syncthreads();
-      if (tid == 0) {
-        p.status[b] = s_st;
-        p.cnt[b] = 0;  // leave the workspace re-usable
-      }
+struct RowsSmem {
+  uint64_t full[kNS], empty[kNS];
+  uint64_t pfull[kNP], pempty[kNP];
+  RowStat part[kNP][2][kCW];  // [slot][p,q][warp]
+  int s_last, s_st;
+  alignas(128) uint8_t buf[kNS][2][kChunk];
+};
+
+// Warp-level reduction of one row's per-thread state.  For q rows the exact first index
+// of the warp maximum is resolved by re-reading the (<= 2) vectors of the chunk where
+// each max-holding lane first saw it; the loads are issued before the sum reduction.
+template <typename T, bool kQ>
+__device__ __forceinline__ RowStat warp_part(const LazyAcc<kQ, 4>& a, const T* row, int nvec_last,
+                                             int nchunks) {
+  constexpr int E = Vec<T>::E;
+  const int tid = threadIdx.x;
+  RowStat s = fold_lazy(a);
+  float mw = s.m;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mw = fmaxf(mw, __shfl_xor_sync(0xffffffffu, mw, o));
+  uint4 x[kVPT];
+  bool have[kVPT];
+  const bool need = kQ && (a.m == mw) && (mw > -CUDART_INF_F) && (a.tag >= 0);
+  const int c = a.tag;
+  if (need) {
+    const int nvec = (c == nchunks - 1) ? nvec_last : kChunk / 16;
+    const uint4* cv = reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(row) + (size_t)c * kChunk);
+#pragma unroll
+    for (int j = 0; j < kVPT; ++j) {
+      const int v = tid + j * kCT;
+      have[j] = v < nvec;
+      if (have[j]) x[j] = __ldg(cv + v);
     }
   }
+  // sums over the warp (fixed xor tree)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    RowStat t = shfl_xor(s, o);
+    t.m = s.m;  // m / idx handled separately
+    s = combine(s, t);
+  }
+  s.m = mw;
+  int cand = 0x7fffffff;
+  if (need) {
+#pragma unroll
+    for (int j = kVPT - 1; j >= 0; --j) {
+      if (!have[j]) continue;
+      float f[E];
+      Vec<T>::unpack(x[j], f);
+#pragma unroll
+      for (int e = E - 1; e >= 0; --e)
+        if (f[e] == mw) cand = c * (kChunk / (int)sizeof(T)) + (tid + j * kCT) * E + e;
+    }
+  }
+  s.idx = kQ ? __reduce_min_sync(0xffffffffu, (unsigned)cand) : 0;
+  return s;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads, 1) k_rows_tma(RowsParams p) {
+  constexpr int E = Vec<T>::E;
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  RowsSmem& S = *reinterpret_cast<RowsSmem*>(smem_raw);
+  const Dims& d = p.d;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < kNS; ++s) {
+      mbar_init(&S.full[s], 1);
+      mbar_init(&S.empty[s], kCW);
+    }
+    for (int s = 0; s < kNP; ++s) {
+      mbar_init(&S.pfull[s], kCW);
+      mbar_init(&S.pempty[s], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int total = __ldg(p.unit_off + d.B);
+  const T* PL = static_cast<const T*>(p.PL);
+  const T* QL = static_cast<const T*>(p.QL);
+  const uint32_t row_bytes = (uint32_t)d.V * sizeof(T);
+  const int nchunks = (row_bytes + kChunk - 1) / kChunk;
+  const int nvec_last = (int)(row_bytes - (uint32_t)(nchunks - 1) * kChunk) / 16;
+
+  if (warp == kCW) {  // ---------------- producer
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      RingPos<kNS> rp;
+      for (int unit = blockIdx.x; unit < total; unit += gridDim.x) {
+        const Unit un = decode_unit(p, unit);
+        const char* prow = reinterpret_cast<const char*>(PL + row_off(d, un.b, un.slot, un.i));
+        const char* qrow = reinterpret_cast<const char*>(QL + row_off(d, un.b, un.slot, un.i));
+        for (int c = 0; c < nchunks; ++c) {
+          const uint32_t bytes = min((uint32_t)kChunk, row_bytes - (uint32_t)c * kChunk);
+          mbar_wait(&S.empty[rp.stage], rp.phase ^ 1u);
+          mbar_expect_tx(&S.full[rp.stage], 2 * bytes);
+          bulk_g2s(S.buf[rp.stage][0], prow + (size_t)c * kChunk, bytes, &S.full[rp.stage], pol);
+          bulk_g2s(S.buf[rp.stage][1], qrow + (size_t)c * kChunk, bytes, &S.full[rp.stage], pol);
+          rp.advance();
+        }
+      }
+    }
+    return;
+  }
+  if (warp == kCW + 1) {  // ---------------- epilogue
+    RingPos<kNP> up;
+    for (int unit = blockIdx.x; unit < total; unit += gridDim.x) {
+      const Unit un = decode_unit(p, unit);
+      mbar_wait(&S.pfull[up.stage], up.phase);
+      RowStat ps = lane < kCW ? S.part[up.stage][0][lane] : rowstat_empty();
+      RowStat qs = lane < kCW ? S.part[up.stage][1][lane] : rowstat_empty();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.pempty[up.stage]);
+      up.advance();
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        ps = combine(ps, shfl_xor(ps, o));
+        qs = combine(qs, shfl_xor(qs, o));
+      }
+      const T* prow = PL + row_off(d, un.b, un.slot, un.i);
+      const T* qrow = QL + row_off(d, un.b, un.slot, un.i);
+      unit_epilogue(p, un, prow, qrow, ps, qs, lane, 32, &S.s_last, &S.s_st, [] { __syncwarp(); });
+    }
+    return;
+  }
+  // ---------------- consumers
+  RingPos<kNS> rp;
+  RingPos<kNP> up;
+  for (int unit = blockIdx.x; unit < total; unit += gridDim.x) {
+    LazyAcc<false, 4> pa;
+    LazyAcc<true, 4> qa;
+    pa.init();
+    qa.init();
+    // full chunks: every lane owns kVPT whole vectors, no guards
+    for (int c = 0; c < nchunks - 1; ++c) {
+      mbar_wait(&S.full[rp.stage], rp.phase);
+      const uint8_t* bp = S.buf[rp.stage][0];
+      const uint8_t* bq = S.buf[rp.stage][1];
+      uint4 xp[kVPT], xq[kVPT];
+#pragma unroll
+      for (int j = 0; j < kVPT; ++j) {
+        xp[j] = lds128(bp + (tid + j * kCT) * 16);
+        xq[j] = lds128(bq + (tid + j * kCT) * 16);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.empty[rp.stage]);
+      rp.advance();
+      float fp[kVPT * E], fq[kVPT * E];
+#pragma unroll
+      for (int j = 0; j < kVPT; ++j) {
+        Vec<T>::unpack(xp[j], fp + j * E);
+        Vec<T>::unpack(xq[j], fq + j * E);
+      }
+      pa.template add<kVPT * E>(fp, c);
+      qa.template add<kVPT * E>(fq, c);
+    }
+    {  // last (possibly partial) chunk
+      const int c = nchunks - 1;
+      mbar_wait(&S.full[rp.stage], rp.phase);
+      const uint8_t* bp = S.buf[rp.stage][0];
+      const uint8_t* bq = S.buf[rp.stage][1];
+      float fp[kVPT * E], fq[kVPT * E];
+#pragma unroll
+      for (int j = 0; j < kVPT; ++j) {
+        const int v = tid + j * kCT;
+        if (v < nvec_last) {
+          Vec<T>::unpack(lds128(bp + v * 16), fp + j * E);
+          Vec<T>::unpack(lds128(bq + v * 16), fq + j * E);
+        } else {
+#pragma unroll
+          for (int e = 0; e < E; ++e) fp[j * E + e] = fq[j * E + e] = -CUDART_INF_F;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.empty[rp.stage]);
+      rp.advance();
+      pa.template add<kVPT * E>(fp, c);
+      qa.template add<kVPT * E>(fq, c);
+    }
+    const Unit un = decode_unit(p, unit);
+    const T* qrow = QL + row_off(d, un.b, un.slot, un.i);
+    const RowStat ps = warp_part<T, false>(pa, qrow, nvec_last, nchunks);
+    const RowStat qs = warp_part<T, true>(qa, qrow, nvec_last, nchunks);
+    if (lane == 0) {
+      mbar_wait(&S.pempty[up.stage], up.phase ^ 1u);
+      S.part[up.stage][0][warp] = ps;
+      S.part[up.stage][1][warp] = qs;
+      mbar_arrive(&S.pfull[up.stage]);
+    }
+    __syncwarp();
+    up.advance();
+  }
+}
+
+template <typename T>
+static sb_status launch_rows_tma(const RowsParams& p, cudaStream_t s) {
+  static bool attr = false;
+  const int smem = (int)sizeof(RowsSmem);
+  if (!attr) {
+    if (cudaFuncSetAttribute(k_rows_tma<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+        cudaSuccess)
+      return SB_ERR_CUDA;
+    attr = true;
+  }
+  const int64_t max_units = (int64_t)p.d.B * p.d.K * (p.d.G + 1);
+  const int grid = (int)std::min<int64_t>(num_sms(), max_units);
+  k_rows_tma<T><<<grid, kThreads, smem, s>>>(p);
+  return cuda_status(cudaGetLastError());
 }
 
 template <typename T, int NT, int U>
@@ -277,6 +531,8 @@ extern "C" sb_status sb_verify_branches(const sb_dims* dd, const void* p_logits,
   p.acc_mask = acc_mask; p.n_acc = n_acc; p.status = status;
   const bool vok = vec_ok(dd, p_logits) && vec_ok(dd, q_logits);
   const size_t row_bytes = (size_t)dd->V * elem_size(dd);
+  if (vok && row_bytes % 16 == 0 && !tma_disabled())
+    return dd->dtype == SB_BF16 ? launch_rows_tma<__nv_bfloat16>(p, s) : launch_rows_tma<float>(p, s);
   if (dd->dtype == SB_BF16) {
     return row_bytes <= 131072 ? launch_rows<__nv_bfloat16, 128, 4>(p, vok, s)
                                : launch_rows<__nv_bfloat16, 256, 4>(p, vok, s);

@@ -41,17 +41,18 @@ class Config:
     extra: dict = field(default_factory=dict)
 
 
-# delta / rho_same come from scripts/calibrate_alpha.py (oracle-measured alpha).
+# delta from scripts/calibrate_alpha.py (alpha measured with the oracle only, 512 rows):
+# c1/c2 alpha 0.617, c3/c5 0.904, c4 0.802 (profiles/r1_calibration.txt).
 CONFIGS = {
-    "c1": Config("c1", 32000, "f32", 1, 2, 8, "fixed", 0.6, 0.15, 1.30, 0.85, rounds=256,
+    "c1": Config("c1", 32000, "f32", 1, 2, 8, "fixed", 0.6, 0.15, 1.34, 0.85, rounds=256,
                  note="Vicuna 68M&13B vocab, batch 1, K=2, gamma=8, fp32, 256 verify rounds"),
-    "c2": Config("c2", 32000, "bf16", 64, 4, 8, "adaptive", 0.6, 0.15, 1.30, 0.85,
+    "c2": Config("c2", 32000, "bf16", 64, 4, 8, "adaptive", 0.6, 0.15, 1.34, 0.85,
                  note="V=32000, batch 64, K=4, gamma<=8 adaptive via draft confidence"),
-    "c3": Config("c3", 128256, "bf16", 256, 4, 16, "adaptive", 0.9, 0.08, 0.45, 0.97,
+    "c3": Config("c3", 128256, "bf16", 256, 4, 16, "adaptive", 0.9, 0.08, 0.318, 0.97,
                  note="Llama-3 V=128256, batch 256, K=4, gamma<=16 adaptive"),
-    "c4": Config("c4", 151936, "bf16", 2048, 4, 8, "fixed", 0.8, 0.08, 0.75, 0.93,
+    "c4": Config("c4", 151936, "bf16", 2048, 4, 8, "fixed", 0.8, 0.08, 0.622, 0.93,
                  note="Qwen V=151936, batch 2048, K=4, gamma=8, sequence-sharded"),
-    "c5": Config("c5", 128256, "bf16", 512, 8, 16, "fixed", 0.9, 0.08, 0.45, 0.97,
+    "c5": Config("c5", 128256, "bf16", 512, 8, 16, "fixed", 0.9, 0.08, 0.318, 0.97,
                  note="Llama-3 V=128256, batch 512, K=8, gamma=16, vocab-sharded"),
 }
 
@@ -93,10 +94,13 @@ def _one_sequence(cfg: Config, seed: int, b: int, device, gamma_b: int, s_b: int
     bulk_at_star = 2.0 * z.gather(2, vstar.unsqueeze(-1)).squeeze(-1)
     noise_star = z2.gather(2, vstar.unsqueeze(-1)).squeeze(-1)
     noise_move = z2.gather(2, vmove.unsqueeze(-1)).squeeze(-1)
-    new_star = torch.where(move, bulk_at_star + cfg.delta * noise_star, h + cfg.delta * noise_star)
+    # the draft bulk mass grows by E[exp(delta z')] = exp(delta^2/2); lifting the draft
+    # peak by delta^2/2 keeps the draft's own top-1 confidence distributed like c
+    hq = h + 0.5 * cfg.delta * cfg.delta
+    new_star = torch.where(move, bulk_at_star + cfg.delta * noise_star, hq + cfg.delta * noise_star)
     lq.scatter_(2, vstar.unsqueeze(-1), new_star.unsqueeze(-1))
     cur_move = lq.gather(2, vmove.unsqueeze(-1)).squeeze(-1)
-    lq.scatter_(2, vmove.unsqueeze(-1), torch.where(move, h + cfg.delta * noise_move, cur_move).unsqueeze(-1))
+    lq.scatter_(2, vmove.unsqueeze(-1), torch.where(move, hq + cfg.delta * noise_move, cur_move).unsqueeze(-1))
     del z, z2
 
     ldt = torch.bfloat16 if cfg.dtype == "bf16" else torch.float32
