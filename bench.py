@@ -45,6 +45,8 @@ class Clocks:
         self.proc = None
 
     def __enter__(self):
+        if self.index < 0:
+            return self
         q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
@@ -77,8 +79,9 @@ class Clocks:
         mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[j] for r in self.rows for j in range(4) if len(r) > 3 + j and r[3 + j] == "Active"})
+        pw = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(self.rows), "power_w_max": max(pw) if pw else None}
 
 
 def verified_tokens(gamma, bpos, K):
@@ -102,6 +105,27 @@ def bytes_model(gamma, bpos, y_kind, K, V, es, G, conf_rows=0):
     return a1, a4, a6, small, units
 
 
+def rank_slice(cfg, rank, world):
+    """Sequences [b0, b1) a rank owns: weak scaling, each rank a full per-GPU batch with
+    global sequence keys rank*B .. (rank+1)*B - 1 (no data-path collective)."""
+    Bl = cfg.B * cfg.rounds
+    return rank * Bl, (rank + 1) * Bl
+
+
+def reduce_over_ranks(ms_step, toks, committed, nbytes, device, world):
+    """Step time = MAX over ranks; tokens / bytes = SUM over ranks (torch.distributed)."""
+    if world <= 1:
+        return ms_step, toks, committed, nbytes
+    import torch
+
+    t = torch.tensor([ms_step, float(toks), float(committed), float(nbytes)], device=device, dtype=torch.float64)
+    mx = t[:1].clone()
+    sm = t[1:].clone()
+    torch.distributed.all_reduce(mx, op=torch.distributed.ReduceOp.MAX)
+    torch.distributed.all_reduce(sm, op=torch.distributed.ReduceOp.SUM)
+    return float(mx[0]), float(sm[0]), float(sm[1]), float(sm[2])
+
+
 def run_ours(args, rank, world, local_rank):
     import numpy as np
     import torch
@@ -112,9 +136,9 @@ def run_ours(args, rank, world, local_rank):
     build()
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
-    cfg = synth.config(args.config)
+    cfg = synth.config(args.config, **({"delta": args.delta} if args.delta is not None else {}))
     Bl = cfg.B * cfg.rounds
-    b0, b1 = rank * Bl, (rank + 1) * Bl
+    b0, b1 = rank_slice(cfg, rank, world)
     t0 = time.time()
     inp = synth.generate(cfg, device=dev, b0=b0, b1=b1)
     gen_s = time.time() - t0
@@ -138,54 +162,65 @@ def run_ours(args, rank, world, local_rank):
     toks = verified_tokens(gamma, bpos, cfg.K)
     committed = int(buf.commit_len.sum())
 
-    # ---- timed region: K steps, per-call events on the launching stream
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    # ---- timed region: exactly K whole steps, replayed from a CUDA graph of the C-ABI
+    # launches (no per-step host/ctypes overhead), bracketed by barrier + synchronize
+    graph = api.StepGraph(d, inp, buf, adaptive=adaptive) if not args.no_graph else None
+    clk = Clocks(local_rank if not args.no_clocks else -1).__enter__()
+    time.sleep(0.3)  # let nvidia-smi start sampling before the timed region
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with Clocks(local_rank) as clk:
-        start.record(stream)
-        for k in range(args.steps):
-            e = ev[k]
-            e[0].record(stream)
-            if adaptive:
-                api.sb_draft_confidence(api.conf_dims(d), inp["QL"], None, api.SB_CONF_TOP1, 0.2, 1.0, 6,
-                                        buf.c_top1, buf.c_id, buf.c_ent, None, buf.c_stat, buf.c_stop,
-                                        buf.c_knext, buf.c_gamma, buf.conf_workspace, stream)
-                g = buf.c_gamma.view(-1)
-            else:
-                g = inp["gamma"]
-            e[1].record(stream)
-            api.sb_verify_branches(d, inp["PL"], inp["QL"], inp["tok"], inp["u"], g, inp["branch_pos"],
-                                   buf.lse_p, buf.lse_q, buf.p_tok, buf.q_tok, buf.acc_mask, buf.n_acc,
-                                   buf.top1_q, buf.top1_id_q, buf.entropy_q, buf.status, buf.workspace,
-                                   stream)
-            e[2].record(stream)
-            api.sb_select_branch(d, inp["PL"], inp["QL"], inp["tok"], inp["u"], inp["us"], g,
-                                 inp["branch_pos"], buf.n_acc, 0, buf.sel_k, buf.commit_len, buf.out_tok,
-                                 buf.y_tok, buf.y_kind, buf.offsets, buf.packed_tok, buf.path_rolled,
-                                 buf.branch_discarded, buf.keep_mask, buf.resid_mass, buf.status,
-                                 buf.workspace, stream)
-            e[3].record(stream)
-        end.record(stream)
-        torch.cuda.synchronize()
+    run_stream = torch.cuda.current_stream()  # CUDAGraph.replay() launches on the current stream
+    start.record(run_stream)
+    for k in range(args.steps):
+        if graph is not None:
+            graph.replay()
+        else:
+            step()
+    end.record(run_stream)
+    torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
     ms = start.elapsed_time(end)
-    t_conf = sum(e[0].elapsed_time(e[1]) for e in ev) / args.steps
-    t_ver = sum(e[1].elapsed_time(e[2]) for e in ev) / args.steps
-    t_sel = sum(e[2].elapsed_time(e[3]) for e in ev) / args.steps
+
+    # ---- kernel timing region (roofline): each C-ABI call captured alone in a CUDA
+    # graph and replayed K times, CUDA events around every replay on the launching stream
+    gam = buf.c_gamma.view(-1) if adaptive else inp["gamma"]
+    calls = {
+        "conf": (lambda s: api.sb_draft_confidence(
+            api.conf_dims(d), inp["QL"], None, api.SB_CONF_TOP1, 0.2, 1.0, 6, buf.c_top1, buf.c_id,
+            buf.c_ent, None, buf.c_stat, buf.c_stop, buf.c_knext, buf.c_gamma, buf.conf_workspace, s))
+        if adaptive else None,
+        "verify": lambda s: api.sb_verify_branches(
+            d, inp["PL"], inp["QL"], inp["tok"], inp["u"], gam, inp["branch_pos"], buf.lse_p, buf.lse_q,
+            buf.p_tok, buf.q_tok, buf.acc_mask, buf.n_acc, buf.top1_q, buf.top1_id_q, buf.entropy_q,
+            buf.status, buf.workspace, s),
+        "select": lambda s: api.sb_select_branch(
+            d, inp["PL"], inp["QL"], inp["tok"], inp["u"], inp["us"], gam, inp["branch_pos"], buf.n_acc, 0,
+            buf.sel_k, buf.commit_len, buf.out_tok, buf.y_tok, buf.y_kind, buf.offsets, buf.packed_tok,
+            buf.path_rolled, buf.branch_discarded, buf.keep_mask, buf.resid_mass, buf.status, buf.workspace, s),
+    }
+    kt = {}
+    for name, fn in calls.items():
+        if fn is None:
+            kt[name] = 0.0
+            continue
+        cg = api.CallGraph(fn) if not args.no_graph else None
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        torch.cuda.synchronize()
+        cur = torch.cuda.current_stream()
+        for e0, e1 in evs:
+            e0.record(cur)
+            cg.replay() if cg is not None else fn(cur)
+            e1.record(cur)
+        torch.cuda.synchronize()
+        kt[name] = sum(e0.elapsed_time(e1) for e0, e1 in evs) / args.steps
+    clk.__exit__()
+    t_conf, t_ver, t_sel = kt["conf"], kt["verify"], kt["select"]
     ms_step = ms / args.steps
-    if world > 1:
-        t = torch.tensor([ms_step, float(toks), float(committed), float(a1 + a4 + a6 + small)], device=dev,
-                         dtype=torch.float64)
-        mx = t.clone()
-        torch.distributed.all_reduce(mx[:1], op=torch.distributed.ReduceOp.MAX)
-        torch.distributed.all_reduce(t[1:], op=torch.distributed.ReduceOp.SUM)
-        ms_step_all, toks_all, comm_all, bytes_all = float(mx[0]), float(t[1]), float(t[2]), float(t[3])
-    else:
-        ms_step_all, toks_all, comm_all, bytes_all = ms_step, toks, committed, a1 + a4 + a6 + small
+    ms_step_all, toks_all, comm_all, bytes_all = reduce_over_ranks(
+        ms_step, toks, committed, a1 + a4 + a6 + small, dev, world)
 
     # ---- e2e through the public API with host buffers (pinned), H2D + D2H inside
     e2e = None
@@ -209,7 +244,9 @@ def run_ours(args, rank, world, local_rank):
         "logit_GBps": round(step_gbs, 1), "logit_frac_of_peak": round(step_gbs / world / peak, 4),
         "committed_tokens_per_s": round(comm_all / (ms_step_all * 1e-3), 1),
         "breakdown_ms": {"draft_confidence": round(t_conf, 4), "verify": round(t_ver, 4),
-                         "select": round(t_sel, 4)},
+                         "select": round(t_sel, 4),
+                         "source": "each call replayed alone from its own CUDA graph, CUDA events"},
+        "timing": "CUDA graph replay of the whole step" if not args.no_graph else "eager C-ABI calls",
         "roofline": {"bound": "hbm", "kernel": "sb_verify_branches (k_plan + k_rows)",
                      "achieved": round(ver_gbs, 1), "peak": peak, "peak_source": peak_src, "unit": "GB/s",
                      "frac": round(ver_gbs / peak, 4), "traffic": traffic_from_profiles(cfg.name),
@@ -372,6 +409,9 @@ def main():
     ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="issue the C-ABI calls eagerly each step")
+    ap.add_argument("--delta", type=float, default=None, help="override the generator's draft noise")
+    ap.add_argument("--no-clocks", action="store_true", help="do not run the nvidia-smi sampler")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)

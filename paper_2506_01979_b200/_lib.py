@@ -7,7 +7,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SO = os.path.join(HERE, "libspecbranch.so")
+SO = os.environ.get("SB_LIB_PATH") or os.path.join(HERE, "libspecbranch.so")  # override: A/B builds
 
 SB_OK, SB_ERR_INVALID_ARG, SB_ERR_UNSUPPORTED, SB_ERR_CUDA, SB_ERR_NCCL, SB_ERR_WORKSPACE = range(6)
 SB_BF16, SB_F32 = 0, 1

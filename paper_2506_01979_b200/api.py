@@ -194,3 +194,32 @@ def verify_step(d: L.sb_dims, inp: dict, buf: StepBuffers, rule: int = SB_SELECT
                      buf.branch_discarded, buf.keep_mask, buf.resid_mass, buf.status,
                      buf.workspace, stream)
     return gamma
+
+
+class CallGraph:
+    """CUDA graph of a sequence of C-ABI calls (captured once after one warm-up run,
+    replayed on the current stream).  Removes per-call host/ctypes overhead; the
+    captured tensors are re-read at every replay (update inputs in place)."""
+
+    def __init__(self, fn):
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            fn(side)  # warm-up: one-time function attributes are set outside capture
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, stream=side):
+            self.result = fn(side)
+
+    def replay(self):
+        self.graph.replay()
+
+
+class StepGraph(CallGraph):
+    """The whole step ([confidence ->] verify -> select) as one CUDA graph."""
+
+    def __init__(self, d: L.sb_dims, inp: dict, buf: StepBuffers, rule: int = SB_SELECT_EQ9,
+                 adaptive: bool = False, eps: float = 0.2, k_max: int = 6):
+        super().__init__(lambda s: verify_step(d, inp, buf, rule, adaptive, eps, k_max, s))
+        self.gamma = self.result

@@ -14,6 +14,7 @@
 //                         status and the sentinels of untested entries.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "sb_host.h"
 #include "sb_ring.cuh"
@@ -255,35 +256,38 @@ __global__ void __launch_bounds__(NT) k_rows(RowsParams p, bool vec_ok) {
 }
 
 // ---------------------------------------------------------------- rows, TMA ring
-// Warp-specialised persistent kernel, one CTA per SM:
-//   warp kCW      producer  : cp.async.bulk of 16 KB p and q row chunks into a kNS-stage
-//                             shared ring (mbarrier full/empty per stage);
-//   warps 0..15   consumers : fold each chunk into the lazy online state, then per unit
-//                             one warp reduction (+ exact first-argmax) -> a partial in
-//                             shared memory (double-buffered, mbarrier handshake);
-//   warp kCW+1    epilogue  : combines the 16 partials, runs the unit epilogue (token
-//                             tests, row outputs, per-sequence completion), concurrently
-//                             with the consumers streaming the next unit.
-constexpr int kNS = 6;                   // ring stages
-constexpr int kCW = 16;                  // consumer warps
-constexpr int kCT = kCW * 32;            // consumer threads
-constexpr int kVPT = 2;                  // 16-byte vectors per consumer thread per row per stage
-constexpr int kChunk = kCT * kVPT * 16;  // bytes per row per stage (16 KB)
-constexpr int kNP = 2;                   // partial slots (units in flight to the epilogue)
-constexpr int kThreads = kCT + 64;
+// Warp-specialised persistent kernel, one CTA per SM (template RC = geometry):
+//   warp CW       producer  : cp.async.bulk of CHUNK-byte p and q row chunks into an
+//                             NS-stage shared ring (mbarrier full/empty per stage);
+//   warps 0..CW-1 consumers : fold each chunk into the lazy online state (VPT 16-byte
+//                             vectors per thread per row per stage), then per unit one
+//                             warp reduction (+ exact first-argmax) -> a partial in
+//                             shared memory (NP slots, mbarrier handshake);
+//   warp CW+1     epilogue  : prefetches the unit's path tokens, uniforms and their two
+//                             logits while the consumers stream, then combines the CW
+//                             partials, runs the token tests in fp64, writes the row
+//                             outputs and the per-sequence completion — concurrently with
+//                             the consumers streaming the next units.
+template <int CW_, int NS_, int VPT_, int NP_>
+struct RC {
+  static constexpr int CW = CW_, NS = NS_, VPT = VPT_, NP = NP_;
+  static constexpr int CT = CW * 32;
+  static constexpr int CHUNK = CT * VPT * 16;
+  static constexpr int THREADS = CT + 64;
+};
 
+template <class C>
 struct RowsSmem {
-  uint64_t full[kNS], empty[kNS];
-  uint64_t pfull[kNP], pempty[kNP];
-  RowStat part[kNP][2][kCW];  // [slot][p,q][warp]
-  int s_last, s_st;
-  alignas(128) uint8_t buf[kNS][2][kChunk];
+  uint64_t full[C::NS], empty[C::NS];
+  uint64_t pfull[C::NP], pempty[C::NP];
+  RowStat part[C::NP][2][C::CW];  // [slot][p,q][warp]
+  alignas(128) uint8_t buf[C::NS][2][C::CHUNK];
 };
 
 // Warp-level reduction of one row's per-thread state.  For q rows the exact first index
-// of the warp maximum is resolved by re-reading the (<= 2) vectors of the chunk where
+// of the warp maximum is resolved by re-reading the (<= VPT) vectors of the chunk where
 // each max-holding lane first saw it; the loads are issued before the sum reduction.
-template <typename T, bool kQ>
+template <class C, typename T, bool kQ>
 __device__ __forceinline__ RowStat warp_part(const LazyAcc<kQ, 4>& a, const T* row, int nvec_last,
                                              int nchunks) {
   constexpr int E = Vec<T>::E;
@@ -292,58 +296,202 @@ __device__ __forceinline__ RowStat warp_part(const LazyAcc<kQ, 4>& a, const T* r
   float mw = s.m;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mw = fmaxf(mw, __shfl_xor_sync(0xffffffffu, mw, o));
-  uint4 x[kVPT];
-  bool have[kVPT];
+  uint4 x[C::VPT];
+  bool have[C::VPT];
   const bool need = kQ && (a.m == mw) && (mw > -CUDART_INF_F) && (a.tag >= 0);
   const int c = a.tag;
   if (need) {
-    const int nvec = (c == nchunks - 1) ? nvec_last : kChunk / 16;
-    const uint4* cv = reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(row) + (size_t)c * kChunk);
+    const int nvec = (c == nchunks - 1) ? nvec_last : C::CHUNK / 16;
+    const uint4* cv =
+        reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(row) + (size_t)c * C::CHUNK);
 #pragma unroll
-    for (int j = 0; j < kVPT; ++j) {
-      const int v = tid + j * kCT;
+    for (int j = 0; j < C::VPT; ++j) {
+      const int v = tid + j * C::CT;
       have[j] = v < nvec;
       if (have[j]) x[j] = __ldg(cv + v);
     }
   }
-  // sums over the warp (fixed xor tree)
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    RowStat t = shfl_xor(s, o);
-    t.m = s.m;  // m / idx handled separately
-    s = combine(s, t);
-  }
+  for (int o = 16; o > 0; o >>= 1) s = combine(s, shfl_xor(s, o));
   s.m = mw;
   int cand = 0x7fffffff;
   if (need) {
 #pragma unroll
-    for (int j = kVPT - 1; j >= 0; --j) {
+    for (int j = C::VPT - 1; j >= 0; --j) {
       if (!have[j]) continue;
       float f[E];
       Vec<T>::unpack(x[j], f);
 #pragma unroll
       for (int e = E - 1; e >= 0; --e)
-        if (f[e] == mw) cand = c * (kChunk / (int)sizeof(T)) + (tid + j * kCT) * E + e;
+        if (f[e] == mw) cand = c * (C::CHUNK / (int)sizeof(T)) + (tid + j * C::CT) * E + e;
     }
   }
-  s.idx = kQ ? __reduce_min_sync(0xffffffffu, (unsigned)cand) : 0;
+  s.idx = kQ ? (int)__reduce_min_sync(0xffffffffu, (unsigned)cand) : 0;
   return s;
 }
 
+// Epilogue of one unit by one warp, with the token data already prefetched.
 template <typename T>
-__global__ void __launch_bounds__(kThreads, 1) k_rows_tma(RowsParams p) {
+__device__ __forceinline__ void warp_epilogue(const RowsParams& p, const Unit& un, const RowStat& ps,
+                                              const RowStat& qs, int x, float lpx, float lqx, float uu,
+                                              int64_t et) {
+  const Dims& d = p.d;
+  const int lane = threadIdx.x & 31;
+  const int b = un.b, slot = un.slot, i = un.i;
+  const SeqInfo& in = un.in;
+  const RowOut po = finish(ps), qo = finish(qs);
+  const bool branch_row = (slot == 0 && i == in.s);
+  const int ntok = branch_row ? d.K : 1;
+  if (lane < ntok) {
+    uint8_t fl = 0;
+    float pt = CUDART_NAN_F, qt = CUDART_NAN_F;
+    if (!(po.finite && qo.finite)) {
+      fl |= 4;
+    } else if (x < 0 || x >= d.V) {
+      fl |= 2;
+    } else {
+      const double Px = tok_prob(lpx, po.MS, po.Z);
+      const double Qx = tok_prob(lqx, qo.MS, qo.Z);
+      pt = (float)Px;
+      qt = (float)Qx;
+      // accept iff r <= p/q (P534, P538), as u*Q[x] <= P[x]; Q[x] = 0 accepts (S127)
+      if ((double)uu * Qx <= Px) fl |= 1;
+    }
+    p.p_tok[et] = pt;
+    p.q_tok[et] = qt;
+    p.pflag[et] = fl;
+  }
+  if (lane == 0) {
+    const int64_t e = ent(d, b, slot, i);
+    const double LN2 = 0.69314718055994530942;
+    p.lse_p[e] = po.finite ? (float)(((double)po.MS + log2((double)po.Z)) * LN2) : CUDART_NAN_F;
+    p.lse_q[e] = qo.finite ? (float)(((double)qo.MS + log2((double)qo.Z)) * LN2) : CUDART_NAN_F;
+    const bool conf_ok = po.finite && qo.finite;  // as the oracle: q stats iff both rows finite
+    if (p.top1_q) p.top1_q[e] = conf_ok ? (float)tok_prob(qs.m, qo.MS, qo.Z) : CUDART_NAN_F;
+    if (p.top1_id_q) p.top1_id_q[e] = conf_ok ? qs.idx : -1;
+    if (p.entropy_q) {
+      const double Z = qo.Z;
+      p.entropy_q[e] = conf_ok ? (float)(LN2 * (log2(Z) - (double)qs.s1 / Z)) : CUDART_NAN_F;
+    }
+    p.rowstat[e] = make_float4(po.MS, po.finite ? po.Z : CUDART_NAN_F, qo.MS,
+                               qo.finite ? qo.Z : CUDART_NAN_F);
+  }
+  __syncwarp();
+  int last = 0;
+  if (lane == 0) {
+    __threadfence();
+    const int units_b = __ldg(p.unit_off + b + 1) - __ldg(p.unit_off + b);
+    last = (atomicAdd(p.cnt + b, 1) == units_b - 1);
+  }
+  last = __shfl_sync(0xffffffffu, last, 0);
+  if (!last) return;
+  __threadfence();
+  // first rejection per branch: lane r holds row r's flags for every branch (loads
+  // issued back to back), then one ballot per branch
+  uint32_t fw[4] = {0u, 0u, 0u, 0u};  // 3 bits per branch, 10 branches per word
+  if (lane < in.L) {
+#pragma unroll 8
+    for (int k = 0; k < d.K; ++k) {
+      const uint32_t f = __ldcg(p.pflag + ent(d, b, (lane < in.s) ? 0 : k, lane));
+      fw[k / 10] |= (f & 7u) << (3 * (k % 10));
+    }
+  }
+  const uint32_t rowmask = in.L >= 32 ? 0xffffffffu : ((1u << in.L) - 1u);
+  uint32_t anyf = 0;
+  for (int k = 0; k < d.K; ++k) {
+    const uint32_t f = (fw[k / 10] >> (3 * (k % 10))) & 7u;
+    const uint32_t mask = __ballot_sync(0xffffffffu, f & 1u) & rowmask;
+    anyf |= f;
+    if (lane == 0) {
+      const uint32_t rej = ~mask & rowmask;
+      p.acc_mask[(int64_t)b * d.K + k] = mask;
+      p.n_acc[(int64_t)b * d.K + k] = rej ? (__ffs(rej) - 1) : in.L;
+    }
+  }
+  anyf = __reduce_or_sync(0xffffffffu, anyf);
+  // sentinels for entries no tested path touches
+  const int R1 = d.G + 1;
+  for (int q = lane; q < d.K * R1; q += 32) {
+    const int k = q / R1, r = q % R1;
+    const int64_t e = ent(d, b, k, r);
+    const bool phys = (k == 0) ? (r < in.L) : (r > in.s && r < in.L);
+    const bool path = (k == 0) ? (r < in.L) : (r >= in.s && r < in.L);
+    if (!phys) {
+      p.lse_p[e] = CUDART_NAN_F;
+      p.lse_q[e] = CUDART_NAN_F;
+      if (p.top1_q) p.top1_q[e] = CUDART_NAN_F;
+      if (p.top1_id_q) p.top1_id_q[e] = -1;
+      if (p.entropy_q) p.entropy_q[e] = CUDART_NAN_F;
+    }
+    if (!path) {
+      p.p_tok[e] = CUDART_NAN_F;
+      p.q_tok[e] = CUDART_NAN_F;
+    }
+  }
+  if (lane == 0) {
+    int st = in.st;
+    if (anyf & 2u) st |= SB_ST_BAD_TOKEN;
+    if (anyf & 4u) st |= SB_ST_NONFINITE;
+    p.status[b] = st;
+    p.cnt[b] = 0;  // leave the workspace re-usable
+  }
+}
+
+// One ring stage as this thread sees it: VPT 16-byte vectors of the p and q chunks.
+template <class C>
+struct StageRegs {
+  uint4 p[C::VPT], q[C::VPT];
+};
+
+template <typename T>
+__device__ __forceinline__ uint4 neg_inf_vec() {
+  return sizeof(T) == 2 ? make_uint4(0xff80ff80u, 0xff80ff80u, 0xff80ff80u, 0xff80ff80u)
+                        : make_uint4(0xff800000u, 0xff800000u, 0xff800000u, 0xff800000u);
+}
+
+template <class C, typename T>
+__device__ __forceinline__ void load_stage(const uint8_t* bp, const uint8_t* bq, int nvec, bool full,
+                                           StageRegs<C>& r) {
+  const int tid = threadIdx.x;
+#pragma unroll
+  for (int j = 0; j < C::VPT; ++j) {
+    const int v = tid + j * C::CT;
+    if (full || v < nvec) {
+      r.p[j] = lds128(bp + v * 16);
+      r.q[j] = lds128(bq + v * 16);
+    } else {
+      r.p[j] = r.q[j] = neg_inf_vec<T>();
+    }
+  }
+}
+
+template <class C, typename T>
+__device__ __forceinline__ void compute_stage(const StageRegs<C>& r, int c, LazyAcc<false, 4>& pa,
+                                              LazyAcc<true, 4>& qa) {
   constexpr int E = Vec<T>::E;
+  float fp[C::VPT * E], fq[C::VPT * E];
+#pragma unroll
+  for (int j = 0; j < C::VPT; ++j) {
+    Vec<T>::unpack(r.p[j], fp + j * E);
+    Vec<T>::unpack(r.q[j], fq + j * E);
+  }
+  pa.template add<C::VPT * E>(fp, c);
+  qa.template add<C::VPT * E>(fq, c);
+}
+
+template <class C, typename T>
+__global__ void __launch_bounds__(C::THREADS, 1) k_rows_tma(RowsParams p) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  RowsSmem& S = *reinterpret_cast<RowsSmem*>(smem_raw);
+  RowsSmem<C>& S = *reinterpret_cast<RowsSmem<C>*>(smem_raw);
   const Dims& d = p.d;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
-    for (int s = 0; s < kNS; ++s) {
+    for (int s = 0; s < C::NS; ++s) {
       mbar_init(&S.full[s], 1);
-      mbar_init(&S.empty[s], kCW);
+      mbar_init(&S.empty[s], C::CW);
     }
-    for (int s = 0; s < kNP; ++s) {
-      mbar_init(&S.pfull[s], kCW);
+    for (int s = 0; s < C::NP; ++s) {
+      mbar_init(&S.pfull[s], C::CW);
       mbar_init(&S.pempty[s], 1);
     }
     fence_mbar_init();
@@ -353,36 +501,53 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tma(RowsParams p) {
   const T* PL = static_cast<const T*>(p.PL);
   const T* QL = static_cast<const T*>(p.QL);
   const uint32_t row_bytes = (uint32_t)d.V * sizeof(T);
-  const int nchunks = (row_bytes + kChunk - 1) / kChunk;
-  const int nvec_last = (int)(row_bytes - (uint32_t)(nchunks - 1) * kChunk) / 16;
+  const int nchunks = (row_bytes + C::CHUNK - 1) / C::CHUNK;
+  const int nvec_last = (int)(row_bytes - (uint32_t)(nchunks - 1) * C::CHUNK) / 16;
 
-  if (warp == kCW) {  // ---------------- producer
+  if (warp == C::CW) {  // ---------------- producer
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
-      RingPos<kNS> rp;
+      RingPos<C::NS> rp;
       for (int unit = blockIdx.x; unit < total; unit += gridDim.x) {
         const Unit un = decode_unit(p, unit);
         const char* prow = reinterpret_cast<const char*>(PL + row_off(d, un.b, un.slot, un.i));
         const char* qrow = reinterpret_cast<const char*>(QL + row_off(d, un.b, un.slot, un.i));
         for (int c = 0; c < nchunks; ++c) {
-          const uint32_t bytes = min((uint32_t)kChunk, row_bytes - (uint32_t)c * kChunk);
+          const uint32_t bytes = min((uint32_t)C::CHUNK, row_bytes - (uint32_t)c * C::CHUNK);
           mbar_wait(&S.empty[rp.stage], rp.phase ^ 1u);
           mbar_expect_tx(&S.full[rp.stage], 2 * bytes);
-          bulk_g2s(S.buf[rp.stage][0], prow + (size_t)c * kChunk, bytes, &S.full[rp.stage], pol);
-          bulk_g2s(S.buf[rp.stage][1], qrow + (size_t)c * kChunk, bytes, &S.full[rp.stage], pol);
+          bulk_g2s(S.buf[rp.stage][0], prow + (size_t)c * C::CHUNK, bytes, &S.full[rp.stage], pol);
+          bulk_g2s(S.buf[rp.stage][1], qrow + (size_t)c * C::CHUNK, bytes, &S.full[rp.stage], pol);
           rp.advance();
         }
       }
     }
     return;
   }
-  if (warp == kCW + 1) {  // ---------------- epilogue
-    RingPos<kNP> up;
+  if (warp == C::CW + 1) {  // ---------------- epilogue
+    RingPos<C::NP> up;
     for (int unit = blockIdx.x; unit < total; unit += gridDim.x) {
       const Unit un = decode_unit(p, unit);
+      const T* prow = PL + row_off(d, un.b, un.slot, un.i);
+      const T* qrow = QL + row_off(d, un.b, un.slot, un.i);
+      // prefetch the path tokens through this row, their uniforms and logits
+      const bool branch_row = (un.slot == 0 && un.i == un.in.s);
+      const int ntok = branch_row ? d.K : 1;
+      int x = 0;
+      float lpx = 0.f, lqx = 0.f, uu = 0.f;
+      int64_t et = 0;
+      if (lane < ntok) {
+        et = ent(d, un.b, branch_row ? lane : un.slot, un.i);
+        x = __ldg(p.tok + et);
+        uu = __ldg(p.u + et);
+        if (x >= 0 && x < d.V) {
+          lpx = ld_scalar(prow + x);
+          lqx = ld_scalar(qrow + x);
+        }
+      }
       mbar_wait(&S.pfull[up.stage], up.phase);
-      RowStat ps = lane < kCW ? S.part[up.stage][0][lane] : rowstat_empty();
-      RowStat qs = lane < kCW ? S.part[up.stage][1][lane] : rowstat_empty();
+      RowStat ps = lane < C::CW ? S.part[up.stage][0][lane] : rowstat_empty();
+      RowStat qs = lane < C::CW ? S.part[up.stage][1][lane] : rowstat_empty();
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.pempty[up.stage]);
       up.advance();
@@ -391,70 +556,33 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tma(RowsParams p) {
         ps = combine(ps, shfl_xor(ps, o));
         qs = combine(qs, shfl_xor(qs, o));
       }
-      const T* prow = PL + row_off(d, un.b, un.slot, un.i);
-      const T* qrow = QL + row_off(d, un.b, un.slot, un.i);
-      unit_epilogue(p, un, prow, qrow, ps, qs, lane, 32, &S.s_last, &S.s_st, [] { __syncwarp(); });
+      warp_epilogue<T>(p, un, ps, qs, x, lpx, lqx, uu, et);
     }
     return;
   }
   // ---------------- consumers
-  RingPos<kNS> rp;
-  RingPos<kNP> up;
+  RingPos<C::NS> rp;
+  RingPos<C::NP> up;
   for (int unit = blockIdx.x; unit < total; unit += gridDim.x) {
     LazyAcc<false, 4> pa;
     LazyAcc<true, 4> qa;
     pa.init();
     qa.init();
-    // full chunks: every lane owns kVPT whole vectors, no guards
-    for (int c = 0; c < nchunks - 1; ++c) {
+    // wait -> 16-byte LDS of this thread's vectors -> release the stage -> math, so the
+    // producer refills the slot while the consumers compute
+    for (int c = 0; c < nchunks; ++c) {
+      StageRegs<C> r;
       mbar_wait(&S.full[rp.stage], rp.phase);
-      const uint8_t* bp = S.buf[rp.stage][0];
-      const uint8_t* bq = S.buf[rp.stage][1];
-      uint4 xp[kVPT], xq[kVPT];
-#pragma unroll
-      for (int j = 0; j < kVPT; ++j) {
-        xp[j] = lds128(bp + (tid + j * kCT) * 16);
-        xq[j] = lds128(bq + (tid + j * kCT) * 16);
-      }
+      load_stage<C, T>(S.buf[rp.stage][0], S.buf[rp.stage][1], nvec_last, c + 1 < nchunks, r);
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.empty[rp.stage]);
       rp.advance();
-      float fp[kVPT * E], fq[kVPT * E];
-#pragma unroll
-      for (int j = 0; j < kVPT; ++j) {
-        Vec<T>::unpack(xp[j], fp + j * E);
-        Vec<T>::unpack(xq[j], fq + j * E);
-      }
-      pa.template add<kVPT * E>(fp, c);
-      qa.template add<kVPT * E>(fq, c);
-    }
-    {  // last (possibly partial) chunk
-      const int c = nchunks - 1;
-      mbar_wait(&S.full[rp.stage], rp.phase);
-      const uint8_t* bp = S.buf[rp.stage][0];
-      const uint8_t* bq = S.buf[rp.stage][1];
-      float fp[kVPT * E], fq[kVPT * E];
-#pragma unroll
-      for (int j = 0; j < kVPT; ++j) {
-        const int v = tid + j * kCT;
-        if (v < nvec_last) {
-          Vec<T>::unpack(lds128(bp + v * 16), fp + j * E);
-          Vec<T>::unpack(lds128(bq + v * 16), fq + j * E);
-        } else {
-#pragma unroll
-          for (int e = 0; e < E; ++e) fp[j * E + e] = fq[j * E + e] = -CUDART_INF_F;
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&S.empty[rp.stage]);
-      rp.advance();
-      pa.template add<kVPT * E>(fp, c);
-      qa.template add<kVPT * E>(fq, c);
+      compute_stage<C, T>(r, c, pa, qa);
     }
     const Unit un = decode_unit(p, unit);
     const T* qrow = QL + row_off(d, un.b, un.slot, un.i);
-    const RowStat ps = warp_part<T, false>(pa, qrow, nvec_last, nchunks);
-    const RowStat qs = warp_part<T, true>(qa, qrow, nvec_last, nchunks);
+    const RowStat ps = warp_part<C, T, false>(pa, qrow, nvec_last, nchunks);
+    const RowStat qs = warp_part<C, T, true>(qa, qrow, nvec_last, nchunks);
     if (lane == 0) {
       mbar_wait(&S.pempty[up.stage], up.phase ^ 1u);
       S.part[up.stage][0][warp] = ps;
@@ -466,26 +594,25 @@ __global__ void __launch_bounds__(kThreads, 1) k_rows_tma(RowsParams p) {
   }
 }
 
-template <typename T>
+template <class C, typename T>
 static sb_status launch_rows_tma(const RowsParams& p, cudaStream_t s) {
   static bool attr = false;
-  const int smem = (int)sizeof(RowsSmem);
+  const int smem = (int)sizeof(RowsSmem<C>);
   if (!attr) {
-    if (cudaFuncSetAttribute(k_rows_tma<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+    if (cudaFuncSetAttribute(k_rows_tma<C, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
         cudaSuccess)
       return SB_ERR_CUDA;
     attr = true;
   }
   const int64_t max_units = (int64_t)p.d.B * p.d.K * (p.d.G + 1);
   const int grid = (int)std::min<int64_t>(num_sms(), max_units);
-  k_rows_tma<T><<<grid, kThreads, smem, s>>>(p);
+  k_rows_tma<C, T><<<grid, C::THREADS, smem, s>>>(p);
   return cuda_status(cudaGetLastError());
 }
 
 template <typename T, int NT, int U>
 static sb_status launch_rows(const RowsParams& p, bool vok, cudaStream_t s) {
-  static int grid_cache[2] = {0, 0};
-  int& g = grid_cache[std::is_same<T, float>::value ? 1 : 0];
+  static int g = 0;
   if (g == 0) {
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_rows<T, NT, U>, NT, 0);
@@ -495,6 +622,26 @@ static sb_status launch_rows(const RowsParams& p, bool vok, cudaStream_t s) {
   const int grid = (int)std::min<int64_t>(g, max_units);
   k_rows<T, NT, U><<<grid, NT, 0, s>>>(p, vok);
   return cuda_status(cudaGetLastError());
+}
+
+// Geometry variants (SB_ROWS_VARIANT selects one for experiments; 0 = default).
+using RC0 = RC<16, 6, 2, 4>;   // 16 consumer warps, 6 x 32 KB stages
+using RC1 = RC<16, 3, 4, 4>;   // 16 warps, 3 x 64 KB stages, 4 vectors/thread/row
+using RC2 = RC<24, 4, 2, 4>;   // 24 warps, 4 x 48 KB stages
+using RC3 = RC<8, 6, 4, 4>;    // 8 warps, 6 x 32 KB stages, 4 vectors/thread/row
+using RC4 = RC<12, 4, 2, 4>;   // 12 warps, 4 x 24 KB stages... (2 CTAs/SM would need <= 113 KB)
+
+template <typename T>
+static sb_status launch_rows_variant(const RowsParams& p, cudaStream_t s) {
+  const char* e = getenv("SB_ROWS_VARIANT");
+  const int v = e ? atoi(e) : 0;
+  switch (v) {
+    case 1: return launch_rows_tma<RC1, T>(p, s);
+    case 2: return launch_rows_tma<RC2, T>(p, s);
+    case 3: return launch_rows_tma<RC3, T>(p, s);
+    case 4: return launch_rows_tma<RC4, T>(p, s);
+    default: return launch_rows_tma<RC0, T>(p, s);
+  }
 }
 
 }  // namespace sb
@@ -532,7 +679,7 @@ extern "C" sb_status sb_verify_branches(const sb_dims* dd, const void* p_logits,
   const bool vok = vec_ok(dd, p_logits) && vec_ok(dd, q_logits);
   const size_t row_bytes = (size_t)dd->V * elem_size(dd);
   if (vok && row_bytes % 16 == 0 && !tma_disabled())
-    return dd->dtype == SB_BF16 ? launch_rows_tma<__nv_bfloat16>(p, s) : launch_rows_tma<float>(p, s);
+    return dd->dtype == SB_BF16 ? launch_rows_variant<__nv_bfloat16>(p, s) : launch_rows_variant<float>(p, s);
   if (dd->dtype == SB_BF16) {
     return row_bytes <= 131072 ? launch_rows<__nv_bfloat16, 128, 4>(p, vok, s)
                                : launch_rows<__nv_bfloat16, 256, 4>(p, vok, s);

@@ -11,6 +11,8 @@ for w in $WHAT; do
   case $w in
     tests) timeout 900 python -m pytest tests -m "gpu and not slow" -q -x 2>&1 | tail -30 > gpurun_out/${TAG}_tests.log ;;
     slow) timeout 1200 python -m pytest tests -m "gpu and slow" -q -x -s 2>&1 | tail -40 > gpurun_out/${TAG}_slow.log ;;
+    readbw) ./scripts/readbw > gpurun_out/${TAG}_readbw.log 2>&1 ;;
+    ref) timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/${TAG}_ref.log 2>&1 ;;
     smoke) timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TAG}_smoke.log 2>&1 ;;
     bench) timeout 900 python bench.py --config c4 --steps 10 > gpurun_out/${TAG}_bench_c4.log 2>&1
            for c in c1 c2 c3 c5; do timeout 600 python bench.py --config $c --steps 20 --no-e2e --no-cpu-baseline > gpurun_out/${TAG}_bench_$c.log 2>&1; done ;;
