@@ -57,7 +57,7 @@ typedef enum {
   SB_ERR_INVALID_ARG = 1, /* bad dims, null required pointer, misaligned workspace   */
   SB_ERR_UNSUPPORTED = 2, /* valid request this build does not implement            */
   SB_ERR_CUDA = 3,        /* a CUDA launch or runtime call failed                   */
-  SB_ERR_NCCL = 4,        /* reserved for the vocabulary-sharded exchange           */
+  SB_ERR_NCCL = 4,        /* an NCCL call of the vocabulary-sharded exchange failed */
   SB_ERR_WORKSPACE = 5    /* workspace_bytes < sb_workspace_bytes(d)                */
 } sb_status;
 
@@ -78,7 +78,7 @@ typedef struct {
   int32_t G;          /* gamma_max, 0..31 (rows per slot = G+1)                       */
   int32_t V;          /* vocabulary columns, >= 2                                     */
   int32_t v_offset;   /* vocabulary shard offset; unsharded: 0                        */
-  int32_t v_total;    /* full vocabulary; unsharded: V                                */
+  int32_t v_total;    /* full vocabulary (token ids are global); unsharded: V or 0    */
   int64_t row_stride; /* elements between rows, >= V                                  */
   int64_t seq_stride; /* elements between sequences; 0 -> K*(G+1)*row_stride         */
   int32_t dtype;      /* sb_dtype of the logits                                       */
@@ -114,8 +114,13 @@ size_t sb_workspace_bytes(const sb_dims* d);
  *          acc_mask            [B][K] uint32, bit i = acc(k,i) for i < L_b;
  *          n_acc               [B][K] accepted prefix lengths;
  *          status              [B] SB_ST_* bits (overwritten).
- * comm must be NULL (vocabulary sharding: see DESIGN.md; SB_ERR_UNSUPPORTED otherwise).
+ * comm: NULL for an unsharded call; a communicator from sb_comm_create for a vocabulary
+ * shard (d->v_offset / d->v_total describe this rank's slice): the library then runs
+ * sb_shard_verify_local, an NCCL all-gather of the partials and sb_shard_verify_combine
+ * on `stream` (a7).  Sharded dims without a communicator are SB_ERR_INVALID_ARG.
  */
+typedef struct sb_comm sb_comm; /* opaque NCCL communicator of the vocabulary-shard ranks */
+
 sb_status sb_verify_branches(const sb_dims* d, const void* p_logits, const void* q_logits,
                              const int32_t* tok, const float* u, const int32_t* gamma,
                              const int32_t* branch_pos, float* lse_p, float* lse_q,
@@ -154,6 +159,8 @@ sb_status sb_verify_branches(const sb_dims* d, const void* p_logits, const void*
  *          P734); keep_mask [B][K] bit i of slot k set iff the draft token at (k,i) is
  *          committed (the KV rows to keep, P241); resid_mass [B] nullable, the mass R of
  *          the sampled vector (1 for a bonus, 0 for none); status [B] (bits OR-ed in).
+ * comm: as for sb_verify_branches (sharded: local masses, NCCL all-gather, owner
+ * sample, NCCL all-reduce MAX of the token, commit).
  */
 sb_status sb_select_branch(const sb_dims* d, const void* p_logits, const void* q_logits,
                            const int32_t* tok, const float* u, const float* us,
@@ -186,6 +193,65 @@ sb_status sb_draft_confidence(const sb_dims* d, const void* q_logits, const int3
                               float* tok_prob, float* stat, int32_t* stop, int32_t* k_next,
                               int32_t* gamma_next, void* comm, void* workspace,
                               size_t workspace_bytes, sb_stream_t stream);
+
+/*
+ * ---- Vocabulary-sharded variant (a7) ----------------------
+ * Rank g of G holds the contiguous slice [v_offset, v_offset + V) of the v_total-token
+ * vocabulary; slices are in rank order (so global ascending-id order = rank order).
+ * tok (global ids), u, us, gamma, branch_pos are identical on every rank.  All outputs
+ * are identical on every rank (decisions are replicated after each exchange).  The
+ * split-phase calls let a caller run the three exchanges itself (tests use an
+ * in-process loopback); sb_comm_* + the comm argument above run them with NCCL.
+ *
+ *   1. sb_shard_verify_local   -> partial (sb_shard_partial_bytes bytes, device)
+ *      exchange: all-gather the G partials, rank-major, contiguous
+ *   2. sb_shard_verify_combine -> the sb_verify_branches outputs
+ *   3. sb_shard_select_local   -> mass [B][2] fp64 (this shard's residual and p mass)
+ *      exchange: all-gather the G mass arrays, rank-major -> gathered_mass [G][B][2]
+ *   4. sb_shard_select_sample  -> ycand [B] (the sampled global id on the owner, -1 else)
+ *      exchange: all-reduce MAX of ycand -> y
+ *   5. sb_shard_select_commit  -> the sb_select_branch outputs
+ * The same workspace (sized by sb_workspace_bytes of the shard dims) must be used by
+ * all five calls of one round.  In sharded mode the verify phase also reads every
+ * branch's bonus row (statistics only) so that the sample needs no extra exchange.
+ */
+size_t sb_shard_partial_bytes(const sb_dims* d);
+sb_status sb_shard_verify_local(const sb_dims* d, const void* p_logits, const void* q_logits,
+                                const int32_t* tok, const float* u, const int32_t* gamma,
+                                const int32_t* branch_pos, void* partial, void* workspace,
+                                size_t workspace_bytes, sb_stream_t stream);
+sb_status sb_shard_verify_combine(const sb_dims* d, const void* gathered, int32_t nranks,
+                                  const int32_t* tok, const float* u, float* lse_p, float* lse_q,
+                                  float* p_tok, float* q_tok, uint32_t* acc_mask, int32_t* n_acc,
+                                  float* top1_q, int32_t* top1_id_q, float* entropy_q,
+                                  int32_t* status, void* workspace, size_t workspace_bytes,
+                                  sb_stream_t stream);
+sb_status sb_shard_select_local(const sb_dims* d, const void* p_logits, const void* q_logits,
+                                const int32_t* tok, const float* u, const int32_t* n_acc,
+                                sb_select_rule rule, double* mass, void* workspace,
+                                size_t workspace_bytes, sb_stream_t stream);
+sb_status sb_shard_select_sample(const sb_dims* d, const double* gathered_mass, int32_t nranks,
+                                 int32_t rank, const void* p_logits, const void* q_logits,
+                                 const float* us, int32_t* ycand, void* workspace,
+                                 size_t workspace_bytes, sb_stream_t stream);
+sb_status sb_shard_select_commit(const sb_dims* d, const int32_t* y, const int32_t* tok,
+                                 int32_t* sel_k, int32_t* commit_len, int32_t* out_tok,
+                                 int32_t* y_tok, int32_t* y_kind, int32_t* offsets,
+                                 int32_t* packed_tok, int32_t* path_rolled,
+                                 int32_t* branch_discarded, uint32_t* keep_mask,
+                                 float* resid_mass, int32_t* status, void* workspace,
+                                 size_t workspace_bytes, sb_stream_t stream);
+
+/* NCCL communicator of the G shard ranks (one process per GPU).  Rank 0 creates the
+ * unique id (sb_comm_unique_id, sb_comm_unique_id_bytes() bytes, host memory) and the
+ * caller broadcasts it (e.g. with torch.distributed); every rank then calls
+ * sb_comm_create with the largest dims it will use (scratch is allocated here, never
+ * on the hot path).  sb_comm_destroy frees it. */
+size_t sb_comm_unique_id_bytes(void);
+sb_status sb_comm_unique_id(void* unique_id_out);
+sb_status sb_comm_create(const void* unique_id, int32_t nranks, int32_t rank,
+                         const sb_dims* max_dims, sb_comm** out);
+sb_status sb_comm_destroy(sb_comm* comm);
 
 #ifdef __cplusplus
 }

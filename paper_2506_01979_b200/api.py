@@ -68,21 +68,21 @@ LOG = (torch.bfloat16, torch.float32)
 
 def sb_verify_branches(d, p_logits, q_logits, tok, u, gamma, branch_pos, lse_p, lse_q, p_tok,
                        q_tok, acc_mask, n_acc, top1_q, top1_id_q, entropy_q, status, workspace,
-                       stream=None):
+                       stream=None, comm=None):
     rc = L.lib().sb_verify_branches(
         ctypes.byref(d), _ptr(p_logits, LOG, "p_logits"), _ptr(q_logits, LOG, "q_logits"),
         _ptr(tok, I32, "tok"), _ptr(u, F32, "u"), _ptr(gamma, I32, "gamma"),
         _ptr(branch_pos, I32, "branch_pos"), _ptr(lse_p, F32, "lse_p"), _ptr(lse_q, F32, "lse_q"),
         _ptr(p_tok, F32, "p_tok"), _ptr(q_tok, F32, "q_tok"), _ptr(acc_mask, I32, "acc_mask"),
         _ptr(n_acc, I32, "n_acc"), _ptr(top1_q, F32, "top1_q"), _ptr(top1_id_q, I32, "top1_id_q"),
-        _ptr(entropy_q, F32, "entropy_q"), _ptr(status, I32, "status"), None,
+        _ptr(entropy_q, F32, "entropy_q"), _ptr(status, I32, "status"), comm.handle if comm else None,
         _ptr(workspace, torch.uint8, "workspace"), workspace.numel(), _stream(stream))
     L.check(rc, "sb_verify_branches")
 
 
 def sb_select_branch(d, p_logits, q_logits, tok, u, us, gamma, branch_pos, n_acc, rule, sel_k,
                      commit_len, out_tok, y_tok, y_kind, offsets, packed_tok, path_rolled,
-                     branch_discarded, keep_mask, resid_mass, status, workspace, stream=None):
+                     branch_discarded, keep_mask, resid_mass, status, workspace, stream=None, comm=None):
     rc = L.lib().sb_select_branch(
         ctypes.byref(d), _ptr(p_logits, LOG, "p_logits"), _ptr(q_logits, LOG, "q_logits"),
         _ptr(tok, I32, "tok"), _ptr(u, F32, "u"), _ptr(us, F32, "us"), _ptr(gamma, I32, "gamma"),
@@ -91,7 +91,7 @@ def sb_select_branch(d, p_logits, q_logits, tok, u, us, gamma, branch_pos, n_acc
         _ptr(y_tok, I32, "y_tok"), _ptr(y_kind, I32, "y_kind"), _ptr(offsets, I32, "offsets"),
         _ptr(packed_tok, I32, "packed_tok"), _ptr(path_rolled, I32, "path_rolled"),
         _ptr(branch_discarded, I32, "branch_discarded"), _ptr(keep_mask, I32, "keep_mask"),
-        _ptr(resid_mass, F32, "resid_mass"), _ptr(status, I32, "status"), None,
+        _ptr(resid_mass, F32, "resid_mass"), _ptr(status, I32, "status"), comm.handle if comm else None,
         _ptr(workspace, torch.uint8, "workspace"), workspace.numel(), _stream(stream))
     L.check(rc, "sb_select_branch")
 
@@ -172,7 +172,8 @@ def conf_dims(d: L.sb_dims) -> L.sb_dims:
 
 
 def verify_step(d: L.sb_dims, inp: dict, buf: StepBuffers, rule: int = SB_SELECT_EQ9,
-                adaptive: bool = False, eps: float = 0.2, k_max: int = 6, stream=None):
+                adaptive: bool = False, eps: float = 0.2, k_max: int = 6, stream=None, comm=None,
+                views=None):
     """One whole hot-path step: [draft confidence -> adaptive gamma] -> verify -> select.
 
     inp: PL, QL, tok, u, us, gamma, branch_pos device tensors (synth.generate layout).
@@ -185,14 +186,15 @@ def verify_step(d: L.sb_dims, inp: dict, buf: StepBuffers, rule: int = SB_SELECT
                             buf.c_top1, buf.c_id, buf.c_ent, None, buf.c_stat, buf.c_stop,
                             buf.c_knext, buf.c_gamma, buf.conf_workspace, stream)
         gamma = buf.c_gamma.view(-1)
-    sb_verify_branches(d, inp["PL"], inp["QL"], inp["tok"], inp["u"], gamma, inp["branch_pos"],
+    PL, QL = views if views is not None else (inp["PL"], inp["QL"])
+    sb_verify_branches(d, PL, QL, inp["tok"], inp["u"], gamma, inp["branch_pos"],
                        buf.lse_p, buf.lse_q, buf.p_tok, buf.q_tok, buf.acc_mask, buf.n_acc,
-                       buf.top1_q, buf.top1_id_q, buf.entropy_q, buf.status, buf.workspace, stream)
-    sb_select_branch(d, inp["PL"], inp["QL"], inp["tok"], inp["u"], inp["us"], gamma,
+                       buf.top1_q, buf.top1_id_q, buf.entropy_q, buf.status, buf.workspace, stream, comm)
+    sb_select_branch(d, PL, QL, inp["tok"], inp["u"], inp["us"], gamma,
                      inp["branch_pos"], buf.n_acc, rule, buf.sel_k, buf.commit_len, buf.out_tok,
                      buf.y_tok, buf.y_kind, buf.offsets, buf.packed_tok, buf.path_rolled,
                      buf.branch_discarded, buf.keep_mask, buf.resid_mass, buf.status,
-                     buf.workspace, stream)
+                     buf.workspace, stream, comm)
     return gamma
 
 
@@ -223,3 +225,128 @@ class StepGraph(CallGraph):
                  adaptive: bool = False, eps: float = 0.2, k_max: int = 6):
         super().__init__(lambda s: verify_step(d, inp, buf, rule, adaptive, eps, k_max, s))
         self.gamma = self.result
+
+
+# ------------------------------------------------------------------ vocabulary shards (a7)
+def shard_bounds(V_total: int, nranks: int, align: int = 8):
+    """Contiguous slices in rank order; every slice starts on a 16-byte boundary."""
+    per = -(-V_total // nranks)
+    per = -(-per // align) * align
+    out, v0 = [], 0
+    for _ in range(nranks):
+        n = max(0, min(per, V_total - v0))
+        out.append((v0, n))
+        v0 += n
+    return out
+
+
+def shard_view(logits: torch.Tensor, V_total: int, v0: int, n: int):
+    """(sb_dims, view) of columns [v0, v0+n) of a full [B][K][G+1][row_stride] tensor;
+    the view shares memory (row_stride of the full tensor, pointer offset v0)."""
+    d = dims_for(logits, V=V_total)
+    dd = L.sb_dims(d.B, d.K, d.G, n, v0, V_total, d.row_stride, d.seq_stride, d.dtype, 0)
+    return dd, logits[..., v0:v0 + n]
+
+
+def sb_shard_partial_bytes(d) -> int:
+    return int(L.lib().sb_shard_partial_bytes(ctypes.byref(d)))
+
+
+def sb_shard_verify_local(d, p_view, q_view, tok, u, gamma, branch_pos, partial, workspace, stream=None):
+    L.check(L.lib().sb_shard_verify_local(
+        ctypes.byref(d), _ptr(p_view, LOG, "p_logits"), _ptr(q_view, LOG, "q_logits"), _ptr(tok, I32, "tok"),
+        _ptr(u, F32, "u"), _ptr(gamma, I32, "gamma"), _ptr(branch_pos, I32, "branch_pos"),
+        _ptr(partial, torch.uint8, "partial"), _ptr(workspace, torch.uint8, "workspace"), workspace.numel(),
+        _stream(stream)), "sb_shard_verify_local")
+
+
+def sb_shard_verify_combine(d, gathered, nranks, tok, u, buf: "StepBuffers", stream=None):
+    L.check(L.lib().sb_shard_verify_combine(
+        ctypes.byref(d), _ptr(gathered, torch.uint8, "gathered"), int(nranks), _ptr(tok, I32, "tok"),
+        _ptr(u, F32, "u"), _ptr(buf.lse_p, F32, "lse_p"), _ptr(buf.lse_q, F32, "lse_q"),
+        _ptr(buf.p_tok, F32, "p_tok"), _ptr(buf.q_tok, F32, "q_tok"), _ptr(buf.acc_mask, I32, "acc_mask"),
+        _ptr(buf.n_acc, I32, "n_acc"), _ptr(buf.top1_q, F32, "top1_q"), _ptr(buf.top1_id_q, I32, "top1_id_q"),
+        _ptr(buf.entropy_q, F32, "entropy_q"), _ptr(buf.status, I32, "status"),
+        _ptr(buf.workspace, torch.uint8, "workspace"), buf.workspace.numel(), _stream(stream)),
+        "sb_shard_verify_combine")
+
+
+def sb_shard_select_local(d, p_view, q_view, tok, u, n_acc, rule, mass, workspace, stream=None):
+    L.check(L.lib().sb_shard_select_local(
+        ctypes.byref(d), _ptr(p_view, LOG, "p_logits"), _ptr(q_view, LOG, "q_logits"), _ptr(tok, I32, "tok"),
+        _ptr(u, F32, "u"), _ptr(n_acc, I32, "n_acc"), int(rule), _ptr(mass, torch.float64, "mass"),
+        _ptr(workspace, torch.uint8, "workspace"), workspace.numel(), _stream(stream)), "sb_shard_select_local")
+
+
+def sb_shard_select_sample(d, gathered_mass, nranks, rank, p_view, q_view, us, ycand, workspace, stream=None):
+    L.check(L.lib().sb_shard_select_sample(
+        ctypes.byref(d), _ptr(gathered_mass, torch.float64, "gathered_mass"), int(nranks), int(rank),
+        _ptr(p_view, LOG, "p_logits"), _ptr(q_view, LOG, "q_logits"), _ptr(us, F32, "us"),
+        _ptr(ycand, I32, "ycand"), _ptr(workspace, torch.uint8, "workspace"), workspace.numel(),
+        _stream(stream)), "sb_shard_select_sample")
+
+
+def sb_shard_select_commit(d, y, tok, buf: "StepBuffers", stream=None):
+    L.check(L.lib().sb_shard_select_commit(
+        ctypes.byref(d), _ptr(y, I32, "y"), _ptr(tok, I32, "tok"), _ptr(buf.sel_k, I32, "sel_k"),
+        _ptr(buf.commit_len, I32, "commit_len"), _ptr(buf.out_tok, I32, "out_tok"), _ptr(buf.y_tok, I32, "y_tok"),
+        _ptr(buf.y_kind, I32, "y_kind"), _ptr(buf.offsets, I32, "offsets"), _ptr(buf.packed_tok, I32, "packed_tok"),
+        _ptr(buf.path_rolled, I32, "path_rolled"), _ptr(buf.branch_discarded, I32, "branch_discarded"),
+        _ptr(buf.keep_mask, I32, "keep_mask"), _ptr(buf.resid_mass, F32, "resid_mass"),
+        _ptr(buf.status, I32, "status"), _ptr(buf.workspace, torch.uint8, "workspace"), buf.workspace.numel(),
+        _stream(stream)), "sb_shard_select_commit")
+
+
+def sharded_step_loopback(inp: dict, nranks: int, rule: int = SB_SELECT_EQ9):
+    """G vocabulary shards emulated in one process on one device: the split-phase C-ABI
+    calls of every rank with the three exchanges done as device concatenations / max.
+    Returns one StepBuffers per rank (all ranks' outputs must be identical)."""
+    PL, QL, V = inp["PL"], inp["QL"], inp["V"]
+    ranks = []
+    for r, (v0, n) in enumerate(shard_bounds(V, nranks)):
+        d, pv = shard_view(PL, V, v0, n)
+        _, qv = shard_view(QL, V, v0, n)
+        buf = StepBuffers.alloc(d, PL.device)
+        part = torch.empty(sb_shard_partial_bytes(d), dtype=torch.uint8, device=PL.device)
+        ranks.append((d, pv, qv, buf, part))
+    for d, pv, qv, buf, part in ranks:
+        sb_shard_verify_local(d, pv, qv, inp["tok"], inp["u"], inp["gamma"], inp["branch_pos"], part, buf.workspace)
+    gathered = torch.cat([r[4] for r in ranks])  # exchange 1 (all-gather)
+    for d, pv, qv, buf, part in ranks:
+        sb_shard_verify_combine(d, gathered, nranks, inp["tok"], inp["u"], buf)
+    masses = []
+    for d, pv, qv, buf, part in ranks:
+        m = torch.empty((d.B, 2), dtype=torch.float64, device=PL.device)
+        sb_shard_select_local(d, pv, qv, inp["tok"], inp["u"], buf.n_acc, rule, m, buf.workspace)
+        masses.append(m)
+    gmass = torch.cat(masses)  # exchange 2 (all-gather)
+    cands = []
+    for r, (d, pv, qv, buf, part) in enumerate(ranks):
+        yc = torch.empty(d.B, dtype=torch.int32, device=PL.device)
+        sb_shard_select_sample(d, gmass, nranks, r, pv, qv, inp["us"], yc, buf.workspace)
+        cands.append(yc)
+    y = torch.stack(cands).max(dim=0).values.contiguous()  # exchange 3 (all-reduce max)
+    for d, pv, qv, buf, part in ranks:
+        sb_shard_select_commit(d, y, inp["tok"], buf)
+    return [r[3] for r in ranks]
+
+
+class Comm:
+    """NCCL communicator of the vocabulary-shard ranks (sb_comm_*).  The unique id is
+    created on rank 0 and broadcast with torch.distributed (plumbing)."""
+
+    def __init__(self, nranks: int, rank: int, max_dims: L.sb_dims, unique_id: bytes | None = None):
+        n = int(L.lib().sb_comm_unique_id_bytes())
+        if unique_id is None:
+            buf = ctypes.create_string_buffer(n)
+            L.check(L.lib().sb_comm_unique_id(buf), "sb_comm_unique_id")
+            unique_id = buf.raw
+        self.unique_id = unique_id
+        self.handle = ctypes.c_void_p()
+        L.check(L.lib().sb_comm_create(ctypes.create_string_buffer(unique_id, n), int(nranks), int(rank),
+                                       ctypes.byref(max_dims), ctypes.byref(self.handle)), "sb_comm_create")
+
+    def close(self):
+        if self.handle:
+            L.check(L.lib().sb_comm_destroy(self.handle), "sb_comm_destroy")
+            self.handle = ctypes.c_void_p()

@@ -15,6 +15,18 @@ SO = os.path.join(HERE, "libspecbranch.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
+def nccl_dir() -> str:
+    """NCCL shipped with the venv's torch (nvidia/nccl: nccl.h + libnccl.so.2)."""
+    import importlib.util
+
+    spec = importlib.util.find_spec("nvidia")
+    for base in (spec.submodule_search_locations if spec else []):
+        d = os.path.join(base, "nccl")
+        if os.path.exists(os.path.join(d, "include", "nccl.h")):
+            return d
+    raise RuntimeError("NCCL headers not found (expected site-packages/nvidia/nccl)")
+
+
 def sources():
     return sorted(glob.glob(os.path.join(HERE, "csrc", "*.cu")))
 
@@ -35,8 +47,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return SO
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+    nccl = nccl_dir()
     cmd = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-shared",
-           "-I", os.path.join(ROOT, "include"), "-o", SO + ".tmp", *sources()]
+           "-I", os.path.join(ROOT, "include"), "-I", os.path.join(nccl, "include"),
+           "-o", SO + ".tmp", *sources(), "-L", os.path.join(nccl, "lib"), "-l:libnccl.so.2",
+           "-Xlinker", "-rpath=" + os.path.join(nccl, "lib")]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     subprocess.check_call(cmd)

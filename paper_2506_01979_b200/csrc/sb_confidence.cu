@@ -331,7 +331,7 @@ extern "C" sb_status sb_draft_confidence(const sb_dims* dd, const void* q_logits
     return SB_ERR_INVALID_ARG;
   if (mode == SB_CONF_TOKEN && !tok) return SB_ERR_INVALID_ARG;
   if (!(eps > 0.f && eps < 1.f) || !(lambda > 0.f) || k_max < 1) return SB_ERR_INVALID_ARG;
-  if (comm) return SB_ERR_UNSUPPORTED;
+  if (comm || sharded(dd)) return SB_ERR_UNSUPPORTED;  // draft rows are not vocabulary-sharded
   if ((uintptr_t)workspace % 256) return SB_ERR_INVALID_ARG;
   const Workspace w = carve(*dd, workspace);
   if (workspace_bytes < w.bytes) return SB_ERR_WORKSPACE;

@@ -11,6 +11,15 @@ namespace sb {
 
 struct SeqInfo {
   int g, s, L, st;  // clamped gamma_b, branch row s_b, path length L_b, clamp bits
+  int Lr;           // rows read per slot-0 path: L_b, or gamma_b+1 when bonus rows are read too
+  int pad_[3];
+};
+
+// Per physical row partial state of one vocabulary shard (sharded mode, a7).
+struct ShardRow {
+  float pm, pms, pz;        // p: max, exponent offset, sum
+  float qm, qms, qz, qs1;   // q: max, offset, sum, entropy sum
+  int qidx;                 // q: first global index of the shard max
 };
 
 // Workspace carve-up (all offsets 256-byte aligned).
@@ -24,6 +33,9 @@ struct Workspace {
   int* conf_cnt;     // [B][K] confidence-kernel completion counters (self-resetting)
   float* conf_stat;  // [B][K][G] statistic per row
   float* conf_c;     // [B][K][G] Eq. 7 confidence per row
+  float* tok_lp;     // [B][K][G+1] sharded: combined target logit of each path token
+  float* segs;       // [B][2][nseg] sharded select: local segment sums (residual, p)
+  int4* dec;         // [B] sharded select: decision record
   size_t bytes;
 };
 
@@ -47,6 +59,12 @@ inline Workspace carve(const sb_dims& d, void* base) {
   w.conf_cnt = (int*)take(sizeof(int) * B * K);
   w.conf_stat = (float*)take(sizeof(float) * B * K * (G ? G : 1));
   w.conf_c = (float*)take(sizeof(float) * B * K * (G ? G : 1));
+  {  // vocabulary-shard state (sb_shard_* calls / a communicator)
+    const size_t nseg = ((size_t)d.V * (d.dtype == SB_BF16 ? 2 : 4) + 511) / 512;
+    w.tok_lp = (float*)take(sizeof(float) * B * K * R1);
+    w.segs = (float*)take(sizeof(float) * B * 2 * nseg);
+    w.dec = (int4*)take(sizeof(int4) * B * 2);
+  }
   w.bytes = off;
   return w;
 }
@@ -56,12 +74,15 @@ inline bool dims_valid(const sb_dims* d) {
   if (d->B < 1 || d->K < 1 || d->K > kMaxK || d->G < 0 || d->G > kMaxG || d->V < 2) return false;
   if (d->row_stride < d->V) return false;
   if (d->dtype != SB_BF16 && d->dtype != SB_F32) return false;
-  if (d->v_offset != 0 || (d->v_total != 0 && d->v_total != d->V)) return false;  // unsharded build
+  if (d->v_offset < 0 || (d->v_total != 0 && (d->v_total < d->V || d->v_offset + d->V > d->v_total)))
+    return false;
   if (d->reserved != 0) return false;
   const int64_t min_ss = (int64_t)d->K * (d->G + 1) * d->row_stride;
   if (d->seq_stride != 0 && d->seq_stride < min_ss) return false;
   return true;
 }
+
+inline bool sharded(const sb_dims* d) { return d->v_total != 0 && d->v_total != d->V; }
 
 inline Dims to_dims(const sb_dims* d) {
   Dims x;

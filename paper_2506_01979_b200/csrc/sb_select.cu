@@ -838,6 +838,14 @@ static sb_status launch_select(const SelParams& p, bool vok, cudaStream_t s) {
 
 using namespace sb;
 
+struct sb_comm;
+sb_status sb_shard_select_nccl(const sb_dims* d, const void* p_logits, const void* q_logits, const int32_t* tok,
+                               const float* u, const float* us, const int32_t* n_acc, sb_select_rule rule,
+                               int32_t* sel_k, int32_t* commit_len, int32_t* out_tok, int32_t* y_tok,
+                               int32_t* y_kind, int32_t* offsets, int32_t* packed_tok, int32_t* path_rolled,
+                               int32_t* branch_discarded, uint32_t* keep_mask, float* resid_mass, int32_t* status,
+                               sb_comm* c, void* workspace, size_t workspace_bytes, cudaStream_t s);
+
 extern "C" sb_status sb_select_branch(const sb_dims* dd, const void* p_logits, const void* q_logits,
                                       const int32_t* tok, const float* u, const float* us,
                                       const int32_t* gamma, const int32_t* branch_pos,
@@ -856,8 +864,13 @@ extern "C" sb_status sb_select_branch(const sb_dims* dd, const void* p_logits, c
       !workspace)
     return SB_ERR_INVALID_ARG;
   if (rule != SB_SELECT_EQ9 && rule != SB_SELECT_ALG1) return SB_ERR_INVALID_ARG;
-  if (comm) return SB_ERR_UNSUPPORTED;
   if ((uintptr_t)workspace % 256) return SB_ERR_INVALID_ARG;
+  if (comm)
+    return sb_shard_select_nccl(dd, p_logits, q_logits, tok, u, us, n_acc, rule, sel_k, commit_len, out_tok,
+                                y_tok, y_kind, offsets, packed_tok, path_rolled, branch_discarded, keep_mask,
+                                resid_mass, status, (sb_comm*)comm, workspace, workspace_bytes,
+                                (cudaStream_t)stream);
+  if (sharded(dd)) return SB_ERR_INVALID_ARG;  // a vocabulary shard needs its exchange (comm)
   const Workspace w = carve(*dd, workspace);
   if (workspace_bytes < w.bytes) return SB_ERR_WORKSPACE;
   SelParams p;

@@ -37,12 +37,16 @@ struct RowsParams {
   uint32_t* acc_mask;
   int* n_acc;
   int* status;
+  // vocabulary-shard partial mode (a7): write the shard's row states / token logits
+  int partial, v_offset;
+  ShardRow* rowpart;  // [B][K][G+1] physical rows
+  float2* tokpart;    // [B][K][G+1] token slots: (p logit, q logit) if the token is in this shard
 };
 
 // ---------------------------------------------------------------- plan
 __global__ void __launch_bounds__(1024) k_plan(Dims d, const int* __restrict__ gamma,
                                                const int* __restrict__ bpos, SeqInfo* info,
-                                               int* unit_off) {
+                                               int* unit_off, int with_bonus) {
   __shared__ int wsum[32];
   const int tid = threadIdx.x, NT = blockDim.x;
   const int per = (d.B + NT - 1) / NT;
@@ -57,8 +61,9 @@ __global__ void __launch_bounds__(1024) k_plan(Dims d, const int* __restrict__ g
     if (s > g) { s = g; st |= SB_ST_BRANCH_CLAMPED; }
     if (s < 0) { s = 0; st |= SB_ST_BRANCH_CLAMPED; }
     const int L = (s < g) ? g : g + 1;
-    info[b] = SeqInfo{g, s, L, st};
-    local += L + (d.K - 1) * (L - 1 - s);  // slot 0: rows 0..L-1; slots k>0: s+1..L-1
+    const int Lr = with_bonus ? g + 1 : L;  // sharded mode also reads every bonus row
+    info[b] = SeqInfo{g, s, L, st, Lr, {0, 0, 0}};
+    local += Lr + (d.K - 1) * (Lr - 1 - s);  // slot 0: rows 0..Lr-1; slots k>0: s+1..Lr-1
   }
   // block exclusive scan of the per-thread sums
   const int lane = tid & 31, w = tid >> 5;
@@ -84,7 +89,7 @@ __global__ void __launch_bounds__(1024) k_plan(Dims d, const int* __restrict__ g
   for (int b = b0; b < b1; ++b) {
     unit_off[b] = run;
     const SeqInfo in = info[b];
-    run += in.L + (d.K - 1) * (in.L - 1 - in.s);
+    run += in.Lr + (d.K - 1) * (in.Lr - 1 - in.s);
   }
   if (tid == NT - 1) unit_off[d.B] = run;
 }
@@ -108,11 +113,11 @@ __device__ __forceinline__ Unit decode_unit(const RowsParams& p, int unit) {
   u.b = lo;
   u.in = p.info[lo];
   const int j = unit - __ldg(p.unit_off + lo);
-  if (j < u.in.L) {
+  if (j < u.in.Lr) {
     u.slot = 0;
     u.i = j;
   } else {
-    const int per = u.in.L - 1 - u.in.s, jj = j - u.in.L;
+    const int per = u.in.Lr - 1 - u.in.s, jj = j - u.in.Lr;
     u.slot = 1 + jj / per;
     u.i = u.in.s + 1 + jj % per;
   }
@@ -536,13 +541,17 @@ __global__ void __launch_bounds__(C::THREADS, 1) k_rows_tma(RowsParams p) {
       int x = 0;
       float lpx = 0.f, lqx = 0.f, uu = 0.f;
       int64_t et = 0;
-      if (lane < ntok) {
+      const bool has_tok = un.i < un.in.L;  // bonus rows (sharded mode) carry no token
+      if (lane < ntok && has_tok) {
         et = ent(d, un.b, branch_row ? lane : un.slot, un.i);
         x = __ldg(p.tok + et);
         uu = __ldg(p.u + et);
-        if (x >= 0 && x < d.V) {
-          lpx = ld_scalar(prow + x);
-          lqx = ld_scalar(qrow + x);
+        const int xl = x - p.v_offset;  // local column in this shard
+        if (xl >= 0 && xl < d.V) {
+          lpx = ld_scalar(prow + xl);
+          lqx = ld_scalar(qrow + xl);
+        } else {
+          lpx = lqx = -CUDART_INF_F;
         }
       }
       mbar_wait(&S.pfull[up.stage], up.phase);
@@ -555,6 +564,17 @@ __global__ void __launch_bounds__(C::THREADS, 1) k_rows_tma(RowsParams p) {
       for (int o = 16; o > 0; o >>= 1) {
         ps = combine(ps, shfl_xor(ps, o));
         qs = combine(qs, shfl_xor(qs, o));
+      }
+      if (p.partial) {  // a7: this shard's state, combined across shards later
+        if (lane < ntok && has_tok) p.tokpart[et] = make_float2(lpx, lqx);
+        if (lane == 0) {
+          ShardRow r;
+          r.pm = ps.m; r.pms = ps.ms; r.pz = ps.z;
+          r.qm = qs.m; r.qms = qs.ms; r.qz = qs.z; r.qs1 = qs.s1;
+          r.qidx = (qs.idx == 0x7fffffff) ? qs.idx : qs.idx + p.v_offset;
+          p.rowpart[ent(d, un.b, un.slot, un.i)] = r;
+        }
+        continue;
       }
       warp_epilogue<T>(p, un, ps, qs, x, lpx, lqx, uu, et);
     }
@@ -648,6 +668,37 @@ static sb_status launch_rows_variant(const RowsParams& p, cudaStream_t s) {
 
 using namespace sb;
 
+struct sb_comm;
+sb_status sb_shard_verify_nccl(const sb_dims* d, const void* p_logits, const void* q_logits, const int32_t* tok,
+                               const float* u, const int32_t* gamma, const int32_t* branch_pos, float* lse_p,
+                               float* lse_q, float* p_tok, float* q_tok, uint32_t* acc_mask, int32_t* n_acc,
+                               float* top1_q, int32_t* top1_id_q, float* entropy_q, int32_t* status, sb_comm* c,
+                               void* workspace, size_t workspace_bytes, cudaStream_t s);
+
+// a7 partial phase: plan with the bonus rows, then the TMA row kernel writing this
+// shard's row states and token logits (sb_shard_verify_local).
+sb_status sb_rows_partial(const sb_dims* dd, const void* p_logits, const void* q_logits, const int32_t* tok,
+                          const float* u, const int32_t* gamma, const int32_t* branch_pos, void* partial,
+                          void* workspace, size_t workspace_bytes, cudaStream_t s) {
+  if ((uintptr_t)workspace % 256) return SB_ERR_INVALID_ARG;
+  const Workspace w = carve(*dd, workspace);
+  if (workspace_bytes < w.bytes) return SB_ERR_WORKSPACE;
+  const bool vok = vec_ok(dd, p_logits) && vec_ok(dd, q_logits);
+  if (!vok || ((size_t)dd->V * elem_size(dd)) % 16) return SB_ERR_UNSUPPORTED;
+  const Dims d = to_dims(dd);
+  k_plan<<<1, 1024, 0, s>>>(d, gamma, branch_pos, w.info, w.unit_off, 1);
+  if (cudaGetLastError() != cudaSuccess) return SB_ERR_CUDA;
+  RowsParams p{};
+  p.d = d; p.PL = p_logits; p.QL = q_logits; p.tok = tok; p.u = u;
+  p.info = w.info; p.unit_off = w.unit_off; p.cnt = w.cnt; p.rowstat = w.rowstat; p.pflag = w.pflag;
+  p.partial = 1;
+  p.v_offset = dd->v_offset;
+  const size_t per = (size_t)dd->B * dd->K * (dd->G + 1);
+  p.rowpart = reinterpret_cast<ShardRow*>(partial);
+  p.tokpart = reinterpret_cast<float2*>(reinterpret_cast<char*>(partial) + per * sizeof(ShardRow));
+  return dd->dtype == SB_BF16 ? launch_rows_variant<__nv_bfloat16>(p, s) : launch_rows_variant<float>(p, s);
+}
+
 extern "C" sb_status sb_verify_branches(const sb_dims* dd, const void* p_logits,
                                         const void* q_logits, const int32_t* tok, const float* u,
                                         const int32_t* gamma, const int32_t* branch_pos,
@@ -660,14 +711,18 @@ extern "C" sb_status sb_verify_branches(const sb_dims* dd, const void* p_logits,
   if (!p_logits || !q_logits || !tok || !u || !lse_p || !lse_q || !p_tok || !q_tok || !acc_mask ||
       !n_acc || !status || !workspace)
     return SB_ERR_INVALID_ARG;
-  if (comm) return SB_ERR_UNSUPPORTED;
   if ((uintptr_t)workspace % 256) return SB_ERR_INVALID_ARG;
+  if (comm)
+    return sb_shard_verify_nccl(dd, p_logits, q_logits, tok, u, gamma, branch_pos, lse_p, lse_q, p_tok, q_tok,
+                                acc_mask, n_acc, top1_q, top1_id_q, entropy_q, status, (sb_comm*)comm, workspace,
+                                workspace_bytes, (cudaStream_t)stream);
+  if (sharded(dd)) return SB_ERR_INVALID_ARG;  // a vocabulary shard needs its exchange (comm)
   const Workspace w = carve(*dd, workspace);
   if (workspace_bytes < w.bytes) return SB_ERR_WORKSPACE;
   const Dims d = to_dims(dd);
   cudaStream_t s = (cudaStream_t)stream;
 
-  k_plan<<<1, 1024, 0, s>>>(d, gamma, branch_pos, w.info, w.unit_off);
+  k_plan<<<1, 1024, 0, s>>>(d, gamma, branch_pos, w.info, w.unit_off, 0);
   if (cudaGetLastError() != cudaSuccess) return SB_ERR_CUDA;
 
   RowsParams p;
@@ -676,6 +731,7 @@ extern "C" sb_status sb_verify_branches(const sb_dims* dd, const void* p_logits,
   p.lse_p = lse_p; p.lse_q = lse_q; p.p_tok = p_tok; p.q_tok = q_tok;
   p.top1_q = top1_q; p.entropy_q = entropy_q; p.top1_id_q = top1_id_q;
   p.acc_mask = acc_mask; p.n_acc = n_acc; p.status = status;
+  p.partial = 0; p.v_offset = 0; p.rowpart = nullptr; p.tokpart = nullptr;
   const bool vok = vec_ok(dd, p_logits) && vec_ok(dd, q_logits);
   const size_t row_bytes = (size_t)dd->V * elem_size(dd);
   if (vok && row_bytes % 16 == 0 && !tma_disabled())
