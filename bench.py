@@ -93,12 +93,14 @@ def verified_tokens(gamma, bpos, K):
     return t
 
 
-def bytes_model(gamma, bpos, y_kind, K, V, es, G, conf_rows=0):
+def bytes_model(gamma, bpos, y_kind, K, V, es, G, conf_rows=0, bonus_rows=False):
     """Algorithmic bytes of one step: a1 row pairs, a4 sampled
     rows (2 for a residual, 1 for a bonus; a bonus row needs 2 passes), a6 draft rows,
     plus 12 B per path token (token + uniform + output)."""
-    units = sum(L + (K - 1) * (L - 1 - s) for g, s in zip(gamma, bpos) for L in [g if s < g else g + 1])
+    units = sum(L + (K - 1) * (L - 1 - s) for g, s in zip(gamma, bpos)
+                for L in [(g if s < g else g + 1) if not bonus_rows else g + 1])
     a1 = units * 2 * V * es
+    # sharded mode reads bonus rows in a1; its sample pass streams the row once per kind
     a4 = sum(2 if k == 1 else (1 if k == 2 else 0) for k in y_kind) * V * es
     a6 = conf_rows * V * es
     small = verified_tokens(gamma, bpos, K) * 12
@@ -139,17 +141,38 @@ def run_ours(args, rank, world, local_rank):
     cfg = synth.config(args.config, **({"delta": args.delta} if args.delta is not None else {}))
     Bl = cfg.B * cfg.rounds
     b0, b1 = rank_slice(cfg, rank, world)
+    vocab = args.mode == "vocab"
+    if vocab:  # every rank sees all sequences and owns a vocabulary slice (a7)
+        b0, b1 = 0, Bl
     t0 = time.time()
     inp = synth.generate(cfg, device=dev, b0=b0, b1=b1)
     gen_s = time.time() - t0
-    d = api.dims_for(inp["PL"], V=inp["V"])
+    comm, views = None, None
+    if vocab:
+        v0, vn = api.shard_bounds(inp["V"], world)[rank]
+        d, pv = api.shard_view(inp["PL"], inp["V"], v0, vn)
+        _, qv = api.shard_view(inp["QL"], inp["V"], v0, vn)
+        views = (pv, qv)
+        uid = [None]
+        if rank == 0:
+            import ctypes
+
+            from paper_2506_01979_b200 import _lib
+            b = ctypes.create_string_buffer(int(_lib.lib().sb_comm_unique_id_bytes()))
+            _lib.check(_lib.lib().sb_comm_unique_id(b), "sb_comm_unique_id")
+            uid = [b.raw]
+        if world > 1:
+            torch.distributed.broadcast_object_list(uid, src=0)
+        comm = api.Comm(world, rank, d, unique_id=uid[0])
+    else:
+        d = api.dims_for(inp["PL"], V=inp["V"])
     buf = api.StepBuffers.alloc(d, dev)
     adaptive = cfg.layout == "adaptive"
     stream = torch.cuda.current_stream()
     es = 2 if cfg.dtype == "bf16" else 4
 
     def step():
-        return api.verify_step(d, inp, buf, adaptive=adaptive, stream=stream)
+        return api.verify_step(d, inp, buf, adaptive=adaptive, stream=stream, comm=comm, views=views)
 
     for _ in range(max(args.warmup, 3)):
         step()
@@ -157,14 +180,15 @@ def run_ours(args, rank, world, local_rank):
     gamma = (buf.c_gamma.view(-1) if adaptive else inp["gamma"]).cpu().tolist()
     bpos = inp["branch_pos"].cpu().tolist()
     ykind = buf.y_kind.cpu().tolist()
-    a1, a4, a6, small, units = bytes_model(gamma, bpos, ykind, cfg.K, cfg.V, es, cfg.G,
-                                           conf_rows=(Bl * cfg.G if adaptive else 0))
+    a1, a4, a6, small, units = bytes_model(gamma, bpos, ykind, cfg.K, d.V, es, cfg.G,
+                                           conf_rows=(Bl * cfg.G if adaptive else 0), bonus_rows=vocab)
     toks = verified_tokens(gamma, bpos, cfg.K)
     committed = int(buf.commit_len.sum())
 
     # ---- timed region: exactly K whole steps, replayed from a CUDA graph of the C-ABI
     # launches (no per-step host/ctypes overhead), bracketed by barrier + synchronize
-    graph = api.StepGraph(d, inp, buf, adaptive=adaptive) if not args.no_graph else None
+    graph = api.CallGraph(lambda s_: api.verify_step(d, inp, buf, adaptive=adaptive, stream=s_, comm=comm,
+                                                     views=views)) if not args.no_graph else None
     clk = Clocks(local_rank if not args.no_clocks else -1).__enter__()
     time.sleep(0.3)  # let nvidia-smi start sampling before the timed region
     if world > 1:
@@ -187,19 +211,21 @@ def run_ours(args, rank, world, local_rank):
     # ---- kernel timing region (roofline): each C-ABI call captured alone in a CUDA
     # graph and replayed K times, CUDA events around every replay on the launching stream
     gam = buf.c_gamma.view(-1) if adaptive else inp["gamma"]
+    PLv, QLv = views if views is not None else (inp["PL"], inp["QL"])
     calls = {
         "conf": (lambda s: api.sb_draft_confidence(
             api.conf_dims(d), inp["QL"], None, api.SB_CONF_TOP1, 0.2, 1.0, 6, buf.c_top1, buf.c_id,
             buf.c_ent, None, buf.c_stat, buf.c_stop, buf.c_knext, buf.c_gamma, buf.conf_workspace, s))
         if adaptive else None,
         "verify": lambda s: api.sb_verify_branches(
-            d, inp["PL"], inp["QL"], inp["tok"], inp["u"], gam, inp["branch_pos"], buf.lse_p, buf.lse_q,
+            d, PLv, QLv, inp["tok"], inp["u"], gam, inp["branch_pos"], buf.lse_p, buf.lse_q,
             buf.p_tok, buf.q_tok, buf.acc_mask, buf.n_acc, buf.top1_q, buf.top1_id_q, buf.entropy_q,
-            buf.status, buf.workspace, s),
+            buf.status, buf.workspace, s, comm),
         "select": lambda s: api.sb_select_branch(
-            d, inp["PL"], inp["QL"], inp["tok"], inp["u"], inp["us"], gam, inp["branch_pos"], buf.n_acc, 0,
+            d, PLv, QLv, inp["tok"], inp["u"], inp["us"], gam, inp["branch_pos"], buf.n_acc, 0,
             buf.sel_k, buf.commit_len, buf.out_tok, buf.y_tok, buf.y_kind, buf.offsets, buf.packed_tok,
-            buf.path_rolled, buf.branch_discarded, buf.keep_mask, buf.resid_mass, buf.status, buf.workspace, s),
+            buf.path_rolled, buf.branch_discarded, buf.keep_mask, buf.resid_mass, buf.status, buf.workspace, s,
+            comm),
     }
     kt = {}
     for name, fn in calls.items():
@@ -221,11 +247,15 @@ def run_ours(args, rank, world, local_rank):
     ms_step = ms / args.steps
     ms_step_all, toks_all, comm_all, bytes_all = reduce_over_ranks(
         ms_step, toks, committed, a1 + a4 + a6 + small, dev, world)
+    if vocab:  # every rank verifies the same tokens: count them once
+        toks_all, comm_all = float(toks), float(committed)
 
     # ---- e2e through the public API with host buffers (pinned), H2D + D2H inside
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not vocab:
         e2e = run_e2e(args, inp, d, buf, adaptive, stream, dev, world)
+    if comm is not None:
+        comm.close()
     if rank != 0:
         return None
     peak, peak_src = peaks()
@@ -235,11 +265,13 @@ def run_ours(args, rank, world, local_rank):
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": "verified draft tokens/s",
         "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
-        "ms_per_step": round(ms_step_all, 4), "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": round(ms_step_all, 4), "higher_is_better": True,
+        "scaling": "strong" if vocab else "weak",
         "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic (seeded, DESIGN.md §Input recipe)",
         "config": {"workload": f"{cfg.name.upper()}: {cfg.note}", "V": cfg.V, "K": cfg.K, "G": cfg.G,
-                   "per_rank_batch": Bl, "global_batch": Bl * world, "layout": cfg.layout,
-                   "parallelism": f"sequence-sharded x{world} (no data-path collective)",
+                   "per_rank_batch": Bl, "global_batch": Bl if vocab else Bl * world, "layout": cfg.layout,
+                   "parallelism": (f"vocabulary-sharded x{world} (NCCL all-gather / all-reduce, sb_comm)"
+                                   if vocab else f"sequence-sharded x{world} (no data-path collective)"),
                    "l2": "inputs larger than L2 (%.1f GB per step vs 126 MB)" % (bytes_all / 1e9 / world)},
         "logit_GBps": round(step_gbs, 1), "logit_frac_of_peak": round(step_gbs / world / peak, 4),
         "committed_tokens_per_s": round(comm_all / (ms_step_all * 1e-3), 1),
@@ -247,17 +279,18 @@ def run_ours(args, rank, world, local_rank):
                          "select": round(t_sel, 4),
                          "source": "each call replayed alone from its own CUDA graph, CUDA events"},
         "timing": "CUDA graph replay of the whole step" if not args.no_graph else "eager C-ABI calls",
-        "roofline": {"bound": "hbm", "kernel": "sb_verify_branches (k_plan + k_rows)",
+        "roofline": {"bound": "hbm", "kernel": "sb_verify_branches (k_plan + k_rows_tma" + (
+                         " + NCCL all-gather + k_shard_combine)" if vocab else ")"),
                      "achieved": round(ver_gbs, 1), "peak": peak, "peak_source": peak_src, "unit": "GB/s",
                      "frac": round(ver_gbs / peak, 4), "traffic": traffic_from_profiles(cfg.name),
                      "algorithmic_bytes_per_launch": a1 + small, "row_pairs_per_launch": units},
-        "gpu_launches": args.steps * ((1 if adaptive else 0) + 2 + 1),
+        "gpu_launches": args.steps * ((1 if adaptive else 0) + (6 if vocab else 3)),
         "clocks": clk.summary(),
         "generation_s": round(gen_s, 1),
     }
     if e2e is not None:
         line["e2e"] = e2e
-    if not args.no_cpu_baseline and world == 1:
+    if not args.no_cpu_baseline and world == 1 and not vocab:
         line["cpu_baseline"] = cpu_baseline(cfg, inp, adaptive, buf, budget_s=args.cpu_budget)
     return line
 
@@ -412,11 +445,16 @@ def main():
     ap.add_argument("--no-graph", action="store_true", help="issue the C-ABI calls eagerly each step")
     ap.add_argument("--delta", type=float, default=None, help="override the generator's draft noise")
     ap.add_argument("--no-clocks", action="store_true", help="do not run the nvidia-smi sampler")
+    ap.add_argument("--mode", default=None, choices=["seq", "vocab"],
+                    help="seq: sequences sharded across ranks; vocab: vocabulary sharded (a7). "
+                         "Default: vocab for c5, seq otherwise")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--ref-seqs", type=int, default=32)
     args = ap.parse_args()
+    if args.mode is None:
+        args.mode = "vocab" if args.config == "c5" else "seq"
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
