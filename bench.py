@@ -221,6 +221,9 @@ def run_ours(args, rank, world, local_rank):
             d, PLv, QLv, inp["tok"], inp["u"], gam, inp["branch_pos"], buf.lse_p, buf.lse_q,
             buf.p_tok, buf.q_tok, buf.acc_mask, buf.n_acc, buf.top1_q, buf.top1_id_q, buf.entropy_q,
             buf.status, buf.workspace, s, comm),
+        "fused": (lambda s: api.sb_verify_select(
+            d, PLv, QLv, inp["tok"], inp["u"], inp["us"], gam, inp["branch_pos"], 0, buf, s))
+        if comm is None else None,
         "select": lambda s: api.sb_select_branch(
             d, PLv, QLv, inp["tok"], inp["u"], inp["us"], gam, inp["branch_pos"], buf.n_acc, 0,
             buf.sel_k, buf.commit_len, buf.out_tok, buf.y_tok, buf.y_kind, buf.offsets, buf.packed_tok,
@@ -243,7 +246,7 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
         kt[name] = sum(e0.elapsed_time(e1) for e0, e1 in evs) / args.steps
     clk.__exit__()
-    t_conf, t_ver, t_sel = kt["conf"], kt["verify"], kt["select"]
+    t_conf, t_ver, t_sel, t_fused = kt["conf"], kt["verify"], kt["select"], kt["fused"]
     ms_step = ms / args.steps
     ms_step_all, toks_all, comm_all, bytes_all = reduce_over_ranks(
         ms_step, toks, committed, a1 + a4 + a6 + small, dev, world)
@@ -259,7 +262,12 @@ def run_ours(args, rank, world, local_rank):
     if rank != 0:
         return None
     peak, peak_src = peaks()
-    ver_gbs = (a1 + small) / (t_ver * 1e-3) / 1e9
+    if t_fused > 0:  # dominant kernel: the fused verify + select launch
+        rf_kernel, rf_bytes, rf_ms = "sb_verify_select (k_plan + k_step_tma)", a1 + a4 + small, t_fused
+    else:
+        rf_kernel = "sb_verify_branches (k_plan + k_rows_tma" + (" + NCCL all-gather + k_shard_combine)" if vocab else ")")
+        rf_bytes, rf_ms = a1 + small, t_ver
+    ver_gbs = rf_bytes / (rf_ms * 1e-3) / 1e9
     step_gbs = bytes_all / (ms_step_all * 1e-3) / 1e9
     value = toks_all / (ms_step_all * 1e-3)
     line = {
@@ -276,15 +284,14 @@ def run_ours(args, rank, world, local_rank):
         "logit_GBps": round(step_gbs, 1), "logit_frac_of_peak": round(step_gbs / world / peak, 4),
         "committed_tokens_per_s": round(comm_all / (ms_step_all * 1e-3), 1),
         "breakdown_ms": {"draft_confidence": round(t_conf, 4), "verify": round(t_ver, 4),
-                         "select": round(t_sel, 4),
+                         "select": round(t_sel, 4), "verify_select_fused": round(t_fused, 4),
                          "source": "each call replayed alone from its own CUDA graph, CUDA events"},
         "timing": "CUDA graph replay of the whole step" if not args.no_graph else "eager C-ABI calls",
-        "roofline": {"bound": "hbm", "kernel": "sb_verify_branches (k_plan + k_rows_tma" + (
-                         " + NCCL all-gather + k_shard_combine)" if vocab else ")"),
+        "roofline": {"bound": "hbm", "kernel": rf_kernel,
                      "achieved": round(ver_gbs, 1), "peak": peak, "peak_source": peak_src, "unit": "GB/s",
                      "frac": round(ver_gbs / peak, 4), "traffic": traffic_from_profiles(cfg.name),
-                     "algorithmic_bytes_per_launch": a1 + small, "row_pairs_per_launch": units},
-        "gpu_launches": args.steps * ((1 if adaptive else 0) + (6 if vocab else 3)),
+                     "algorithmic_bytes_per_launch": rf_bytes, "row_pairs_per_launch": units},
+        "gpu_launches": args.steps * ((1 if adaptive else 0) + (6 if vocab else 2)),
         "clocks": clk.summary(),
         "generation_s": round(gen_s, 1),
     }

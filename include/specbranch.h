@@ -174,6 +174,25 @@ sb_status sb_select_branch(const sb_dims* d, const void* p_logits, const void* q
                            sb_stream_t stream);
 
 /*
+ * sb_verify_select — sb_verify_branches followed by sb_select_branch: every output of
+ * both calls, with the same meaning, in one call (one workspace, one stream).  By default
+ * the two kernels run back to back; with SB_FUSED_STEP=1 in the environment a single
+ * persistent launch interleaves each sequence's sample unit a few waves of row pairs
+ * behind its last row pair (correct, but measured slower on B200).
+ * Unsharded only.
+ */
+sb_status sb_verify_select(const sb_dims* d, const void* p_logits, const void* q_logits,
+                           const int32_t* tok, const float* u, const float* us,
+                           const int32_t* gamma, const int32_t* branch_pos, sb_select_rule rule,
+                           float* lse_p, float* lse_q, float* p_tok, float* q_tok,
+                           uint32_t* acc_mask, int32_t* n_acc, float* top1_q, int32_t* top1_id_q,
+                           float* entropy_q, int32_t* status, int32_t* sel_k, int32_t* commit_len,
+                           int32_t* out_tok, int32_t* y_tok, int32_t* y_kind, int32_t* offsets,
+                           int32_t* packed_tok, int32_t* path_rolled, int32_t* branch_discarded,
+                           uint32_t* keep_mask, float* resid_mass, void* workspace,
+                           size_t workspace_bytes, sb_stream_t stream);
+
+/*
  * sb_draft_confidence — the implicit draft-confidence statistic and adaptive gamma.
  *   (§4.2 P170; Eq. 6 P194-202; Eq. 7 P218; Alg. 1 P517; App. E.6 P954/P965)
  *

@@ -96,6 +96,24 @@ def sb_select_branch(d, p_logits, q_logits, tok, u, us, gamma, branch_pos, n_acc
     L.check(rc, "sb_select_branch")
 
 
+def sb_verify_select(d, p_logits, q_logits, tok, u, us, gamma, branch_pos, rule, buf: "StepBuffers",
+                     stream=None):
+    """The fused verify + select call (outputs into a StepBuffers)."""
+    rc = L.lib().sb_verify_select(
+        ctypes.byref(d), _ptr(p_logits, LOG, "p_logits"), _ptr(q_logits, LOG, "q_logits"), _ptr(tok, I32, "tok"),
+        _ptr(u, F32, "u"), _ptr(us, F32, "us"), _ptr(gamma, I32, "gamma"), _ptr(branch_pos, I32, "branch_pos"),
+        int(rule), _ptr(buf.lse_p, F32, "lse_p"), _ptr(buf.lse_q, F32, "lse_q"), _ptr(buf.p_tok, F32, "p_tok"),
+        _ptr(buf.q_tok, F32, "q_tok"), _ptr(buf.acc_mask, I32, "acc_mask"), _ptr(buf.n_acc, I32, "n_acc"),
+        _ptr(buf.top1_q, F32, "top1_q"), _ptr(buf.top1_id_q, I32, "top1_id_q"),
+        _ptr(buf.entropy_q, F32, "entropy_q"), _ptr(buf.status, I32, "status"), _ptr(buf.sel_k, I32, "sel_k"),
+        _ptr(buf.commit_len, I32, "commit_len"), _ptr(buf.out_tok, I32, "out_tok"), _ptr(buf.y_tok, I32, "y_tok"),
+        _ptr(buf.y_kind, I32, "y_kind"), _ptr(buf.offsets, I32, "offsets"), _ptr(buf.packed_tok, I32, "packed_tok"),
+        _ptr(buf.path_rolled, I32, "path_rolled"), _ptr(buf.branch_discarded, I32, "branch_discarded"),
+        _ptr(buf.keep_mask, I32, "keep_mask"), _ptr(buf.resid_mass, F32, "resid_mass"),
+        _ptr(buf.workspace, torch.uint8, "workspace"), buf.workspace.numel(), _stream(stream))
+    L.check(rc, "sb_verify_select")
+
+
 def sb_draft_confidence(d, q_logits, tok, mode, eps, lam, k_max, top1_prob, top1_id, entropy,
                         tok_prob, stat, stop, k_next, gamma_next, workspace, stream=None):
     rc = L.lib().sb_draft_confidence(
@@ -173,12 +191,13 @@ def conf_dims(d: L.sb_dims) -> L.sb_dims:
 
 def verify_step(d: L.sb_dims, inp: dict, buf: StepBuffers, rule: int = SB_SELECT_EQ9,
                 adaptive: bool = False, eps: float = 0.2, k_max: int = 6, stream=None, comm=None,
-                views=None):
+                views=None, fused: bool = True):
     """One whole hot-path step: [draft confidence -> adaptive gamma] -> verify -> select.
 
     inp: PL, QL, tok, u, us, gamma, branch_pos device tensors (synth.generate layout).
     With adaptive=True gamma_b = max(1, stop_b) of the slot-0 draft rows (Eq. 6, TOP1)
-    replaces inp["gamma"] and s_b = 0.
+    replaces inp["gamma"] and s_b = 0.  fused=True runs verify +
+    select as one launch (sb_verify_select); fused=False issues the two calls.
     """
     gamma = inp["gamma"]
     if adaptive:
@@ -187,6 +206,9 @@ def verify_step(d: L.sb_dims, inp: dict, buf: StepBuffers, rule: int = SB_SELECT
                             buf.c_knext, buf.c_gamma, buf.conf_workspace, stream)
         gamma = buf.c_gamma.view(-1)
     PL, QL = views if views is not None else (inp["PL"], inp["QL"])
+    if fused and comm is None:
+        sb_verify_select(d, PL, QL, inp["tok"], inp["u"], inp["us"], gamma, inp["branch_pos"], rule, buf, stream)
+        return gamma
     sb_verify_branches(d, PL, QL, inp["tok"], inp["u"], gamma, inp["branch_pos"],
                        buf.lse_p, buf.lse_q, buf.p_tok, buf.q_tok, buf.acc_mask, buf.n_acc,
                        buf.top1_q, buf.top1_id_q, buf.entropy_q, buf.status, buf.workspace, stream, comm)

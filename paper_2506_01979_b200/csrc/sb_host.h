@@ -36,6 +36,8 @@ struct Workspace {
   float* tok_lp;     // [B][K][G+1] sharded: combined target logit of each path token
   float* segs;       // [B][2][nseg] sharded select: local segment sums (residual, p)
   int4* dec;         // [B] sharded select: decision record
+  int* ready;        // [B] fused step: per-sequence phase-1 completion flags
+  int* plan;         // [4] fused step: delta, total units
   size_t bytes;
 };
 
@@ -65,6 +67,8 @@ inline Workspace carve(const sb_dims& d, void* base) {
     w.segs = (float*)take(sizeof(float) * B * 2 * nseg);
     w.dec = (int4*)take(sizeof(int4) * B * 2);
   }
+  w.ready = (int*)take(sizeof(int) * B);
+  w.plan = (int*)take(sizeof(int) * 4);
   w.bytes = off;
   return w;
 }

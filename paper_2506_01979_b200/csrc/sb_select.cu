@@ -18,6 +18,7 @@
 
 #include "sb_host.h"
 #include "sb_ring.cuh"
+#include "sb_sample.cuh"
 
 namespace sb {
 
@@ -370,63 +371,41 @@ struct SelSmem {
   alignas(128) uint8_t buf[sNS][2][sChunk];
 };
 
-// r(v) for the E ids of one 16-byte vector.  Explicit rounding intrinsics keep the
-// arithmetic identical wherever it is inlined (consumers and epilogue must agree).
-template <typename T>
-__device__ __forceinline__ void r_values(const uint4& vp, const uint4& vq, bool resid, float MSp,
-                                         float iZp, float MSq, float iZq, float* r) {
+// Consumer pass A over one sampled row (pair): one sum per 1 KB segment.  RESID is a
+// template parameter so neither path is predicated into the other.
+template <typename T, bool RESID>
+__device__ __forceinline__ void seg_pass(SelSmem& S, RingPos<sNS>& rp, int q, int nchunks, int nvec_last,
+                                         bool ok, float MSp, float MSq, float kq) {
   constexpr int E = Vec<T>::E;
-  float lp[E], lq[E];
-  Vec<T>::unpack(vp, lp);
-  Vec<T>::unpack(vq, lq);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int c = 0; c < nchunks; ++c) {
+    const int nvec = (c == nchunks - 1) ? nvec_last : sChunk / 16;
+    mbar_wait(&S.full[rp.stage], rp.phase);
+    uint4 vp[2], vq[2];
 #pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const float P = __fmul_rn(ex2(__fmaf_rn(lp[e], kC, -MSp)), iZp);
-    if (resid) {
-      const float Q = __fmul_rn(ex2(__fmaf_rn(lq[e], kC, -MSq)), iZq);
-      r[e] = fmaxf(__fsub_rn(P, Q), 0.f);
-    } else {
-      r[e] = P;
+    for (int j = 0; j < 2; ++j) {  // lane owns 2 adjacent vectors of its warp's 1 KB segment
+      const int v = warp * 64 + lane * 2 + j;
+      if (v < nvec) {
+        vp[j] = lds128(S.buf[rp.stage][0] + v * 16);
+        if (RESID) vq[j] = lds128(S.buf[rp.stage][1] + v * 16);
+      } else {
+        vp[j] = vq[j] = (sizeof(T) == 2) ? make_uint4(0xff80ff80u, 0xff80ff80u, 0xff80ff80u, 0xff80ff80u)
+                                         : make_uint4(0xff800000u, 0xff800000u, 0xff800000u, 0xff800000u);
+      }
     }
-  }
-}
-template <int E>
-__device__ __forceinline__ float seq_sum(const float* r) {
-  float s = 0.f;
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&S.empty[rp.stage]);
+    rp.advance();
+    float own = 0.f;
 #pragma unroll
-  for (int e = 0; e < E; ++e) s = __fadd_rn(s, r[e]);
-  return s;
-}
-__device__ __forceinline__ float warp_scan_rn(float x) {
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const float y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x = __fadd_rn(x, y);
-  }
-  return x;
-}
-
-// The epilogue warp's own pass over a whole row (rare: zero residual mass fallback).
-template <typename T>
-__device__ void warp_segments(const T* prow, const T* qrow, uint32_t row_bytes, int nseg, bool resid,
-                              float MSp, float iZp, float MSq, float iZq, float* seg) {
-  constexpr int E = Vec<T>::E;
-  const int lane = threadIdx.x & 31;
-  for (int sI = 0; sI < nseg; ++sI) {
-    const uint32_t off = (uint32_t)sI * 512 + lane * 16;
-    uint4 vp = make_uint4(0xff80ff80u, 0xff80ff80u, 0xff80ff80u, 0xff80ff80u), vq = vp;
-    if (sizeof(T) == 4) vp = vq = make_uint4(0xff800000u, 0xff800000u, 0xff800000u, 0xff800000u);
-    if (off < row_bytes) {
-      vp = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(prow) + off));
-      if (resid) vq = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(qrow) + off));
+    for (int j = 0; j < 2; ++j) {
+      float r[E];
+      r_scaled<T>(vp[j], vq[j], RESID, MSp, MSq, kq, r);
+      own = seq_sum<E>(r, own);
     }
-    float r[E];
-    r_values<T>(vp, vq, resid, MSp, iZp, MSq, iZq, r);
-    const float incl = warp_scan_rn(seq_sum<E>(r));
-    if (lane == 31) seg[sI] = incl;
+    const float tot = warp_sum_rn(ok ? own : 0.f);
+    if (lane == 0) S.seg[q][c * (sChunk / kSegBytes) + warp] = tot;
   }
-  __syncwarp();
 }
 
 template <typename T>
@@ -454,7 +433,7 @@ __global__ void __launch_bounds__(sThreads, 1) k_select_tma(SelParams p) {
   const uint32_t row_bytes = (uint32_t)d.V * sizeof(T);
   const int nchunks = (row_bytes + sChunk - 1) / sChunk;
   const int nvec_last = (int)(row_bytes - (uint32_t)(nchunks - 1) * sChunk) / 16;
-  const int nseg = nchunks * (sChunk / 512);
+  const int nseg = nchunks * (sChunk / kSegBytes);
 
   if (warp == sCW + 2) {  // ---------------- decider
     RingPos<sNQ> dq;
@@ -579,7 +558,7 @@ __global__ void __launch_bounds__(sThreads, 1) k_select_tma(SelParams p) {
         } else {
           const T* prow = PL + row_off(d, b, D.slot, D.row);
           const T* qrow = QL + row_off(d, b, D.slot, D.row);
-          const float iZp = 1.f / Zp, iZq = 1.f / Zq;
+          const float kq = Zp / Zq;
           bool resid = (kind == 1);
           float* seg = S.seg[q];
           const int per = (nseg + 31) / 32;
@@ -602,7 +581,7 @@ __global__ void __launch_bounds__(sThreads, 1) k_select_tma(SelParams p) {
             if (R > 0.0 || !resid) break;
             resid = false;  // "no residual mass" (S134-140): sample from P
             st |= SB_ST_ZERO_RESID;
-            warp_segments<T>(prow, qrow, row_bytes, nseg, false, MSp, iZp, MSq, iZq, seg);
+            warp_segments<T>(prow, qrow, row_bytes, nseg, false, MSp, MSq, kq, seg);
           }
           const double t = (double)__ldg(p.us + b) * R;
           // exactly one lane's [excl, incl) holds t; it rescans its segments in fp64
@@ -639,32 +618,34 @@ __global__ void __launch_bounds__(sThreads, 1) k_select_tma(SelParams p) {
             trem = CUDART_INF;
           }
           if (sStar >= 0) {
-            // pass B: re-read segment sStar (one 16-byte vector per lane) from L2
-            const uint32_t off = (uint32_t)sStar * 512 + lane * 16;
-            uint4 vp, vq;
-            if (sizeof(T) == 2) vp = vq = make_uint4(0xff80ff80u, 0xff80ff80u, 0xff80ff80u, 0xff80ff80u);
-            else vp = vq = make_uint4(0xff800000u, 0xff800000u, 0xff800000u, 0xff800000u);
-            if (off < row_bytes) {
-              vp = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(prow) + off));
-              if (resid) vq = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(qrow) + off));
+            // pass B: re-read segment sStar (two 16-byte vectors per lane) from L2
+            float r[2][E], own = 0.f;
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              const uint32_t off = (uint32_t)sStar * kSegBytes + lane * 32 + j * 16;
+              r_scaled<T>(seg_vec(prow, row_bytes, off), resid ? seg_vec(qrow, row_bytes, off) : uint4{}, resid,
+                          MSp, MSq, kq, r[j]);
+              own = seq_sum<E>(r[j], own);
             }
-            float r[E];
-            r_values<T>(vp, vq, resid, MSp, iZp, MSq, iZq, r);
-            const float incl = warp_scan_rn(seq_sum<E>(r));
+            const float incl = warp_scan_rn(own);
             float F = __shfl_up_sync(0xffffffffu, incl, 1);
             if (lane == 0) F = 0.f;
             int cand = 0x7fffffff, lastv = -1;
-            const int vbase = (int)(off / sizeof(T));
+            const int vbase = (int)(((uint32_t)sStar * kSegBytes + lane * 32) / sizeof(T));
 #pragma unroll
-            for (int e = 0; e < E; ++e) {
-              F = __fadd_rn(F, r[e]);
-              if (cand == 0x7fffffff && (double)F > trem && r[e] > 0.f) cand = vbase + e;
-              if (r[e] > 0.f) lastv = vbase + e;
-            }
+            for (int j = 0; j < 2; ++j)
+#pragma unroll
+              for (int e = 0; e < E; ++e) {
+                F = __fadd_rn(F, r[j][e]);
+                const int v = vbase + j * E + e;
+                if (cand == 0x7fffffff && (double)F > trem && r[j][e] > 0.f) cand = v;
+                if (r[j][e] > 0.f) lastv = v;
+              }
             const int pick = (int)__reduce_min_sync(0xffffffffu, (unsigned)cand);
             y = (pick != 0x7fffffff) ? pick : (int)__reduce_max_sync(0xffffffffu, (unsigned)(lastv + 1)) - 1;
+            if (y >= d.V) y = -1;
           }
-          mass = R;
+          mass = R / (double)Zp;  // back to probability mass
         }
       }
       // commit (SURVEY §8.0 "Commit")
@@ -779,33 +760,11 @@ __global__ void __launch_bounds__(sThreads, 1) k_select_tma(SelParams p) {
       const bool resid = (D.kind == 1);
       const float4 rsv = resid ? D.rs : make_float4(S.rs[q][0], S.rs[q][1], S.rs[q][2], S.rs[q][3]);
       const bool ok = resid ? ((rsv.y == rsv.y) && (rsv.w == rsv.w)) : (S.ok[q] != 0);
-      const float MSp = rsv.x, iZp = 1.f / rsv.y, MSq = rsv.z, iZq = 1.f / rsv.w;
-      for (int c = 0; c < nchunks; ++c) {
-        const int nvec = (c == nchunks - 1) ? nvec_last : sChunk / 16;
-        mbar_wait(&S.full[rp.stage], rp.phase);
-        uint4 vp[sVPT], vq[sVPT];
-#pragma unroll
-        for (int j = 0; j < sVPT; ++j) {
-          const int v = tid + j * sCT;
-          if (v < nvec) {
-            vp[j] = lds128(S.buf[rp.stage][0] + v * 16);
-            vq[j] = resid ? lds128(S.buf[rp.stage][1] + v * 16) : vp[j];
-          } else {
-            vp[j] = vq[j] = (sizeof(T) == 2) ? make_uint4(0xff80ff80u, 0xff80ff80u, 0xff80ff80u, 0xff80ff80u)
-                                             : make_uint4(0xff800000u, 0xff800000u, 0xff800000u, 0xff800000u);
-          }
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&S.empty[rp.stage]);
-        rp.advance();
-#pragma unroll
-        for (int j = 0; j < sVPT; ++j) {
-          float r[E];
-          r_values<T>(vp[j], vq[j], resid, MSp, iZp, MSq, iZq, r);
-          const float incl = warp_scan_rn(ok ? seq_sum<E>(r) : 0.f);
-          if (lane == 31) S.seg[q][c * (sChunk / 512) + j * sCW + warp] = incl;
-        }
-      }
+      const float MSp = rsv.x, MSq = rsv.z, kq = rsv.y / rsv.w;
+      if (resid)
+        seg_pass<T, true>(S, rp, q, nchunks, nvec_last, ok, MSp, MSq, kq);
+      else
+        seg_pass<T, false>(S, rp, q, nchunks, nvec_last, ok, MSp, MSq, kq);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&S.sfull[q]);
@@ -883,7 +842,7 @@ extern "C" sb_status sb_select_branch(const sb_dims* dd, const void* p_logits, c
   const bool vok = vec_ok(dd, p_logits) && vec_ok(dd, q_logits);
   cudaStream_t s = (cudaStream_t)stream;
   const size_t row_bytes = (size_t)dd->V * elem_size(dd);
-  if (vok && row_bytes % 16 == 0 && row_bytes <= (size_t)sSegMax * 512 && !tma_disabled())
+  if (vok && row_bytes % 16 == 0 && row_bytes <= (size_t)sSegMax * kSegBytes && !tma_disabled())
     return dd->dtype == SB_BF16 ? launch_select_tma<__nv_bfloat16>(p, s) : launch_select_tma<float>(p, s);
   if (dd->dtype == SB_BF16) {
     if ((dd->V + 256 * 8 - 1) / (256 * 8) > kMaxTiles) return SB_ERR_UNSUPPORTED;

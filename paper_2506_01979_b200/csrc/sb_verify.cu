@@ -18,6 +18,7 @@
 
 #include "sb_host.h"
 #include "sb_ring.cuh"
+#include "sb_sample.cuh"
 
 namespace sb {
 
@@ -37,6 +38,7 @@ struct RowsParams {
   uint32_t* acc_mask;
   int* n_acc;
   int* status;
+  int* ready;  // fused step: per-sequence "n_k known" flags (NULL otherwise)
   // vocabulary-shard partial mode (a7): write the shard's row states / token logits
   int partial, v_offset;
   ShardRow* rowpart;  // [B][K][G+1] physical rows
@@ -46,7 +48,8 @@ struct RowsParams {
 // ---------------------------------------------------------------- plan
 __global__ void __launch_bounds__(1024) k_plan(Dims d, const int* __restrict__ gamma,
                                                const int* __restrict__ bpos, SeqInfo* info,
-                                               int* unit_off, int with_bonus) {
+                                               int* unit_off, int with_bonus, int fused_grid, int* plan,
+                                               int* ready) {
   __shared__ int wsum[32];
   const int tid = threadIdx.x, NT = blockDim.x;
   const int per = (d.B + NT - 1) / NT;
@@ -86,6 +89,24 @@ __global__ void __launch_bounds__(1024) k_plan(Dims d, const int* __restrict__ g
   }
   __syncthreads();
   int run = incl - local + (w > 0 ? wsum[w - 1] : 0);
+  if (fused_grid > 0) {
+    // fused step: the sample unit of sequence b follows the phase-1 units of sequence
+    // b + delta (delta ~ 3 waves of units behind), the last delta sample units at the end
+    const int p1total = wsum[NT / 32 - 1];
+    const int delta = max(1, min(d.B, (3 * fused_grid * d.B + max(1, p1total) - 1) / max(1, p1total)));
+    for (int b = b0; b < b1; ++b) {
+      unit_off[b] = run + max(0, b - delta);
+      const SeqInfo in = info[b];
+      run += in.Lr + (d.K - 1) * (in.Lr - 1 - in.s);
+      ready[b] = 0;
+    }
+    if (tid == NT - 1) {
+      unit_off[d.B] = run + max(0, d.B - delta);
+      plan[0] = delta;
+      plan[1] = run + d.B;  // total units
+    }
+    return;
+  }
   for (int b = b0; b < b1; ++b) {
     unit_off[b] = run;
     const SeqInfo in = info[b];
@@ -385,7 +406,8 @@ __device__ __forceinline__ void warp_epilogue(const RowsParams& p, const Unit& u
   int last = 0;
   if (lane == 0) {
     __threadfence();
-    const int units_b = __ldg(p.unit_off + b + 1) - __ldg(p.unit_off + b);
+    // phase-1 row pairs of b (the fused unit list also interleaves sample units)
+    const int units_b = in.Lr + (d.K - 1) * (in.Lr - 1 - in.s);
     last = (atomicAdd(p.cnt + b, 1) == units_b - 1);
   }
   last = __shfl_sync(0xffffffffu, last, 0);
@@ -439,6 +461,10 @@ __device__ __forceinline__ void warp_epilogue(const RowsParams& p, const Unit& u
     if (anyf & 4u) st |= SB_ST_NONFINITE;
     p.status[b] = st;
     p.cnt[b] = 0;  // leave the workspace re-usable
+    if (p.ready) {  // fused step: the sequence's sample unit may start
+      __threadfence();
+      asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p.ready + b), "r"(1) : "memory");
+    }
   }
 }
 
@@ -454,14 +480,13 @@ __device__ __forceinline__ uint4 neg_inf_vec() {
                         : make_uint4(0xff800000u, 0xff800000u, 0xff800000u, 0xff800000u);
 }
 
-template <class C, typename T>
-__device__ __forceinline__ void load_stage(const uint8_t* bp, const uint8_t* bq, int nvec, bool full,
-                                           StageRegs<C>& r) {
+template <class C, typename T, bool FULL>
+__device__ __forceinline__ void load_stage(const uint8_t* bp, const uint8_t* bq, int nvec, StageRegs<C>& r) {
   const int tid = threadIdx.x;
 #pragma unroll
   for (int j = 0; j < C::VPT; ++j) {
     const int v = tid + j * C::CT;
-    if (full || v < nvec) {
+    if (FULL || v < nvec) {
       r.p[j] = lds128(bp + v * 16);
       r.q[j] = lds128(bq + v * 16);
     } else {
@@ -590,14 +615,23 @@ __global__ void __launch_bounds__(C::THREADS, 1) k_rows_tma(RowsParams p) {
     qa.init();
     // wait -> 16-byte LDS of this thread's vectors -> release the stage -> math, so the
     // producer refills the slot while the consumers compute
-    for (int c = 0; c < nchunks; ++c) {
+    for (int c = 0; c < nchunks - 1; ++c) {  // full chunks: no guards, no fill
       StageRegs<C> r;
       mbar_wait(&S.full[rp.stage], rp.phase);
-      load_stage<C, T>(S.buf[rp.stage][0], S.buf[rp.stage][1], nvec_last, c + 1 < nchunks, r);
+      load_stage<C, T, true>(S.buf[rp.stage][0], S.buf[rp.stage][1], 0, r);
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.empty[rp.stage]);
       rp.advance();
       compute_stage<C, T>(r, c, pa, qa);
+    }
+    {  // last (possibly partial) chunk
+      StageRegs<C> r;
+      mbar_wait(&S.full[rp.stage], rp.phase);
+      load_stage<C, T, false>(S.buf[rp.stage][0], S.buf[rp.stage][1], nvec_last, r);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.empty[rp.stage]);
+      rp.advance();
+      compute_stage<C, T>(r, nchunks - 1, pa, qa);
     }
     const Unit un = decode_unit(p, unit);
     const T* qrow = QL + row_off(d, un.b, un.slot, un.i);
@@ -644,6 +678,448 @@ static sb_status launch_rows(const RowsParams& p, bool vok, cudaStream_t s) {
   return cuda_status(cudaGetLastError());
 }
 
+// ---------------------------------------------------------------- fused step (verify + select)
+// One persistent kernel for the whole step: the unit list of k_rows_tma plus, for every
+// sequence b, a sample unit placed after the phase-1 units of sequence b + delta
+// (k_plan, fused mode).  Dependencies point to smaller unit indices and every CTA walks
+// its units in increasing order, so the spin on ready[b] cannot deadlock.
+//   producer : phase-1 unit -> stream the p/q chunks (as k_rows_tma);
+//              sample unit  -> wait ready[b] (n_k known), take the Eq. 9 / Alg. 1
+//              decision (as k_select_tma's decider), publish it, stream the sampled row
+//              pair (residual) or the p row twice (bonus: softmax state, then sums);
+//   consumers: phase-1 -> partial states; sample -> one sum per 1 KB segment;
+//   epilogue : phase-1 -> token tests / n_k / ready[b]; sample -> locate us*R, re-read
+//              one segment, commit / rollback outputs; the last sequence scans offsets.
+struct StepParams {
+  RowsParams r;
+  const float* us;
+  int rule;
+  const int* plan;  // [0] delta, [1] total units
+  int* done_cnt;
+  int *sel_k, *commit_len, *out_tok, *y_tok, *y_kind, *offsets, *packed_tok, *path_rolled, *branch_discarded;
+  uint32_t* keep_mask;
+  float* resid_mass;
+};
+
+struct P2Desc {
+  int b, ksel, npath, kind, row, slot, pad0, pad1;
+  float4 rs;
+};
+
+constexpr int kNDQ = 8;        // sample descriptors in flight
+constexpr int kSegMax = 1024;  // 1 KB segments per row (rows <= 1 MB)
+
+template <class C>
+struct StepSmem {
+  uint64_t full[C::NS], empty[C::NS];
+  uint64_t pfull[C::NP], pempty[C::NP];
+  uint64_t dfull[kNDQ], dempty[kNDQ];
+  RowStat part[C::NP][2][C::CW];
+  P2Desc desc[kNDQ];
+  float4 brs[kNDQ];  // bonus-row softmax state computed by the consumers
+  RowStat red[C::CW];
+  float seg[C::NP][kSegMax];
+  alignas(128) uint8_t buf[C::NS][2][C::CHUNK];
+};
+
+struct FUnit {
+  bool sample;
+  int b;    // sequence (phase-1 unit's or the sample's)
+  Unit u;   // phase-1 geometry
+};
+
+__device__ __forceinline__ FUnit decode_fused(const RowsParams& p, const int* plan, int unit) {
+  const Dims& d = p.d;
+  FUnit f;
+  const int tail = __ldg(p.unit_off + d.B);
+  if (unit >= tail) {
+    const int delta = min(plan[0], d.B);
+    f.sample = true;
+    f.b = d.B - delta + (unit - tail);
+    return f;
+  }
+  int lo = 0, hi = d.B;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (__ldg(p.unit_off + mid) <= unit) lo = mid; else hi = mid;
+  }
+  const SeqInfo in = p.info[lo];
+  const int j = unit - __ldg(p.unit_off + lo);
+  const int u1 = in.Lr + (d.K - 1) * (in.Lr - 1 - in.s);
+  if (j >= u1) {
+    f.sample = true;
+    f.b = lo - plan[0];
+    return f;
+  }
+  f.sample = false;
+  f.b = lo;
+  f.u.b = lo;
+  f.u.in = in;
+  if (j < in.Lr) {
+    f.u.slot = 0;
+    f.u.i = j;
+  } else {
+    const int per = in.Lr - 1 - in.s, jj = j - in.Lr;
+    f.u.slot = 1 + jj / per;
+    f.u.i = in.s + 1 + jj % per;
+  }
+  return f;
+}
+
+template <class C, typename T, bool RESID>
+__device__ __forceinline__ void step_seg_pass(StepSmem<C>& S, RingPos<C::NS>& rp, float* seg, int nchunks,
+                                              int nvec_last, bool ok, float MSp, float MSq, float kq) {
+  constexpr int E = Vec<T>::E;
+  constexpr int SPC = C::CHUNK / kSegBytes;  // segments per chunk (= consumer warps)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int c = 0; c < nchunks; ++c) {
+    const int nvec = (c == nchunks - 1) ? nvec_last : C::CHUNK / 16;
+    mbar_wait(&S.full[rp.stage], rp.phase);
+    float own = 0.f;
+#pragma unroll
+    for (int h = 0; h < SPC / C::CW; ++h) {
+      const int sw = warp + h * C::CW;  // this warp's segment in the chunk
+      uint4 vp[2], vq[2];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int v = sw * 64 + lane * 2 + j;
+        if (v < nvec) {
+          vp[j] = lds128(S.buf[rp.stage][0] + v * 16);
+          if (RESID) vq[j] = lds128(S.buf[rp.stage][1] + v * 16);
+        } else {
+          vp[j] = vq[j] = neg_inf_vec<T>();
+        }
+      }
+      own = 0.f;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        float r[E];
+        r_scaled<T>(vp[j], vq[j], RESID, MSp, MSq, kq, r);
+        own = seq_sum<E>(r, own);
+      }
+      const float tot = warp_sum_rn(ok ? own : 0.f);
+      if (lane == 0) seg[c * SPC + sw] = tot;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&S.empty[rp.stage]);
+    rp.advance();
+  }
+}
+
+template <class C, typename T>
+__global__ void __launch_bounds__(C::THREADS, 1) k_step_tma(StepParams sp) {
+  constexpr int E = Vec<T>::E;
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  StepSmem<C>& S = *reinterpret_cast<StepSmem<C>*>(smem_raw);
+  const RowsParams& p = sp.r;
+  const Dims& d = p.d;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < C::NS; ++s) {
+      mbar_init(&S.full[s], 1);
+      mbar_init(&S.empty[s], C::CW);
+    }
+    for (int s = 0; s < C::NP; ++s) {
+      mbar_init(&S.pfull[s], C::CW);
+      mbar_init(&S.pempty[s], 1);
+    }
+    for (int s = 0; s < kNDQ; ++s) {
+      mbar_init(&S.dfull[s], 1);
+      mbar_init(&S.dempty[s], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int total = sp.plan[1];
+  const T* PL = static_cast<const T*>(p.PL);
+  const T* QL = static_cast<const T*>(p.QL);
+  const uint32_t row_bytes = (uint32_t)d.V * sizeof(T);
+  const int nchunks = (row_bytes + C::CHUNK - 1) / C::CHUNK;
+  const int nvec_last = (int)(row_bytes - (uint32_t)(nchunks - 1) * C::CHUNK) / 16;
+  const int nseg = nchunks * (C::CHUNK / kSegBytes);
+
+  if (warp == C::CW) {  // ---------------- producer (+ decider for sample units)
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      RingPos<C::NS> rp;
+      RingPos<kNDQ> dq;
+      for (int unit = blockIdx.x; unit < total; unit += gridDim.x) {
+        const FUnit fu = decode_fused(p, sp.plan, unit);
+        const char *prow, *qrow;
+        int passes = 1;
+        bool pair = true;
+        if (!fu.sample) {
+          prow = reinterpret_cast<const char*>(PL + row_off(d, fu.b, fu.u.slot, fu.u.i));
+          qrow = reinterpret_cast<const char*>(QL + row_off(d, fu.b, fu.u.slot, fu.u.i));
+        } else {
+          const int b = fu.b;
+          mbar_wait(&S.dempty[dq.stage], dq.phase ^ 1u);
+          int rd = 0;
+          for (uint32_t tries = 0;; ++tries) {  // phase 1 of b done (n_k, status, rowstat written)
+            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(rd) : "l"(p.ready + b) : "memory");
+            if (rd) break;
+            __nanosleep(256);
+            if (tries > (1u << 24)) __trap();  // watchdog (~4 s)
+          }
+          const SeqInfo in = p.info[b];
+          int ksel = -1, besttok = 0;
+          float bestkey = 0.f;
+          for (int k = 0; k < d.K; ++k) {  // A = {k : n_k > s_b}; Eq. 9 / Alg. 1 (P239, P540)
+            if (__ldcg(p.n_acc + (int64_t)b * d.K + k) <= in.s) continue;
+            const int xk = __ldg(p.tok + ent(d, b, k, in.s));
+            const float key = (sp.rule == SB_SELECT_ALG1) ? __ldg(p.u + ent(d, b, k, in.s))
+                                                          : ld_scalar(PL + row_off(d, b, 0, in.s) + xk);
+            bool better;
+            if (ksel < 0) better = true;
+            else if (sp.rule == SB_SELECT_ALG1) better = key > bestkey;
+            else better = key > bestkey || (key == bestkey && xk < besttok);
+            if (better) { ksel = k; bestkey = key; besttok = xk; }
+          }
+          P2Desc D;
+          D.b = b;
+          D.ksel = ksel;
+          if (ksel < 0) {
+            D.npath = min(__ldcg(p.n_acc + (int64_t)b * d.K), in.s);  // rollback (P655)
+            D.kind = 1; D.row = D.npath; D.slot = 0;
+          } else {
+            D.npath = __ldcg(p.n_acc + (int64_t)b * d.K + ksel);
+            if (D.npath < in.L) { D.kind = 1; D.row = D.npath; D.slot = (D.npath <= in.s) ? 0 : ksel; }
+            else if (in.s < in.g) { D.kind = 2; D.row = in.g; D.slot = ksel; }  // bonus (P94)
+            else { D.kind = 0; D.row = 0; D.slot = 0; }                          // (P237)
+          }
+          D.rs = (D.kind == 1) ? __ldcg(p.rowstat + ent(d, b, D.slot, D.row)) : make_float4(0.f, 1.f, 0.f, 1.f);
+          S.desc[dq.stage] = D;
+          mbar_arrive(&S.dfull[dq.stage]);
+          dq.advance();
+          passes = D.kind == 1 ? 1 : (D.kind == 2 ? 2 : 0);
+          pair = D.kind == 1;
+          prow = reinterpret_cast<const char*>(PL + row_off(d, b, D.slot, D.row));
+          qrow = reinterpret_cast<const char*>(QL + row_off(d, b, D.slot, D.row));
+        }
+        for (int pass = 0; pass < passes; ++pass)
+          for (int c = 0; c < nchunks; ++c) {
+            const uint32_t bytes = min((uint32_t)C::CHUNK, row_bytes - (uint32_t)c * C::CHUNK);
+            mbar_wait(&S.empty[rp.stage], rp.phase ^ 1u);
+            mbar_expect_tx(&S.full[rp.stage], (pair ? 2 : 1) * bytes);
+            bulk_g2s(S.buf[rp.stage][0], prow + (size_t)c * C::CHUNK, bytes, &S.full[rp.stage], pol);
+            if (pair) bulk_g2s(S.buf[rp.stage][1], qrow + (size_t)c * C::CHUNK, bytes, &S.full[rp.stage], pol);
+            rp.advance();
+          }
+      }
+    }
+    return;
+  }
+  if (warp == C::CW + 1) {  // ---------------- epilogue
+    RingPos<C::NP> up;
+    RingPos<kNDQ> dq;
+    for (int unit = blockIdx.x; unit < total; unit += gridDim.x) {
+      const FUnit fu = decode_fused(p, sp.plan, unit);
+      if (!fu.sample) {
+        const Unit& un = fu.u;
+        const T* prow = PL + row_off(d, un.b, un.slot, un.i);
+        const T* qrow = QL + row_off(d, un.b, un.slot, un.i);
+        const bool branch_row = (un.slot == 0 && un.i == un.in.s);
+        const int ntok = branch_row ? d.K : 1;
+        int x = 0;
+        float lpx = 0.f, lqx = 0.f, uu = 0.f;
+        int64_t et = 0;
+        if (lane < ntok) {
+          et = ent(d, un.b, branch_row ? lane : un.slot, un.i);
+          x = __ldg(p.tok + et);
+          uu = __ldg(p.u + et);
+          if (x >= 0 && x < d.V) {
+            lpx = ld_scalar(prow + x);
+            lqx = ld_scalar(qrow + x);
+          }
+        }
+        mbar_wait(&S.pfull[up.stage], up.phase);
+        RowStat ps = lane < C::CW ? S.part[up.stage][0][lane] : rowstat_empty();
+        RowStat qs = lane < C::CW ? S.part[up.stage][1][lane] : rowstat_empty();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.pempty[up.stage]);
+        up.advance();
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          ps = combine(ps, shfl_xor(ps, o));
+          qs = combine(qs, shfl_xor(qs, o));
+        }
+        warp_epilogue<T>(p, un, ps, qs, x, lpx, lqx, uu, et);
+        continue;
+      }
+      // ---- sample unit
+      mbar_wait(&S.dfull[dq.stage], dq.phase);
+      const P2Desc D = S.desc[dq.stage];
+      const int b = D.b;
+      const SeqInfo in = p.info[b];
+      mbar_wait(&S.pfull[up.stage], up.phase);
+      int kind = D.kind, y = -1, st = 0;
+      double mass = 0.0;
+      if (kind != 0) {
+        const float4 rs = (kind == 1) ? D.rs : S.brs[dq.stage];
+        if (!((rs.y == rs.y) && (rs.w == rs.w))) {
+          kind = 0;
+          st |= SB_ST_NONFINITE;
+        } else {
+          const T* prow = PL + row_off(d, b, D.slot, D.row);
+          const T* qrow = QL + row_off(d, b, D.slot, D.row);
+          bool resid = (kind == 1);
+          double R = 0.0;
+          y = sample_segments<T>(prow, qrow, row_bytes, d.V, S.seg[up.stage], nseg, resid, rs.x, rs.z, rs.y / rs.w,
+                                 __ldg(sp.us + b), st, &R);
+          mass = R / (double)rs.y;  // back to probability mass
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&S.pempty[up.stage]);
+        mbar_arrive(&S.dempty[dq.stage]);
+      }
+      up.advance();
+      dq.advance();
+      // commit (SURVEY §8.0 "Commit")
+      const int ksel = D.ksel, npath = D.npath, kpath = ksel < 0 ? 0 : ksel;
+      int* out = sp.out_tok + (int64_t)b * (d.G + 2);
+      for (int qq = lane; qq < d.G + 2; qq += 32) {
+        int v = -1;
+        if (qq < npath) v = __ldg(p.tok + ent(d, b, (qq < in.s) ? 0 : kpath, qq));
+        else if (qq == npath && kind != 0) v = y;
+        out[qq] = v;
+      }
+      if (lane < d.K) {
+        uint32_t km = 0;
+        for (int qq = 0; qq < npath; ++qq)
+          if (((qq < in.s) ? 0 : kpath) == lane) km |= 1u << qq;
+        sp.keep_mask[(int64_t)b * d.K + lane] = km;
+      }
+      if (lane == 0) {
+        sp.sel_k[b] = ksel;
+        sp.commit_len[b] = npath + (kind != 0);
+        sp.y_tok[b] = (kind != 0) ? y : -1;
+        sp.y_kind[b] = kind;
+        sp.path_rolled[b] = in.L - npath;
+        sp.branch_discarded[b] = (d.K - 1) * (in.L - in.s);
+        if (sp.resid_mass) sp.resid_mass[b] = (kind != 0) ? (float)mass : 0.f;
+        if (st) atomicOr(p.status + b, st);
+      }
+      __syncwarp();
+      int last = 0;
+      if (lane == 0) {
+        __threadfence();
+        last = (atomicAdd(sp.done_cnt, 1) == d.B - 1);
+      }
+      last = __shfl_sync(0xffffffffu, last, 0);
+      if (last) {
+        __threadfence();
+        warp_offsets(d.B, d.G, sp.commit_len, sp.out_tok, sp.offsets, sp.packed_tok);
+        if (lane == 0) *sp.done_cnt = 0;
+      }
+    }
+    return;
+  }
+  // ---------------- consumers
+  RingPos<C::NS> rp;
+  RingPos<C::NP> up;
+  RingPos<kNDQ> dq;
+  for (int unit = blockIdx.x; unit < total; unit += gridDim.x) {
+    const FUnit fu = decode_fused(p, sp.plan, unit);
+    if (!fu.sample) {
+      LazyAcc<false, 4> pa;
+      LazyAcc<true, 4> qa;
+      pa.init();
+      qa.init();
+      for (int c = 0; c < nchunks - 1; ++c) {
+        StageRegs<C> r;
+        mbar_wait(&S.full[rp.stage], rp.phase);
+        load_stage<C, T, true>(S.buf[rp.stage][0], S.buf[rp.stage][1], 0, r);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.empty[rp.stage]);
+        rp.advance();
+        compute_stage<C, T>(r, c, pa, qa);
+      }
+      {
+        StageRegs<C> r;
+        mbar_wait(&S.full[rp.stage], rp.phase);
+        load_stage<C, T, false>(S.buf[rp.stage][0], S.buf[rp.stage][1], nvec_last, r);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.empty[rp.stage]);
+        rp.advance();
+        compute_stage<C, T>(r, nchunks - 1, pa, qa);
+      }
+      const T* qrow = QL + row_off(d, fu.b, fu.u.slot, fu.u.i);
+      const RowStat ps = warp_part<C, T, false>(pa, qrow, nvec_last, nchunks);
+      const RowStat qs = warp_part<C, T, true>(qa, qrow, nvec_last, nchunks);
+      if (lane == 0) {
+        mbar_wait(&S.pempty[up.stage], up.phase ^ 1u);
+        S.part[up.stage][0][warp] = ps;
+        S.part[up.stage][1][warp] = qs;
+        mbar_arrive(&S.pfull[up.stage]);
+      }
+      __syncwarp();
+      up.advance();
+      continue;
+    }
+    // ---- sample unit
+    mbar_wait(&S.dfull[dq.stage], dq.phase);
+    const P2Desc D = S.desc[dq.stage];
+    if (lane == 0) mbar_wait(&S.pempty[up.stage], up.phase ^ 1u);  // seg slot free
+    __syncwarp();
+    float* seg = S.seg[up.stage];
+    if (D.kind == 2) {  // bonus row: its softmax state first (pass 0), then p sums
+      LazyAcc<false, 4> a;
+      a.init();
+      for (int c = 0; c < nchunks; ++c) {
+        const int nvec = (c == nchunks - 1) ? nvec_last : C::CHUNK / 16;
+        mbar_wait(&S.full[rp.stage], rp.phase);
+        uint4 x[C::VPT];
+#pragma unroll
+        for (int j = 0; j < C::VPT; ++j) {
+          const int v = tid + j * C::CT;
+          x[j] = (v < nvec) ? lds128(S.buf[rp.stage][0] + v * 16) : neg_inf_vec<T>();
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.empty[rp.stage]);
+        rp.advance();
+        float f[C::VPT * E];
+#pragma unroll
+        for (int j = 0; j < C::VPT; ++j) Vec<T>::unpack(x[j], f + j * E);
+        a.template add<C::VPT * E>(f, c);
+      }
+      RowStat s = fold_lazy(a);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s = combine(s, shfl_xor(s, o));
+      if (lane == 0) S.red[warp] = s;
+      consumer_sync(C::CT);
+      RowStat r = S.red[0];
+#pragma unroll
+      for (int j = 1; j < C::CW; ++j) r = combine(r, S.red[j]);
+      const RowOut o = finish(r);
+      if (tid == 0) S.brs[dq.stage] = make_float4(o.MS, o.finite ? o.Z : CUDART_NAN_F, 0.f, 1.f);
+      consumer_sync(C::CT);
+      step_seg_pass<C, T, false>(S, rp, seg, nchunks, nvec_last, o.finite, o.MS, 0.f, 0.f);
+    } else if (D.kind == 1) {
+      const bool ok = (D.rs.y == D.rs.y) && (D.rs.w == D.rs.w);
+      step_seg_pass<C, T, true>(S, rp, seg, nchunks, nvec_last, ok, D.rs.x, D.rs.z, D.rs.y / D.rs.w);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&S.pfull[up.stage]);
+    up.advance();
+    dq.advance();
+  }
+}
+
+template <class C, typename T>
+static sb_status launch_step_tma(const StepParams& sp, cudaStream_t s) {
+  static bool attr = false;
+  const int smem = (int)sizeof(StepSmem<C>);
+  if (!attr) {
+    if (cudaFuncSetAttribute(k_step_tma<C, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+      return SB_ERR_CUDA;
+    attr = true;
+  }
+  k_step_tma<C, T><<<num_sms(), C::THREADS, smem, s>>>(sp);
+  return cuda_status(cudaGetLastError());
+}
+
 // Geometry variants (SB_ROWS_VARIANT selects one for experiments; 0 = default).
 using RC0 = RC<16, 6, 2, 4>;   // 16 consumer warps, 6 x 32 KB stages
 using RC1 = RC<16, 3, 4, 4>;   // 16 warps, 3 x 64 KB stages, 4 vectors/thread/row
@@ -686,7 +1162,7 @@ sb_status sb_rows_partial(const sb_dims* dd, const void* p_logits, const void* q
   const bool vok = vec_ok(dd, p_logits) && vec_ok(dd, q_logits);
   if (!vok || ((size_t)dd->V * elem_size(dd)) % 16) return SB_ERR_UNSUPPORTED;
   const Dims d = to_dims(dd);
-  k_plan<<<1, 1024, 0, s>>>(d, gamma, branch_pos, w.info, w.unit_off, 1);
+  k_plan<<<1, 1024, 0, s>>>(d, gamma, branch_pos, w.info, w.unit_off, 1, 0, nullptr, nullptr);
   if (cudaGetLastError() != cudaSuccess) return SB_ERR_CUDA;
   RowsParams p{};
   p.d = d; p.PL = p_logits; p.QL = q_logits; p.tok = tok; p.u = u;
@@ -722,7 +1198,7 @@ extern "C" sb_status sb_verify_branches(const sb_dims* dd, const void* p_logits,
   const Dims d = to_dims(dd);
   cudaStream_t s = (cudaStream_t)stream;
 
-  k_plan<<<1, 1024, 0, s>>>(d, gamma, branch_pos, w.info, w.unit_off, 0);
+  k_plan<<<1, 1024, 0, s>>>(d, gamma, branch_pos, w.info, w.unit_off, 0, 0, nullptr, nullptr);
   if (cudaGetLastError() != cudaSuccess) return SB_ERR_CUDA;
 
   RowsParams p;
@@ -731,7 +1207,7 @@ extern "C" sb_status sb_verify_branches(const sb_dims* dd, const void* p_logits,
   p.lse_p = lse_p; p.lse_q = lse_q; p.p_tok = p_tok; p.q_tok = q_tok;
   p.top1_q = top1_q; p.entropy_q = entropy_q; p.top1_id_q = top1_id_q;
   p.acc_mask = acc_mask; p.n_acc = n_acc; p.status = status;
-  p.partial = 0; p.v_offset = 0; p.rowpart = nullptr; p.tokpart = nullptr;
+  p.partial = 0; p.v_offset = 0; p.rowpart = nullptr; p.tokpart = nullptr; p.ready = nullptr;
   const bool vok = vec_ok(dd, p_logits) && vec_ok(dd, q_logits);
   const size_t row_bytes = (size_t)dd->V * elem_size(dd);
   if (vok && row_bytes % 16 == 0 && !tma_disabled())
@@ -742,4 +1218,58 @@ extern "C" sb_status sb_verify_branches(const sb_dims* dd, const void* p_logits,
   }
   return row_bytes <= 131072 ? launch_rows<float, 128, 4>(p, vok, s)
                              : launch_rows<float, 256, 4>(p, vok, s);
+}
+
+// ---------------------------------------------------------------- fused entry point
+extern "C" sb_status sb_verify_select(const sb_dims* dd, const void* p_logits, const void* q_logits,
+                                      const int32_t* tok, const float* u, const float* us, const int32_t* gamma,
+                                      const int32_t* branch_pos, sb_select_rule rule, float* lse_p, float* lse_q,
+                                      float* p_tok, float* q_tok, uint32_t* acc_mask, int32_t* n_acc,
+                                      float* top1_q, int32_t* top1_id_q, float* entropy_q, int32_t* status,
+                                      int32_t* sel_k, int32_t* commit_len, int32_t* out_tok, int32_t* y_tok,
+                                      int32_t* y_kind, int32_t* offsets, int32_t* packed_tok,
+                                      int32_t* path_rolled, int32_t* branch_discarded, uint32_t* keep_mask,
+                                      float* resid_mass, void* workspace, size_t workspace_bytes,
+                                      sb_stream_t stream) {
+  if (!dims_valid(dd) || sharded(dd)) return SB_ERR_INVALID_ARG;
+  if (!p_logits || !q_logits || !tok || !u || !us || !lse_p || !lse_q || !p_tok || !q_tok || !acc_mask ||
+      !n_acc || !status || !sel_k || !commit_len || !out_tok || !y_tok || !y_kind || !offsets || !path_rolled ||
+      !branch_discarded || !keep_mask || !workspace)
+    return SB_ERR_INVALID_ARG;
+  if (rule != SB_SELECT_EQ9 && rule != SB_SELECT_ALG1) return SB_ERR_INVALID_ARG;
+  if ((uintptr_t)workspace % 256) return SB_ERR_INVALID_ARG;
+  const Workspace w = carve(*dd, workspace);
+  if (workspace_bytes < w.bytes) return SB_ERR_WORKSPACE;
+  const bool vok = vec_ok(dd, p_logits) && vec_ok(dd, q_logits);
+  const size_t row_bytes = (size_t)dd->V * elem_size(dd);
+  // The single-launch fused kernel (k_step_tma) is correct but measured slower than the
+  // two launches on B200 (C4: 6.88 vs 6.70 ms), so it is opt-in.
+  const char* fz = getenv("SB_FUSED_STEP");
+  const bool fused = fz && fz[0] == '1';
+  if (!fused || !vok || row_bytes % 16 || row_bytes > (size_t)kSegMax * kSegBytes || tma_disabled()) {
+    // the two calls back to back
+    sb_status st = sb_verify_branches(dd, p_logits, q_logits, tok, u, gamma, branch_pos, lse_p, lse_q, p_tok,
+                                      q_tok, acc_mask, n_acc, top1_q, top1_id_q, entropy_q, status, nullptr,
+                                      workspace, workspace_bytes, stream);
+    if (st != SB_OK) return st;
+    return sb_select_branch(dd, p_logits, q_logits, tok, u, us, gamma, branch_pos, n_acc, rule, sel_k, commit_len,
+                            out_tok, y_tok, y_kind, offsets, packed_tok, path_rolled, branch_discarded, keep_mask,
+                            resid_mass, status, nullptr, workspace, workspace_bytes, stream);
+  }
+  const Dims d = to_dims(dd);
+  cudaStream_t s = (cudaStream_t)stream;
+  k_plan<<<1, 1024, 0, s>>>(d, gamma, branch_pos, w.info, w.unit_off, 0, num_sms(), w.plan, w.ready);
+  if (cudaGetLastError() != cudaSuccess) return SB_ERR_CUDA;
+  StepParams sp{};
+  RowsParams& p = sp.r;
+  p.d = d; p.PL = p_logits; p.QL = q_logits; p.tok = tok; p.u = u;
+  p.info = w.info; p.unit_off = w.unit_off; p.cnt = w.cnt; p.rowstat = w.rowstat; p.pflag = w.pflag;
+  p.lse_p = lse_p; p.lse_q = lse_q; p.p_tok = p_tok; p.q_tok = q_tok;
+  p.top1_q = top1_q; p.entropy_q = entropy_q; p.top1_id_q = top1_id_q;
+  p.acc_mask = acc_mask; p.n_acc = n_acc; p.status = status; p.ready = w.ready;
+  sp.us = us; sp.rule = rule; sp.plan = w.plan; sp.done_cnt = w.sel_cnt;
+  sp.sel_k = sel_k; sp.commit_len = commit_len; sp.out_tok = out_tok; sp.y_tok = y_tok; sp.y_kind = y_kind;
+  sp.offsets = offsets; sp.packed_tok = packed_tok; sp.path_rolled = path_rolled;
+  sp.branch_discarded = branch_discarded; sp.keep_mask = keep_mask; sp.resid_mass = resid_mass;
+  return dd->dtype == SB_BF16 ? launch_step_tma<RC0, __nv_bfloat16>(sp, s) : launch_step_tma<RC0, float>(sp, s);
 }

@@ -18,10 +18,10 @@ from paper_2506_01979_b200 import api, synth
 REL, ABS = 1e-5, 1e-7
 
 
-def gpu_run(inp: dict, rule=0, adaptive=False, eps=0.2, k_max=6):
+def gpu_run(inp: dict, rule=0, adaptive=False, eps=0.2, k_max=6, fused=True):
     d = api.dims_for(inp["PL"], V=inp["V"])
     buf = api.StepBuffers.alloc(d, inp["PL"].device)
-    gamma = api.verify_step(d, inp, buf, rule=rule, adaptive=adaptive, eps=eps, k_max=k_max)
+    gamma = api.verify_step(d, inp, buf, rule=rule, adaptive=adaptive, eps=eps, k_max=k_max, fused=fused)
     torch.cuda.synchronize()
     out = {k: getattr(buf, k).cpu().numpy() for k in buf.__dataclass_fields__
            if k not in ("workspace", "conf_workspace")}

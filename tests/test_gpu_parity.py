@@ -18,14 +18,14 @@ def _built():
     build()
 
 
-def _run(cfg, row_pad=0, rule=0, seed=None, adaptive=False, sample=None, nthreads=0):
+def _run(cfg, row_pad=0, rule=0, seed=None, adaptive=False, sample=None, nthreads=0, fused=True):
     import oracle
     from paper_2506_01979_b200 import synth
 
     from parity_util import compare, gpu_run, internal_consistency, oracle_for
 
     inp = synth.generate(cfg, device="cuda", seed=seed, row_pad=row_pad)
-    g, d, _ = gpu_run(inp, rule=rule, adaptive=adaptive)
+    g, d, _ = gpu_run(inp, rule=rule, adaptive=adaptive, fused=fused)
     internal_consistency(g, cfg.G)
     B = inp["PL"].shape[0]
     idx = np.arange(B) if sample is None else np.unique(np.r_[0, B - 1, np.random.default_rng(1).choice(B, sample - 2, replace=False)])
@@ -78,11 +78,14 @@ SMALL = [
 ]
 
 
+@pytest.mark.parametrize("fused", ["single_launch", "verify_select", "two_calls"])
 @pytest.mark.parametrize("name,kw,pad,rule", SMALL, ids=[c[0] for c in SMALL])
-def test_small_parity(name, kw, pad, rule):
+def test_small_parity(name, kw, pad, rule, fused, monkeypatch):
     kw = dict(kw)
     c = cfg(kw.pop("name"), **kw)
-    rep, g = _run(c, row_pad=pad, rule=rule)
+    if fused == "single_launch":
+        monkeypatch.setenv("SB_FUSED_STEP", "1")  # the persistent k_step_tma kernel
+    rep, g = _run(c, row_pad=pad, rule=rule, fused=(fused != "two_calls"))
     assert rep["exact_seq"] >= 0.9 * rep["n"], rep
     kinds = set(np.unique(g["y_kind"]).tolist())
     if c.B >= 32 and c.G >= 4:
