@@ -33,26 +33,34 @@ def raw(rep):
 
 
 def sass_mix(rep):
+    """Per kernel: executed-instruction mix and stall samples from the SASS source page."""
     out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    if len(rows) < 3:
-        return {}, {}
-    h = rows[1]
-    idx = {n: i for i, n in enumerate(h)}
-    ops, stalls = Counter(), Counter()
-    for r in rows[2:]:
-        if len(r) < 5:
+    res, cur, h = [], None, None
+    for r in rows:
+        if r and r[0] == "Kernel Name":
+            cur = {"name": r[1] if len(r) > 1 else "?", "ops": Counter(), "stalls": Counter()}
+            res.append(cur)
+            h = None
+            continue
+        if cur is None:
+            continue
+        if h is None:
+            h = r
+            idx = {n: i for i, n in enumerate(h)}
+            continue
+        if len(r) < 5 or r[0] == "Address":
             continue
         t = r[idx["Source"]].strip().split()
         if not t:
             continue
         o = (t[1] if t[0].startswith("@") else t[0]).split(".")[0]
-        ops[o] += int(r[idx["Instructions Executed"]] or 0)
+        cur["ops"][o] += int(r[idx["Instructions Executed"]] or 0)
         for k in h:
             if k.startswith("stall_") and "Not Issued" not in k:
-                stalls[k] += int(r[idx[k]] or 0)
-    return ops, stalls
+                cur["stalls"][k] += int(r[idx[k]] or 0)
+    return res
 
 
 def main():
@@ -97,23 +105,23 @@ def main():
                 if a.algo_bytes:
                     lines.append(f"{'algorithmic bytes per launch':60s} {a.algo_bytes:16.0f}")
                     lines.append(f"{'traffic / algorithmic':60s} {traffic / a.algo_bytes:16.4f}")
-                if a.out:
+                if a.out and "rows" in name:  # the dominant kernel's traffic, read by bench.py
                     js = a.out.rsplit(".", 1)[0] + ".json"
                     json.dump({"kernel": name, "dram_bytes_per_launch": traffic,
                                "algorithmic_bytes": a.algo_bytes}, open(js, "w"), indent=1)
             except Exception:
                 pass
-        ops, stalls = sass_mix(a.report)
-        if ops:
+        for k in sass_mix(a.report):
+            ops, stalls = k["ops"], k["stalls"]
             tot = sum(ops.values())
-            lines.append(f"# executed warp instructions: {tot}")
-            if a.elements:
+            lines.append(f"# SASS mix of {k['name'][:80]}: executed warp instructions {tot}")
+            if a.elements and "rows" in k["name"]:
                 lines.append(f"# thread instructions per element: {tot * 32 / a.elements:.2f}")
-            for o, n in ops.most_common(16):
-                lines.append(f"  {o:10s} {n:14d} {n / tot:6.3f}")
+            for o, n in ops.most_common(14):
+                lines.append(f"  {o:10s} {n:14d} {n / max(tot, 1):6.3f}")
             st = sum(stalls.values())
             lines.append("# warp stall samples")
-            for o, n in stalls.most_common(10):
+            for o, n in stalls.most_common(8):
                 lines.append(f"  {o:28s} {n:10d} {n / max(st, 1):6.3f}")
     txt = "\n".join(lines) + "\n"
     if a.out:
