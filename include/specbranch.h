@@ -214,6 +214,36 @@ sb_status sb_draft_confidence(const sb_dims* d, const void* q_logits, const int3
                               size_t workspace_bytes, sb_stream_t stream);
 
 /*
+ * sb_spawn_branches — branch spawn at the branch point (Eq. 7 P216-220).
+ * For each sequence, on the shared draft row s_b of slot 0 (branch_pos, NULL -> 0):
+ *   c = q(x_b): max_x q(x) (SB_CONF_TOP1) or q of tok[b][0][s_b] (SB_CONF_TOKEN);
+ *   k_b = min(V, max(1, floor(k_max (1 - c))))  (Eq. 7, k_max <= 16);
+ *   branch_tok[b][0..k_b) = TopK(q(x_b), k_b) in descending q, ties -> smaller id (S393),
+ *   -1 padded to k_max; branch_prob the matching q (nullable); conf[b] = c (nullable).
+ * A non-finite row gives k_b = 0.  The tokens feed tok[b][k][s_b] of the next verify.
+ */
+sb_status sb_spawn_branches(const sb_dims* d, const void* q_logits, const int32_t* branch_pos,
+                            const int32_t* tok, sb_conf_mode mode, int32_t k_max, int32_t* k_out,
+                            int32_t* branch_tok, float* branch_prob, float* conf,
+                            sb_stream_t stream);
+
+/*
+ * sb_kv_rollback — keep the surviving branch's draft KV rows (P241,
+ * shared-prefix KV P220).  kv: the draft KV of the round, [B][K][G+1] positions of
+ * row_bytes each (16-byte multiple) at row_stride_bytes, token-slot layout (as tok).
+ * With the decisions of sb_select_branch (sel_k, commit_len, y_kind) and branch_pos
+ * (NULL -> 0): the committed draft positions i < n_b = commit_len[b] - [y_kind[b] != 0]
+ * come from slot ts(k*, i) = (i < s_b ? 0 : k*) (slot 0 when k* = -1).
+ *   out_kv != NULL: out_kv[b][i] (layout [B][G+1] at row_stride_bytes) = that row, i < n_b;
+ *   out_kv == NULL: in place, rows i in [s_b, n_b) of slot k* are moved into slot 0.
+ * Rows at i >= n_b are not touched (they are the rolled-back positions).
+ */
+sb_status sb_kv_rollback(int32_t B, int32_t K, int32_t G, const void* kv, int64_t row_bytes,
+                         int64_t row_stride_bytes, const int32_t* branch_pos, const int32_t* sel_k,
+                         const int32_t* commit_len, const int32_t* y_kind, void* out_kv,
+                         sb_stream_t stream);
+
+/*
  * ---- Vocabulary-sharded variant (a7) ----------------------
  * Rank g of G holds the contiguous slice [v_offset, v_offset + V) of the v_total-token
  * vocabulary; slices are in rank order (so global ascending-id order = rank order).

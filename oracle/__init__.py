@@ -69,6 +69,14 @@ _CONF_FIELDS = [
 ]
 
 
+_SPAWN_FIELDS = [("k", np.int32, "b"), ("btok", np.int32, "bkm"), ("bprob", np.float64, "bkm"),
+                 ("conf", np.float64, "b"), ("ties", np.uint32, "b")]
+
+
+class _SpawnOut(ctypes.Structure):
+    _fields_ = [(n, _P) for n, _, _ in _SPAWN_FIELDS]
+
+
 class _VerifyOut(ctypes.Structure):
     _fields_ = [(n, _P) for n, _, _ in _VERIFY_FIELDS]
 
@@ -174,3 +182,38 @@ def row_softmax(L, b, slot, i, V=None):
 
 def adaptive_k(c: float, k_max: int) -> int:
     return lib().oracle_adaptive_k(c, k_max)
+
+
+def spawn(QL, branch_pos=None, tok=None, mode=CONF_TOP1, k_max=6, nthreads=0, V=None):
+    """Eq. 7 branch spawn at each sequence's branch row (slot 0): k_b and TopK tokens."""
+    B, K, R1, stride = QL.shape
+    V = stride if V is None else V
+    d = _dims(QL, B, K, R1 - 1, V)
+    d.row_stride = stride
+    shapes = {"b": (B,), "bkm": (B, k_max)}
+    out = {n: np.empty(shapes[kind], dtype=dt) for n, dt, kind in _SPAWN_FIELDS}
+    o = _SpawnOut(*[_ptr(out[n]) for n, _, _ in _SPAWN_FIELDS])
+    s = None if branch_pos is None else np.ascontiguousarray(branch_pos, dtype=np.int32)
+    t = None if tok is None else np.ascontiguousarray(tok, dtype=np.int32)
+    lib().oracle_spawn.restype = ctypes.c_int
+    rc = lib().oracle_spawn(ctypes.byref(d), _ptr(QL), _ptr(s), _ptr(t), ctypes.c_int(mode), ctypes.c_int(k_max),
+                            ctypes.c_int(nthreads), ctypes.byref(o))
+    if rc != 0:
+        raise ValueError("oracle_spawn rejected its arguments")
+    return out
+
+
+def kv_rollback(kv, branch_pos, sel_k, commit_len, y_kind):
+    """Plain gather of the committed draft KV rows: out[b][i] =
+    kv[b][ts(k*, i)][i] for i < commit_len - [y sampled], ts(k, i) = (i < s_b ? 0 : k).
+    Rows past n_b are left as NaN-free zeros in the returned array."""
+    B, K, R1 = kv.shape[:3]
+    out = np.zeros((B, R1) + kv.shape[3:], dtype=kv.dtype)
+    for b in range(B):
+        n = int(commit_len[b]) - (1 if y_kind[b] != 0 else 0)
+        ks = int(sel_k[b])
+        s = int(branch_pos[b])
+        for i in range(n):
+            slot = 0 if (i < s or ks < 0) else ks
+            out[b, i] = kv[b, slot, i]
+    return out

@@ -348,3 +348,56 @@ int oracle_confidence(const or_dims* d, const void* QL, const int32_t* tok, int 
   }
   return 0;
 }
+
+/* Eq. 7 branch spawn, plain (k_b argmax scans over the fp64 draft distribution). */
+int oracle_spawn(const or_dims* d, const void* QL, const int32_t* branch_pos, const int32_t* tok,
+                 int mode, int k_max, int nthreads, or_spawn_out* o) {
+  if (!dims_ok(d) || !QL || !o || k_max < 1 || (mode == 1 && !tok) || mode < 0 || mode > 1) return -1;
+  const int V = d->V, R1 = d->G + 1;
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nthreads > 0 ? nthreads : omp_default_threads())
+  for (int b = 0; b < d->B; ++b) {
+    int s = branch_pos ? branch_pos[b] : 0;
+    if (s < 0) s = 0;
+    if (s > d->G) s = d->G;
+    double* Q = (double*)malloc(sizeof(double) * V);
+    char* taken = (char*)calloc(V, 1);
+    for (int j = 0; j < k_max; ++j) {
+      o->btok[(int64_t)b * k_max + j] = -1;
+      o->bprob[(int64_t)b * k_max + j] = NAN;
+    }
+    double lse = oracle_row_softmax(d, QL, b, 0, s, Q);
+    uint32_t ties = 0;
+    int k = 0;
+    double c = NAN;
+    if (!isnan(lse)) {
+      if (mode == 0) {
+        c = -1.0;
+        for (int v = 0; v < V; ++v)
+          if (Q[v] > c) c = Q[v];
+      } else {
+        const int x = tok[((int64_t)b * d->K + 0) * R1 + s];
+        c = (x >= 0 && x < V) ? Q[x] : NAN;
+      }
+      if (!isnan(c)) {
+        const double a = (double)k_max * (1.0 - c);
+        if (fabs(a - nearbyint(a)) < TIE_BAND) ties |= OR_TIE_EQ7;
+        k = oracle_adaptive_k(c, k_max); /* Eq. 7 */
+        if (k > V) k = V;
+        for (int j = 0; j < k; ++j) { /* TopK(q(x_b), k): highest q, ties -> smaller id */
+          int best = -1;
+          for (int v = 0; v < V; ++v)
+            if (!taken[v] && (best < 0 || Q[v] > Q[best])) best = v;
+          taken[best] = 1;
+          o->btok[(int64_t)b * k_max + j] = best;
+          o->bprob[(int64_t)b * k_max + j] = Q[best];
+        }
+      }
+    }
+    o->k[b] = k;
+    o->conf[b] = c;
+    o->ties[b] = ties;
+    free(Q);
+    free(taken);
+  }
+  return 0;
+}

@@ -122,6 +122,20 @@ int oracle_confidence(const or_dims* d, const void* QL, const int32_t* tok, int 
 /* Eq. 7 alone (for the SPEC pins): max(1, floor(k_max (1 - c))). */
 int oracle_adaptive_k(double c, int k_max);
 
+/* Branch spawn (Eq. 7 P216-220): at the branch row s_b of slot 0,
+ * c = q(x_b) (mode 0: max_x q(x); mode 1: q of tok[b][0][s_b]),
+ * k_b = min(V, max(1, floor(k_max (1 - c)))), and the k_b tokens of highest q
+ * (ties -> smaller id, S393), found by k_b plain argmax scans. */
+typedef struct {
+  int32_t *k;       /* [B]                                   */
+  int32_t *btok;    /* [B][k_max], -1 padded                 */
+  double *bprob;    /* [B][k_max], NaN padded                */
+  double *conf;     /* [B] c = q(x_b)                        */
+  uint32_t *ties;   /* [B] OR_TIE_EQ7                        */
+} or_spawn_out;
+int oracle_spawn(const or_dims* d, const void* QL, const int32_t* branch_pos, const int32_t* tok,
+                 int mode, int k_max, int nthreads, or_spawn_out* o);
+
 #ifdef __cplusplus
 }
 #endif

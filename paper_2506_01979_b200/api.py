@@ -126,6 +126,24 @@ def sb_draft_confidence(d, q_logits, tok, mode, eps, lam, k_max, top1_prob, top1
     L.check(rc, "sb_draft_confidence")
 
 
+def sb_spawn_branches(d, q_logits, branch_pos, tok, mode, k_max, k_out, branch_tok, branch_prob=None,
+                      conf=None, stream=None):
+    L.check(L.lib().sb_spawn_branches(
+        ctypes.byref(d), _ptr(q_logits, LOG, "q_logits"), _ptr(branch_pos, I32, "branch_pos"), _ptr(tok, I32, "tok"),
+        int(mode), int(k_max), _ptr(k_out, I32, "k_out"), _ptr(branch_tok, I32, "branch_tok"),
+        _ptr(branch_prob, F32, "branch_prob"), _ptr(conf, F32, "conf"), _stream(stream)), "sb_spawn_branches")
+
+
+def sb_kv_rollback(kv: torch.Tensor, branch_pos, sel_k, commit_len, y_kind, out_kv=None, stream=None):
+    """kv: [B][K][G+1][...] (any dtype, row = the trailing dims, contiguous)."""
+    B, K, R1 = kv.shape[:3]
+    row = kv[0, 0, 0].numel() * kv.element_size()
+    L.check(L.lib().sb_kv_rollback(
+        B, K, R1 - 1, ctypes.c_void_p(kv.data_ptr()), row, row, _ptr(branch_pos, I32, "branch_pos"),
+        _ptr(sel_k, I32, "sel_k"), _ptr(commit_len, I32, "commit_len"), _ptr(y_kind, I32, "y_kind"),
+        None if out_kv is None else ctypes.c_void_p(out_kv.data_ptr()), _stream(stream)), "sb_kv_rollback")
+
+
 # ------------------------------------------------------------------ convenience layer
 @dataclass
 class StepBuffers:

@@ -1,0 +1,72 @@
+// sb_kv.cu — sb_kv_rollback: keep the surviving branch's draft KV rows and drop the
+// rest (PAPER P241 "discarding all non-selected branches and their
+// associated KV-Cache", shared-prefix KV P220).  A pure HBM gather: for sequence b the
+// committed draft positions i < n_b (n_b = commit_len - [y sampled]) live in token slot
+// ts(k*, i) = (i < s_b ? 0 : k*); they are copied to out[b][i] (out-of-place), or into
+// slot 0 in place (out = NULL: rows i >= s_b of slot k* move to slot 0, the shared
+// prefix already is slot 0).  16-byte vectors, 8 in flight per thread.
+#include "sb_host.h"
+
+namespace sb {
+
+struct KvParams {
+  int B, K, R1;
+  int64_t row_bytes, stride;  // bytes per position, bytes between positions
+  const char* kv;
+  char* out;
+  const int* bpos;
+  const int* sel_k;
+  const int* commit_len;
+  const int* y_kind;
+};
+
+// one CTA per (sequence, position)
+__global__ void __launch_bounds__(256) k_kv_rollback(KvParams p) {
+  const int b = blockIdx.x / p.R1, i = blockIdx.x % p.R1;
+  const int ks = __ldg(p.sel_k + b);
+  const int n = __ldg(p.commit_len + b) - (__ldg(p.y_kind + b) != 0 ? 1 : 0);
+  int s = p.bpos ? __ldg(p.bpos + b) : 0;
+  s = max(0, s);
+  if (i >= n) return;
+  const int slot = (i < s || ks < 0) ? 0 : ks;
+  const char* src = p.kv + (((int64_t)b * p.K + slot) * p.R1 + i) * p.stride;
+  char* dst;
+  if (p.out) {
+    dst = p.out + ((int64_t)b * p.R1 + i) * p.stride;
+  } else {
+    if (slot == 0) return;  // already in place
+    dst = const_cast<char*>(p.kv) + (((int64_t)b * p.K + 0) * p.R1 + i) * p.stride;
+  }
+  const int64_t nv = p.row_bytes / 16;
+  const uint4* s4 = reinterpret_cast<const uint4*>(src);
+  uint4* d4 = reinterpret_cast<uint4*>(dst);
+  constexpr int U = 8;
+  for (int64_t v = threadIdx.x; v < nv; v += U * blockDim.x) {
+    uint4 x[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j)
+      if (v + j * blockDim.x < nv) x[j] = ldg_stream(s4 + v + j * blockDim.x);
+#pragma unroll
+    for (int j = 0; j < U; ++j)
+      if (v + j * blockDim.x < nv) d4[v + j * blockDim.x] = x[j];
+  }
+}
+
+}  // namespace sb
+
+using namespace sb;
+
+extern "C" sb_status sb_kv_rollback(int32_t B, int32_t K, int32_t G, const void* kv, int64_t row_bytes,
+                                    int64_t row_stride_bytes, const int32_t* branch_pos, const int32_t* sel_k,
+                                    const int32_t* commit_len, const int32_t* y_kind, void* out_kv,
+                                    sb_stream_t stream) {
+  if (B < 1 || K < 1 || G < 0 || G > kMaxG || !kv || !sel_k || !commit_len || !y_kind) return SB_ERR_INVALID_ARG;
+  if (row_bytes <= 0 || row_bytes % 16 || row_stride_bytes < row_bytes || row_stride_bytes % 16) return SB_ERR_INVALID_ARG;
+  if ((uintptr_t)kv % 16 || (uintptr_t)out_kv % 16) return SB_ERR_INVALID_ARG;
+  KvParams p;
+  p.B = B; p.K = K; p.R1 = G + 1; p.row_bytes = row_bytes; p.stride = row_stride_bytes;
+  p.kv = static_cast<const char*>(kv); p.out = static_cast<char*>(out_kv); p.bpos = branch_pos;
+  p.sel_k = sel_k; p.commit_len = commit_len; p.y_kind = y_kind;
+  k_kv_rollback<<<B * (G + 1), 256, 0, (cudaStream_t)stream>>>(p);
+  return cuda_status(cudaGetLastError());
+}

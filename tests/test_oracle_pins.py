@@ -490,3 +490,67 @@ def test_status_flags(orc):
     o = orc.verify(PL * 0, PL * 0, np.zeros((1, 1, 2), np.int32), np.zeros((1, 1, 2)), np.array([0.5]),
                    gamma=[5], branch_pos=[9])
     assert o["status"][0] & orc.ST_GAMMA_CLAMPED and o["status"][0] & orc.ST_BRANCH_CLAMPED
+
+
+# ---------------------------------------------------------------- branch spawn (f1, Eq. 7)
+@pytest.mark.parametrize("case", GOLD["spawn_branches"])
+def test_spawn_examples(orc, case):
+    q = case["q"]
+    QL = logits_from_probs([q, q])[None, None]
+    o = orc.spawn(QL, k_max=case["k_max"])
+    k = case["k"]
+    assert o["k"][0] == k
+    assert o["btok"][0, :k].tolist() == case["tokens"]
+    assert (o["btok"][0, k:] == -1).all()
+    assert np.allclose(o["bprob"][0, :k], np.asarray(q)[case["tokens"]], rtol=1e-6)
+
+
+def test_spawn_topk_is_max_mass_subset_bruteforce(orc):
+    """The spawned set has the largest q-mass of all k-subsets (S437) and respects Eq. 7."""
+    import itertools
+
+    rng = np.random.default_rng(77)
+    for t in range(200):
+        V = int(rng.integers(2, 9))
+        q = rng.dirichlet(np.ones(V) * 0.7)
+        if t % 5 == 0:  # ties
+            q = np.round(q * 8) / 8 + 1e-3
+            q /= q.sum()
+        k_max = int(rng.integers(1, 9))
+        QL = logits_from_probs([q, q])[None, None]
+        o = orc.spawn(QL, k_max=k_max)
+        Q = softmax64(QL[0, 0, 0])
+        c = Q.max()
+        k_ref = min(V, max(1, math.floor(k_max * (1 - c) + 0.0)))
+        if not (o["ties"][0] & orc.TIE_EQ7):
+            assert o["k"][0] == k_ref
+        k = o["k"][0]
+        chosen = o["btok"][0, :k]
+        assert len(set(chosen.tolist())) == k
+        best = max(sum(Q[list(sub)]) for sub in itertools.combinations(range(V), k))
+        assert abs(Q[chosen].sum() - best) < 1e-12
+        # order: descending q, ties -> smaller id
+        pairs = [(-Q[x], x) for x in chosen]
+        assert pairs == sorted(pairs)
+
+
+def test_kv_rollback_rows_are_keep_mask(orc):
+    """f2 pin: the gathered rows are exactly the verify oracle's keep_mask positions
+    (P241 keep the selected branch's KV, discard the rest) — two independent statements
+    of the committed draft positions — and nothing at or past n_b is kept."""
+    import oracle
+    from paper_2506_01979_b200 import synth
+
+    c = synth.config("c2", V=512, B=32, K=3, G=6, layout="mixed")
+    inp_np = synth.to_numpy_inputs(synth.generate(c, device="cpu", seed=41))
+    o = oracle.verify(inp_np["PL"], inp_np["QL"], inp_np["tok"], inp_np["u"], inp_np["us"], inp_np["gamma"],
+                      inp_np["branch_pos"])
+    kv = np.arange(c.B * c.K * (c.G + 1) * 4, dtype=np.int64).reshape(c.B, c.K, c.G + 1, 4)
+    out = oracle.kv_rollback(kv, inp_np["branch_pos"], o["sel_k"], o["commit_len"], o["y_kind"])
+    for b in range(c.B):
+        n = int(o["commit_len"][b]) - int(o["y_kind"][b] != 0)
+        kept = [(k, i) for k in range(c.K) for i in range(c.G + 1) if (int(o["keep_mask"][b, k]) >> i) & 1]
+        assert sorted(i for _, i in kept) == list(range(n)), b  # one kept row per committed position
+        for k, i in kept:
+            assert np.array_equal(out[b, i], kv[b, k, i])
+        assert not out[b, n:].any()
