@@ -21,7 +21,7 @@ _SO = os.path.join(_HERE, "liboracle.so")
 _SRC = os.path.join(_HERE, "oracle.c")
 
 OR_BF16, OR_F32 = 0, 1
-ST_GAMMA_CLAMPED, ST_BRANCH_CLAMPED, ST_BAD_TOKEN, ST_NONFINITE, ST_ZERO_RESID = 1, 2, 4, 8, 16
+ST_GAMMA_CLAMPED, ST_BRANCH_CLAMPED, ST_BAD_TOKEN, ST_NONFINITE, ST_ZERO_RESID, ST_BAD_PARENT = 1, 2, 4, 8, 16, 32
 TIE_ACC_MASK, TIE_ACC_DEC, TIE_SAMPLE, TIE_ILLCOND, TIE_CONF, TIE_EQ7 = 1, 2, 4, 8, 16, 32
 CONF_TOP1, CONF_TOKEN, CONF_ENTROPY = 0, 1, 2
 
@@ -71,6 +71,16 @@ _CONF_FIELDS = [
 
 _SPAWN_FIELDS = [("k", np.int32, "b"), ("btok", np.int32, "bkm"), ("bprob", np.float64, "bkm"),
                  ("conf", np.float64, "b"), ("ties", np.uint32, "b")]
+
+
+_TREE_FIELDS = [("acc_mask", np.uint64, "b"), ("keep_mask", np.uint64, "b"), ("stop_node", np.int32, "b"),
+                ("commit_len", np.int32, "b"), ("out_tok", np.int32, "bn1"), ("y_tok", np.int32, "b"),
+                ("y_kind", np.int32, "b"), ("resid_mass", np.float64, "b"), ("status", np.int32, "b"),
+                ("ties", np.uint32, "b")]
+
+
+class _TreeOut(ctypes.Structure):
+    _fields_ = [(n, _P) for n, _, _ in _TREE_FIELDS]
 
 
 class _SpawnOut(ctypes.Structure):
@@ -200,6 +210,30 @@ def spawn(QL, branch_pos=None, tok=None, mode=CONF_TOP1, k_max=6, nthreads=0, V=
                             ctypes.c_int(nthreads), ctypes.byref(o))
     if rc != 0:
         raise ValueError("oracle_spawn rejected its arguments")
+    return out
+
+
+def tree_verify(PL, QL, parent, tok, u, us, nthreads=0, V=None):
+    """Tree-structured verify (oracle.h oracle_tree_verify; R31).
+    PL, QL [B][N+1][stride] context rows; parent, tok int32 [B][N]; u f32 [B][N]; us f32 [B]."""
+    B, R1, stride = PL.shape
+    N = R1 - 1
+    V = stride if V is None else V
+    d = _dims(PL.reshape(B, 1, R1, stride), B, 1, N, V)
+    d.row_stride = stride
+    assert QL.shape == PL.shape and QL.dtype == PL.dtype
+    shapes = {"b": (B,), "bn1": (B, N + 1)}
+    out = {n: np.empty(shapes[kind], dtype=dt) for n, dt, kind in _TREE_FIELDS}
+    o = _TreeOut(*[_ptr(out[n]) for n, _, _ in _TREE_FIELDS])
+    par = np.ascontiguousarray(parent, dtype=np.int32)
+    t = np.ascontiguousarray(tok, dtype=np.int32)
+    uu = np.ascontiguousarray(u, dtype=np.float32)
+    uss = np.ascontiguousarray(us, dtype=np.float32)
+    lib().oracle_tree_verify.restype = ctypes.c_int
+    rc = lib().oracle_tree_verify(ctypes.byref(d), _ptr(PL), _ptr(QL), _ptr(par), _ptr(t), _ptr(uu), _ptr(uss),
+                                  ctypes.c_int(nthreads), ctypes.byref(o))
+    if rc != 0:
+        raise ValueError("oracle_tree_verify rejected its arguments")
     return out
 
 

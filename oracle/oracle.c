@@ -401,3 +401,100 @@ int oracle_spawn(const or_dims* d, const void* QL, const int32_t* branch_pos, co
   }
   return 0;
 }
+
+/* Tree verify, one sequence (oracle.h; R31).  Every context row that is read
+ * gets its own two-pass softmax; children are scanned linearly in node order. */
+static void tree_one(const or_dims* d, const void* PL, const void* QL, const int32_t* parent,
+                     const int32_t* tok, const float* u, const float* us, or_tree_out* o, int b) {
+  const int N = d->G, V = d->V;
+  const int32_t* par = parent + (int64_t)b * N;
+  const int32_t* tk = tok + (int64_t)b * N;
+  const float* ub = u + (int64_t)b * N;
+  uint32_t st = 0, ties = 0;
+  double* P = (double*)malloc(sizeof(double) * V);
+  double* Q = (double*)malloc(sizeof(double) * V);
+  double* r = (double*)malloc(sizeof(double) * V);
+  uint64_t acc = 0;
+  double* gap = (double*)malloc(sizeof(double) * (N + 1));
+  /* the Match test of every node against its parent's context row (P94, P538) */
+  for (int j = 0; j < N; ++j) {
+    gap[j] = INFINITY;
+    const int pj = par[j];
+    if (pj < -1 || pj >= j) { st |= OR_ST_BAD_PARENT; continue; }
+    const int row = pj + 1;
+    double lp = oracle_row_softmax(d, PL, b, 0, row, P);
+    double lq = oracle_row_softmax(d, QL, b, 0, row, Q);
+    if (isnan(lp) || isnan(lq)) { st |= OR_ST_NONFINITE; continue; }
+    const int x = tk[j];
+    if (x < 0 || x >= V) { st |= OR_ST_BAD_TOKEN; continue; }
+    const double ui = (double)ub[j];
+    if (ui * Q[x] <= P[x]) acc |= 1ull << j; /* Q[x] = 0 accepts (S127) */
+    if (Q[x] > 0.0) gap[j] = fabs(ui - P[x] / Q[x]);
+  }
+  /* the walk: Eq. 9 at every node, no backtracking */
+  int c = -1, npath = 0;
+  uint64_t keep = 0;
+  int32_t* out = o->out_tok + (int64_t)b * (N + 1);
+  for (int i = 0; i <= N; ++i) out[i] = -1;
+  for (;;) {
+    int best = -1, has_child = 0;
+    for (int j = 0; j < N; ++j) {
+      if (par[j] != c || par[j] >= j) continue;
+      has_child = 1;
+      if (gap[j] < TIE_BAND) ties |= OR_TIE_ACC_DEC; /* every child of a walked node decides */
+      if (!((acc >> j) & 1)) continue;
+      if (best < 0) { best = j; continue; }
+      const double kj = oracle_logit(d, PL, b, 0, c + 1, tk[j]);
+      const double kb = oracle_logit(d, PL, b, 0, c + 1, tk[best]);
+      if (kj > kb || (kj == kb && tk[j] < tk[best])) best = j; /* raw target logit (P241) */
+    }
+    if (best < 0) {
+      /* y from row c+1: residual if c has children (all rejected), else bonus */
+      int ykind = has_child ? 1 : 2, y = -1;
+      double mass = 0.0;
+      double lp = oracle_row_softmax(d, PL, b, 0, c + 1, P);
+      double lq = ykind == 1 ? oracle_row_softmax(d, QL, b, 0, c + 1, Q) : 0.0;
+      if (isnan(lp) || isnan(lq)) {
+        st |= OR_ST_NONFINITE;
+        ykind = 0;
+      } else {
+        for (int v = 0; v < V; ++v) r[v] = (ykind == 1) ? fmax(0.0, P[v] - Q[v]) : P[v];
+        double R = 0.0, mg = 0.0;
+        for (int v = 0; v < V; ++v) R += r[v];
+        if (ykind == 1 && R == 0.0) {
+          st |= OR_ST_ZERO_RESID;
+          for (int v = 0; v < V; ++v) r[v] = P[v];
+        }
+        y = inverse_cdf(r, V, (double)us[b], &R, &mg);
+        mass = R;
+        if (mg < TIE_BAND) ties |= OR_TIE_SAMPLE;
+        if (ykind == 1 && R < 1e-4) ties |= OR_TIE_ILLCOND;
+      }
+      if (ykind != 0) out[npath] = y;
+      o->stop_node[b] = c;
+      o->commit_len[b] = npath + (ykind != 0);
+      o->y_tok[b] = ykind ? y : -1;
+      o->y_kind[b] = ykind;
+      o->resid_mass[b] = mass;
+      break;
+    }
+    out[npath++] = tk[best];
+    keep |= 1ull << best;
+    c = best;
+  }
+  o->acc_mask[b] = acc;
+  o->keep_mask[b] = keep;
+  o->status[b] = (int32_t)st;
+  o->ties[b] = ties;
+  free(P); free(Q); free(r); free(gap);
+}
+
+int oracle_tree_verify(const or_dims* d, const void* PL, const void* QL, const int32_t* parent,
+                       const int32_t* tok, const float* u, const float* us, int nthreads, or_tree_out* o) {
+  if (!d || d->K != 1 || d->G < 1 || d->G > 63 || d->V < 2 || d->row_stride < d->V ||
+      (d->dtype != OR_BF16 && d->dtype != OR_F32) || !PL || !QL || !parent || !tok || !u || !us || !o)
+    return -1;
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nthreads > 0 ? nthreads : omp_default_threads())
+  for (int b = 0; b < d->B; ++b) tree_one(d, PL, QL, parent, tok, u, us, o, b);
+  return 0;
+}

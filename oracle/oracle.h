@@ -39,6 +39,7 @@ extern "C" {
 #define OR_ST_BAD_TOKEN 4u      /* a path token outside [0, V): counted rejected */
 #define OR_ST_NONFINITE 8u      /* a row read has NaN/+inf, or is all -inf       */
 #define OR_ST_ZERO_RESID 16u    /* residual mass R == 0 after a rejection -> P   */
+#define OR_ST_BAD_PARENT 32u    /* tree: parent[j] outside [-1, j): node rejected */
 
 /* near-tie flags (oracle only): the decision is within the fp32 error band */
 #define OR_TIE_ACC_MASK 1u  /* |u - P/Q| < 1e-6 at some tested row             */
@@ -135,6 +136,32 @@ typedef struct {
 } or_spawn_out;
 int oracle_spawn(const or_dims* d, const void* QL, const int32_t* branch_pos, const int32_t* tok,
                  int mode, int k_max, int nthreads, or_spawn_out* o);
+
+/* Tree-structured verify (the dense-tree structure of Appendix F,
+ * P1057, that the paper compares against), read as Eq. 9 applied at every node
+ * (reading R31).  Per sequence: N draft nodes j with token tok[j], parent
+ * parent[j] in [-1, j) (-1 = the committed context), uniform u[j].  Logit rows are
+ * contexts: row 0 = the committed context, row j+1 = the context after node j; d->K
+ * must be 1 and d->G = N (rows [B][N+1]).
+ *   acc(j)  = u_j Q_r[x_j] <= P_r[x_j], r = parent[j] + 1            (P94 Match, P538)
+ *   walk:   c = -1; while some child of c is accepted: c = the accepted child of
+ *           largest raw target logit P-logit_r[x_j] (ties: smaller token, smaller j)
+ *                                                                   (Eq. 9, P236-241)
+ *   commit: the path's tokens, then y from row c+1: norm(max(0, p - q)) if c has a
+ *           child (all rejected), else the bonus p (c is a leaf).     (P94, P554) */
+typedef struct {
+  uint64_t *acc_mask;   /* [B] bit j = acc(j)                               */
+  uint64_t *keep_mask;  /* [B] bit j = node j is on the committed path      */
+  int32_t *stop_node;   /* [B] c (-1 = the root)                            */
+  int32_t *commit_len;  /* [B] path length + [y]                            */
+  int32_t *out_tok;     /* [B][N+1] path tokens, then y; -1 padded          */
+  int32_t *y_tok, *y_kind; /* [B] kind 1 residual, 2 bonus, 0 none (bad row) */
+  double *resid_mass;   /* [B]                                              */
+  int32_t *status;      /* [B] OR_ST_*                                      */
+  uint32_t *ties;       /* [B] OR_TIE_ACC_DEC | OR_TIE_SAMPLE | OR_TIE_ILLCOND */
+} or_tree_out;
+int oracle_tree_verify(const or_dims* d, const void* PL, const void* QL, const int32_t* parent,
+                       const int32_t* tok, const float* u, const float* us, int nthreads, or_tree_out* o);
 
 #ifdef __cplusplus
 }

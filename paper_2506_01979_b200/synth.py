@@ -73,36 +73,42 @@ def _peak_height(c: torch.Tensor, V: int) -> torch.Tensor:
     return torch.log(c / (1.0 - c)) + math.log(V - 1) + 2.0
 
 
+def _rows(cfg: Config, g: torch.Generator, shape: tuple, device):
+    """Target / draft logit rows of the recipe (DESIGN.md §"Input recipe"), shape + (V,)."""
+    V = cfg.V
+    f32 = torch.float32
+    z = torch.randn(shape + (V,), generator=g, device=device, dtype=f32)
+    lp = 2.0 * z
+    vstar = torch.randint(0, V, shape, generator=g, device=device)
+    low = torch.rand(shape, generator=g, device=device) < cfg.pi_low
+    c_low = 0.02 + 0.18 * torch.rand(shape, generator=g, device=device)
+    c_high = 0.30 + 0.69 * torch.rand(shape, generator=g, device=device)
+    h = _peak_height(torch.where(low, c_low, c_high), V)
+    lp.scatter_(-1, vstar.unsqueeze(-1), h.unsqueeze(-1))
+    # draft logits: target plus noise; with prob 1 - rho_same the draft peak moves
+    z2 = torch.randn(shape + (V,), generator=g, device=device, dtype=f32)
+    lq = lp + cfg.delta * z2
+    move = torch.rand(shape, generator=g, device=device) >= cfg.rho_same
+    vmove = torch.randint(0, V, shape, generator=g, device=device)
+    bulk_at_star = 2.0 * z.gather(-1, vstar.unsqueeze(-1)).squeeze(-1)
+    noise_star = z2.gather(-1, vstar.unsqueeze(-1)).squeeze(-1)
+    noise_move = z2.gather(-1, vmove.unsqueeze(-1)).squeeze(-1)
+    # the draft bulk mass grows by E[exp(delta z')] = exp(delta^2/2); lifting the draft
+    # peak by delta^2/2 keeps the draft's own top-1 confidence distributed like c
+    hq = h + 0.5 * cfg.delta * cfg.delta
+    new_star = torch.where(move, bulk_at_star + cfg.delta * noise_star, hq + cfg.delta * noise_star)
+    lq.scatter_(-1, vstar.unsqueeze(-1), new_star.unsqueeze(-1))
+    cur_move = lq.gather(-1, vmove.unsqueeze(-1)).squeeze(-1)
+    lq.scatter_(-1, vmove.unsqueeze(-1), torch.where(move, hq + cfg.delta * noise_move, cur_move).unsqueeze(-1))
+    return lp, lq
+
+
 def _one_sequence(cfg: Config, seed: int, b: int, device, gamma_b: int, s_b: int):
     K, G, V = cfg.K, cfg.G, cfg.V
     R1 = G + 1
     g = _gen(seed, b, device)
     f32 = torch.float32
-    z = torch.randn((K, R1, V), generator=g, device=device, dtype=f32)
-    lp = 2.0 * z
-    vstar = torch.randint(0, V, (K, R1), generator=g, device=device)
-    low = torch.rand((K, R1), generator=g, device=device) < cfg.pi_low
-    c_low = 0.02 + 0.18 * torch.rand((K, R1), generator=g, device=device)
-    c_high = 0.30 + 0.69 * torch.rand((K, R1), generator=g, device=device)
-    h = _peak_height(torch.where(low, c_low, c_high), V)
-    lp.scatter_(2, vstar.unsqueeze(-1), h.unsqueeze(-1))
-    # draft logits: target plus noise; with prob 1 - rho_same the draft peak moves
-    z2 = torch.randn((K, R1, V), generator=g, device=device, dtype=f32)
-    lq = lp + cfg.delta * z2
-    move = torch.rand((K, R1), generator=g, device=device) >= cfg.rho_same
-    vmove = torch.randint(0, V, (K, R1), generator=g, device=device)
-    bulk_at_star = 2.0 * z.gather(2, vstar.unsqueeze(-1)).squeeze(-1)
-    noise_star = z2.gather(2, vstar.unsqueeze(-1)).squeeze(-1)
-    noise_move = z2.gather(2, vmove.unsqueeze(-1)).squeeze(-1)
-    # the draft bulk mass grows by E[exp(delta z')] = exp(delta^2/2); lifting the draft
-    # peak by delta^2/2 keeps the draft's own top-1 confidence distributed like c
-    hq = h + 0.5 * cfg.delta * cfg.delta
-    new_star = torch.where(move, bulk_at_star + cfg.delta * noise_star, hq + cfg.delta * noise_star)
-    lq.scatter_(2, vstar.unsqueeze(-1), new_star.unsqueeze(-1))
-    cur_move = lq.gather(2, vmove.unsqueeze(-1)).squeeze(-1)
-    lq.scatter_(2, vmove.unsqueeze(-1), torch.where(move, hq + cfg.delta * noise_move, cur_move).unsqueeze(-1))
-    del z, z2
-
+    lp, lq = _rows(cfg, g, (K, R1), device)
     ldt = torch.bfloat16 if cfg.dtype == "bf16" else torch.float32
     PL = lp.to(ldt)
     QL = lq.to(ldt)
@@ -183,4 +189,97 @@ def to_numpy_inputs(inp: dict):
     for k in ("tok", "u", "us", "gamma", "branch_pos"):
         out[k] = inp[k].detach().cpu().contiguous().numpy()
     out["V"] = inp["V"]
+    return out
+
+
+# ---------------------------------------------------------------- token trees (f3)
+def tree_parents(shape: str, N: int | None = None, branching=(2, 2, 2, 2), depth: int = 6, b: int = 0,
+                 seed: int = 0) -> list[int]:
+    """Parent pointers in topological (BFS) order, -1 = the committed context.
+
+    dense:  every node of level l has branching[l] children (SpecInfer-style dense tree,
+            Appendix F P1057: (k^gamma - 1)/(k - 1) nodes for a k-ary tree);
+    chain:  N nodes in one path (plain speculative decoding, Alg. 1);
+    random: N nodes, each attached to a uniformly drawn earlier node (or the root) of
+            depth < `depth` (a sparse tree of mixed widths)."""
+    if shape == "dense":
+        par, level = [], [-1]
+        for k in branching:
+            nxt = []
+            for p in level:
+                for _ in range(k):
+                    par.append(p)
+                    nxt.append(len(par) - 1)
+            level = nxt
+        return par
+    if shape == "chain":
+        return list(range(-1, N - 1))
+    if shape == "random":
+        g = torch.Generator().manual_seed(seed * 7_919 + b * 104_729 + 3)
+        par, dep = [], []
+        for j in range(N):
+            while True:
+                p = int(torch.randint(-1, j, (1,), generator=g)) if j > 0 else -1
+                d = 0 if p < 0 else dep[p] + 1
+                if d < depth:
+                    break
+            par.append(p)
+            dep.append(d)
+        # BFS renumbering keeps parent < child and groups siblings
+        order = sorted(range(N), key=lambda j: (dep[j], j))
+        new = {old: i for i, old in enumerate(order)}
+        return [(-1 if par[o] < 0 else new[par[o]]) for o in order]
+    raise ValueError(shape)
+
+
+def generate_tree(cfg: Config, shape: str = "dense", B: int | None = None, N: int | None = None,
+                  branching=(2, 2, 2, 2), depth: int = 6, device="cpu", seed: int = 7):
+    """Seeded token-tree inputs: rows [B][N+1][V] (row 0 = committed context, row j+1 =
+    context after node j), parent / tok int32 [B][N], u f32 [B][N], us f32 [B].
+    Children of one context are the TopK of its draft row (distinct tokens, the SpecInfer
+    expansion); a lone child is a Gumbel-max sample of the draft row (x ~ q)."""
+    B = cfg.B if B is None else B
+    ldt = torch.bfloat16 if cfg.dtype == "bf16" else torch.float32
+    pars = [tree_parents(shape, N, branching, depth, b, seed) for b in range(B)]
+    N = len(pars[0])
+    assert all(len(p) == N for p in pars) and 1 <= N <= 63
+    V = cfg.V
+    PL = torch.empty((B, N + 1, V), dtype=ldt, device=device)
+    QL = torch.empty((B, N + 1, V), dtype=ldt, device=device)
+    tok = torch.empty((B, N), dtype=torch.int32)
+    u = torch.empty((B, N), dtype=torch.float32)
+    us = torch.empty((B,), dtype=torch.float32)
+    for b in range(B):
+        g = _gen(seed + 77, b, device)
+        lp, lq = _rows(cfg, g, (N + 1,), device)
+        PL[b] = lp.to(ldt)
+        QL[b] = lq.to(ldt)
+        q = QL[b].float()
+        kids: dict[int, list[int]] = {}
+        for j, p in enumerate(pars[b]):
+            kids.setdefault(p, []).append(j)
+        for p, js in kids.items():
+            row = q[p + 1]
+            if len(js) == 1:
+                gum = torch.rand((V,), generator=g, device=device).clamp_(min=1e-12)
+                t = [int(torch.argmax(row - torch.log(-torch.log(gum))))]
+            else:
+                t = torch.topk(row, min(len(js), V)).indices.tolist()
+            for j, x in zip(js, t + [t[-1]] * (len(js) - len(t))):
+                tok[b, j] = x
+        u[b] = torch.rand((N,), generator=g, device=device).cpu()
+        us[b] = float(torch.rand((1,), generator=g, device=device))
+    parent = torch.tensor(pars, dtype=torch.int32)
+    return dict(PL=PL, QL=QL, parent=parent.to(device), tok=tok.to(device), u=u.to(device), us=us.to(device),
+                V=V, N=N)
+
+
+def tree_to_numpy(inp: dict):
+    out = {}
+    for k in ("PL", "QL"):
+        t = inp[k].detach().cpu().contiguous()
+        out[k] = t.view(torch.int16).numpy().view("uint16") if t.dtype == torch.bfloat16 else t.numpy()
+    for k in ("parent", "tok", "u", "us"):
+        out[k] = inp[k].detach().cpu().contiguous().numpy()
+    out["V"], out["N"] = inp["V"], inp["N"]
     return out

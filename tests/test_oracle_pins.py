@@ -554,3 +554,111 @@ def test_kv_rollback_rows_are_keep_mask(orc):
         for k, i in kept:
             assert np.array_equal(out[b, i], kv[b, k, i])
         assert not out[b, n:].any()
+
+
+def _branch_as_tree(inp_np, b):
+    """Map sequence b of a branch-layout round (SURVEY §8.0 slot maps) to a token tree:
+    shared prefix tokens i < s as a chain, then K chains for i in [s, L).  Context row
+    after token i of branch k is the physical row ls(k, i+1) = (i+1 <= s ? 0 : k)."""
+    PL, QL, tok, u = inp_np["PL"][b], inp_np["QL"][b], inp_np["tok"][b], inp_np["u"][b]
+    K, R1, V = PL.shape
+    g, s = int(inp_np["gamma"][b]), int(inp_np["branch_pos"][b])
+    L = g if s < g else g + 1
+    rows_p, rows_q = [PL[0, 0]], [QL[0, 0]]
+    par, tk, uu, where = [], [], [], {}
+    for i in range(s):
+        par.append(i - 1)
+        tk.append(tok[0, i]); uu.append(u[0, i])
+        rows_p.append(PL[0, i + 1]); rows_q.append(QL[0, i + 1])
+        where[(0, i)] = len(par) - 1
+    for k in range(K):
+        prev = s - 1
+        for i in range(s, L):
+            par.append(prev)
+            tk.append(tok[k, i]); uu.append(u[k, i])
+            ls = 0 if i + 1 <= s else k
+            rows_p.append(PL[ls, i + 1]); rows_q.append(QL[ls, i + 1])
+            prev = len(par) - 1
+            where[(k, i)] = prev
+    return (np.stack(rows_p), np.stack(rows_q), np.array(par, np.int32), np.array(tk, np.int32),
+            np.array(uu, np.float32), L, s, where)
+
+
+@pytest.mark.parametrize("K,dtype", [(1, "f32"), (3, "bf16"), (4, "f32")])
+def test_tree_verify_reduces_to_branch_contract(orc, K, dtype):
+    """f3 pin: a prefix-plus-K-chains tree is exactly SpecBranch's branch layout, so the
+    tree walk (Eq. 9 at every node) must reproduce oracle.verify's commit, selected
+    path and sampled y; K = 1 is the chain of plain speculative decoding (Alg. 1, P94).
+    Cases with s = gamma (no bonus row inside the tensor) are skipped by construction."""
+    import oracle
+    from paper_2506_01979_b200 import synth
+
+    c = synth.config("c2", V=400, B=40, K=K, G=6, layout="mixed", dtype=dtype)
+    inp_np = synth.to_numpy_inputs(synth.generate(c, device="cpu", seed=71))
+    o = oracle.verify(inp_np["PL"], inp_np["QL"], inp_np["tok"], inp_np["u"], inp_np["us"], inp_np["gamma"],
+                      inp_np["branch_pos"])
+    checked = 0
+    for b in range(c.B):
+        if int(inp_np["branch_pos"][b]) >= int(inp_np["gamma"][b]):
+            continue
+        PLt, QLt, par, tk, uu, L, s, where = _branch_as_tree(inp_np, b)
+        t = oracle.tree_verify(PLt[None], QLt[None], par[None], tk[None], uu[None], inp_np["us"][b:b + 1])
+        assert t["commit_len"][0] == o["commit_len"][b], b
+        assert np.array_equal(t["out_tok"][0, : t["commit_len"][0]], o["out_tok"][b, : o["commit_len"][b]]), b
+        assert t["y_kind"][0] == o["y_kind"][b] and t["y_tok"][0] == o["y_tok"][b], b
+        for (k, i), j in where.items():
+            assert ((int(t["acc_mask"][0]) >> j) & 1) == ((int(o["acc_mask"][b, k]) >> i) & 1), (b, k, i)
+            assert ((int(t["keep_mask"][0]) >> j) & 1) == ((int(o["keep_mask"][b, k]) >> i) & 1), (b, k, i)
+        checked += 1
+    assert checked >= 10
+
+
+@pytest.mark.parametrize("shape,kw", [("dense", dict(branching=(3, 2, 2))), ("random", dict(N=40, depth=7)),
+                                      ("chain", dict(N=12))])
+def test_tree_walk_is_valid(orc, shape, kw):
+    """f3 pin: the committed path is a root path of accepted nodes; at every step the
+    chosen child has the largest raw target logit among its accepted siblings (ties to
+    the smaller token); the walk stops at a node none of whose children is accepted,
+    and y is residual there iff that node has children (a leaf gives the bonus)."""
+    import oracle
+    from paper_2506_01979_b200 import synth
+
+    c = synth.config("c2", V=257, dtype="f32")
+    t = synth.tree_to_numpy(synth.generate_tree(c, shape, B=48, seed=5, **kw))
+    o = oracle.tree_verify(t["PL"], t["QL"], t["parent"], t["tok"], t["u"], t["us"])
+    N = t["N"]
+    for b in range(48):
+        par, tk, acc = t["parent"][b], t["tok"][b], int(o["acc_mask"][b])
+        kids = lambda p: [j for j in range(N) if par[j] == p]  # noqa: E731
+        c_node, path = -1, []
+        while True:
+            a = [j for j in kids(c_node) if (acc >> j) & 1]
+            if not a:
+                break
+            key = lambda j: (-float(t["PL"][b, c_node + 1, tk[j]]), int(tk[j]), j)  # noqa: E731
+            c_node = min(a, key=key)
+            path.append(c_node)
+        assert o["stop_node"][b] == c_node
+        n = len(path)
+        assert np.array_equal(o["out_tok"][b, :n], tk[path])
+        assert int(o["keep_mask"][b]) == sum(1 << j for j in path)
+        assert o["y_kind"][b] == (1 if kids(c_node) else 2)
+        assert o["commit_len"][b] == n + 1 and 0 <= o["y_tok"][b] < c.V
+
+
+def test_tree_accept_test_closed_form(orc):
+    """f3 pin: a two-node tree with hand-set rows.  Root context p = (1/2, 1/4, 1/4),
+    q = (1/4, 1/4, 1/2) (logits ln of these): child token 2 has p/q = 1/2 so u = 0.4
+    accepts and u = 0.6 rejects (P94); token 0 has p/q = 2 and always accepts."""
+    import oracle
+
+    lp = np.log(np.array([0.5, 0.25, 0.25], np.float32))
+    lq = np.log(np.array([0.25, 0.25, 0.5], np.float32))
+    PL = np.stack([lp, lp, lp])[None].astype(np.float32)
+    QL = np.stack([lq, lq, lq])[None].astype(np.float32)
+    for u2, acc2 in [(0.4, 1), (0.6, 0)]:
+        t = oracle.tree_verify(PL, QL, np.array([[-1, -1]], np.int32), np.array([[2, 0]], np.int32),
+                               np.array([[u2, 0.99]], np.float32), np.array([0.5], np.float32))
+        assert int(t["acc_mask"][0]) == (acc2 * 1 | 2)
+        # both accepted -> Eq. 9 picks the larger target logit: token 0 (p = 1/2)
+        assert t["stop_node"][0] == 1 and t["out_tok"][0, 0] == 0 and t["y_kind"][0] == 2
