@@ -71,6 +71,7 @@ typedef enum { SB_CONF_TOP1 = 0, SB_CONF_TOKEN = 1, SB_CONF_ENTROPY = 2 } sb_con
 #define SB_ST_BAD_TOKEN 4u      /* a path token outside [0,V): that test counts rejected */
 #define SB_ST_NONFINITE 8u      /* a row read holds NaN/+inf or is all -inf              */
 #define SB_ST_ZERO_RESID 16u    /* residual mass R == 0 after a rejection: sampled from p */
+#define SB_ST_BAD_PARENT 32u    /* tree: parent[j] outside [-1, j): node j counts rejected */
 
 typedef struct {
   int32_t B;          /* sequences, >= 1                                              */
@@ -242,6 +243,32 @@ sb_status sb_kv_rollback(int32_t B, int32_t K, int32_t G, const void* kv, int64_
                          int64_t row_stride_bytes, const int32_t* branch_pos, const int32_t* sel_k,
                          const int32_t* commit_len, const int32_t* y_kind, void* out_kv,
                          sb_stream_t stream);
+
+/*
+ * sb_tree_verify — token-tree verification (the dense-tree structure of
+ * Appendix F, P1057/P1073), read as Eq. 9 (P236-241) applied at every node
+ * (R31).  Per sequence: N = d->G draft nodes (1 <= N <= 63, d->K must be 1),
+ * node j with token tok[b][j], parent[b][j] in [-1, j) (-1 = the committed context;
+ * topological order), uniform u[b][j]; us[b] for the sample.  Logit rows are contexts,
+ * [B][N+1][row_stride] (seq_stride 0 -> (N+1)*row_stride): row 0 = the committed context,
+ * row j+1 = the context after node j.  The q row of a childless context is never read.
+ *   acc(j) = u_j Q_r[x_j] <= P_r[x_j], r = parent[j] + 1                        (P94)
+ *   walk:  c = -1; while a child of c is accepted, c = the accepted child of largest
+ *          raw target logit at row c+1 (ties: smaller token, then smaller j)   (Eq. 9)
+ *   y:     from row c+1, residual norm(max(0,p-q)) if c has a child, else bonus p.
+ * Outputs (device, overwritten): acc_mask [B] (bit j = acc(j)), keep_mask [B] (bit j =
+ * node j committed), stop_node [B] (c), commit_len [B], out_tok [B][N+1] (path tokens,
+ * y, -1 padded), y_tok, y_kind [B] (1 residual, 2 bonus, 0 none), resid_mass [B] (may be
+ * NULL), status [B] (SB_ST_*).  workspace: >= sb_tree_workspace_bytes(d), 16-byte aligned.
+ * Errors: SB_ERR_INVALID_ARG (dims / pointers), SB_ERR_WORKSPACE, SB_ERR_UNSUPPORTED
+ * (V too large for the sampler's tile table), SB_ERR_CUDA (launch).
+ */
+size_t sb_tree_workspace_bytes(const sb_dims* d);
+sb_status sb_tree_verify(const sb_dims* d, const void* p_logits, const void* q_logits, const int32_t* parent,
+                         const int32_t* tok, const float* u, const float* us, uint64_t* acc_mask,
+                         uint64_t* keep_mask, int32_t* stop_node, int32_t* commit_len, int32_t* out_tok,
+                         int32_t* y_tok, int32_t* y_kind, float* resid_mass, int32_t* status, void* workspace,
+                         size_t workspace_bytes, sb_stream_t stream);
 
 /*
  * ---- Vocabulary-sharded variant (a7) ----------------------

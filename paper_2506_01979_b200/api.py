@@ -144,6 +144,46 @@ def sb_kv_rollback(kv: torch.Tensor, branch_pos, sel_k, commit_len, y_kind, out_
         None if out_kv is None else ctypes.c_void_p(out_kv.data_ptr()), _stream(stream)), "sb_kv_rollback")
 
 
+class TreeBuffers:
+    """Outputs + workspace of sb_tree_verify for B sequences of N nodes."""
+
+    def __init__(self, d: L.sb_dims, device="cuda"):
+        B, N = d.B, d.G
+        i32 = dict(dtype=I32, device=device)
+        self.acc_mask = torch.zeros(B, dtype=torch.int64, device=device)
+        self.keep_mask = torch.zeros(B, dtype=torch.int64, device=device)
+        self.stop_node = torch.empty(B, **i32)
+        self.commit_len = torch.empty(B, **i32)
+        self.out_tok = torch.empty((B, N + 1), **i32)
+        self.y_tok = torch.empty(B, **i32)
+        self.y_kind = torch.empty(B, **i32)
+        self.resid_mass = torch.empty(B, dtype=F32, device=device)
+        self.status = torch.empty(B, **i32)
+        n = int(L.lib().sb_tree_workspace_bytes(ctypes.byref(d)))
+        if n == 0:
+            raise ValueError("invalid tree dims")
+        self.workspace = torch.empty(n, dtype=torch.uint8, device=device)
+
+
+def tree_dims(logits: torch.Tensor, V: int | None = None) -> L.sb_dims:
+    """sb_dims of [B][N+1][row_stride] context rows (K = 1, G = N)."""
+    if logits.dim() != 3:
+        raise ValueError("tree logits must be [B][N+1][row_stride]")
+    return dims_for(logits.unsqueeze(1), V=V)
+
+
+def sb_tree_verify(d, p_logits, q_logits, parent, tok, u, us, buf: TreeBuffers, stream=None):
+    """Token-tree verify (include/specbranch.h sb_tree_verify)."""
+    L.check(L.lib().sb_tree_verify(
+        ctypes.byref(d), _ptr(p_logits, LOG, "p_logits"), _ptr(q_logits, LOG, "q_logits"),
+        _ptr(parent, I32, "parent"), _ptr(tok, I32, "tok"), _ptr(u, F32, "u"), _ptr(us, F32, "us"),
+        _ptr(buf.acc_mask, torch.int64, "acc_mask"), _ptr(buf.keep_mask, torch.int64, "keep_mask"),
+        _ptr(buf.stop_node, I32, "stop_node"), _ptr(buf.commit_len, I32, "commit_len"),
+        _ptr(buf.out_tok, I32, "out_tok"), _ptr(buf.y_tok, I32, "y_tok"), _ptr(buf.y_kind, I32, "y_kind"),
+        _ptr(buf.resid_mass, F32, "resid_mass"), _ptr(buf.status, I32, "status"),
+        _ptr(buf.workspace, torch.uint8, "workspace"), buf.workspace.numel(), _stream(stream)), "sb_tree_verify")
+
+
 # ------------------------------------------------------------------ convenience layer
 @dataclass
 class StepBuffers:

@@ -353,10 +353,10 @@ __device__ __forceinline__ void stream_row(const T* __restrict__ row, int V, boo
 }
 
 // Two rows (p and q) interleaved so both streams keep loads in flight.
-template <typename T, int NA, int NT, int U>
+template <typename T, int NA, int NT, int U, bool kQq = true>
 __device__ __forceinline__ void stream_pair(const T* __restrict__ prow, const T* __restrict__ qrow,
                                             int V, bool vec_ok, RowAcc<false, NA>& pa,
-                                            RowAcc<true, NA>& qa) {
+                                            RowAcc<kQq, NA>& qa) {
   constexpr int E = Vec<T>::E;
   const int tid = threadIdx.x;
   int done = 0;

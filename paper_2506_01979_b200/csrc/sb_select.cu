@@ -18,6 +18,7 @@
 
 #include "sb_host.h"
 #include "sb_ring.cuh"
+#include "sb_block_sample.cuh"
 #include "sb_sample.cuh"
 
 namespace sb {
@@ -40,77 +41,13 @@ struct SelParams {
   float* resid_mass;
 };
 
-constexpr int kMaxTiles = 512;
-
-template <typename T, int NT>
-struct Sampler {
-  static constexpr int E = Vec<T>::E;
-  static constexpr int TE = NT * E;  // ids per tile
-  static constexpr int NW = NT / 32;
-
-  const T* prow;
-  const T* qrow;
-  int V;
-  bool vec_ok;
-  bool resid;  // residual max(0,P-Q) (else P)
-  float MSp, iZp, MSq, iZq;
-
-  // raw logits of the E ids this thread owns in tile t (-inf past V)
-  __device__ __forceinline__ void load(int t, float* lp, float* lq) const {
-    const int v0 = t * TE + threadIdx.x * E;
-    if (vec_ok && v0 + E <= V) {
-      Vec<T>::unpack(ldg_stream(prow + v0), lp);
-      if (resid) Vec<T>::unpack(ldg_stream(qrow + v0), lq);
-    } else {
-#pragma unroll
-      for (int j = 0; j < E; ++j) {
-        const bool in = v0 + j < V;
-        lp[j] = in ? ld_scalar(prow + v0 + j) : -CUDART_INF_F;
-        lq[j] = (in && resid) ? ld_scalar(qrow + v0 + j) : -CUDART_INF_F;
-      }
-    }
-  }
-  // r = max(0, P - Q) (or P) from the raw logits
-  __device__ __forceinline__ void compute(const float* lp, const float* lq, float* r) const {
-#pragma unroll
-    for (int j = 0; j < E; ++j) {
-      const float P = ex2(fmaf(lp[j], kC, -MSp)) * iZp;
-      if (resid) {
-        const float Q = ex2(fmaf(lq[j], kC, -MSq)) * iZq;
-        r[j] = fmaxf(P - Q, 0.f);
-      } else {
-        r[j] = P;
-      }
-    }
-  }
-  __device__ __forceinline__ void values(int t, float* r) const {
-    float lp[E], lq[E];
-    load(t, lp, lq);
-    compute(lp, lq, r);
-  }
-};
-
-// Row softmax state of one row by the whole block (used for the bonus row).
-template <typename T, int NT>
-__device__ RowOut block_row_stats(const T* row, int V, bool vec_ok, RowStat* red, float* m_out) {
-  RowAcc<false, 4> a;
-  a.init();
-  stream_row<T, false, 4, NT, 4>(row, V, vec_ok, a);
-  const RowStat s = block_reduce<NT>(fold(a), red);
-  *m_out = s.m;
-  return finish(s);
-}
-
 template <typename T, int NT>
 __global__ void __launch_bounds__(NT) k_select(SelParams p, bool vec_ok) {
   using S = Sampler<T, NT>;
   constexpr int NW = S::NW;
-  __shared__ float wtot[kMaxTiles][NW];
-  __shared__ float tsum[kMaxTiles];
-  __shared__ RowStat red[NW];
-  __shared__ int sh_ksel, sh_npath, sh_kind, sh_row, sh_slot, sh_st, sh_tile, sh_pick, sh_last,
-      sh_fb;
-  __shared__ double sh_trem, sh_R;
+  __shared__ SampleSmem<NW> sm;
+  RowStat* red = sm.red;
+  __shared__ int sh_ksel, sh_npath, sh_kind, sh_row, sh_slot, sh_st, sh_last;
   const Dims& d = p.d;
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const SeqInfo in = p.info[b];
@@ -146,8 +83,6 @@ __global__ void __launch_bounds__(NT) k_select(SelParams p, bool vec_ok) {
     }
     sh_ksel = ksel; sh_npath = npath; sh_kind = kind; sh_row = row; sh_slot = slot;
     sh_st = 0;
-    sh_pick = 0x7fffffff;
-    sh_fb = -1;
   }
   __syncthreads();
   const int ksel = sh_ksel, npath = sh_npath;
@@ -179,92 +114,9 @@ __global__ void __launch_bounds__(NT) k_select(SelParams p, bool vec_ok) {
     } else {
       smp.MSp = MSp; smp.iZp = 1.f / Zp; smp.MSq = MSq; smp.iZq = 1.f / Zq;
       smp.resid = (kind == 1);
-      const int ntiles = (d.V + S::TE - 1) / S::TE;
-      for (int attempt = 0; attempt < 2; ++attempt) {
-        // pass A: per-tile warp totals
-        constexpr int UT = 4;  // tiles in flight per thread
-        for (int t0 = 0; t0 < ntiles; t0 += UT) {
-          float lp[UT][S::E], lq[UT][S::E];
-#pragma unroll
-          for (int q = 0; q < UT; ++q)
-            if (t0 + q < ntiles) smp.load(t0 + q, lp[q], lq[q]);
-#pragma unroll
-          for (int q = 0; q < UT; ++q) {
-            if (t0 + q >= ntiles) break;
-            float r[S::E];
-            smp.compute(lp[q], lq[q], r);
-            float own = 0.f;
-#pragma unroll
-            for (int j = 0; j < S::E; ++j) own += r[j];
-            const float incl = warp_incl_scan(own);
-            if (lane == 31) wtot[t0 + q][w] = incl;
-          }
-        }
-        __syncthreads();
-        for (int t = tid; t < ntiles; t += NT) {
-          float s = 0.f;
-#pragma unroll
-          for (int q = 0; q < NW; ++q) s += wtot[t][q];
-          tsum[t] = s;
-        }
-        __syncthreads();
-        if (tid == 0) {
-          double R = 0.0;
-          for (int t = 0; t < ntiles; ++t) R += (double)tsum[t];
-          sh_R = R;
-        }
-        __syncthreads();
-        if (sh_R > 0.0 || !smp.resid) break;
-        smp.resid = false;  // "no residual mass" (S134-140): sample from P instead
-        if (tid == 0) sh_st |= SB_ST_ZERO_RESID;
-        __syncthreads();
-      }
-      if (tid == 0) {
-        const double R = sh_R, t = (double)__ldg(p.us + b) * R;
-        double F = 0.0;
-        int tile = -1;
-        for (int q = 0; q < ntiles; ++q) {
-          if (F + (double)tsum[q] > t) { tile = q; break; }
-          F += (double)tsum[q];
-        }
-        if (tile < 0) {  // rounding: fall back to the last tile holding mass
-          for (int q = ntiles - 1; q >= 0; --q)
-            if (tsum[q] > 0.f) { tile = q; break; }
-          F = -1e300;  // no id qualifies -> the in-tile fallback (last id with mass)
-        }
-        sh_tile = tile;
-        sh_trem = t - F;
-      }
-      __syncthreads();
-      const int tile = sh_tile;
-      if (tile >= 0) {
-        // pass B on the located tile: identical arithmetic -> same warp totals
-        float r[S::E];
-        smp.values(tile, r);
-        float own = 0.f;
-#pragma unroll
-        for (int j = 0; j < S::E; ++j) own += r[j];
-        const float incl = warp_incl_scan(own);
-        float excl = __shfl_up_sync(0xffffffffu, incl, 1);
-        if (lane == 0) excl = 0.f;
-        float base = 0.f;
-        for (int q = 0; q < w; ++q) base += wtot[tile][q];
-        float F = base + excl;
-        const double trem = sh_trem;
-        int mine = 0x7fffffff, last_pos = -1;
-#pragma unroll
-        for (int j = 0; j < S::E; ++j) {
-          F += r[j];
-          const int v = tile * S::TE + tid * S::E + j;
-          if (mine == 0x7fffffff && (double)F > trem && r[j] > 0.f) mine = v;
-          if (r[j] > 0.f) last_pos = v;
-        }
-        if (mine != 0x7fffffff) atomicMin(&sh_pick, mine);
-        if (last_pos >= 0) atomicMax(&sh_fb, last_pos);
-        __syncthreads();
-        y = (sh_pick != 0x7fffffff) ? sh_pick : sh_fb;
-      }
-      mass = sh_R;
+      int st = 0;
+      y = block_sample<T, NT>(smp, __ldg(p.us + b), sm, st, mass);
+      if (tid == 0) sh_st |= st;
     }
   }
 

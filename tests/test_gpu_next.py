@@ -86,3 +86,74 @@ def test_kv_rollback_matches_oracle(inplace):
         got = out.cpu().numpy()
     for b in range(c.B):
         assert np.array_equal(got[b, : n[b]], ref[b, : n[b]]), b
+
+
+TREES = [("dense_2222_bf16_V32000", "c2", dict(), "dense", dict(branching=(2, 2, 2, 2)), 64),
+         ("dense_32_f32_V3001", "c1", dict(V=3001), "dense", dict(branching=(3, 2, 2)), 48),
+         ("random63_bf16_V128256", "c3", dict(), "random", dict(N=63, depth=8), 24),
+         ("chain8_bf16_V151936", "c4", dict(), "chain", dict(N=8), 32),
+         ("random_tiny_V7", "c2", dict(V=7), "random", dict(N=30, depth=5), 96)]
+
+
+@pytest.mark.parametrize("name,cfg,over,shape,kw,B", TREES, ids=[t[0] for t in TREES])
+def test_tree_verify_matches_oracle(name, cfg, over, shape, kw, B):
+    """f3 tree verify through the C-ABI against oracle.tree_verify: acceptance masks
+    exact except at near-ties the oracle flags; the walk, commit and sample bit-exact
+    on every sequence the oracle does not flag."""
+    import oracle
+    from paper_2506_01979_b200 import api, synth
+
+    c = synth.config(cfg, **over)
+    inp = synth.generate_tree(c, shape, B=B, seed=13, **kw)
+    t = synth.tree_to_numpy(inp)
+    o = oracle.tree_verify(t["PL"], t["QL"], t["parent"], t["tok"], t["u"], t["us"])
+    dev = {k: (v.cuda() if isinstance(v, torch.Tensor) else v) for k, v in inp.items()}
+    d = api.tree_dims(dev["PL"])
+    buf = api.TreeBuffers(d)
+    api.sb_tree_verify(d, dev["PL"], dev["QL"], dev["parent"], dev["tok"], dev["u"], dev["us"], buf)
+    torch.cuda.synchronize()
+    g = {k: getattr(buf, k).cpu().numpy() for k in ("acc_mask", "keep_mask", "stop_node", "commit_len", "out_tok",
+                                                     "y_tok", "y_kind", "status", "resid_mass")}
+    assert np.array_equal(g["status"], o["status"])
+    # decisions: every sequence without an acceptance near-tie (|u - P/Q| < 1e-6)
+    dec = (o["ties"] & oracle.TIE_ACC_DEC) == 0
+    assert dec.mean() > 0.9
+    assert np.array_equal(g["acc_mask"].view(np.uint64)[dec], o["acc_mask"][dec])
+    assert np.array_equal(g["keep_mask"].view(np.uint64)[dec], o["keep_mask"][dec])
+    for k in ("stop_node", "commit_len", "y_kind"):
+        assert np.array_equal(g[k][dec], o[k][dec]), k
+    n = o["commit_len"] - (o["y_kind"] != 0)
+    for b in np.where(dec)[0]:
+        assert np.array_equal(g["out_tok"][b, : n[b]], o["out_tok"][b, : n[b]]), b
+    # the sample: bit-exact unless the oracle's CDF puts t within 1e-6 of a breakpoint
+    # (bulk tokens of a V = 152k row carry ~3e-6 each) or the residual is ill-conditioned
+    smp = dec & ((o["ties"] & (oracle.TIE_SAMPLE | oracle.TIE_ILLCOND)) == 0)
+    assert smp.sum() >= len(smp) // 2
+    assert np.array_equal(g["y_tok"][smp], o["y_tok"][smp])
+    assert np.array_equal(g["out_tok"][smp], o["out_tok"][smp])
+    assert ((g["y_tok"] >= 0) & (g["y_tok"] < c.V))[o["y_kind"] != 0].all()
+    assert np.allclose(g["resid_mass"][dec], o["resid_mass"][dec], rtol=1e-4, atol=1e-6)
+
+
+def test_tree_bad_parent_and_nonfinite():
+    """Status bits: a parent pointer that is not earlier in topological order rejects
+    that node (SB_ST_BAD_PARENT); a NaN context row rejects its children (NONFINITE)."""
+    import oracle
+    from paper_2506_01979_b200 import api, synth
+
+    c = synth.config("c2", V=1000, dtype="f32")
+    inp = synth.generate_tree(c, "dense", B=8, seed=3, branching=(2, 2))
+    inp["parent"][1, 3] = 5  # not < 3
+    inp["PL"][2, 1, 17] = float("nan")  # context after node 0
+    t = synth.tree_to_numpy(inp)
+    o = oracle.tree_verify(t["PL"], t["QL"], t["parent"], t["tok"], t["u"], t["us"])
+    assert o["status"][1] & oracle.ST_BAD_PARENT and o["status"][2] & oracle.ST_NONFINITE
+    dev = {k: (v.cuda() if isinstance(v, torch.Tensor) else v) for k, v in inp.items()}
+    d = api.tree_dims(dev["PL"])
+    buf = api.TreeBuffers(d)
+    api.sb_tree_verify(d, dev["PL"], dev["QL"], dev["parent"], dev["tok"], dev["u"], dev["us"], buf)
+    torch.cuda.synchronize()
+    assert np.array_equal(buf.status.cpu().numpy(), o["status"])
+    ok = o["ties"] == 0
+    assert np.array_equal(buf.commit_len.cpu().numpy()[ok], o["commit_len"][ok])
+    assert np.array_equal(buf.out_tok.cpu().numpy()[ok], o["out_tok"][ok])
