@@ -42,7 +42,8 @@ double oracle_logit(const or_dims* d, const void* L, int b, int slot, int i, int
 
 /* Softmax of one row, plain two-pass definition (SURVEY §8.0 "Per-row definitions"):
  * m = max l, Z = sum exp(l - m), lse = m + ln Z, P(v) = exp(l(v) - lse).
- * A row containing NaN or +inf, or one that is all -inf, has no distribution: NaN. */
+ * A row containing NaN or +inf, or one whose entries are all masked (-inf; an entry
+ * <= -2^97 counts as masked, reading 34), has no distribution: NaN. */
 double oracle_row_softmax(const or_dims* d, const void* L, int b, int slot, int i, double* P) {
   const int V = d->V;
   double m = -INFINITY;
@@ -51,7 +52,7 @@ double oracle_row_softmax(const or_dims* d, const void* L, int b, int slot, int 
     if (isnan(l) || l == INFINITY) return NAN;
     if (l > m) m = l;
   }
-  if (m == -INFINITY) return NAN;
+  if (m <= -0x1p97) return NAN; /* all entries masked (-inf, or <= -2^97: DESIGN reading 34) */
   double Z = 0.0;
   for (int v = 0; v < V; ++v) Z += exp(oracle_logit(d, L, b, slot, i, v) - m);
   double lse = m + log(Z);

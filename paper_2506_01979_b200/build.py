@@ -43,9 +43,7 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(f) <= t for f in deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
-        return SO
+def nvcc_cmd(verbose: bool = False):
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
     nccl = nccl_dir()
     cmd = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-shared",
@@ -54,10 +52,25 @@ def build(force: bool = False, verbose: bool = False) -> str:
            "-Xlinker", "-rpath=" + os.path.join(nccl, "lib")]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
+    return cmd
+
+
+def build(force: bool = False, verbose: bool = False, extra=(), out: str = SO) -> str:
+    """Compile libspecbranch.so (``extra`` nvcc flags and ``out`` only for A/B experiment
+    builds, loaded through SB_LIB_PATH)."""
+    if out == SO and not extra and not force and up_to_date():
+        return SO
+    cmd = nvcc_cmd(verbose)
+    cmd[cmd.index(SO + ".tmp")] = out + ".tmp"
+    cmd[1:1] = list(extra)
     subprocess.check_call(cmd)
-    os.replace(SO + ".tmp", SO)
-    return SO
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force=True, verbose="--verbose" in sys.argv))
+    # python -m paper_2506_01979_b200.build [--verbose] [--out PATH] [-- nvcc flags...]
+    args = sys.argv[1:]
+    extra = args[args.index("--") + 1:] if "--" in args else []
+    out = args[args.index("--out") + 1] if "--out" in args else SO
+    print(build(force=True, verbose="--verbose" in args, extra=extra, out=out))

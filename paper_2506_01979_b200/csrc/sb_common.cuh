@@ -27,6 +27,12 @@ constexpr float kMsEmpty = -1e30f;  // exponent offset of a state that has seen 
 constexpr float kRescaleP = 20.f;
 constexpr float kRescaleQ = 6.f;
 constexpr int kMaxG = 31;
+// Masked logits (DESIGN reading 34): an entry <= -2^97 counts as -inf.  The bf16 q-row
+// path clamps its inputs to -2^97 (one HMNMX2.NAN per two values, NaN kept) so the
+// entropy sum e*a never meets 0 * -inf; a row whose maximum is <= -2^97 has no
+// distribution (finish()).
+constexpr float kMaskedLogit = -1.5845632502852868e29f;  // -2^97, exact in bf16 (0xf000)
+constexpr uint32_t kMaskedBf16x2 = 0xf000f000u;
 
 struct Dims {
   int B, K, G, V;
@@ -58,6 +64,11 @@ __device__ __forceinline__ uint4 ldg_stream(const void* p) {
   asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint32_t bf16x2_max_nan(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("max.NaN.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
   return r;
 }
 __device__ __forceinline__ float bf16_lo(uint32_t w) { return __uint_as_float(w << 16); }
@@ -221,7 +232,79 @@ struct LazyAcc {
       if (kQ) s1[j % NA] = fmaf(e, fmaxf(a, -200.f), s1[j % NA]);
     }
   }
+
+  // The same as add<2*NW>() on NW packed bf16 pairs, with the fp32 arithmetic paired
+  // into FFMA2 / FADD2 (same IEEE fp32 operations, same accumulator order: element j
+  // goes to z[j % 4]).  q rows clamp their inputs at -2^97 instead of clamping the
+  // exponent: identical results for every logit > -2^97, since ex2.approx.ftz is 0
+  // below 2^-126 either way.
+  template <int NW>
+  __device__ __forceinline__ void add_bf16(const uint32_t* win, int t) {
+    static_assert(NA == 4 && NW % 2 == 0, "pairs map to (z0,z1), (z2,z3)");
+    constexpr int N = 2 * NW;
+    float f[N];
+#pragma unroll
+    for (int j = 0; j < NW; ++j) {
+      const uint32_t w = kQ ? bf16x2_max_nan(win[j], kMaskedBf16x2) : win[j];
+      f[2 * j] = bf16_lo(w);
+      f[2 * j + 1] = bf16_hi(w);
+    }
+    float cm = f[0];
+#pragma unroll
+    for (int j = 1; j + 1 < N; j += 2) cm = fmax3(cm, f[j], f[j + 1]);
+    cm = fmaxf(cm, f[N - 1]);
+    if (kQ) tag = (cm > m) ? t : tag;
+    m = fmaxf(m, cm);
+    bool up = cm * kC - ms > (kQ ? kRescaleQ : kRescaleP);
+    // rare; written as a loop so the compiler keeps it a branch instead of predicating
+    // the rescale into every iteration
+    while (__builtin_expect(__any_sync(0xffffffffu, up), 0)) {
+      if (up) rescale(cm * kC);
+      up = false;
+    }
+    const float2 c2 = make_float2(kC, kC), n2 = make_float2(-ms, -ms);
+    float2 za = make_float2(z[0], z[1]), zb = make_float2(z[2], z[3]);
+    float2 sa = make_float2(0.f, 0.f), sb = sa;
+    if (kQ) {
+      sa = make_float2(s1[0], s1[1]);
+      sb = make_float2(s1[2], s1[3]);
+    }
+#pragma unroll
+    for (int j = 0; j < NW; ++j) {
+      const float2 a = __ffma2_rn(make_float2(f[2 * j], f[2 * j + 1]), c2, n2);
+      const float2 e = make_float2(ex2(a.x), ex2(a.y));
+      if (j % 2 == 0) {
+        za = __fadd2_rn(za, e);
+        if (kQ) sa = __ffma2_rn(e, a, sa);
+      } else {
+        zb = __fadd2_rn(zb, e);
+        if (kQ) sb = __ffma2_rn(e, a, sb);
+      }
+    }
+    z[0] = za.x; z[1] = za.y; z[2] = zb.x; z[3] = zb.y;
+    if (kQ) {
+      s1[0] = sa.x; s1[1] = sa.y; s1[2] = sb.x; s1[3] = sb.y;
+    }
+  }
 };
+
+// A 16-byte vector of -inf (fill for lanes past the end of a row).
+template <typename T>
+__device__ __forceinline__ uint4 neg_inf_vec() {
+  return sizeof(T) == 2 ? make_uint4(0xff80ff80u, 0xff80ff80u, 0xff80ff80u, 0xff80ff80u)
+                        : make_uint4(0xff800000u, 0xff800000u, 0xff800000u, 0xff800000u);
+}
+
+// Accumulate NV 16-byte bf16 vectors of one row chunk (tag t) into a LazyAcc.
+template <int NV, bool kQ>
+__device__ __forceinline__ void acc_vecs_bf16(LazyAcc<kQ, 4>& a, const uint4* x, int t) {
+  uint32_t w[4 * NV];
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    w[4 * j] = x[j].x; w[4 * j + 1] = x[j].y; w[4 * j + 2] = x[j].z; w[4 * j + 3] = x[j].w;
+  }
+  a.template add_bf16<4 * NV>(w, t);
+}
 
 // Reduced row state (one per thread after folding accumulators, then across threads).
 struct RowStat {
@@ -406,7 +489,7 @@ __device__ __forceinline__ RowOut finish(const RowStat& r) {
   RowOut o;
   o.MS = r.ms;
   o.Z = r.z;
-  o.finite = (r.m != -CUDART_INF_F) && (r.m != CUDART_INF_F) && (r.z == r.z) && (r.z > 0.f) &&
+  o.finite = (r.m > kMaskedLogit) && (r.m != CUDART_INF_F) && (r.z == r.z) && (r.z > 0.f) &&
              (r.z != CUDART_INF_F);
   return o;
 }

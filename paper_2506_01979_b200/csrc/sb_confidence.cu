@@ -239,29 +239,35 @@ __global__ void __launch_bounds__(cThreads, 1) k_conf_tma(ConfParams p) {
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.empty[rp.stage]);
       rp.advance();
-      float f[cVPT * E];
+      if constexpr (sizeof(T) == 2) {
+        acc_vecs_bf16<cVPT>(a, x, c);
+      } else {
+        float f[cVPT * E];
 #pragma unroll
-      for (int j = 0; j < cVPT; ++j) Vec<T>::unpack(x[j], f + j * E);
-      a.template add<cVPT * E>(f, c);
+        for (int j = 0; j < cVPT; ++j) Vec<T>::unpack(x[j], f + j * E);
+        a.template add<cVPT * E>(f, c);
+      }
     }
     {
       const int c = nchunks - 1;
       mbar_wait(&S.full[rp.stage], rp.phase);
-      float f[cVPT * E];
+      uint4 x[cVPT];
 #pragma unroll
       for (int j = 0; j < cVPT; ++j) {
         const int v = tid + j * cCT;
-        if (v < nvec_last) {
-          Vec<T>::unpack(lds128(S.buf[rp.stage] + v * 16), f + j * E);
-        } else {
-#pragma unroll
-          for (int e = 0; e < E; ++e) f[j * E + e] = -CUDART_INF_F;
-        }
+        x[j] = v < nvec_last ? lds128(S.buf[rp.stage] + v * 16) : neg_inf_vec<T>();
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.empty[rp.stage]);
       rp.advance();
-      a.template add<cVPT * E>(f, c);
+      if constexpr (sizeof(T) == 2) {
+        acc_vecs_bf16<cVPT>(a, x, c);
+      } else {
+        float f[cVPT * E];
+#pragma unroll
+        for (int j = 0; j < cVPT; ++j) Vec<T>::unpack(x[j], f + j * E);
+        a.template add<cVPT * E>(f, c);
+      }
     }
     const int grp = unit / G, i = unit % G;
     const T* row = QL + row_off(d, grp / d.K, grp % d.K, i);

@@ -307,6 +307,7 @@ struct RowsSmem {
   uint64_t full[C::NS], empty[C::NS];
   uint64_t pfull[C::NP], pempty[C::NP];
   RowStat part[C::NP][2][C::CW];  // [slot][p,q][warp]
+  uint2 cand[C::NP][C::CW];       // q-row argmax candidates per warp (tag, lane mask)
   alignas(128) uint8_t buf[C::NS][2][C::CHUNK];
 };
 
@@ -354,6 +355,61 @@ __device__ __forceinline__ RowStat warp_part(const LazyAcc<kQ, 4>& a, const T* r
   }
   s.idx = kQ ? (int)__reduce_min_sync(0xffffffffu, (unsigned)cand) : 0;
   return s;
+}
+
+// Consumer side of a q row without the argmax lookup: the warp's reduced state (idx
+// unresolved) and its argmax candidates: the smallest chunk tag among the lanes holding
+// the warp maximum and the mask of those lanes with that tag.  The epilogue warp
+// resolves the index (resolve_argmax) off the consumers' critical path.
+template <bool kQ>
+__device__ __forceinline__ RowStat warp_part_deferred(const LazyAcc<kQ, 4>& a, uint2& cand) {
+  RowStat s = fold_lazy(a);
+  float mw = s.m;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mw = fmaxf(mw, __shfl_xor_sync(0xffffffffu, mw, o));
+  const bool hold = (a.m == mw) && (mw > -CUDART_INF_F) && (a.tag >= 0);
+  const unsigned t = hold ? (unsigned)a.tag : 0xffffffffu;
+  const unsigned tmin = __reduce_min_sync(0xffffffffu, t);
+  cand = make_uint2(tmin, __ballot_sync(0xffffffffu, hold && t == tmin));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s = combine(s, shfl_xor(s, o));
+  s.m = mw;
+  s.idx = 0x7fffffff;
+  return s;
+}
+
+// Epilogue side: lane w < CW holds warp w's part (mw = its maximum) and candidates;
+// M = the row maximum.  The first index of M lies in the smallest candidate chunk of
+// the warps holding M; the candidate lanes re-read their vectors of that chunk (one
+// load round, normally one lane).  Returns the index in every lane.
+template <class C, typename T>
+__device__ __forceinline__ int resolve_argmax(float mw, uint2 cand, float M, const T* row, int nvec_last,
+                                              int nchunks) {
+  constexpr int E = Vec<T>::E;
+  const int lane = threadIdx.x & 31;
+  const unsigned t = (lane < C::CW && mw == M && M > -CUDART_INF_F) ? cand.x : 0xffffffffu;
+  const unsigned tmin = __reduce_min_sync(0xffffffffu, t);
+  int best = 0x7fffffff;
+  if (t == tmin && tmin != 0xffffffffu) {
+    const int c = (int)tmin;
+    const int nvec = (c == nchunks - 1) ? nvec_last : C::CHUNK / 16;
+    const uint4* cv =
+        reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(row) + (size_t)c * C::CHUNK);
+    for (uint32_t m = cand.y; m; m &= m - 1) {
+      const int tid = lane * 32 + __ffs(m) - 1;
+#pragma unroll
+      for (int j = 0; j < C::VPT; ++j) {
+        const int v = tid + j * C::CT;
+        if (v >= nvec) continue;
+        float f[E];
+        Vec<T>::unpack(__ldg(cv + v), f);
+#pragma unroll
+        for (int e = E - 1; e >= 0; --e)
+          if (f[e] == M) best = min(best, c * (C::CHUNK / (int)sizeof(T)) + v * E + e);
+      }
+    }
+  }
+  return (int)__reduce_min_sync(0xffffffffu, (unsigned)best);
 }
 
 // Epilogue of one unit by one warp, with the token data already prefetched.
@@ -474,11 +530,6 @@ struct StageRegs {
   uint4 p[C::VPT], q[C::VPT];
 };
 
-template <typename T>
-__device__ __forceinline__ uint4 neg_inf_vec() {
-  return sizeof(T) == 2 ? make_uint4(0xff80ff80u, 0xff80ff80u, 0xff80ff80u, 0xff80ff80u)
-                        : make_uint4(0xff800000u, 0xff800000u, 0xff800000u, 0xff800000u);
-}
 
 template <class C, typename T, bool FULL>
 __device__ __forceinline__ void load_stage(const uint8_t* bp, const uint8_t* bq, int nvec, StageRegs<C>& r) {
@@ -498,15 +549,27 @@ __device__ __forceinline__ void load_stage(const uint8_t* bp, const uint8_t* bq,
 template <class C, typename T>
 __device__ __forceinline__ void compute_stage(const StageRegs<C>& r, int c, LazyAcc<false, 4>& pa,
                                               LazyAcc<true, 4>& qa) {
-  constexpr int E = Vec<T>::E;
-  float fp[C::VPT * E], fq[C::VPT * E];
+#ifdef SB_EXP_NOCOMPUTE  // experiment builds only: the ring without the arithmetic
+  uint32_t x = 0;
 #pragma unroll
-  for (int j = 0; j < C::VPT; ++j) {
-    Vec<T>::unpack(r.p[j], fp + j * E);
-    Vec<T>::unpack(r.q[j], fq + j * E);
+  for (int j = 0; j < C::VPT; ++j) x ^= r.p[j].x ^ r.q[j].w;
+  pa.z[0] += __uint_as_float(x & 1u);
+  return;
+#endif
+  if constexpr (sizeof(T) == 2) {
+    acc_vecs_bf16<C::VPT>(pa, r.p, c);
+    acc_vecs_bf16<C::VPT>(qa, r.q, c);
+  } else {
+    constexpr int E = Vec<T>::E;
+    float fp[C::VPT * E], fq[C::VPT * E];
+#pragma unroll
+    for (int j = 0; j < C::VPT; ++j) {
+      Vec<T>::unpack(r.p[j], fp + j * E);
+      Vec<T>::unpack(r.q[j], fq + j * E);
+    }
+    pa.template add<C::VPT * E>(fp, c);
+    qa.template add<C::VPT * E>(fq, c);
   }
-  pa.template add<C::VPT * E>(fp, c);
-  qa.template add<C::VPT * E>(fq, c);
 }
 
 template <class C, typename T>
@@ -582,14 +645,17 @@ __global__ void __launch_bounds__(C::THREADS, 1) k_rows_tma(RowsParams p) {
       mbar_wait(&S.pfull[up.stage], up.phase);
       RowStat ps = lane < C::CW ? S.part[up.stage][0][lane] : rowstat_empty();
       RowStat qs = lane < C::CW ? S.part[up.stage][1][lane] : rowstat_empty();
+      const uint2 cand = lane < C::CW ? S.cand[up.stage][lane] : make_uint2(0xffffffffu, 0u);
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.pempty[up.stage]);
       up.advance();
+      const float qmw = qs.m;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         ps = combine(ps, shfl_xor(ps, o));
         qs = combine(qs, shfl_xor(qs, o));
       }
+      qs.idx = resolve_argmax<C, T>(qmw, cand, qs.m, qrow, nvec_last, nchunks);
       if (p.partial) {  // a7: this shard's state, combined across shards later
         if (lane < ntok && has_tok) p.tokpart[et] = make_float2(lpx, lqx);
         if (lane == 0) {
@@ -633,14 +699,14 @@ __global__ void __launch_bounds__(C::THREADS, 1) k_rows_tma(RowsParams p) {
       rp.advance();
       compute_stage<C, T>(r, nchunks - 1, pa, qa);
     }
-    const Unit un = decode_unit(p, unit);
-    const T* qrow = QL + row_off(d, un.b, un.slot, un.i);
-    const RowStat ps = warp_part<C, T, false>(pa, qrow, nvec_last, nchunks);
-    const RowStat qs = warp_part<C, T, true>(qa, qrow, nvec_last, nchunks);
+    uint2 cand;
+    const RowStat ps = warp_part<C, T, false>(pa, nullptr, nvec_last, nchunks);
+    const RowStat qs = warp_part_deferred(qa, cand);
     if (lane == 0) {
       mbar_wait(&S.pempty[up.stage], up.phase ^ 1u);
       S.part[up.stage][0][warp] = ps;
       S.part[up.stage][1][warp] = qs;
+      S.cand[up.stage][warp] = cand;
       mbar_arrive(&S.pfull[up.stage]);
     }
     __syncwarp();
@@ -715,6 +781,7 @@ struct StepSmem {
   uint64_t pfull[C::NP], pempty[C::NP];
   uint64_t dfull[kNDQ], dempty[kNDQ];
   RowStat part[C::NP][2][C::CW];
+  uint2 cand[C::NP][C::CW];
   P2Desc desc[kNDQ];
   float4 brs[kNDQ];  // bonus-row softmax state computed by the consumers
   RowStat red[C::CW];
@@ -935,14 +1002,17 @@ __global__ void __launch_bounds__(C::THREADS, 1) k_step_tma(StepParams sp) {
         mbar_wait(&S.pfull[up.stage], up.phase);
         RowStat ps = lane < C::CW ? S.part[up.stage][0][lane] : rowstat_empty();
         RowStat qs = lane < C::CW ? S.part[up.stage][1][lane] : rowstat_empty();
+        const uint2 cand = lane < C::CW ? S.cand[up.stage][lane] : make_uint2(0xffffffffu, 0u);
         __syncwarp();
         if (lane == 0) mbar_arrive(&S.pempty[up.stage]);
         up.advance();
+        const float qmw = qs.m;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
           ps = combine(ps, shfl_xor(ps, o));
           qs = combine(qs, shfl_xor(qs, o));
         }
+        qs.idx = resolve_argmax<C, T>(qmw, cand, qs.m, qrow, nvec_last, nchunks);
         warp_epilogue<T>(p, un, ps, qs, x, lpx, lqx, uu, et);
         continue;
       }
@@ -1045,13 +1115,14 @@ __global__ void __launch_bounds__(C::THREADS, 1) k_step_tma(StepParams sp) {
         rp.advance();
         compute_stage<C, T>(r, nchunks - 1, pa, qa);
       }
-      const T* qrow = QL + row_off(d, fu.b, fu.u.slot, fu.u.i);
-      const RowStat ps = warp_part<C, T, false>(pa, qrow, nvec_last, nchunks);
-      const RowStat qs = warp_part<C, T, true>(qa, qrow, nvec_last, nchunks);
+      uint2 cand;
+      const RowStat ps = warp_part<C, T, false>(pa, nullptr, nvec_last, nchunks);
+      const RowStat qs = warp_part_deferred(qa, cand);
       if (lane == 0) {
         mbar_wait(&S.pempty[up.stage], up.phase ^ 1u);
         S.part[up.stage][0][warp] = ps;
         S.part[up.stage][1][warp] = qs;
+        S.cand[up.stage][warp] = cand;
         mbar_arrive(&S.pfull[up.stage]);
       }
       __syncwarp();
@@ -1121,11 +1192,11 @@ static sb_status launch_step_tma(const StepParams& sp, cudaStream_t s) {
 }
 
 // Geometry variants (SB_ROWS_VARIANT selects one for experiments; 0 = default).
-using RC0 = RC<16, 6, 2, 4>;   // 16 consumer warps, 6 x 32 KB stages
-using RC1 = RC<16, 3, 4, 4>;   // 16 warps, 3 x 64 KB stages, 4 vectors/thread/row
-using RC2 = RC<24, 4, 2, 4>;   // 24 warps, 4 x 48 KB stages
-using RC3 = RC<8, 6, 4, 4>;    // 8 warps, 6 x 32 KB stages, 4 vectors/thread/row
-using RC4 = RC<12, 4, 2, 4>;   // 12 warps, 4 x 24 KB stages... (2 CTAs/SM would need <= 113 KB)
+using RC0 = RC<16, 7, 2, 2>;   // 16 consumer warps, 7 x 32 KB stages, 2 partial slots
+using RC1 = RC<16, 6, 2, 4>;   // 16 warps, 6 x 32 KB stages, 4 partial slots
+using RC2 = RC<16, 12, 1, 4>;  // 16 warps, 12 x 16 KB stages (finer row tail)
+using RC3 = RC<16, 13, 1, 2>;  // 16 warps, 13 x 16 KB stages
+using RC4 = RC<20, 5, 2, 4>;   // 20 warps, 5 x 40 KB stages
 
 template <typename T>
 static sb_status launch_rows_variant(const RowsParams& p, cudaStream_t s) {
@@ -1271,5 +1342,5 @@ extern "C" sb_status sb_verify_select(const sb_dims* dd, const void* p_logits, c
   sp.sel_k = sel_k; sp.commit_len = commit_len; sp.out_tok = out_tok; sp.y_tok = y_tok; sp.y_kind = y_kind;
   sp.offsets = offsets; sp.packed_tok = packed_tok; sp.path_rolled = path_rolled;
   sp.branch_discarded = branch_discarded; sp.keep_mask = keep_mask; sp.resid_mass = resid_mass;
-  return dd->dtype == SB_BF16 ? launch_step_tma<RC0, __nv_bfloat16>(sp, s) : launch_step_tma<RC0, float>(sp, s);
+  return dd->dtype == SB_BF16 ? launch_step_tma<RC1, __nv_bfloat16>(sp, s) : launch_step_tma<RC1, float>(sp, s);
 }

@@ -182,11 +182,16 @@ def test_special_values_and_status():
     inp["branch_pos"][7] = 3
     inp["gamma"][7] = 2
     inp["QL"][8, 0, 2, :100] = float("-inf")  # masked draft logits
+    inp["QL"][9, 0, 1, :] = -(2.0 ** 98)  # finite but all <= -2^97: masked (reading 34)
+    inp["PL"][10, 0, 0, ::2] = float("-inf")  # half-masked target and draft rows
+    inp["QL"][10, 0, 0, 1::3] = float("-inf")
+    inp["QL"][11, 0, 1, 3:] = -(2.0 ** 97)  # masked tail at exactly -2^97
     g, _, _ = gpu_run(inp)
     inp_np = synth.to_numpy_inputs(inp)
     o = oracle_for(inp_np, inp_np["gamma"])
     compare(g, o)
     assert g["status"][0] & 8 and g["status"][4] & 4 and g["status"][6] & 1 and g["status"][7] & 2
+    assert g["status"][9] & 8 and not g["status"][10] & 8 and not g["status"][11] & 8
 
 
 @pytest.mark.slow

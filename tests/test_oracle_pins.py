@@ -487,6 +487,16 @@ def test_status_flags(orc):
     o = orc.verify(PL, PL, np.zeros((1, 1, 2), np.int32), np.zeros((1, 1, 2)), np.array([0.5]),
                    gamma=[1], branch_pos=[0])
     assert o["status"][0] & orc.ST_NONFINITE
+    # a row whose entries are all <= -2^97 is masked (DESIGN reading 34); one finite
+    # entry above it is a point mass
+    M = np.full_like(PL, -(2.0 ** 98))
+    o = orc.verify(M, M, np.zeros((1, 1, 2), np.int32), np.zeros((1, 1, 2)), np.array([0.5]),
+                   gamma=[1], branch_pos=[0])
+    assert o["status"][0] & orc.ST_NONFINITE
+    M[..., 1] = -3.0
+    o = orc.verify(M, M, np.ones((1, 1, 2), np.int32), np.zeros((1, 1, 2)), np.array([0.5]),
+                   gamma=[1], branch_pos=[0])
+    assert not o["status"][0] & orc.ST_NONFINITE and o["n_acc"][0, 0] == 1
     o = orc.verify(PL * 0, PL * 0, np.zeros((1, 1, 2), np.int32), np.zeros((1, 1, 2)), np.array([0.5]),
                    gamma=[5], branch_pos=[9])
     assert o["status"][0] & orc.ST_GAMMA_CLAMPED and o["status"][0] & orc.ST_BRANCH_CLAMPED
