@@ -30,6 +30,7 @@ struct RowsParams {
   const float* u;
   const SeqInfo* info;
   const int* unit_off;
+  const int4* units;  // unit table (k_plan); NULL -> decode_unit's search
   int* cnt;
   float4* rowstat;
   uint8_t* pflag;
@@ -46,10 +47,16 @@ struct RowsParams {
 };
 
 // ---------------------------------------------------------------- plan
+// Unit table entry: sequence, row geometry and the sequence's layout in one 16-byte
+// load, so the streaming kernels' producer and epilogue warps never search unit_off.
+__host__ __device__ inline int4 unit_entry(int b, int slot, int i, const SeqInfo& in) {
+  return make_int4(b, slot | (i << 8) | (in.s << 16) | (in.g << 24), in.L | (in.Lr << 8) | (in.st << 16), 0);
+}
+
 __global__ void __launch_bounds__(1024) k_plan(Dims d, const int* __restrict__ gamma,
                                                const int* __restrict__ bpos, SeqInfo* info,
                                                int* unit_off, int with_bonus, int fused_grid, int* plan,
-                                               int* ready) {
+                                               int* ready, int4* units = nullptr) {
   __shared__ int wsum[32];
   const int tid = threadIdx.x, NT = blockDim.x;
   const int per = (d.B + NT - 1) / NT;
@@ -110,6 +117,12 @@ __global__ void __launch_bounds__(1024) k_plan(Dims d, const int* __restrict__ g
   for (int b = b0; b < b1; ++b) {
     unit_off[b] = run;
     const SeqInfo in = info[b];
+    if (units) {  // slot 0 rows 0..Lr-1, then rows s+1..Lr-1 of slots 1..K-1
+      int4* ub = units + run;
+      for (int i = 0; i < in.Lr; ++i) *ub++ = unit_entry(b, 0, i, in);
+      for (int k = 1; k < d.K; ++k)
+        for (int i = in.s + 1; i < in.Lr; ++i) *ub++ = unit_entry(b, k, i, in);
+    }
     run += in.Lr + (d.K - 1) * (in.Lr - 1 - in.s);
   }
   if (tid == NT - 1) unit_off[d.B] = run;
@@ -143,6 +156,25 @@ __device__ __forceinline__ Unit decode_unit(const RowsParams& p, int unit) {
     u.i = u.in.s + 1 + jj % per;
   }
   return u;
+}
+
+__device__ __forceinline__ Unit unit_from(int4 e) {
+  Unit u;
+  u.b = e.x;
+  u.slot = e.y & 0xff;
+  u.i = (e.y >> 8) & 0xff;
+  u.in.s = (e.y >> 16) & 0xff;
+  u.in.g = (e.y >> 24) & 0xff;
+  u.in.L = e.z & 0xff;
+  u.in.Lr = (e.z >> 8) & 0xff;
+  u.in.st = e.z >> 16;
+  return u;
+}
+
+// The table entry of `unit` (issued one unit ahead by the streaming kernels), or a
+// zero entry past the end.
+__device__ __forceinline__ int4 unit_prefetch(const RowsParams& p, int unit, int total) {
+  return unit < total ? __ldg(p.units + unit) : make_int4(0, 0, 0, 0);
 }
 
 // Everything after a row pair's statistics are known: path-token probabilities and the
@@ -299,7 +331,10 @@ struct RC {
   static constexpr int CW = CW_, NS = NS_, VPT = VPT_, NP = NP_;
   static constexpr int CT = CW * 32;
   static constexpr int CHUNK = CT * VPT * 16;
+  static constexpr int NE = 2;  // epilogue warps (k_rows_tma), alternating units
   static constexpr int THREADS = CT + 64;
+  static constexpr int ROWS_THREADS = CT + 32 * (1 + NE);
+  static_assert(NP % NE == 0, "each epilogue warp owns NP / NE partial slots");
 };
 
 template <class C>
@@ -573,7 +608,7 @@ __device__ __forceinline__ void compute_stage(const StageRegs<C>& r, int c, Lazy
 }
 
 template <class C, typename T>
-__global__ void __launch_bounds__(C::THREADS, 1) k_rows_tma(RowsParams p) {
+__global__ void __launch_bounds__(C::ROWS_THREADS, 1) k_rows_tma(RowsParams p) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   RowsSmem<C>& S = *reinterpret_cast<RowsSmem<C>*>(smem_raw);
   const Dims& d = p.d;
@@ -601,8 +636,10 @@ __global__ void __launch_bounds__(C::THREADS, 1) k_rows_tma(RowsParams p) {
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
       RingPos<C::NS> rp;
+      int4 nxt = unit_prefetch(p, blockIdx.x, total);
       for (int unit = blockIdx.x; unit < total; unit += gridDim.x) {
-        const Unit un = decode_unit(p, unit);
+        const Unit un = unit_from(nxt);
+        nxt = unit_prefetch(p, unit + gridDim.x, total);
         const char* prow = reinterpret_cast<const char*>(PL + row_off(d, un.b, un.slot, un.i));
         const char* qrow = reinterpret_cast<const char*>(QL + row_off(d, un.b, un.slot, un.i));
         for (int c = 0; c < nchunks; ++c) {
@@ -617,10 +654,15 @@ __global__ void __launch_bounds__(C::THREADS, 1) k_rows_tma(RowsParams p) {
     }
     return;
   }
-  if (warp == C::CW + 1) {  // ---------------- epilogue
-    RingPos<C::NP> up;
-    for (int unit = blockIdx.x; unit < total; unit += gridDim.x) {
-      const Unit un = decode_unit(p, unit);
+  if (warp > C::CW) {  // ---------------- epilogue warps: warp e takes local units e, e+NE, ...
+    const int e = warp - C::CW - 1;
+    int4 nxt = unit_prefetch(p, blockIdx.x + e * gridDim.x, total);
+    for (int li = e, unit = blockIdx.x + e * gridDim.x; unit < total; li += C::NE, unit += C::NE * gridDim.x) {
+      RingPos<C::NP> up;
+      up.stage = li % C::NP;
+      up.phase = (uint32_t)(li / C::NP) & 1u;
+      const Unit un = unit_from(nxt);
+      nxt = unit_prefetch(p, unit + C::NE * gridDim.x, total);
       const T* prow = PL + row_off(d, un.b, un.slot, un.i);
       const T* qrow = QL + row_off(d, un.b, un.slot, un.i);
       // prefetch the path tokens through this row, their uniforms and logits
@@ -726,7 +768,7 @@ static sb_status launch_rows_tma(const RowsParams& p, cudaStream_t s) {
   }
   const int64_t max_units = (int64_t)p.d.B * p.d.K * (p.d.G + 1);
   const int grid = (int)std::min<int64_t>(num_sms(), max_units);
-  k_rows_tma<C, T><<<grid, C::THREADS, smem, s>>>(p);
+  k_rows_tma<C, T><<<grid, C::ROWS_THREADS, smem, s>>>(p);
   return cuda_status(cudaGetLastError());
 }
 
@@ -1233,11 +1275,11 @@ sb_status sb_rows_partial(const sb_dims* dd, const void* p_logits, const void* q
   const bool vok = vec_ok(dd, p_logits) && vec_ok(dd, q_logits);
   if (!vok || ((size_t)dd->V * elem_size(dd)) % 16) return SB_ERR_UNSUPPORTED;
   const Dims d = to_dims(dd);
-  k_plan<<<1, 1024, 0, s>>>(d, gamma, branch_pos, w.info, w.unit_off, 1, 0, nullptr, nullptr);
+  k_plan<<<1, 1024, 0, s>>>(d, gamma, branch_pos, w.info, w.unit_off, 1, 0, nullptr, nullptr, w.units);
   if (cudaGetLastError() != cudaSuccess) return SB_ERR_CUDA;
   RowsParams p{};
   p.d = d; p.PL = p_logits; p.QL = q_logits; p.tok = tok; p.u = u;
-  p.info = w.info; p.unit_off = w.unit_off; p.cnt = w.cnt; p.rowstat = w.rowstat; p.pflag = w.pflag;
+  p.info = w.info; p.unit_off = w.unit_off; p.units = w.units; p.cnt = w.cnt; p.rowstat = w.rowstat; p.pflag = w.pflag;
   p.partial = 1;
   p.v_offset = dd->v_offset;
   const size_t per = (size_t)dd->B * dd->K * (dd->G + 1);
@@ -1269,12 +1311,12 @@ extern "C" sb_status sb_verify_branches(const sb_dims* dd, const void* p_logits,
   const Dims d = to_dims(dd);
   cudaStream_t s = (cudaStream_t)stream;
 
-  k_plan<<<1, 1024, 0, s>>>(d, gamma, branch_pos, w.info, w.unit_off, 0, 0, nullptr, nullptr);
+  k_plan<<<1, 1024, 0, s>>>(d, gamma, branch_pos, w.info, w.unit_off, 0, 0, nullptr, nullptr, w.units);
   if (cudaGetLastError() != cudaSuccess) return SB_ERR_CUDA;
 
   RowsParams p;
   p.d = d; p.PL = p_logits; p.QL = q_logits; p.tok = tok; p.u = u;
-  p.info = w.info; p.unit_off = w.unit_off; p.cnt = w.cnt; p.rowstat = w.rowstat; p.pflag = w.pflag;
+  p.info = w.info; p.unit_off = w.unit_off; p.units = w.units; p.cnt = w.cnt; p.rowstat = w.rowstat; p.pflag = w.pflag;
   p.lse_p = lse_p; p.lse_q = lse_q; p.p_tok = p_tok; p.q_tok = q_tok;
   p.top1_q = top1_q; p.entropy_q = entropy_q; p.top1_id_q = top1_id_q;
   p.acc_mask = acc_mask; p.n_acc = n_acc; p.status = status;

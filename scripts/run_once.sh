@@ -4,6 +4,7 @@ export PYTHONUNBUFFERED=1
 T=${TAG:-x}
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/${T}_build.log 2>&1
-SB_LIB_PATH=$PWD/build/libsb_nocomp.so timeout 600 python bench.py --config c4 --steps 10 --no-e2e --no-cpu-baseline > gpurun_out/${T}_nocomp_c4.log 2>&1
-for v in 0 1 2 3 4; do SB_ROWS_VARIANT=$v timeout 600 python bench.py --config c4 --steps 10 --no-e2e --no-cpu-baseline > gpurun_out/${T}_v${v}_c4.log 2>&1; done
-for v in 1 2 3 4; do SB_ROWS_VARIANT=$v timeout 300 python -m pytest tests/test_gpu_parity.py -q -x -k "small_parity" > gpurun_out/${T}_v${v}_tests.log 2>&1; done
+timeout 900 python -m pytest tests -m "gpu and not slow" -q -x 2>&1 | tail -30 > gpurun_out/${T}_tests.log
+for c in c4 c1 c2 c3 c5; do timeout 600 python bench.py --config $c --steps 10 --no-e2e --no-cpu-baseline > gpurun_out/${T}_bench_$c.log 2>&1; done
+
+for c in c1 c2; do timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${T}_launches_$c.csv python bench.py --config $c --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1; done
