@@ -10,6 +10,7 @@
 
 #include "sb_host.h"
 #include "sb_ring.cuh"
+#include "sb_stream.cuh"
 
 namespace sb {
 
@@ -109,63 +110,24 @@ __global__ void __launch_bounds__(NT) k_conf(ConfParams p, bool vec_ok) {
 
 // TMA ring version (same warp roles as k_rows_tma): producer warp streams 16 KB chunks
 // of each q row, 16 consumer warps fold them, an epilogue warp finishes each row.
-constexpr int cNS = 8;
+constexpr int cNS = 12;
 constexpr int cCW = 16;
 constexpr int cCT = cCW * 32;
 constexpr int cVPT = 2;
 constexpr int cChunk = cCT * cVPT * 16;
 constexpr int cNP = 4;
-constexpr int cThreads = cCT + 64;
+constexpr int cNE = 2;  // epilogue warps, alternating units
+constexpr int cThreads = cCT + 32 * (1 + cNE);
+using ConfGeo = RC<cCW, cNS, cVPT, cNP>;  // ring geometry (resolve_argmax)
 
 struct ConfSmem {
   uint64_t full[cNS], empty[cNS];
   uint64_t pfull[cNP], pempty[cNP];
   RowStat part[cNP][cCW];
-  int s_last;
+  uint2 cand[cNP][cCW];
+  int s_last[cNE];
   alignas(128) uint8_t buf[cNS][cChunk];
 };
-
-template <typename T>
-__device__ __forceinline__ RowStat conf_warp_part(const LazyAcc<true, 4>& a, const T* row,
-                                                  int nvec_last, int nchunks) {
-  constexpr int E = Vec<T>::E;
-  const int tid = threadIdx.x;
-  RowStat s = fold_lazy(a);
-  float mw = s.m;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mw = fmaxf(mw, __shfl_xor_sync(0xffffffffu, mw, o));
-  uint4 x[cVPT];
-  bool have[cVPT];
-  const bool need = (a.m == mw) && (mw > -CUDART_INF_F) && (a.tag >= 0);
-  const int c = a.tag;
-  if (need) {
-    const int nvec = (c == nchunks - 1) ? nvec_last : cChunk / 16;
-    const uint4* cv = reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(row) + (size_t)c * cChunk);
-#pragma unroll
-    for (int j = 0; j < cVPT; ++j) {
-      const int v = tid + j * cCT;
-      have[j] = v < nvec;
-      if (have[j]) x[j] = __ldg(cv + v);
-    }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) s = combine(s, shfl_xor(s, o));
-  s.m = mw;
-  int cand = 0x7fffffff;
-  if (need) {
-#pragma unroll
-    for (int j = cVPT - 1; j >= 0; --j) {
-      if (!have[j]) continue;
-      float f[E];
-      Vec<T>::unpack(x[j], f);
-#pragma unroll
-      for (int e = E - 1; e >= 0; --e)
-        if (f[e] == mw) cand = c * (cChunk / (int)sizeof(T)) + (tid + j * cCT) * E + e;
-    }
-  }
-  s.idx = __reduce_min_sync(0xffffffffu, (unsigned)cand);
-  return s;
-}
 
 template <typename T>
 __global__ void __launch_bounds__(cThreads, 1) k_conf_tma(ConfParams p) {
@@ -210,19 +172,22 @@ __global__ void __launch_bounds__(cThreads, 1) k_conf_tma(ConfParams p) {
     }
     return;
   }
-  if (warp == cCW + 1) {
-    RingPos<cNP> up;
-    for (int unit = blockIdx.x; unit < total; unit += gridDim.x) {
+  if (warp > cCW) {  // epilogue warp e takes local units e, e + cNE, ...
+    const int e = warp - cCW - 1;
+    for (int li = e, unit = blockIdx.x + e * gridDim.x; unit < total; li += cNE, unit += cNE * gridDim.x) {
       const int grp = unit / G, i = unit % G;
-      mbar_wait(&S.pfull[up.stage], up.phase);
-      RowStat r = lane < cCW ? S.part[up.stage][lane] : rowstat_empty();
+      const int stage = li % cNP;
+      mbar_wait(&S.pfull[stage], (uint32_t)(li / cNP) & 1u);
+      RowStat r = lane < cCW ? S.part[stage][lane] : rowstat_empty();
+      const uint2 cand = lane < cCW ? S.cand[stage][lane] : make_uint2(0xffffffffu, 0u);
       __syncwarp();
-      if (lane == 0) mbar_arrive(&S.pempty[up.stage]);
-      up.advance();
+      if (lane == 0) mbar_arrive(&S.pempty[stage]);
+      const float mw = r.m;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) r = combine(r, shfl_xor(r, o));
       const T* row = QL + row_off(d, grp / d.K, grp % d.K, i);
-      conf_epilogue(p, grp, i, row, r, lane, &S.s_last, [] { __syncwarp(); });
+      r.idx = resolve_argmax<ConfGeo, T>(mw, cand, r.m, row, nvec_last, nchunks);
+      conf_epilogue(p, grp, i, row, r, lane, &S.s_last[e], [] { __syncwarp(); });
     }
     return;
   }
@@ -269,12 +234,12 @@ __global__ void __launch_bounds__(cThreads, 1) k_conf_tma(ConfParams p) {
         a.template add<cVPT * E>(f, c);
       }
     }
-    const int grp = unit / G, i = unit % G;
-    const T* row = QL + row_off(d, grp / d.K, grp % d.K, i);
-    const RowStat s = conf_warp_part<T>(a, row, nvec_last, nchunks);
+    uint2 cand;
+    const RowStat s = warp_part_deferred(a, cand);
     if (lane == 0) {
       mbar_wait(&S.pempty[up.stage], up.phase ^ 1u);
       S.part[up.stage][warp] = s;
+      S.cand[up.stage][warp] = cand;
       mbar_arrive(&S.pfull[up.stage]);
     }
     __syncwarp();

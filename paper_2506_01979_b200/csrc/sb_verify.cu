@@ -19,6 +19,7 @@
 #include "sb_host.h"
 #include "sb_ring.cuh"
 #include "sb_sample.cuh"
+#include "sb_stream.cuh"
 
 namespace sb {
 
@@ -114,19 +115,44 @@ __global__ void __launch_bounds__(1024) k_plan(Dims d, const int* __restrict__ g
     }
     return;
   }
+  extern __shared__ int s_off[];  // [B+1] when the unit table is built
   for (int b = b0; b < b1; ++b) {
     unit_off[b] = run;
+    if (units) s_off[b] = run;
     const SeqInfo in = info[b];
-    if (units) {  // slot 0 rows 0..Lr-1, then rows s+1..Lr-1 of slots 1..K-1
-      int4* ub = units + run;
-      for (int i = 0; i < in.Lr; ++i) *ub++ = unit_entry(b, 0, i, in);
-      for (int k = 1; k < d.K; ++k)
-        for (int i = in.s + 1; i < in.Lr; ++i) *ub++ = unit_entry(b, k, i, in);
-    }
     run += in.Lr + (d.K - 1) * (in.Lr - 1 - in.s);
   }
-  if (tid == NT - 1) unit_off[d.B] = run;
+  if (tid == NT - 1) {
+    unit_off[d.B] = run;
+    if (units) s_off[d.B] = run;
+  }
+  if (!units) return;
+  // unit table, coalesced: unit -> sequence by a search over the offsets in smem, then
+  // slot 0 rows 0..Lr-1 followed by rows s+1..Lr-1 of slots 1..K-1
+  __syncthreads();
+  const int total = s_off[d.B];
+  for (int unit = tid; unit < total; unit += NT) {
+    int lo = 0, hi = d.B;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (s_off[mid] <= unit) lo = mid; else hi = mid;
+    }
+    const SeqInfo in = info[lo];
+    const int j = unit - s_off[lo];
+    int slot = 0, i = j;
+    if (j >= in.Lr) {
+      const int per = in.Lr - 1 - in.s, jj = j - in.Lr;
+      slot = 1 + jj / per;
+      i = in.s + 1 + jj % per;
+    }
+    units[unit] = unit_entry(lo, slot, i, in);
+  }
 }
+
+// k_plan's unit table needs B+1 offsets in shared memory; above this the streaming
+// kernels fall back to searching unit_off.
+constexpr int kPlanTableMaxB = 16383;
+inline size_t plan_smem(int B, bool table) { return table ? sizeof(int) * ((size_t)B + 1) : 0; }
 
 // ---------------------------------------------------------------- shared unit logic
 struct Unit {
@@ -174,7 +200,10 @@ __device__ __forceinline__ Unit unit_from(int4 e) {
 // The table entry of `unit` (issued one unit ahead by the streaming kernels), or a
 // zero entry past the end.
 __device__ __forceinline__ int4 unit_prefetch(const RowsParams& p, int unit, int total) {
-  return unit < total ? __ldg(p.units + unit) : make_int4(0, 0, 0, 0);
+  if (unit >= total) return make_int4(0, 0, 0, 0);
+  if (p.units) return __ldg(p.units + unit);
+  const Unit u = decode_unit(p, unit);
+  return unit_entry(u.b, u.slot, u.i, u.in);
 }
 
 // Everything after a row pair's statistics are known: path-token probabilities and the
@@ -321,21 +350,11 @@ __global__ void __launch_bounds__(NT) k_rows(RowsParams p, bool vec_ok) {
 //                             vectors per thread per row per stage), then per unit one
 //                             warp reduction (+ exact first-argmax) -> a partial in
 //                             shared memory (NP slots, mbarrier handshake);
-//   warp CW+1     epilogue  : prefetches the unit's path tokens, uniforms and their two
+//   warps CW+1..  epilogue  : (NE warps, alternating units) prefetch the unit's path tokens, uniforms and their two
 //                             logits while the consumers stream, then combines the CW
 //                             partials, runs the token tests in fp64, writes the row
 //                             outputs and the per-sequence completion — concurrently with
 //                             the consumers streaming the next units.
-template <int CW_, int NS_, int VPT_, int NP_>
-struct RC {
-  static constexpr int CW = CW_, NS = NS_, VPT = VPT_, NP = NP_;
-  static constexpr int CT = CW * 32;
-  static constexpr int CHUNK = CT * VPT * 16;
-  static constexpr int NE = 2;  // epilogue warps (k_rows_tma), alternating units
-  static constexpr int THREADS = CT + 64;
-  static constexpr int ROWS_THREADS = CT + 32 * (1 + NE);
-  static_assert(NP % NE == 0, "each epilogue warp owns NP / NE partial slots");
-};
 
 template <class C>
 struct RowsSmem {
@@ -390,61 +409,6 @@ __device__ __forceinline__ RowStat warp_part(const LazyAcc<kQ, 4>& a, const T* r
   }
   s.idx = kQ ? (int)__reduce_min_sync(0xffffffffu, (unsigned)cand) : 0;
   return s;
-}
-
-// Consumer side of a q row without the argmax lookup: the warp's reduced state (idx
-// unresolved) and its argmax candidates: the smallest chunk tag among the lanes holding
-// the warp maximum and the mask of those lanes with that tag.  The epilogue warp
-// resolves the index (resolve_argmax) off the consumers' critical path.
-template <bool kQ>
-__device__ __forceinline__ RowStat warp_part_deferred(const LazyAcc<kQ, 4>& a, uint2& cand) {
-  RowStat s = fold_lazy(a);
-  float mw = s.m;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mw = fmaxf(mw, __shfl_xor_sync(0xffffffffu, mw, o));
-  const bool hold = (a.m == mw) && (mw > -CUDART_INF_F) && (a.tag >= 0);
-  const unsigned t = hold ? (unsigned)a.tag : 0xffffffffu;
-  const unsigned tmin = __reduce_min_sync(0xffffffffu, t);
-  cand = make_uint2(tmin, __ballot_sync(0xffffffffu, hold && t == tmin));
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) s = combine(s, shfl_xor(s, o));
-  s.m = mw;
-  s.idx = 0x7fffffff;
-  return s;
-}
-
-// Epilogue side: lane w < CW holds warp w's part (mw = its maximum) and candidates;
-// M = the row maximum.  The first index of M lies in the smallest candidate chunk of
-// the warps holding M; the candidate lanes re-read their vectors of that chunk (one
-// load round, normally one lane).  Returns the index in every lane.
-template <class C, typename T>
-__device__ __forceinline__ int resolve_argmax(float mw, uint2 cand, float M, const T* row, int nvec_last,
-                                              int nchunks) {
-  constexpr int E = Vec<T>::E;
-  const int lane = threadIdx.x & 31;
-  const unsigned t = (lane < C::CW && mw == M && M > -CUDART_INF_F) ? cand.x : 0xffffffffu;
-  const unsigned tmin = __reduce_min_sync(0xffffffffu, t);
-  int best = 0x7fffffff;
-  if (t == tmin && tmin != 0xffffffffu) {
-    const int c = (int)tmin;
-    const int nvec = (c == nchunks - 1) ? nvec_last : C::CHUNK / 16;
-    const uint4* cv =
-        reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(row) + (size_t)c * C::CHUNK);
-    for (uint32_t m = cand.y; m; m &= m - 1) {
-      const int tid = lane * 32 + __ffs(m) - 1;
-#pragma unroll
-      for (int j = 0; j < C::VPT; ++j) {
-        const int v = tid + j * C::CT;
-        if (v >= nvec) continue;
-        float f[E];
-        Vec<T>::unpack(__ldg(cv + v), f);
-#pragma unroll
-        for (int e = E - 1; e >= 0; --e)
-          if (f[e] == M) best = min(best, c * (C::CHUNK / (int)sizeof(T)) + v * E + e);
-      }
-    }
-  }
-  return (int)__reduce_min_sync(0xffffffffu, (unsigned)best);
 }
 
 // Epilogue of one unit by one warp, with the token data already prefetched.
@@ -1275,11 +1239,15 @@ sb_status sb_rows_partial(const sb_dims* dd, const void* p_logits, const void* q
   const bool vok = vec_ok(dd, p_logits) && vec_ok(dd, q_logits);
   if (!vok || ((size_t)dd->V * elem_size(dd)) % 16) return SB_ERR_UNSUPPORTED;
   const Dims d = to_dims(dd);
-  k_plan<<<1, 1024, 0, s>>>(d, gamma, branch_pos, w.info, w.unit_off, 1, 0, nullptr, nullptr, w.units);
+  const bool table = d.B <= kPlanTableMaxB;
+  if (table && plan_smem(d.B, true) > 48 * 1024)
+    cudaFuncSetAttribute(k_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan_smem(kPlanTableMaxB, true));
+  k_plan<<<1, 1024, plan_smem(d.B, table), s>>>(d, gamma, branch_pos, w.info, w.unit_off, 1, 0, nullptr, nullptr,
+                                                table ? w.units : nullptr);
   if (cudaGetLastError() != cudaSuccess) return SB_ERR_CUDA;
   RowsParams p{};
   p.d = d; p.PL = p_logits; p.QL = q_logits; p.tok = tok; p.u = u;
-  p.info = w.info; p.unit_off = w.unit_off; p.units = w.units; p.cnt = w.cnt; p.rowstat = w.rowstat; p.pflag = w.pflag;
+  p.info = w.info; p.unit_off = w.unit_off; p.units = table ? w.units : nullptr; p.cnt = w.cnt; p.rowstat = w.rowstat; p.pflag = w.pflag;
   p.partial = 1;
   p.v_offset = dd->v_offset;
   const size_t per = (size_t)dd->B * dd->K * (dd->G + 1);
@@ -1311,12 +1279,16 @@ extern "C" sb_status sb_verify_branches(const sb_dims* dd, const void* p_logits,
   const Dims d = to_dims(dd);
   cudaStream_t s = (cudaStream_t)stream;
 
-  k_plan<<<1, 1024, 0, s>>>(d, gamma, branch_pos, w.info, w.unit_off, 0, 0, nullptr, nullptr, w.units);
+  const bool table = d.B <= kPlanTableMaxB;
+  if (table && plan_smem(d.B, true) > 48 * 1024)
+    cudaFuncSetAttribute(k_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan_smem(kPlanTableMaxB, true));
+  k_plan<<<1, 1024, plan_smem(d.B, table), s>>>(d, gamma, branch_pos, w.info, w.unit_off, 0, 0, nullptr, nullptr,
+                                                table ? w.units : nullptr);
   if (cudaGetLastError() != cudaSuccess) return SB_ERR_CUDA;
 
   RowsParams p;
   p.d = d; p.PL = p_logits; p.QL = q_logits; p.tok = tok; p.u = u;
-  p.info = w.info; p.unit_off = w.unit_off; p.units = w.units; p.cnt = w.cnt; p.rowstat = w.rowstat; p.pflag = w.pflag;
+  p.info = w.info; p.unit_off = w.unit_off; p.units = table ? w.units : nullptr; p.cnt = w.cnt; p.rowstat = w.rowstat; p.pflag = w.pflag;
   p.lse_p = lse_p; p.lse_q = lse_q; p.p_tok = p_tok; p.q_tok = q_tok;
   p.top1_q = top1_q; p.entropy_q = entropy_q; p.top1_id_q = top1_id_q;
   p.acc_mask = acc_mask; p.n_acc = n_acc; p.status = status;
