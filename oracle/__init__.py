@@ -251,3 +251,27 @@ def kv_rollback(kv, branch_pos, sel_k, commit_len, y_kind):
             slot = 0 if (i < s or ks < 0) else ks
             out[b, i] = kv[b, slot, i]
     return out
+
+
+def hrad(z, w1, b1, w2, b2, w3, b3, stop=None, G=0, nthreads=0):
+    """H-RAD MLP + H_t mapping (oracle.h oracle_hrad; reading 35).
+    z [B][Dz], w1 [256][Dz] as uint16 (raw bf16); the rest float32."""
+    z = np.ascontiguousarray(z, dtype=np.uint16)
+    w1 = np.ascontiguousarray(w1, dtype=np.uint16)
+    B, Dz = z.shape
+    assert w1.shape == (256, Dz)
+    f32 = lambda a: np.ascontiguousarray(a, dtype=np.float32)  # noqa: E731
+    b1, w2, b2, w3, b3 = f32(b1), f32(w2), f32(b2), f32(w3), f32(b3)
+    assert b1.shape == (256,) and w2.shape == (64, 256) and b2.shape == (64,)
+    assert w3.shape == (3, 64) and b3.shape == (3,)
+    st = None if stop is None else np.ascontiguousarray(stop, dtype=np.int32)
+    o = {"h1": np.empty((B, 256)), "logits": np.empty((B, 3)), "s_t": np.empty(B, np.int32),
+         "gamma": np.empty(B, np.int32), "branch_pos": np.empty(B, np.int32), "margin": np.empty(B)}
+    f = lib().oracle_hrad
+    f.restype = ctypes.c_int
+    rc = f(ctypes.c_int(B), ctypes.c_int(Dz), _ptr(z), _ptr(w1), _ptr(b1), _ptr(w2), _ptr(b2), _ptr(w3),
+           _ptr(b3), _ptr(st), ctypes.c_int(G), ctypes.c_int(nthreads), _ptr(o["h1"]), _ptr(o["logits"]),
+           _ptr(o["s_t"]), _ptr(o["gamma"]), _ptr(o["branch_pos"]), _ptr(o["margin"]))
+    if rc != 0:
+        raise ValueError("oracle_hrad rejected its arguments")
+    return o

@@ -499,3 +499,71 @@ int oracle_tree_verify(const or_dims* d, const void* PL, const void* QL, const i
   for (int b = 0; b < d->B; ++b) tree_one(d, PL, QL, parent, tok, u, us, o, b);
   return 0;
 }
+
+/* ---------------------------------------------------------------- H-RAD (f4)
+ * Eq. 4-5 (P190-191) with the architecture of P745 (two hidden layers of 256 and 64
+ * ReLU units, a 3-way classification layer; dropout is a training-time operation and
+ * absent at inference):
+ *   h1 = relu(W1 z + b1), h2 = relu(W2 h1 + b2), l = W3 h2 + b3,
+ *   s_t = argmax softmax(l) = argmax l (softmax is monotone; ties -> smaller class).
+ * H_t (P194-201, read with the stage-transition cases of P669, DESIGN reading 35):
+ *   s_t = 0 (all reject)  -> gamma_b = 0,    s_b = 0     (branch at this round's first token)
+ *   s_t = 1 (confidence)  -> gamma_b = stop, s_b = stop  (branch at the first q(x) <= eps)
+ *   s_t = 2 (all accept)  -> gamma_b = G,    s_b = G     (branch at the next round's first token)
+ * z and W1 are the exact bf16 bytes (widened exactly), the rest fp32; all sums fp64,
+ * in index order.  margin[b] = l(best) - l(second) (the near-tie distance). */
+static double bf16_to_double(uint16_t h) {
+  uint32_t bits = (uint32_t)h << 16;
+  float f;
+  memcpy(&f, &bits, sizeof f);
+  return (double)f;
+}
+
+int oracle_hrad(int B, int Dz, const uint16_t* z, const uint16_t* w1, const float* b1, const float* w2,
+                const float* b2, const float* w3, const float* b3, const int32_t* stop, int G, int nthreads,
+                double* h1_out, double* logits, int32_t* s_t, int32_t* gamma, int32_t* branch_pos,
+                double* margin) {
+  if (B < 1 || Dz < 1 || !z || !w1 || !b1 || !w2 || !b2 || !w3 || !b3 || !logits || !s_t || G < 0)
+    return -1;
+#pragma omp parallel for schedule(dynamic, 8) num_threads(nthreads > 0 ? nthreads : omp_default_threads())
+  for (int b = 0; b < B; ++b) {
+    double h1[256], h2[64], l[3];
+    for (int j = 0; j < 256; ++j) {
+      double acc = 0.0;
+      for (int c = 0; c < Dz; ++c)
+        acc += bf16_to_double(w1[(int64_t)j * Dz + c]) * bf16_to_double(z[(int64_t)b * Dz + c]);
+      acc += (double)b1[j];
+      h1[j] = acc > 0.0 ? acc : 0.0;
+      if (h1_out) h1_out[(int64_t)b * 256 + j] = h1[j];
+    }
+    for (int j = 0; j < 64; ++j) {
+      double acc = 0.0;
+      for (int c = 0; c < 256; ++c) acc += (double)w2[j * 256 + c] * h1[c];
+      acc += (double)b2[j];
+      h2[j] = acc > 0.0 ? acc : 0.0;
+    }
+    for (int k = 0; k < 3; ++k) {
+      double acc = 0.0;
+      for (int c = 0; c < 64; ++c) acc += (double)w3[k * 64 + c] * h2[c];
+      l[k] = acc + (double)b3[k];
+      logits[(int64_t)b * 3 + k] = l[k];
+    }
+    int best = 0;
+    for (int k = 1; k < 3; ++k)
+      if (l[k] > l[best]) best = k;
+    double second = -INFINITY;
+    for (int k = 0; k < 3; ++k)
+      if (k != best && l[k] > second) second = l[k];
+    if (margin) margin[b] = l[best] - second;
+    s_t[b] = best;
+    if (gamma && branch_pos) {
+      int st = stop ? stop[b] : G;
+      if (st < 0) st = 0;
+      if (st > G) st = G;
+      const int g = best == 0 ? 0 : (best == 1 ? st : G);
+      gamma[b] = g;
+      branch_pos[b] = g;
+    }
+  }
+  return 0;
+}

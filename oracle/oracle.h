@@ -163,6 +163,16 @@ typedef struct {
 int oracle_tree_verify(const or_dims* d, const void* PL, const void* QL, const int32_t* parent,
                        const int32_t* tok, const float* u, const float* us, int nthreads, or_tree_out* o);
 
+/* H-RAD MLP (Eq. 4-5 P190-191, architecture P745, H_t P194-201 with
+ * the cases of P669): z [B][Dz] and W1 [256][Dz] raw bf16, b1 [256], W2 [64][256],
+ * b2 [64], W3 [3][64], b3 [3] fp32; stop [B] (a6's confidence stop, may be NULL -> G).
+ * Outputs: h1 [B][256] (may be NULL), logits [B][3], s_t [B], gamma / branch_pos [B]
+ * (may be NULL), margin [B] (top-2 logit gap, may be NULL). */
+int oracle_hrad(int B, int Dz, const uint16_t* z, const uint16_t* w1, const float* b1, const float* w2,
+                const float* b2, const float* w3, const float* b3, const int32_t* stop, int G, int nthreads,
+                double* h1_out, double* logits, int32_t* s_t, int32_t* gamma, int32_t* branch_pos,
+                double* margin);
+
 #ifdef __cplusplus
 }
 #endif

@@ -283,3 +283,39 @@ def tree_to_numpy(inp: dict):
         out[k] = inp[k].detach().cpu().contiguous().numpy()
     out["V"], out["N"] = inp["V"], inp["N"]
     return out
+
+
+# ---------------------------------------------------------------- H-RAD (f4)
+# Feature width of z_t = Concat(h^1..h^{L_f}, e_t) (Eq. 4, P190): L_f = 4 target layers
+# (P400, Table 5) of the target hidden size plus the token embedding.  LLaMA-3.1-8B
+# (hidden 4096) -> 5 * 4096 = 20480; Vicuna-13B (hidden 5120) -> 25600.
+HRAD_DZ = {"llama31_8b": 5 * 4096, "vicuna_13b": 5 * 5120}
+
+
+def hrad_inputs(B: int, Dz: int, G: int = 8, seed: int = 0, device="cpu"):
+    """Synthetic H-RAD inputs (random-init weights: no trained checkpoint exists here).
+
+    z ~ N(0, 1) rounded to bf16 (hidden-state-like scale); W1 ~ N(0, 2/Dz) bf16 (He
+    init for the ReLU layer), b1 ~ N(0, 0.1); W2 ~ N(0, 2/256), b2 ~ N(0, 0.1);
+    W3 ~ N(0, 1/64), b3 = 0; stop ~ U{0..G} stands in for a6's confidence stop.
+    Holds none of the MLP's arithmetic."""
+    g = torch.Generator(device="cpu").manual_seed(SEED_BASE + 7919 * seed + 17)
+    z = torch.randn(B, Dz, generator=g).to(torch.bfloat16)
+    w1 = (torch.randn(256, Dz, generator=g) * math.sqrt(2.0 / Dz)).to(torch.bfloat16)
+    b1 = torch.randn(256, generator=g) * 0.1
+    w2 = torch.randn(64, 256, generator=g) * math.sqrt(2.0 / 256)
+    b2 = torch.randn(64, generator=g) * 0.1
+    w3 = torch.randn(3, 64, generator=g) * math.sqrt(1.0 / 64)
+    b3 = torch.zeros(3)
+    stop = torch.randint(0, G + 1, (B,), generator=g, dtype=torch.int32)
+    out = {"z": z, "w1": w1, "b1": b1, "w2": w2, "b2": b2, "w3": w3, "b3": b3, "stop": stop, "G": G}
+    return {k: (v.to(device) if torch.is_tensor(v) else v) for k, v in out.items()}
+
+
+def hrad_to_numpy(inp: dict):
+    """The exact bytes both sides consume: bf16 as raw uint16, the rest float32 / int32."""
+    u16 = lambda t: t.detach().cpu().contiguous().view(torch.int16).numpy().view("uint16")  # noqa: E731
+    f = lambda t: t.detach().cpu().float().numpy()  # noqa: E731
+    return {"z": u16(inp["z"]), "w1": u16(inp["w1"]), "b1": f(inp["b1"]), "w2": f(inp["w2"]),
+            "b2": f(inp["b2"]), "w3": f(inp["w3"]), "b3": f(inp["b3"]),
+            "stop": inp["stop"].cpu().numpy().astype("int32"), "G": inp["G"]}

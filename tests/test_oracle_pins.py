@@ -672,3 +672,64 @@ def test_tree_accept_test_closed_form(orc):
         assert int(t["acc_mask"][0]) == (acc2 * 1 | 2)
         # both accepted -> Eq. 9 picks the larger target logit: token 0 (p = 1/2)
         assert t["stop_node"][0] == 1 and t["out_tok"][0, 0] == 0 and t["y_kind"][0] == 2
+
+
+# ---------------------------------------------------------------- H-RAD MLP (f4, Eq. 4-5, P745)
+def _bf16_bits(x):
+    import torch
+
+    return torch.tensor(np.asarray(x, np.float32)).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+
+
+def _bf16_vals(bits):
+    return (bits.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+
+
+def test_hrad_matches_library_matmul(orc):
+    """Plain-loop oracle vs numpy's float64 matmul on the same widened bytes (a library
+    routine, an independent implementation of the three affine layers)."""
+    from paper_2506_01979_b200 import synth
+
+    n = synth.hrad_to_numpy(synth.hrad_inputs(37, 320, G=6, seed=3))
+    o = orc.hrad(n["z"], n["w1"], n["b1"], n["w2"], n["b2"], n["w3"], n["b3"], n["stop"], n["G"])
+    z, w1 = _bf16_vals(n["z"]), _bf16_vals(n["w1"])
+    h1 = np.maximum(z @ w1.T + n["b1"].astype(np.float64), 0.0)
+    h2 = np.maximum(h1 @ n["w2"].astype(np.float64).T + n["b2"], 0.0)
+    lg = h2 @ n["w3"].astype(np.float64).T + n["b3"]
+    assert np.allclose(o["h1"], h1, rtol=1e-12, atol=1e-12)
+    assert np.allclose(o["logits"], lg, rtol=1e-12, atol=1e-12)
+    assert np.array_equal(o["s_t"], np.argmax(lg, axis=1))
+
+
+def test_hrad_closed_form_identity_network(orc):
+    """W1 = I, W2 = [I 0], W3 = [I 0] -> logits = relu(relu(z[:3]) ) + b3, so the class is
+    the argmax of the first three (bf16-exact) features; ReLU clips negatives."""
+    Dz = 256
+    rng = np.random.default_rng(5)
+    zv = rng.choice([-2.0, -0.5, 0.25, 0.75, 1.5, 3.0], size=(9, Dz))
+    z = _bf16_bits(zv)
+    w1 = _bf16_bits(np.eye(256, Dz))
+    w2 = np.eye(64, 256, dtype=np.float32)
+    w3 = np.eye(3, 64, dtype=np.float32)
+    zero = lambda n: np.zeros(n, np.float32)  # noqa: E731
+    o = orc.hrad(z, w1, zero(256), w2, zero(64), w3, zero(3))
+    expect = np.maximum(zv[:, :3], 0.0)
+    assert np.array_equal(o["logits"], expect)
+    first_max = np.array([int(np.flatnonzero(r == r.max())[0]) for r in expect])
+    assert np.array_equal(o["s_t"], first_max)  # ties -> smaller class (incl. all-zero rows)
+
+
+def test_hrad_ties_and_branch_layout(orc):
+    """Ties go to the smaller class; H_t maps s_t = 0/1/2 to (gamma, s) = (0,0) /
+    (stop, stop) / (G, G) (P194-201, P669; DESIGN reading 35)."""
+    Dz, G = 64, 8
+    z = _bf16_bits(np.zeros((6, Dz)))
+    w1 = _bf16_bits(np.zeros((256, Dz)))
+    zero = lambda n: np.zeros(n, np.float32)  # noqa: E731
+    w2, w3 = np.zeros((64, 256), np.float32), np.zeros((3, 64), np.float32)
+    stop = np.array([0, 3, 8, 11, -2, 5], np.int32)
+    for b3, cls in (([1, 1, 0], 0), ([0, 2, 2], 1), ([0, 1, 2], 2), ([5, 5, 5], 0)):
+        o = orc.hrad(z, w1, zero(256), w2, zero(64), w3, np.array(b3, np.float32), stop, G)
+        assert (o["s_t"] == cls).all()
+        exp = {0: np.zeros(6), 1: np.clip(stop, 0, G), 2: np.full(6, G)}[cls]
+        assert np.array_equal(o["gamma"], exp) and np.array_equal(o["branch_pos"], exp)
