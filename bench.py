@@ -317,6 +317,97 @@ def run_ours(args, rank, world, local_rank):
     return line
 
 
+def tensor_peak():
+    try:
+        pk = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return float(pk["bf16_tflops"]), "measured (MEASURED_PEAKS.json bf16_tflops, burst)"
+    except Exception:
+        return 1590.0, "fallback (B200_PROFILING.md 1.59 PFLOP/s)"
+
+
+def run_hrad(args, rank, world, local_rank):
+    """--config hrad: the f4 row, H-RAD MLP inference (sb_hrad_predict) on synthetic
+    LLaMA-3.1-8B-shaped features (Dz = 4 layers x 4096 + 4096 embedding = 20480, P400)
+    for a batch of sequences per rank.  Three input sets rotate so no launch finds its
+    z / W1 in L2 (3 x 94 MB > 126 MB)."""
+    import numpy as np
+    import torch
+
+    from paper_2506_01979_b200 import _lib, api, synth
+    from paper_2506_01979_b200.build import build
+
+    build()
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    B, Dz, G = args.hrad_batch, synth.HRAD_DZ["llama31_8b"], 16
+    sets = [synth.hrad_inputs(B, Dz, G=G, seed=1000 * rank + j, device=dev) for j in range(3)]
+    nws = int(_lib.lib().sb_hrad_workspace_bytes(B, Dz))
+    outs = [(torch.empty(B, dtype=torch.int32, device=dev), torch.empty((B, 3), device=dev),
+             torch.empty(B, dtype=torch.int32, device=dev), torch.empty(B, dtype=torch.int32, device=dev),
+             torch.empty(nws, dtype=torch.uint8, device=dev)) for _ in range(3)]
+
+    def call(j, s_):
+        x, o = sets[j], outs[j]
+        api.sb_hrad_predict(x["z"], x["w1"], x["b1"], x["w2"], x["b2"], x["w3"], x["b3"], G, stop=x["stop"],
+                            s_t=o[0], logits=o[1], gamma=o[2], branch_pos=o[3], workspace=o[4], stream=s_)
+
+    graphs = [api.CallGraph(lambda s_, j=j: call(j, s_)) for j in range(3)]
+    for k in range(max(args.warmup, 3)):
+        graphs[k % 3].replay()
+    torch.cuda.synchronize()
+    clk = Clocks(local_rank if not args.no_clocks else -1).__enter__()
+    time.sleep(0.3)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    cur = torch.cuda.current_stream()
+    for k, (e0, e1) in enumerate(evs):
+        e0.record(cur)
+        graphs[k % 3].replay()
+        e1.record(cur)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    clk.__exit__()
+    ms = sum(e0.elapsed_time(e1) for e0, e1 in evs) / args.steps
+    ms_all, rows_all, _, _ = reduce_over_ranks(ms, B, 0, 0, dev, world)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle
+
+        n = synth.hrad_to_numpy({k: (v[:64] if k in ("z", "stop") else v) for k, v in sets[0].items()})
+        nthreads = os.cpu_count() or 1
+        t0 = time.time()
+        oracle.hrad(n["z"], n["w1"], n["b1"], n["w2"], n["b2"], n["w3"], n["b3"], n["stop"], G, nthreads=nthreads)
+        dt = time.time() - t0
+        cpu = {"value": round(64 / dt, 1), "unit": "H-RAD predictions/s", "cores": nthreads, "kind": "oracle",
+               "sample": f"64 of {B} sequences, {dt:.2f} s, fp64 plain loops, OpenMP over sequences"}
+    if rank != 0:
+        return None
+    peak, peak_src = peaks()
+    tpk, tpk_src = tensor_peak()
+    nbytes = B * Dz * 2 + 256 * Dz * 2 + B * 4 * 4 + 256 * 4 + 64 * 256 * 4
+    flops = 2.0 * B * Dz * 256 + 2.0 * B * 256 * 64 + 2.0 * B * 64 * 3
+    gbs = nbytes / (ms * 1e-3) / 1e9
+    tfs = flops / (ms * 1e-3) / 1e12
+    return {
+        "metric": "H-RAD length predictions/s (SURVEY §8.6 f4)", "value": round(rows_all / (ms_all * 1e-3), 1),
+        "unit": "predictions/s", "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
+        "ms_per_step": round(ms_all, 5), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16", "data": "synthetic (seeded features and random-init weights; no trained H-RAD exists)",
+        "config": {"workload": f"H-RAD MLP {Dz}-256-64-3, batch {B} per GPU (LLaMA-3.1-8B features, L_f = 4)",
+                   "l2": "3 rotating input sets (3 x %.0f MB > 126 MB L2)" % (nbytes / 1e6)},
+        "roofline": {"bound": "hbm", "kernel": "k_hrad (tcgen05 layer 1, split-K) + k_hrad_tail (PDL)",
+                     "achieved": round(gbs, 1), "peak": peak, "peak_source": peak_src, "unit": "GB/s",
+                     "frac": round(gbs / peak, 4), "traffic": None, "algorithmic_bytes_per_launch": nbytes},
+        "tensor": {"achieved_tflops": round(tfs, 1), "peak": tpk, "peak_source": tpk_src,
+                   "frac": round(tfs / tpk, 4), "flops_per_launch": flops},
+        "gpu_launches": args.steps, "clocks": clk.summary(),
+        **({"cpu_baseline": cpu} if cpu else {}),
+    }
+
+
 def traffic_from_profiles(name):
     p = os.path.join(ROOT, "profiles", f"traffic_{name}.json")
     try:
@@ -461,7 +552,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4", "c5", "hrad"])
+    ap.add_argument("--hrad-batch", type=int, default=2048)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="issue the C-ABI calls eagerly each step")
@@ -490,7 +582,7 @@ def main():
 
         torch.cuda.set_device(local_rank)
         torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    line = run_ours(args, rank, world, local_rank)
+    line = (run_hrad if args.config == "hrad" else run_ours)(args, rank, world, local_rank)
     if line is not None:
         print(json.dumps(line), flush=True)
     if world > 1:

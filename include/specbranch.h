@@ -271,6 +271,34 @@ sb_status sb_tree_verify(const sb_dims* d, const void* p_logits, const void* q_l
                          size_t workspace_bytes, sb_stream_t stream);
 
 /*
+ * sb_hrad_predict — H-RAD draft-length predictor inference: the
+ * lightweight MLP of Eq. 4-5 (P190-191) with the architecture of P745 and the hybrid
+ * strategy H_t (P194-201) mapped onto this library's branch layout (P669; DESIGN.md
+ * reading 35):
+ *   h1 = relu(W1 z + b1), h2 = relu(W2 h1 + b2), l = W3 h2 + b3, s_t = argmax l
+ *   (softmax is monotone; ties -> smaller class); (gamma_b, branch_pos_b) =
+ *   (0, 0) if s_t = 0 (all reject), (stop_b, stop_b) if s_t = 1 (confidence; stop_b
+ *   from sb_draft_confidence, clamped to [0, G]; NULL stop -> G), (G, G) if s_t = 2.
+ * z: [B][Dz] bf16 row-major (features Concat(h^1..h^4, e_t), Eq. 4), w1: [256][Dz] bf16,
+ * b1 [256], w2 [64][256], b2 [64], w3 [3][64], b3 [3] fp32 — all device pointers,
+ * caller-owned, z / w1 16-byte aligned.  Outputs (device, overwritten): s_t [B];
+ * logits [B][3], gamma [B], branch_pos [B] may be NULL.  Layer 1 runs on the tensor
+ * cores (tcgen05, fp32 accumulation, split along K; the split partials — the
+ * workspace, sb_hrad_workspace_bytes(B, Dz) bytes, 16-byte aligned, no initialisation
+ * needed — are summed in a fixed order, so results are run-to-run deterministic);
+ * layers 2-3 in fp32.  Errors: SB_ERR_INVALID_ARG (B < 1, G outside [0, 31], NULL
+ * required pointer), SB_ERR_UNSUPPORTED (Dz not a multiple of 64, misaligned z / w1),
+ * SB_ERR_WORKSPACE (too small), SB_ERR_CUDA (tensor-map encode or launch).
+ * Stream-ordered, no host synchronisation.
+ */
+size_t sb_hrad_workspace_bytes(int32_t B, int32_t Dz);
+sb_status sb_hrad_predict(int32_t B, int32_t Dz, int32_t G, const void* z, const void* w1, const float* b1,
+                          const float* w2, const float* b2, const float* w3, const float* b3,
+                          const int32_t* stop, float* logits, int32_t* s_t, int32_t* gamma,
+                          int32_t* branch_pos, void* workspace, size_t workspace_bytes,
+                          sb_stream_t stream);
+
+/*
  * ---- Vocabulary-sharded variant (a7) ----------------------
  * Rank g of G holds the contiguous slice [v_offset, v_offset + V) of the v_total-token
  * vocabulary; slices are in rank order (so global ascending-id order = rank order).

@@ -17,7 +17,7 @@ SB_ST_GAMMA_CLAMPED, SB_ST_BRANCH_CLAMPED, SB_ST_BAD_TOKEN, SB_ST_NONFINITE, SB_
 
 # every symbol include/specbranch.h declares
 EXPORTS = ("sb_version", "sb_status_string", "sb_workspace_bytes", "sb_verify_branches",
-           "sb_select_branch", "sb_verify_select", "sb_draft_confidence", "sb_spawn_branches", "sb_kv_rollback", "sb_tree_workspace_bytes", "sb_tree_verify", "sb_shard_partial_bytes", "sb_shard_verify_local",
+           "sb_select_branch", "sb_verify_select", "sb_draft_confidence", "sb_spawn_branches", "sb_kv_rollback", "sb_tree_workspace_bytes", "sb_tree_verify", "sb_hrad_workspace_bytes", "sb_hrad_predict", "sb_shard_partial_bytes", "sb_shard_verify_local",
            "sb_shard_verify_combine", "sb_shard_select_local", "sb_shard_select_sample",
            "sb_shard_select_commit", "sb_comm_unique_id_bytes", "sb_comm_unique_id", "sb_comm_create",
            "sb_comm_destroy")
@@ -49,6 +49,8 @@ _SIGS = {
     "sb_spawn_branches": ([_D, _P, _P, _P, _I, ctypes.c_int32] + [_P] * 4 + [_P], _I),
     "sb_kv_rollback": ([_I, _I, _I, _P, ctypes.c_int64, ctypes.c_int64] + [_P] * 5 + [_P], _I),
     "sb_tree_workspace_bytes": ([_D], _S),
+    "sb_hrad_workspace_bytes": ([_I, _I], _S),
+    "sb_hrad_predict": ([_I, _I, _I] + [_P] * 12 + [_P, _S, _P], _I),
     "sb_tree_verify": ([_D] + [_P] * 16 + [_S, _P], _I),
     "sb_shard_partial_bytes": ([_D], _S),
     "sb_shard_verify_local": ([_D] + [_P] * 8 + [_S, _P], _I),

@@ -430,3 +430,27 @@ class Comm:
         if self.handle:
             L.check(L.lib().sb_comm_destroy(self.handle), "sb_comm_destroy")
             self.handle = ctypes.c_void_p()
+
+
+def sb_hrad_predict(z: torch.Tensor, w1: torch.Tensor, b1, w2, b2, w3, b3, G: int, stop=None,
+                    logits=None, s_t=None, gamma=None, branch_pos=None, workspace=None, stream=None):
+    """H-RAD MLP inference (include/specbranch.h sb_hrad_predict).  z [B][Dz] and
+    w1 [256][Dz] bf16; b1, w2, b2, w3, b3 fp32; stop int32 [B] or None.  Returns
+    (s_t, logits, gamma, branch_pos), allocating any output not given."""
+    B, Dz = z.shape
+    dev = z.device
+    s_t = torch.empty(B, dtype=I32, device=dev) if s_t is None else s_t
+    logits = torch.empty((B, 3), dtype=F32, device=dev) if logits is None else logits
+    gamma = torch.empty(B, dtype=I32, device=dev) if gamma is None else gamma
+    branch_pos = torch.empty(B, dtype=I32, device=dev) if branch_pos is None else branch_pos
+    BF = torch.bfloat16
+    nws = int(L.lib().sb_hrad_workspace_bytes(B, Dz))
+    if workspace is None or workspace.numel() < nws:
+        workspace = torch.empty(max(nws, 16), dtype=torch.uint8, device=dev)
+    L.check(L.lib().sb_hrad_predict(
+        B, Dz, int(G), _ptr(z, BF, "z"), _ptr(w1, BF, "w1"), _ptr(b1, F32, "b1"), _ptr(w2, F32, "w2"),
+        _ptr(b2, F32, "b2"), _ptr(w3, F32, "w3"), _ptr(b3, F32, "b3"), _ptr(stop, I32, "stop"),
+        _ptr(logits, F32, "logits"), _ptr(s_t, I32, "s_t"), _ptr(gamma, I32, "gamma"),
+        _ptr(branch_pos, I32, "branch_pos"), _ptr(workspace, torch.uint8, "workspace"), ctypes.c_size_t(nws),
+        _stream(stream)), "sb_hrad_predict")
+    return s_t, logits, gamma, branch_pos

@@ -1,13 +1,9 @@
-# scratch driver for one gpurun call (edited per experiment): A/B of build/libsb_head.so vs the tree
 set -u
 export PYTHONUNBUFFERED=1
 T=${TAG:-x}
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/${T}_build.log 2>&1
-timeout 900 python -m pytest tests -m "gpu and not slow" -q -x 2>&1 | tail -30 > gpurun_out/${T}_tests.log
-for c in c2 c3 c1 c4; do
-  for r in 1 2; do
-  SB_LIB_PATH=$PWD/build/libsb_head.so timeout 600 python bench.py --config $c --steps 10 --no-e2e --no-cpu-baseline > gpurun_out/${T}_A${r}_$c.log 2>&1
-  timeout 600 python bench.py --config $c --steps 10 --no-e2e --no-cpu-baseline > gpurun_out/${T}_B${r}_$c.log 2>&1
-  done
-done
+timeout 300 python -m pytest tests/test_gpu_next.py -q -x -k hrad 2>&1 | tail -30 > gpurun_out/${T}_tests.log
+SB_HRAD_CM=2 timeout 300 python -m pytest tests/test_gpu_next.py -q -x -k hrad 2>&1 | tail -30 > gpurun_out/${T}_tests_cm4.log
+for cm in 1 2; do for b in 2048 256; do SB_HRAD_CM=$cm timeout 300 python bench.py --config hrad --hrad-batch $b --steps 30 --no-cpu-baseline > gpurun_out/${T}_hrad_${b}_cm$cm.log 2>&1; done; done
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_hrad" -s 6 -c 2 -o gpurun_out/${T}_hrad python bench.py --config hrad --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/${T}_ncu_hrad.log 2>&1

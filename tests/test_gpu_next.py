@@ -157,3 +157,45 @@ def test_tree_bad_parent_and_nonfinite():
     ok = o["ties"] == 0
     assert np.array_equal(buf.commit_len.cpu().numpy()[ok], o["commit_len"][ok])
     assert np.array_equal(buf.out_tok.cpu().numpy()[ok], o["out_tok"][ok])
+
+
+# ---------------------------------------------------------------- f4: H-RAD MLP (tcgen05)
+HRAD = [("B1_Dz64", 1, 64), ("B100_Dz320", 100, 320), ("B129_Dz256", 129, 256), ("B128_Dz5120", 128, 5120),
+        ("B300_Dz2048", 300, 2048), ("B2048_Dz20480", 2048, 20480)]
+
+
+@pytest.mark.parametrize("name,B,Dz", HRAD, ids=[h[0] for h in HRAD])
+def test_hrad_matches_oracle(name, B, Dz):
+    """Layer 1 on the tensor cores (fp32 accumulation of exact bf16 products), layers 2-3
+    in fp32, vs the fp64 oracle.  Tolerance: a fp32 sum of Dz O(1)-bounded partials is
+    off by ~sqrt(Dz/16) * 2^-24 relative; 1e-4 absolute on O(1) logits leaves > 10x
+    margin.  s_t is exact except where the oracle's top-2 gap is below 1e-3 (flagged)."""
+    import oracle
+    from paper_2506_01979_b200 import api, synth
+
+    G = 8
+    inp = synth.hrad_inputs(B, Dz, G=G, seed=B + Dz, device="cuda")
+    s_t, lg, gm, bp = api.sb_hrad_predict(inp["z"], inp["w1"], inp["b1"], inp["w2"], inp["b2"], inp["w3"],
+                                          inp["b3"], G, stop=inp["stop"])
+    torch.cuda.synchronize()
+    n = synth.hrad_to_numpy(inp)
+    o = oracle.hrad(n["z"], n["w1"], n["b1"], n["w2"], n["b2"], n["w3"], n["b3"], n["stop"], G)
+    lg = lg.cpu().numpy()
+    assert np.allclose(lg, o["logits"], rtol=1e-4, atol=1e-4), np.abs(lg - o["logits"]).max()
+    tie = o["margin"] < 1e-3
+    assert tie.mean() < 0.05
+    assert np.array_equal(s_t.cpu().numpy()[~tie], o["s_t"][~tie])
+    assert np.array_equal(gm.cpu().numpy()[~tie], o["gamma"][~tie])
+    assert np.array_equal(bp.cpu().numpy()[~tie], o["branch_pos"][~tie])
+    # run-to-run deterministic (fixed-order cluster reduction, no atomics)
+    s2, lg2, _, _ = api.sb_hrad_predict(inp["z"], inp["w1"], inp["b1"], inp["w2"], inp["b2"], inp["w3"],
+                                        inp["b3"], G, stop=inp["stop"])
+    assert np.array_equal(lg2.cpu().numpy(), lg) and torch.equal(s2, s_t)
+
+
+def test_hrad_rejects_unsupported_shapes():
+    from paper_2506_01979_b200 import api, synth
+
+    inp = synth.hrad_inputs(4, 200, G=4, seed=1, device="cuda")  # Dz not a multiple of 64
+    with pytest.raises(RuntimeError):
+        api.sb_hrad_predict(inp["z"], inp["w1"], inp["b1"], inp["w2"], inp["b2"], inp["w3"], inp["b3"], 4)
