@@ -50,7 +50,7 @@ constexpr uint32_t kAccBytes = kHM * kAccStride * 4;
 constexpr size_t kHradSmem = kRingBytes + 1024;  // + alignment slack (SWIZZLE_128B: 1 KB)
 static_assert(kAccBytes <= kRingBytes, "the staged partial reuses the ring");
 constexpr int kTailRowsMax = 16;  // rows per k_hrad_tail CTA (<=)
-constexpr int kTailThreads = 256;
+constexpr int kTailThreads = 512;  // two split-sums and two layer-2 outputs per thread at 16 rows
 constexpr int kMaxCM = 4;         // CTAs per cluster sharing a W1 tile (multicast)
 
 // Instruction descriptor of tcgen05.mma.kind::f16: fp32 accumulator (bits 4-5 = 1),
@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(kHThreads, 1)
 // griddepcontrol.wait, so it overlaps k_hrad's tail.
 constexpr int kW2Stride = kHN + 1;
 constexpr size_t kTailSmem = (size_t)(kH2 * kW2Stride + kTailRowsMax * kHN + kTailRowsMax * kH2) * 4;
-__global__ void __launch_bounds__(kTailThreads) k_hrad_tail(HradParams p) {
+__global__ void __launch_bounds__(kTailThreads, 1) k_hrad_tail(HradParams p) {
   extern __shared__ float tsm[];
   float* w2s = tsm;                        // [64][257]
   float* h1s = w2s + kH2 * kW2Stride;      // [R][256]

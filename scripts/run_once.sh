@@ -4,6 +4,5 @@ T=${TAG:-x}
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/${T}_build.log 2>&1
 timeout 300 python -m pytest tests/test_gpu_next.py -q -x -k hrad 2>&1 | tail -30 > gpurun_out/${T}_tests.log
-SB_HRAD_CM=2 timeout 300 python -m pytest tests/test_gpu_next.py -q -x -k hrad 2>&1 | tail -30 > gpurun_out/${T}_tests_cm4.log
-for cm in 1 2; do for b in 2048 256; do SB_HRAD_CM=$cm timeout 300 python bench.py --config hrad --hrad-batch $b --steps 30 --no-cpu-baseline > gpurun_out/${T}_hrad_${b}_cm$cm.log 2>&1; done; done
+for b in 2048 256 8192; do timeout 300 python bench.py --config hrad --hrad-batch $b --steps 30 --no-cpu-baseline > gpurun_out/${T}_hrad_${b}.log 2>&1; done
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_hrad" -s 6 -c 2 -o gpurun_out/${T}_hrad python bench.py --config hrad --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/${T}_ncu_hrad.log 2>&1
