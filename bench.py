@@ -403,7 +403,7 @@ def run_hrad(args, rank, world, local_rank):
                      "frac": round(gbs / peak, 4), "traffic": None, "algorithmic_bytes_per_launch": nbytes},
         "tensor": {"achieved_tflops": round(tfs, 1), "peak": tpk, "peak_source": tpk_src,
                    "frac": round(tfs / tpk, 4), "flops_per_launch": flops},
-        "gpu_launches": args.steps, "clocks": clk.summary(),
+        "gpu_launches": 2 * args.steps, "clocks": clk.summary(),
         **({"cpu_baseline": cpu} if cpu else {}),
     }
 
