@@ -175,6 +175,50 @@ __device__ __forceinline__ int sample_segments(const T* prow, const T* qrow, uin
 
 // Offsets (exclusive scan of commit_len) and the packed commit stream, by one warp
 // (the epilogue that completes the last sequence).
+// Block-wide version (NT threads): exclusive scan of commit_len into offsets[0..B] and
+// the packed token stream; each thread owns a contiguous run of sequences, all its
+// loads are independent (one round trip per phase instead of one per sequence).
+template <int NT>
+__device__ __forceinline__ void block_offsets(int B, int G, const int* commit_len, const int* out_tok, int* offsets,
+                                              int* packed_tok, int* scan /* smem, >= NT/32 ints */) {
+  constexpr int NW = (NT + 31) / 32;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int per = (B + NT - 1) / NT;
+  const int b0 = min(B, tid * per), b1 = min(B, b0 + per);
+  int loc = 0;
+  for (int qq = b0; qq < b1; ++qq) loc += __ldcg(commit_len + qq);
+  int incl = loc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int yv = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += yv;
+  }
+  if (lane == 31) scan[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    int x = lane < NW ? scan[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int yv = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += yv;
+    }
+    if (lane < NW) scan[lane] = x;  // inclusive over warps
+  }
+  __syncthreads();
+  int run = incl - loc + (w > 0 ? scan[w - 1] : 0);
+  for (int qq = b0; qq < b1; ++qq) {
+    offsets[qq] = run;
+    const int cl = __ldcg(commit_len + qq);
+    if (packed_tok) {
+      const int* src = out_tok + (int64_t)qq * (G + 2);
+#pragma unroll 4
+      for (int c = 0; c < cl; ++c) packed_tok[run + c] = __ldcg(src + c);
+    }
+    run += cl;
+  }
+  if (tid == NT - 1) offsets[B] = scan[NW - 1];
+}
+
 __device__ __forceinline__ void warp_offsets(int B, int G, const int* commit_len, const int* out_tok, int* offsets,
                                              int* packed_tok) {
   const int lane = threadIdx.x & 31;

@@ -220,6 +220,7 @@ struct SelSmem {
   RowStat red[sCW];
   float seg[sNQ][sSegMax];
   int s_last;
+  int scan[32];
   alignas(128) uint8_t buf[sNS][2][sChunk];
 };
 
@@ -277,6 +278,7 @@ __global__ void __launch_bounds__(sThreads, 1) k_select_tma(SelParams p) {
       mbar_init(&S.dempty[s], 1);
       mbar_init(&S.sfull[s], sCW);
     }
+    S.s_last = 0;
     fence_mbar_init();
   }
   __syncthreads();
@@ -360,9 +362,7 @@ __global__ void __launch_bounds__(sThreads, 1) k_select_tma(SelParams p) {
       }
       dq.advance();
     }
-    return;
-  }
-  if (warp == sCW) {  // ---------------- producer
+  } else if (warp == sCW) {  // ---------------- producer
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
       RingPos<sNQ> dq;
@@ -388,9 +388,7 @@ __global__ void __launch_bounds__(sThreads, 1) k_select_tma(SelParams p) {
           }
       }
     }
-    return;
-  }
-  if (warp == sCW + 1) {  // ---------------- epilogue
+  } else if (warp == sCW + 1) {  // ---------------- epilogue
     RingPos<sNQ> dq;
     for (;;) {
       mbar_wait(&S.dfull[dq.stage], dq.phase);
@@ -535,33 +533,9 @@ __global__ void __launch_bounds__(sThreads, 1) k_select_tma(SelParams p) {
         last = (atomicAdd(p.sel_cnt, 1) == d.B - 1);
       }
       last = __shfl_sync(0xffffffffu, last, 0);
-      if (last) {
-        __threadfence();
-        const int per = (d.B + 31) / 32;
-        const int b0 = min(d.B, lane * per), b1 = min(d.B, b0 + per);
-        int loc = 0;
-        for (int qq = b0; qq < b1; ++qq) loc += __ldcg(p.commit_len + qq);
-        int incl = loc;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int yv = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += yv;
-        }
-        int run = incl - loc;
-        for (int qq = b0; qq < b1; ++qq) {
-          p.offsets[qq] = run;
-          const int cl = __ldcg(p.commit_len + qq);
-          if (p.packed_tok)
-            for (int c = 0; c < cl; ++c) p.packed_tok[run + c] = __ldcg(p.out_tok + (int64_t)qq * (d.G + 2) + c);
-          run += cl;
-        }
-        if (lane == 31) p.offsets[d.B] = incl;
-        if (lane == 0) p.sel_cnt[0] = 0;  // leave the workspace re-usable
-      }
+      if (last && lane == 0) S.s_last = 1;  // the whole CTA compacts once every role is done
     }
-    return;
-  }
-  // ---------------- consumers
+  } else {  // ---------------- consumers
   RingPos<sNQ> dq;
   RingPos<sNS> rp;
   for (;;) {
@@ -621,6 +595,14 @@ __global__ void __launch_bounds__(sThreads, 1) k_select_tma(SelParams p) {
     __syncwarp();
     if (lane == 0) mbar_arrive(&S.sfull[q]);
     dq.advance();
+  }
+  }
+  // ---------------- the CTA that finished the last sequence: offsets + packed stream
+  __syncthreads();
+  if (S.s_last) {
+    __threadfence();
+    block_offsets<sThreads>(d.B, d.G, p.commit_len, p.out_tok, p.offsets, p.packed_tok, S.scan);
+    if (tid == 0) p.sel_cnt[0] = 0;  // leave the workspace re-usable
   }
 }
 
