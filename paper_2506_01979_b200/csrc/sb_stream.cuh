@@ -6,12 +6,12 @@
 
 namespace sb {
 
-template <int CW_, int NS_, int VPT_, int NP_>
+template <int CW_, int NS_, int VPT_, int NP_, int NE_ = 2>
 struct RC {
   static constexpr int CW = CW_, NS = NS_, VPT = VPT_, NP = NP_;
   static constexpr int CT = CW * 32;
   static constexpr int CHUNK = CT * VPT * 16;
-  static constexpr int NE = 2;  // epilogue warps (k_rows_tma), alternating units
+  static constexpr int NE = NE_;  // epilogue warps (k_rows_tma), alternating units
   static constexpr int THREADS = CT + 64;
   static constexpr int ROWS_THREADS = CT + 32 * (1 + NE);
   static_assert(NP % NE == 0, "each epilogue warp owns NP / NE partial slots");

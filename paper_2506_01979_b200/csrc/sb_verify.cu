@@ -1198,10 +1198,10 @@ static sb_status launch_step_tma(const StepParams& sp, cudaStream_t s) {
 }
 
 // Geometry variants (SB_ROWS_VARIANT selects one for experiments; 0 = default).
-using RC0 = RC<16, 7, 2, 2>;   // 16 consumer warps, 7 x 32 KB stages, 2 partial slots
-using RC1 = RC<16, 6, 2, 4>;   // 16 warps, 6 x 32 KB stages, 4 partial slots
-using RC2 = RC<16, 12, 1, 4>;  // 16 warps, 12 x 16 KB stages (finer row tail)
-using RC3 = RC<16, 13, 1, 2>;  // 16 warps, 13 x 16 KB stages
+using RC0 = RC<16, 6, 2, 4, 4>;  // 16 consumer warps, 6 x 32 KB stages, 4 epilogue warps
+using RC1 = RC<16, 6, 2, 4>;   // 16 warps, 6 x 32 KB stages, 4 partial slots, 2 epilogue warps
+using RC2 = RC<16, 7, 2, 2>;   // 16 warps, 7 x 32 KB stages, 2 partial slots
+using RC3 = RC<16, 12, 1, 4, 4>; // 16 warps, 12 x 16 KB stages, 4 epilogue warps
 using RC4 = RC<20, 5, 2, 4>;   // 20 warps, 5 x 40 KB stages
 
 template <typename T>
