@@ -408,6 +408,94 @@ def run_hrad(args, rank, world, local_rank):
     }
 
 
+def run_next(args, rank, world, local_rank):
+    """--config spawn | kv | tree: the SURVEY §8.6 NEXT rows f1-f3, each timed alone
+    (CUDA graph of the C-ABI call, CUDA events per replay) against the HBM roofline."""
+    import torch
+
+    from paper_2506_01979_b200 import api, synth
+    from paper_2506_01979_b200.build import build
+
+    build()
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    t0 = time.time()
+    if args.config == "spawn":  # f1: Eq. 7 TopK spawn on the branch row, C4 shape
+        c = synth.config("c4")
+        B, V, k_max = c.B, c.V, 6
+        QL = synth.draft_rows(c, B, seed=1, device=dev).view(B, 1, 1, V)  # the branch rows (s_b = 0)
+        d = api.dims_for(QL, V=V)
+        bpos = torch.zeros(B, dtype=torch.int32, device=dev)
+        k = torch.empty(B, dtype=torch.int32, device=dev)
+        bt = torch.empty((B, k_max), dtype=torch.int32, device=dev)
+        bp = torch.empty((B, k_max), dtype=torch.float32, device=dev)
+        cf = torch.empty(B, dtype=torch.float32, device=dev)
+        fn = lambda s_: api.sb_spawn_branches(d, QL, bpos, None, api.SB_CONF_TOP1, k_max, k, bt, bp, cf, s_)  # noqa
+        nbytes, units, unit = B * V * 2, B, "branch spawns/s"
+        work = f"f1 Eq. 7 branch spawn (k_max = {k_max}), batch {B}, V = {V} bf16 (C4 shape)"
+        kern = "k_spawn"
+    elif args.config == "kv":  # f2: KV rollback of a C4-shaped round, 8 KB of draft KV per position
+        c = synth.config("c4")
+        B, K, G, row = c.B, c.K, c.G, 8192
+        g = torch.Generator(device="cpu").manual_seed(11)
+        kv = torch.empty((B, K, G + 1, row // 2), dtype=torch.bfloat16, device=dev)
+        kv.view(torch.int16).random_(-30000, 30000)
+        out = torch.empty((B, G + 1, row // 2), dtype=torch.bfloat16, device=dev)
+        sel = torch.randint(-1, K, (B,), generator=g, dtype=torch.int32).to(dev)
+        cl = torch.randint(1, G + 2, (B,), generator=g, dtype=torch.int32).to(dev)
+        yk = torch.ones(B, dtype=torch.int32, device=dev)
+        bpos = torch.zeros(B, dtype=torch.int32, device=dev)
+        fn = lambda s_: api.sb_kv_rollback(kv, bpos, sel, cl, yk, out_kv=out, stream=s_)  # noqa: E731
+        moved = int((cl - 1).clamp(min=0).sum())
+        nbytes, units, unit = 2 * moved * row, moved, "KV positions kept/s"
+        work = f"f2 KV rollback, batch {B}, K = {K}, gamma = {G}, {row} B per position (out of place)"
+        kern = "k_kv_rollback"
+    else:  # f3: dense SpecInfer-style trees (branching 2,2,2,2: 30 nodes), Vicuna vocab
+        c = synth.config("c2")
+        B = 256
+        inp = synth.generate_tree(c, "dense", B=B, seed=13, branching=(2, 2, 2, 2), device=dev)
+        d = api.tree_dims(inp["PL"])
+        buf = api.TreeBuffers(d, dev)
+        fn = lambda s_: api.sb_tree_verify(d, inp["PL"], inp["QL"], inp["parent"], inp["tok"], inp["u"],  # noqa
+                                           inp["us"], buf, s_)
+        par = inp["parent"][0].tolist()
+        inner = len(set(par))  # contexts with children: their p and q rows are read
+        nbytes, units, unit = B * inner * 2 * c.V * 2, B * inp["N"], "tree nodes verified/s"
+        work = f"f3 token-tree verify, {B} dense trees of {inp['N']} nodes (2,2,2,2), V = {c.V} bf16"
+        kern = "k_tree_* (context-row stats + walk + sample)"
+    gen_s = time.time() - t0
+    g = api.CallGraph(fn)
+    for _ in range(max(args.warmup, 3)):
+        g.replay()
+    torch.cuda.synchronize()
+    clk = Clocks(local_rank if not args.no_clocks else -1).__enter__()
+    time.sleep(0.3)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    cur = torch.cuda.current_stream()
+    for e0, e1 in evs:
+        e0.record(cur)
+        g.replay()
+        e1.record(cur)
+    torch.cuda.synchronize()
+    clk.__exit__()
+    ms = sum(e0.elapsed_time(e1) for e0, e1 in evs) / args.steps
+    if rank != 0:
+        return None
+    peak, peak_src = peaks()
+    gbs = nbytes / (ms * 1e-3) / 1e9
+    return {
+        "metric": f"SURVEY §8.6 {args.config}: {unit}", "value": round(units / (ms * 1e-3), 1), "unit": unit,
+        "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": round(ms, 5),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (seeded, DESIGN.md §Input recipe)",
+        "config": {"workload": work, "l2": "inputs %.0f MB per call vs 126 MB L2" % (nbytes / 1e6)},
+        "roofline": {"bound": "hbm", "kernel": kern, "achieved": round(gbs, 1), "peak": peak,
+                     "peak_source": peak_src, "unit": "GB/s", "frac": round(gbs / peak, 4), "traffic": None,
+                     "algorithmic_bytes_per_launch": nbytes},
+        "gpu_launches": args.steps, "clocks": clk.summary(), "generation_s": round(gen_s, 1),
+    }
+
+
 def traffic_from_profiles(name):
     p = os.path.join(ROOT, "profiles", f"traffic_{name}.json")
     try:
@@ -552,7 +640,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4", "c5", "hrad"])
+    ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4", "c5", "hrad", "spawn", "kv", "tree"])
     ap.add_argument("--hrad-batch", type=int, default=2048)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
@@ -582,7 +670,8 @@ def main():
 
         torch.cuda.set_device(local_rank)
         torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    line = (run_hrad if args.config == "hrad" else run_ours)(args, rank, world, local_rank)
+    runner = {"hrad": run_hrad, "spawn": run_next, "kv": run_next, "tree": run_next}.get(args.config, run_ours)
+    line = runner(args, rank, world, local_rank)
     if line is not None:
         print(json.dumps(line), flush=True)
     if world > 1:

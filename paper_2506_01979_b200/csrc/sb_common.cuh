@@ -218,6 +218,11 @@ struct LazyAcc {
 #pragma unroll
     for (int j = 1; j + 1 < N; j += 2) cm = fmax3(cm, f[j], f[j + 1]);
     if (N % 2 == 0) cm = fmaxf(cm, f[N - 1]);
+    add_cm<N>(f, cm, t);
+  }
+  // the same with the group maximum cm = max(f[0..N)) already known
+  template <int N>
+  __device__ __forceinline__ void add_cm(const float* f, float cm, int t) {
     if (kQ) tag = (cm > m) ? t : tag;
     m = fmaxf(m, cm);
     const bool up = cm * kC - ms > (kQ ? kRescaleQ : kRescaleP);
@@ -239,7 +244,7 @@ struct LazyAcc {
   // exponent: identical results for every logit > -2^97, since ex2.approx.ftz is 0
   // below 2^-126 either way.
   template <int NW>
-  __device__ __forceinline__ void add_bf16(const uint32_t* win, int t) {
+  __device__ __forceinline__ float add_bf16(const uint32_t* win, int t) {
     static_assert(NA == 4 && NW % 2 == 0, "pairs map to (z0,z1), (z2,z3)");
     constexpr int N = 2 * NW;
     float f[N];
@@ -285,6 +290,7 @@ struct LazyAcc {
     if (kQ) {
       s1[0] = sa.x; s1[1] = sa.y; s1[2] = sb.x; s1[3] = sb.y;
     }
+    return cm;  // this group's maximum (of the clamped values for q rows)
   }
 };
 
@@ -297,13 +303,13 @@ __device__ __forceinline__ uint4 neg_inf_vec() {
 
 // Accumulate NV 16-byte bf16 vectors of one row chunk (tag t) into a LazyAcc.
 template <int NV, bool kQ>
-__device__ __forceinline__ void acc_vecs_bf16(LazyAcc<kQ, 4>& a, const uint4* x, int t) {
+__device__ __forceinline__ float acc_vecs_bf16(LazyAcc<kQ, 4>& a, const uint4* x, int t) {
   uint32_t w[4 * NV];
 #pragma unroll
   for (int j = 0; j < NV; ++j) {
     w[4 * j] = x[j].x; w[4 * j + 1] = x[j].y; w[4 * j + 2] = x[j].z; w[4 * j + 3] = x[j].w;
   }
-  a.template add_bf16<4 * NV>(w, t);
+  return a.template add_bf16<4 * NV>(w, t);
 }
 
 // Reduced row state (one per thread after folding accumulators, then across threads).

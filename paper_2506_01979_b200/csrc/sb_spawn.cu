@@ -4,10 +4,12 @@
 // floor(k_max (1 - c))) and B = TopK(q(x_b), k_b) (ties -> smaller id, S393).
 //
 // One CTA per sequence streams the draft row once (16-byte loads, U vectors in flight
-// per thread): online max / sum (exact-offset state) for the probabilities, plus a
-// per-thread sorted top-KL list by raw logit (the order of q), insertion only when a
-// vector's max beats the list's tail.  Lists merge by KL rounds of warp argmax, then
-// once more across warps.  Logit order == q order, so the token set is exact.
+// per thread): lazy-offset online sum and exact max for the probabilities, plus one
+// warp-wide sorted top-KL list by raw logit (the order of q) per warp; a vector enters
+// the insertion path only if its max reaches max(block seed, warp list tail) — the
+// seed, the KL-th largest of the threads' first-vector maxima, is a lower bound of the
+// row's KL-th value, so almost every vector is filtered by one compare + one ballot.  The warps' lists merge by KL rounds of
+// warp argmax.  Logit order == q order, so the token set is exact (ties: smaller id).
 #include <algorithm>
 
 #include "sb_host.h"
@@ -84,12 +86,42 @@ __device__ __forceinline__ void warp_merge(TopList<KL>& L, float* outv, int* out
   }
 }
 
-template <typename T, int KL, int U>
-__global__ void __launch_bounds__(kSpawnNT) k_spawn(SpawnParams p, bool vec_ok) {
-  constexpr int E = Vec<T>::E, NT = kSpawnNT, NW = NT / 32;
+// Warp-wide sorted top-KL list (value desc, id asc): lane t < KL holds entry t.  An
+// element enters only if it beats the tail, so after the first vectors almost every
+// 16-byte vector is filtered by one compare + one ballot per warp.
+template <int KL>
+struct WarpTop {
+  float v;
+  int id;
+  __device__ __forceinline__ void init() { v = -CUDART_INF_F; id = 0x7fffffff; }
+  __device__ __forceinline__ void tail(float& tv, int& ti) const {
+    tv = __shfl_sync(0xffffffffu, v, KL - 1);
+    ti = __shfl_sync(0xffffffffu, id, KL - 1);
+  }
+  // warp-uniform (f, x): insert if it ranks inside the list
+  __device__ __forceinline__ void insert(float f, int x) {
+    const int lane = threadIdx.x & 31;
+    const bool above = lane < KL && (v > f || (v == f && id < x));
+    const int pos = __popc(__ballot_sync(0xffffffffu, above));
+    if (pos >= KL) return;
+    const float pv = __shfl_up_sync(0xffffffffu, v, 1);
+    const int pi = __shfl_up_sync(0xffffffffu, id, 1);
+    if (lane > pos && lane < KL) { v = pv; id = pi; }
+    if (lane == pos) { v = f; id = x; }
+  }
+  // insert, then return the tail value (warp-uniform)
+  __device__ __forceinline__ float insert_tail(float f, int x) {
+    insert(f, x);
+    return __shfl_sync(0xffffffffu, v, KL - 1);
+  }
+};
+
+template <typename T, int KL, int U, int NT>
+__global__ void __launch_bounds__(NT) k_spawn(SpawnParams p, bool vec_ok) {
+  constexpr int E = Vec<T>::E, NW = NT / 32;
   __shared__ RowStat red[NW];
-  __shared__ float wv[NW][KL];
-  __shared__ int wi[NW][KL];
+  __shared__ float wv[NW * KL];
+  __shared__ int wi[NW * KL];
   __shared__ float fv[KL];
   __shared__ int fi[KL];
   const Dims& d = p.d;
@@ -97,51 +129,135 @@ __global__ void __launch_bounds__(kSpawnNT) k_spawn(SpawnParams p, bool vec_ok) 
   int s = p.bpos ? __ldg(p.bpos + b) : 0;
   s = max(0, min(s, d.G));
   const T* row = static_cast<const T*>(p.QL) + row_off(d, b, 0, s);
-  RowAcc<false, 4> acc;
+  LazyAcc<false, 4> acc;  // lazy-offset sum, exact running max
   acc.init();
-  TopList<KL> L;
-  L.init();
+  WarpTop<KL> W;
+  W.init();
+  // filter threshold: max(list tail, lower bound); the lower bound is the KL-th largest
+  // of the 32 lane maxima of the first vector group (KL distinct elements of this warp,
+  // so <= the warp's true KL-th largest) -> no warm-up flood of candidates
+  // block-wide seed: the KL-th largest of the NT threads' first-vector maxima (KL
+  // distinct elements of the row, so <= the row's KL-th largest value)
+  float filt;
+  {
+    float vm0 = -CUDART_INF_F;
+    if (vec_ok && tid < d.V / E) {
+      float f[E];
+      Vec<T>::unpack(ldg_stream(reinterpret_cast<const uint4*>(row) + tid), f);
+      vm0 = Vec<T>::vmax(f);
+    } else if (!vec_ok && tid < d.V) {
+      vm0 = ld_scalar(row + tid);
+    }
+    float cur = vm0;
+    for (int r = 0; r < KL; ++r) {
+      float mx = cur;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      const unsigned who = __ballot_sync(0xffffffffu, cur == mx);
+      if (lane == __ffs(who) - 1) cur = -CUDART_INF_F;
+      if (lane == 0) wv[warp * KL + r] = mx;
+    }
+    __syncthreads();
+    TopList<(NW * KL + 31) / 32> M;
+    M.init();
+#pragma unroll
+    for (int t = 0; t < (NW * KL + 31) / 32; ++t) {
+      const int c = lane + 32 * t;
+      if (c < NW * KL) M.insert(wv[c], c);
+    }
+    float kth = -CUDART_INF_F;
+    for (int r = 0; r < KL; ++r) {
+      float cv = M.v[0];
+      int ci = M.id[0];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, cv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, ci, o);
+        if (ov > cv || (ov == cv && oi < ci)) { cv = ov; ci = oi; }
+      }
+      if (M.id[0] == ci && M.v[0] == cv) M.pop();
+      kth = cv;
+    }
+    filt = kth;
+    __syncthreads();  // wv is reused by the final merge
+  }
   int done = 0;
   if (vec_ok) {
     const int nvec = d.V / E;
     const uint4* rv = reinterpret_cast<const uint4*>(row);
-    for (int vb = tid; vb < nvec; vb += U * NT) {
+    const int nv_round = (nvec + 32 * U * NW - 1) / (32 * U * NW) * (32 * U * NW);
+    for (int vb = tid; vb < nv_round; vb += U * NT) {  // warp-uniform trip count
       uint4 x[U];
 #pragma unroll
       for (int j = 0; j < U; ++j)
-        if (vb + j * NT < nvec) x[j] = ldg_stream(rv + vb + j * NT);
+        x[j] = (vb + j * NT < nvec) ? ldg_stream(rv + vb + j * NT) : neg_inf_vec<T>();
 #pragma unroll
       for (int j = 0; j < U; ++j) {
-        if (vb + j * NT >= nvec) break;
         float f[E];
         Vec<T>::unpack(x[j], f);
+        const bool valid = vb + j * NT < nvec;
         const float vm = Vec<T>::vmax(f);
-        const int base = (vb + j * NT) * E;
-        acc.template add<E>(f, vm, base);
-        if (vm > L.v[KL - 1] || vm == L.v[KL - 1]) {  // rare after the first vectors
+        acc.template add_cm<E>(f, vm, vb + j * NT);
+        unsigned cand = __ballot_sync(0xffffffffu, valid && vm >= filt);
+        while (cand) {  // rare once warm: one lane's values, broadcast, qualifying ones inserted
+          const int src = __ffs(cand) - 1;
+          cand &= cand - 1;
+          const int bb = (vb - lane + src + j * NT) * E;
 #pragma unroll
-          for (int e = 0; e < E; ++e) L.insert(f[e], base + e);
+          for (int e = 0; e < E; ++e) {
+            const float xv = __shfl_sync(0xffffffffu, f[e], src);
+            if (xv >= filt) filt = fmaxf(filt, W.insert_tail(xv, bb + e));
+          }
         }
       }
     }
     done = nvec * E;
   }
-  for (int v = done + tid; v < d.V; v += NT) {
-    const float f = ld_scalar(row + v);
-    acc.add1(f, v);
-    L.insert(f, v);
-  }
-  const RowStat st = block_reduce<NT>(fold(acc), red);
-  warp_merge<KL>(L, wv[warp], wi[warp]);
-  __syncthreads();
-  if (warp == 0) {
-    TopList<KL> M;
+  for (int v0 = done; v0 < d.V; v0 += NT) {  // scalar tail / unaligned rows: one value per thread
+    const int v = v0 + tid;
+    float f[E];
+    f[0] = v < d.V ? ld_scalar(row + v) : -CUDART_INF_F;
 #pragma unroll
-    for (int t = 0; t < KL; ++t) {
-      M.v[t] = lane < NW ? wv[lane][t] : -CUDART_INF_F;
-      M.id[t] = lane < NW ? wi[lane][t] : 0x7fffffff;
+    for (int e = 1; e < E; ++e) f[e] = -CUDART_INF_F;
+    acc.template add<E>(f, 0);
+    unsigned cand = __ballot_sync(0xffffffffu, v < d.V && f[0] >= filt);
+    while (cand) {
+      const int src = __ffs(cand) - 1;
+      cand &= cand - 1;
+      const float xv = __shfl_sync(0xffffffffu, f[0], src);
+      if (xv >= filt) filt = fmaxf(filt, W.insert_tail(xv, v0 + warp * 32 + src));
     }
-    warp_merge<KL>(M, fv, fi);
+  }
+  RowStat st = fold_lazy(acc);
+  st.idx = 0x7fffffff;
+  st = block_reduce<NT>(st, red);
+  if (lane < KL) { wv[warp * KL + lane] = W.v; wi[warp * KL + lane] = W.id; }
+  __syncthreads();
+  if (warp == 0) {  // merge the warps' lists: KL rounds of argmax over NW*KL candidates
+    TopList<(NW * KL + 31) / 32> M;
+    M.init();
+#pragma unroll
+    for (int t = 0; t < (NW * KL + 31) / 32; ++t) {
+      const int c = lane + 32 * t;
+      if (c < NW * KL) M.insert(wv[c], wi[c]);
+    }
+    float bv[KL];
+    int bi[KL];
+    for (int r = 0; r < KL; ++r) {
+      float cv = M.v[0];
+      int ci = M.id[0];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, cv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, ci, o);
+        if (ov > cv || (ov == cv && oi < ci)) { cv = ov; ci = oi; }
+      }
+      if (M.id[0] == ci && M.v[0] == cv && ci != 0x7fffffff) M.pop();
+      bv[r] = cv;
+      bi[r] = ci;
+    }
+    if (lane == 0)
+      for (int r = 0; r < KL; ++r) { fv[r] = bv[r]; fi[r] = bi[r]; }
   }
   __syncthreads();
   if (tid == 0) {
@@ -173,7 +289,7 @@ __global__ void __launch_bounds__(kSpawnNT) k_spawn(SpawnParams p, bool vec_ok) 
 
 template <typename T, int KL>
 static sb_status launch_spawn(const SpawnParams& p, bool vok, cudaStream_t s) {
-  k_spawn<T, KL, 4><<<p.d.B, kSpawnNT, 0, s>>>(p, vok);
+  k_spawn<T, KL, 4, kSpawnNT><<<p.d.B, kSpawnNT, 0, s>>>(p, vok);
   return cuda_status(cudaGetLastError());
 }
 

@@ -103,6 +103,18 @@ def _rows(cfg: Config, g: torch.Generator, shape: tuple, device):
     return lp, lq
 
 
+def draft_rows(cfg: Config, B: int, seed: int = 0, device="cpu", chunk: int = 128):
+    """B draft rows of the recipe (the branch rows Eq. 7 spawns from), [B][V] in the
+    config's dtype; row b from its own counter-keyed generator."""
+    ldt = torch.bfloat16 if cfg.dtype == "bf16" else torch.float32
+    out = torch.empty((B, cfg.V), dtype=ldt, device=device)
+    for b0 in range(0, B, chunk):
+        n = min(chunk, B - b0)
+        _, lq = _rows(cfg, _gen(SEED_BASE + 31 * seed, b0, device), (n,), device)
+        out[b0:b0 + n] = lq.to(ldt)
+    return out
+
+
 def _one_sequence(cfg: Config, seed: int, b: int, device, gamma_b: int, s_b: int):
     K, G, V = cfg.K, cfg.G, cfg.V
     R1 = G + 1
