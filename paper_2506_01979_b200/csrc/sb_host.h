@@ -38,7 +38,6 @@ struct Workspace {
   int4* dec;         // [B] sharded select: decision record
   int* ready;        // [B] fused step: per-sequence phase-1 completion flags
   int* plan;         // [4] fused step: delta, total units
-  int4* units;       // [B*K*(G+1)] row-pair unit table written by k_plan (see unit_entry)
   size_t bytes;
 };
 
@@ -70,7 +69,6 @@ inline Workspace carve(const sb_dims& d, void* base) {
   }
   w.ready = (int*)take(sizeof(int) * B);
   w.plan = (int*)take(sizeof(int) * 4);
-  w.units = (int4*)take(sizeof(int4) * B * K * R1);
   w.bytes = off;
   return w;
 }

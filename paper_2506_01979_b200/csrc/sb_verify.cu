@@ -31,7 +31,6 @@ struct RowsParams {
   const float* u;
   const SeqInfo* info;
   const int* unit_off;
-  const int4* units;  // unit table (k_plan); NULL -> decode_unit's search
   int* cnt;
   float4* rowstat;
   uint8_t* pflag;
@@ -48,8 +47,7 @@ struct RowsParams {
 };
 
 // ---------------------------------------------------------------- plan
-// Unit table entry: sequence, row geometry and the sequence's layout in one 16-byte
-// load, so the streaming kernels' producer and epilogue warps never search unit_off.
+// A unit's sequence, row geometry and the sequence's layout packed in 16 bytes.
 __host__ __device__ inline int4 unit_entry(int b, int slot, int i, const SeqInfo& in) {
   return make_int4(b, slot | (i << 8) | (in.s << 16) | (in.g << 24), in.L | (in.Lr << 8) | (in.st << 16), 0);
 }
@@ -57,7 +55,7 @@ __host__ __device__ inline int4 unit_entry(int b, int slot, int i, const SeqInfo
 __global__ void __launch_bounds__(1024) k_plan(Dims d, const int* __restrict__ gamma,
                                                const int* __restrict__ bpos, SeqInfo* info,
                                                int* unit_off, int with_bonus, int fused_grid, int* plan,
-                                               int* ready, int4* units = nullptr) {
+                                               int* ready) {
   __shared__ int wsum[32];
   const int tid = threadIdx.x, NT = blockDim.x;
   const int per = (d.B + NT - 1) / NT;
@@ -115,44 +113,13 @@ __global__ void __launch_bounds__(1024) k_plan(Dims d, const int* __restrict__ g
     }
     return;
   }
-  extern __shared__ int s_off[];  // [B+1] when the unit table is built
   for (int b = b0; b < b1; ++b) {
     unit_off[b] = run;
-    if (units) s_off[b] = run;
     const SeqInfo in = info[b];
     run += in.Lr + (d.K - 1) * (in.Lr - 1 - in.s);
   }
-  if (tid == NT - 1) {
-    unit_off[d.B] = run;
-    if (units) s_off[d.B] = run;
-  }
-  if (!units) return;
-  // unit table, coalesced: unit -> sequence by a search over the offsets in smem, then
-  // slot 0 rows 0..Lr-1 followed by rows s+1..Lr-1 of slots 1..K-1
-  __syncthreads();
-  const int total = s_off[d.B];
-  for (int unit = tid; unit < total; unit += NT) {
-    int lo = 0, hi = d.B;
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (s_off[mid] <= unit) lo = mid; else hi = mid;
-    }
-    const SeqInfo in = info[lo];
-    const int j = unit - s_off[lo];
-    int slot = 0, i = j;
-    if (j >= in.Lr) {
-      const int per = in.Lr - 1 - in.s, jj = j - in.Lr;
-      slot = 1 + jj / per;
-      i = in.s + 1 + jj % per;
-    }
-    units[unit] = unit_entry(lo, slot, i, in);
-  }
+  if (tid == NT - 1) unit_off[d.B] = run;
 }
-
-// k_plan's unit table needs B+1 offsets in shared memory; above this the streaming
-// kernels fall back to searching unit_off.
-constexpr int kPlanTableMaxB = 16383;
-inline size_t plan_smem(int B, bool table) { return table ? sizeof(int) * ((size_t)B + 1) : 0; }
 
 // ---------------------------------------------------------------- shared unit logic
 struct Unit {
@@ -197,11 +164,10 @@ __device__ __forceinline__ Unit unit_from(int4 e) {
   return u;
 }
 
-// The table entry of `unit` (issued one unit ahead by the streaming kernels), or a
-// zero entry past the end.
+// The packed geometry of `unit` (decoded one unit ahead by the streaming kernels, so
+// the search's dependent loads overlap the current unit's stream), or zeros past the end.
 __device__ __forceinline__ int4 unit_prefetch(const RowsParams& p, int unit, int total) {
   if (unit >= total) return make_int4(0, 0, 0, 0);
-  if (p.units) return __ldg(p.units + unit);
   const Unit u = decode_unit(p, unit);
   return unit_entry(u.b, u.slot, u.i, u.in);
 }
@@ -1239,15 +1205,11 @@ sb_status sb_rows_partial(const sb_dims* dd, const void* p_logits, const void* q
   const bool vok = vec_ok(dd, p_logits) && vec_ok(dd, q_logits);
   if (!vok || ((size_t)dd->V * elem_size(dd)) % 16) return SB_ERR_UNSUPPORTED;
   const Dims d = to_dims(dd);
-  const bool table = d.B <= kPlanTableMaxB;
-  if (table && plan_smem(d.B, true) > 48 * 1024)
-    cudaFuncSetAttribute(k_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan_smem(kPlanTableMaxB, true));
-  k_plan<<<1, 1024, plan_smem(d.B, table), s>>>(d, gamma, branch_pos, w.info, w.unit_off, 1, 0, nullptr, nullptr,
-                                                table ? w.units : nullptr);
+  k_plan<<<1, 1024, 0, s>>>(d, gamma, branch_pos, w.info, w.unit_off, 1, 0, nullptr, nullptr);
   if (cudaGetLastError() != cudaSuccess) return SB_ERR_CUDA;
   RowsParams p{};
   p.d = d; p.PL = p_logits; p.QL = q_logits; p.tok = tok; p.u = u;
-  p.info = w.info; p.unit_off = w.unit_off; p.units = table ? w.units : nullptr; p.cnt = w.cnt; p.rowstat = w.rowstat; p.pflag = w.pflag;
+  p.info = w.info; p.unit_off = w.unit_off; p.cnt = w.cnt; p.rowstat = w.rowstat; p.pflag = w.pflag;
   p.partial = 1;
   p.v_offset = dd->v_offset;
   const size_t per = (size_t)dd->B * dd->K * (dd->G + 1);
@@ -1279,16 +1241,12 @@ extern "C" sb_status sb_verify_branches(const sb_dims* dd, const void* p_logits,
   const Dims d = to_dims(dd);
   cudaStream_t s = (cudaStream_t)stream;
 
-  const bool table = d.B <= kPlanTableMaxB;
-  if (table && plan_smem(d.B, true) > 48 * 1024)
-    cudaFuncSetAttribute(k_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan_smem(kPlanTableMaxB, true));
-  k_plan<<<1, 1024, plan_smem(d.B, table), s>>>(d, gamma, branch_pos, w.info, w.unit_off, 0, 0, nullptr, nullptr,
-                                                table ? w.units : nullptr);
+  k_plan<<<1, 1024, 0, s>>>(d, gamma, branch_pos, w.info, w.unit_off, 0, 0, nullptr, nullptr);
   if (cudaGetLastError() != cudaSuccess) return SB_ERR_CUDA;
 
   RowsParams p;
   p.d = d; p.PL = p_logits; p.QL = q_logits; p.tok = tok; p.u = u;
-  p.info = w.info; p.unit_off = w.unit_off; p.units = table ? w.units : nullptr; p.cnt = w.cnt; p.rowstat = w.rowstat; p.pflag = w.pflag;
+  p.info = w.info; p.unit_off = w.unit_off; p.cnt = w.cnt; p.rowstat = w.rowstat; p.pflag = w.pflag;
   p.lse_p = lse_p; p.lse_q = lse_q; p.p_tok = p_tok; p.q_tok = q_tok;
   p.top1_q = top1_q; p.entropy_q = entropy_q; p.top1_id_q = top1_id_q;
   p.acc_mask = acc_mask; p.n_acc = n_acc; p.status = status;
