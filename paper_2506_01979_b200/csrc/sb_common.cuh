@@ -49,6 +49,13 @@ __host__ __device__ inline int64_t ent(const Dims& d, int b, int k, int i) {  //
 }
 
 // ------------------------------------------------------------------ small PTX helpers
+// Programmatic dependent launch (launch_pdl): wait for the predecessor grid's memory,
+// then let the next grid be scheduled.
+__device__ __forceinline__ void pdl_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));

@@ -148,6 +148,7 @@ __global__ void __launch_bounds__(cThreads, 1) k_conf_tma(ConfParams p) {
     fence_mbar_init();
   }
   __syncthreads();
+  pdl_wait();
   const int total = d.B * d.K * G;
   const T* QL = static_cast<const T*>(p.QL);
   const uint32_t row_bytes = (uint32_t)d.V * sizeof(T);
@@ -282,8 +283,7 @@ static sb_status launch_conf_tma(const ConfParams& p, cudaStream_t s) {
   }
   const int64_t units = (int64_t)p.d.B * p.d.K * p.d.G;
   const int grid = (int)std::min<int64_t>(num_sms(), units);
-  k_conf_tma<T><<<grid, cThreads, smem, s>>>(p);
-  return cuda_status(cudaGetLastError());
+  return cuda_status(launch_pdl(k_conf_tma<T>, dim3(grid), dim3(cThreads), smem, s, p));
 }
 
 }  // namespace sb

@@ -109,6 +109,26 @@ inline bool vec_ok(const sb_dims* d, const void* p) {
 
 inline sb_status cuda_status(cudaError_t e) { return e == cudaSuccess ? SB_OK : SB_ERR_CUDA; }
 
+// Programmatic dependent launch: the grid may be scheduled while its predecessor in the
+// stream drains (launch latency and prologue overlap the predecessor's tail).  Every
+// kernel launched this way calls pdl_wait() before its first global-memory access, so
+// stream order is preserved for data; without the attribute pdl_wait() is a no-op.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at;
+  at.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at.val.programmaticStreamSerializationAllowed = 1;
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = &at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
 int num_sms();        // cached cudaDevAttrMultiProcessorCount of the current device
 bool tma_disabled();  // SB_DISABLE_TMA=1 forces the register-staged kernels (tests)
 

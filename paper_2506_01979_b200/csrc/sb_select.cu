@@ -282,6 +282,7 @@ __global__ void __launch_bounds__(sThreads, 1) k_select_tma(SelParams p) {
     fence_mbar_init();
   }
   __syncthreads();
+  pdl_wait();
   const T* PL = static_cast<const T*>(p.PL);
   const T* QL = static_cast<const T*>(p.QL);
   const uint32_t row_bytes = (uint32_t)d.V * sizeof(T);
@@ -617,8 +618,7 @@ static sb_status launch_select_tma(const SelParams& p, cudaStream_t s) {
     attr = true;
   }
   const int grid = std::min(num_sms(), p.d.B);
-  k_select_tma<T><<<grid, sThreads, smem, s>>>(p);
-  return cuda_status(cudaGetLastError());
+  return cuda_status(launch_pdl(k_select_tma<T>, dim3(grid), dim3(sThreads), smem, s, p));
 }
 
 template <typename T, int NT>

@@ -57,6 +57,7 @@ __global__ void __launch_bounds__(1024) k_plan(Dims d, const int* __restrict__ g
                                                int* unit_off, int with_bonus, int fused_grid, int* plan,
                                                int* ready) {
   __shared__ int wsum[32];
+  pdl_wait();
   const int tid = threadIdx.x, NT = blockDim.x;
   const int per = (d.B + NT - 1) / NT;
   const int b0 = min(d.B, tid * per), b1 = min(d.B, b0 + per);
@@ -555,6 +556,7 @@ __global__ void __launch_bounds__(C::ROWS_THREADS, 1) k_rows_tma(RowsParams p) {
     fence_mbar_init();
   }
   __syncthreads();
+  pdl_wait();
   const int total = __ldg(p.unit_off + d.B);
   const T* PL = static_cast<const T*>(p.PL);
   const T* QL = static_cast<const T*>(p.QL);
@@ -698,8 +700,7 @@ static sb_status launch_rows_tma(const RowsParams& p, cudaStream_t s) {
   }
   const int64_t max_units = (int64_t)p.d.B * p.d.K * (p.d.G + 1);
   const int grid = (int)std::min<int64_t>(num_sms(), max_units);
-  k_rows_tma<C, T><<<grid, C::ROWS_THREADS, smem, s>>>(p);
-  return cuda_status(cudaGetLastError());
+  return cuda_status(launch_pdl(k_rows_tma<C, T>, dim3(grid), dim3(C::ROWS_THREADS), smem, s, p));
 }
 
 template <typename T, int NT, int U>
@@ -1205,8 +1206,9 @@ sb_status sb_rows_partial(const sb_dims* dd, const void* p_logits, const void* q
   const bool vok = vec_ok(dd, p_logits) && vec_ok(dd, q_logits);
   if (!vok || ((size_t)dd->V * elem_size(dd)) % 16) return SB_ERR_UNSUPPORTED;
   const Dims d = to_dims(dd);
-  k_plan<<<1, 1024, 0, s>>>(d, gamma, branch_pos, w.info, w.unit_off, 1, 0, nullptr, nullptr);
-  if (cudaGetLastError() != cudaSuccess) return SB_ERR_CUDA;
+  if (launch_pdl(k_plan, dim3(1), dim3(1024), 0, s, d, gamma, branch_pos, w.info, w.unit_off, 1, 0,
+                 (int*)nullptr, (int*)nullptr) != cudaSuccess)
+    return SB_ERR_CUDA;
   RowsParams p{};
   p.d = d; p.PL = p_logits; p.QL = q_logits; p.tok = tok; p.u = u;
   p.info = w.info; p.unit_off = w.unit_off; p.cnt = w.cnt; p.rowstat = w.rowstat; p.pflag = w.pflag;
@@ -1241,8 +1243,9 @@ extern "C" sb_status sb_verify_branches(const sb_dims* dd, const void* p_logits,
   const Dims d = to_dims(dd);
   cudaStream_t s = (cudaStream_t)stream;
 
-  k_plan<<<1, 1024, 0, s>>>(d, gamma, branch_pos, w.info, w.unit_off, 0, 0, nullptr, nullptr);
-  if (cudaGetLastError() != cudaSuccess) return SB_ERR_CUDA;
+  if (launch_pdl(k_plan, dim3(1), dim3(1024), 0, s, d, gamma, branch_pos, w.info, w.unit_off, 0, 0,
+                 (int*)nullptr, (int*)nullptr) != cudaSuccess)
+    return SB_ERR_CUDA;
 
   RowsParams p;
   p.d = d; p.PL = p_logits; p.QL = q_logits; p.tok = tok; p.u = u;
