@@ -5,6 +5,8 @@
 // ts(k*, i) = (i < s_b ? 0 : k*); they are copied to out[b][i] (out-of-place), or into
 // slot 0 in place (out = NULL: rows i >= s_b of slot k* move to slot 0, the shared
 // prefix already is slot 0).  16-byte vectors, 8 in flight per thread.
+#include <algorithm>
+
 #include "sb_host.h"
 
 namespace sb {
@@ -20,7 +22,8 @@ struct KvParams {
   const int* y_kind;
 };
 
-// one CTA per (sequence, position)
+// one CTA per (sequence, position), sized so every thread has its 8 vectors of the row
+// in flight at once (many small CTAs per SM hide the decision loads' latency)
 __global__ void __launch_bounds__(256) k_kv_rollback(KvParams p) {
   const int b = blockIdx.x / p.R1, i = blockIdx.x % p.R1;
   const int ks = __ldg(p.sel_k + b);
@@ -67,6 +70,7 @@ extern "C" sb_status sb_kv_rollback(int32_t B, int32_t K, int32_t G, const void*
   p.B = B; p.K = K; p.R1 = G + 1; p.row_bytes = row_bytes; p.stride = row_stride_bytes;
   p.kv = static_cast<const char*>(kv); p.out = static_cast<char*>(out_kv); p.bpos = branch_pos;
   p.sel_k = sel_k; p.commit_len = commit_len; p.y_kind = y_kind;
-  k_kv_rollback<<<B * (G + 1), 256, 0, (cudaStream_t)stream>>>(p);
+  const int nt = (int)std::min<int64_t>(256, std::max<int64_t>(32, (row_bytes / 16 + 7) / 8 + 31) / 32 * 32);
+  k_kv_rollback<<<B * (G + 1), nt, 0, (cudaStream_t)stream>>>(p);
   return cuda_status(cudaGetLastError());
 }

@@ -46,12 +46,47 @@ __global__ void __launch_bounds__(NT) k_tree_rows(TreeParams p, bool vec_ok) {
   if (!__any_sync(0xffffffffu, has)) return;
   const T* prow = static_cast<const T*>(p.PL) + row_off(d, b, 0, r);
   const T* qrow = static_cast<const T*>(p.QL) + row_off(d, b, 0, r);
-  RowAcc<false, 4> pa, qa;
-  pa.init();
-  qa.init();
-  stream_pair<T, 4, NT, U, false>(prow, qrow, d.V, vec_ok, pa, qa);
-  const RowStat sp = block_reduce<NT>(fold(pa), red);
-  const RowStat sq = block_reduce<NT>(fold(qa), red);
+  RowStat sp, sq;
+  if (vec_ok && sizeof(T) == 2) {  // lazy-offset packed bf16 path (as the verify kernels)
+    LazyAcc<false, 4> pa, qa;
+    pa.init();
+    qa.init();
+    constexpr int E = Vec<T>::E;
+    const int nvec = d.V / E;
+    const uint4* pv = reinterpret_cast<const uint4*>(prow);
+    const uint4* qv = reinterpret_cast<const uint4*>(qrow);
+    const int nround = (nvec + U * NT - 1) / (U * NT) * (U * NT);
+    for (int vb = threadIdx.x; vb < nround; vb += U * NT) {  // block-uniform trip count
+      uint4 xp[U], xq[U];
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const bool in = vb + j * NT < nvec;
+        xp[j] = in ? ldg_stream(pv + vb + j * NT) : neg_inf_vec<T>();
+        xq[j] = in ? ldg_stream(qv + vb + j * NT) : neg_inf_vec<T>();
+      }
+#pragma unroll
+      for (int j = 0; j + 1 < U; j += 2) {
+        acc_vecs_bf16<2>(pa, xp + j, 0);
+        acc_vecs_bf16<2>(qa, xq + j, 0);
+      }
+    }
+    RowAcc<false, 4> pt, qt;  // the V % 8 tail, exact-offset state, merged below
+    pt.init();
+    qt.init();
+    for (int v = nvec * E + threadIdx.x; v < d.V; v += NT) {
+      pt.add1(ld_scalar(prow + v), v);
+      qt.add1(ld_scalar(qrow + v), v);
+    }
+    sp = block_reduce<NT>(combine(fold_lazy(pa), fold(pt)), red);
+    sq = block_reduce<NT>(combine(fold_lazy(qa), fold(qt)), red);
+  } else {
+    RowAcc<false, 4> pa, qa;
+    pa.init();
+    qa.init();
+    stream_pair<T, 4, NT, U, false>(prow, qrow, d.V, vec_ok, pa, qa);
+    sp = block_reduce<NT>(fold(pa), red);
+    sq = block_reduce<NT>(fold(qa), red);
+  }
   if (threadIdx.x == 0) {
     const RowOut op = finish(sp), oq = finish(sq);
     p.rowstat[(int64_t)b * R1 + r] = (op.finite && oq.finite) ? make_float4(op.MS, op.Z, oq.MS, oq.Z)
