@@ -1165,11 +1165,12 @@ static sb_status launch_step_tma(const StepParams& sp, cudaStream_t s) {
 }
 
 // Geometry variants (SB_ROWS_VARIANT selects one for experiments; 0 = default).
-using RC0 = RC<16, 6, 2, 4, 4>;  // 16 consumer warps, 6 x 32 KB stages, 4 epilogue warps
-using RC1 = RC<16, 6, 2, 4>;   // 16 warps, 6 x 32 KB stages, 4 partial slots, 2 epilogue warps
-using RC2 = RC<16, 7, 2, 2>;   // 16 warps, 7 x 32 KB stages, 2 partial slots
-using RC3 = RC<16, 12, 1, 4, 4>; // 16 warps, 12 x 16 KB stages, 4 epilogue warps
-using RC4 = RC<20, 5, 2, 4>;   // 20 warps, 5 x 40 KB stages
+using RC0 = RC<20, 5, 2, 4, 4>;  // 20 consumer warps, 5 x 40 KB stages, 4 epilogue warps
+using RC1 = RC<24, 4, 2, 4, 4>;  // 24 consumer warps, 4 x 48 KB stages
+using RC2 = RC<16, 6, 2, 4, 4>;  // 16 consumer warps, 6 x 32 KB stages
+using RC3 = RC<24, 8, 1, 4, 4>;  // 24 consumer warps, 1 vector per row per stage, 8 x 24 KB stages
+using RC4 = RC<16, 12, 1, 4, 4>; // 16 consumer warps, 12 x 16 KB stages
+using RCF = RC<16, 6, 2, 4>;   // the fused step kernel's geometry
 
 template <typename T>
 static sb_status launch_rows_variant(const RowsParams& p, cudaStream_t s) {
@@ -1317,5 +1318,5 @@ extern "C" sb_status sb_verify_select(const sb_dims* dd, const void* p_logits, c
   sp.sel_k = sel_k; sp.commit_len = commit_len; sp.out_tok = out_tok; sp.y_tok = y_tok; sp.y_kind = y_kind;
   sp.offsets = offsets; sp.packed_tok = packed_tok; sp.path_rolled = path_rolled;
   sp.branch_discarded = branch_discarded; sp.keep_mask = keep_mask; sp.resid_mass = resid_mass;
-  return dd->dtype == SB_BF16 ? launch_step_tma<RC1, __nv_bfloat16>(sp, s) : launch_step_tma<RC1, float>(sp, s);
+  return dd->dtype == SB_BF16 ? launch_step_tma<RCF, __nv_bfloat16>(sp, s) : launch_step_tma<RCF, float>(sp, s);
 }
