@@ -110,13 +110,22 @@ __global__ void __launch_bounds__(NT) k_conf(ConfParams p, bool vec_ok) {
 
 // TMA ring version (same warp roles as k_rows_tma): producer warp streams 16 KB chunks
 // of each q row, 16 consumer warps fold them, an epilogue warp finishes each row.
-constexpr int cNS = 12;
-constexpr int cCW = 16;
+#ifndef SB_CONF_NS
+#define SB_CONF_NS 12
+#endif
+#ifndef SB_CONF_CW
+#define SB_CONF_CW 16
+#endif
+#ifndef SB_CONF_NE
+#define SB_CONF_NE 2
+#endif
+constexpr int cNS = SB_CONF_NS;  // (macros: A/B experiment builds only)
+constexpr int cCW = SB_CONF_CW;
 constexpr int cCT = cCW * 32;
 constexpr int cVPT = 2;
 constexpr int cChunk = cCT * cVPT * 16;
 constexpr int cNP = 4;
-constexpr int cNE = 2;  // epilogue warps, alternating units
+constexpr int cNE = SB_CONF_NE;  // epilogue warps, alternating units
 constexpr int cThreads = cCT + 32 * (1 + cNE);
 using ConfGeo = RC<cCW, cNS, cVPT, cNP>;  // ring geometry (resolve_argmax)
 

@@ -8,24 +8,23 @@
 //
 // Layer 1 is the only dense contraction (2*B*Dz*256 flops over B*Dz + 256*Dz bf16
 // inputs).  k_hrad: grid = 128-row tiles of z x S K-splits, S chosen so the grid fills
-// the SMs (one CTA per SM); clusters of CM CTAs along the row tiles share each W1 tile:
-//   warp 0    TMA producer : its z k-block (64 columns = one 128-byte swizzle atom) and
-//                            1/CM of the W1 k-block, multicast to the CM CTAs of the
-//                            cluster (W1 leaves L2 once per cluster, not once per tile),
-//                            into a 4-stage ring of 16 + 32 KB (SWIZZLE_128B tensor maps);
-//   warp 1    MMA issuer   : allocates 256 TMEM columns; one elected thread issues
+// the SMs (one CTA per SM):
+//   warp 0    TMA producer : per k-block (64 columns = one 128-byte swizzle atom) the two
+//                            128-row z tiles and the W1 tile into a 3-stage ring of
+//                            2 x 16 + 32 KB (SWIZZLE_128B tensor maps);
+//   warp 1    MMA issuer   : allocates 512 TMEM columns; one elected thread issues
 //                            tcgen05.mma.kind::f16 (M=128, N=256, K=16, fp32 accumulate
-//                            in TMEM); tcgen05.commit multicast to the cluster frees each
-//                            stage once every CTA reading the shared W1 slot is done;
-//   warps 2-5 epilogue     : tcgen05.ld of the 128 x 256 fp32 partial, staged through
+//                            in TMEM; one accumulator per row tile, both fed by the same
+//                            W1 slot: half the W1 bytes per flop); tcgen05.commit frees
+//                            each stage;
+//   warps 2-5 epilogue     : tcgen05.ld of each 128 x 256 fp32 partial, staged through
 //                            shared memory and stored coalesced to partial[s] (L2-sized).
 // k_hrad_tail (programmatic dependent launch): sums the S partials of a row in split
-// order (deterministic), + b1, ReLU, layers 2-3 (a warp per output, W2 rows coalesced),
+// order (deterministic), + b1, ReLU, layers 2-3 (W2 staged in padded shared memory),
 // argmax, H_t.
 #include <cuda.h>
 
 #include <algorithm>
-#include <cstdlib>
 
 #include "sb_host.h"
 #include "sb_ring.cuh"
@@ -51,7 +50,6 @@ constexpr size_t kHradSmem = kRingBytes + 1024;  // + alignment slack (SWIZZLE_1
 static_assert(kAccBytes <= kRingBytes, "the staged partial reuses the ring");
 constexpr int kTailRowsMax = 16;  // rows per k_hrad_tail CTA (<=)
 constexpr int kTailThreads = 512;  // two split-sums and two layer-2 outputs per thread at 16 rows
-constexpr int kMaxCM = 4;         // CTAs per cluster sharing a W1 tile (multicast)
 
 // Instruction descriptor of tcgen05.mma.kind::f16: fp32 accumulator (bits 4-5 = 1),
 // A and B bf16 (bits 7-9, 10-12 = 1), both K-major (bits 15, 16 = 0), N>>3 at 17-22,
@@ -91,40 +89,6 @@ __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint6
       "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(accumulate));
 }
 
-// W1 piece multicast into the same shared offset of every CTA in cta_mask, completing
-// on each destination's barrier at the same offset.
-__device__ __forceinline__ void tma_load_2d_mc(uint32_t dst, const CUtensorMap* map, int x, int y,
-                                               uint64_t* bar, uint16_t cta_mask) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
-      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
-      "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar)), "h"(cta_mask)
-      : "memory");
-}
-
-// Arrive (once all prior tcgen05 ops of this thread complete) on the barrier at the
-// same offset in every CTA of cta_mask.
-__device__ __forceinline__ void umma_commit_mc(uint64_t* bar, uint16_t cta_mask) {
-  asm volatile(
-      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-          smem_u32(bar)),
-      "h"(cta_mask)
-      : "memory");
-}
-
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ uint32_t cluster_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ uint32_t cluster_nrank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
-  return r;
-}
 
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -152,8 +116,7 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
 }
 
-// Layer 1 partial of one (128-row tile, K split): grid (S, tiles rounded up to CM),
-// clusters (1, CM, 1).  tmW1 boxes are 256 / CM rows of W1.
+// Layer 1 partial of one (256-row block, K split): grid (S, ceil(B / 256)).
 __global__ void __launch_bounds__(kHThreads, 1)
     k_hrad(const __grid_constant__ CUtensorMap tmZ, const __grid_constant__ CUtensorMap tmW1, HradParams p) {
   extern __shared__ uint8_t hsm_raw[];
@@ -167,19 +130,15 @@ __global__ void __launch_bounds__(kHThreads, 1)
   const int split = blockIdx.x, S = gridDim.x;
   const int m0 = blockIdx.y * (kTP * kHM);
   const int kb0 = (int)((int64_t)p.nkb * split / S), kb1 = (int)((int64_t)p.nkb * (split + 1) / S);
-  const uint32_t CM = cluster_nrank(), crank = cluster_rank();
-  const uint16_t cmask = (uint16_t)((1u << CM) - 1u);
-  const uint32_t piece = kStageB / CM;  // bytes of W1 this CTA multicasts per stage
 
   if (tid == 0) {
     for (int s = 0; s < kHS; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], CM);  // every CTA reading the multicast slot releases it
+      mbar_init(&empty[s], 1);
     }
     mbar_init(&done, 1);
     fence_mbar_init();
   }
-  cluster_sync_all();  // remote barriers initialised before any multicast / remote arrive
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_slot)),
                  "r"(kTP * kHN));
@@ -203,10 +162,7 @@ __global__ void __launch_bounds__(kHThreads, 1)
 #pragma unroll
         for (int t = 0; t < kTP; ++t) tma_load_2d(a + t * kStageA, &tmZ, kb * kHK, m0 + t * kHM, &full[stage]);
         const uint32_t bb = a + kTP * kStageA;
-        if (CM == 1)
-          tma_load_2d(bb, &tmW1, kb * kHK, 0, &full[stage]);
-        else
-          tma_load_2d_mc(bb + crank * piece, &tmW1, kb * kHK, (int)(crank * (kHN / CM)), &full[stage], cmask);
+        tma_load_2d(bb, &tmW1, kb * kHK, 0, &full[stage]);
         if (++stage == kHS) { stage = 0; phase ^= 1u; }
       }
     }
@@ -224,7 +180,7 @@ __global__ void __launch_bounds__(kHThreads, 1)
           for (int t = 0; t < kTP; ++t)
             umma_bf16(tmem + t * kHN, umma_desc_sw128(a + t * kStageA + k * 32), umma_desc_sw128(bb + k * 32),
                       (kb > kb0 || k > 0) ? 1u : 0u);
-        if (CM == 1) umma_commit(&empty[stage]); else umma_commit_mc(&empty[stage], cmask);
+        umma_commit(&empty[stage]);
         if (++stage == kHS) { stage = 0; phase ^= 1u; }
       }
       umma_commit(&done);  // all MMAs of this CTA complete -> accumulator final
@@ -265,7 +221,6 @@ __global__ void __launch_bounds__(kHThreads, 1)
   }
   tc_fence_before();
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  cluster_sync_all();  // the cluster's multicast commits into this CTA have all landed
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTP * kHN));
 }
 
@@ -377,18 +332,8 @@ static bool make_map(CUtensorMap* m, const void* base, int rows, int cols, int b
 
 // Cluster width along the row tiles (W1 multicast) and K splits per tile: as many
 // splits as fill the SMs (one CTA each), <= k-blocks, <= 16 (the tail sums them).
-static int hrad_cm(int mtiles) {
-  static int cm = -1;  // SB_HRAD_CM (1, 2, 4) selects the multicast width; default 1
-  if (cm < 0) {
-    const char* e = getenv("SB_HRAD_CM");
-    cm = e ? std::max(1, std::min(kMaxCM, atoi(e))) : 1;
-    if (cm == 3) cm = 2;
-  }
-  return std::min(cm, mtiles >= 4 ? 4 : (mtiles >= 2 ? 2 : 1));
-}
-static int hrad_tiles(int mtiles) { const int cm = hrad_cm(mtiles); return (mtiles + cm - 1) / cm * cm; }
 static int hrad_splits(int mtiles, int nkb) {
-  return std::max(1, std::min(nkb, num_sms() / hrad_tiles(mtiles)));
+  return std::max(1, std::min(nkb, num_sms() / mtiles));
 }
 
 }  // namespace sb
@@ -421,9 +366,8 @@ extern "C" sb_status sb_hrad_predict(int32_t B, int32_t Dz, int32_t G, const voi
     attr = true;
   }
   const int mtiles = (B + kTP * kHM - 1) / (kTP * kHM);
-  const int CM = hrad_cm(mtiles);
   CUtensorMap tmZ, tmW1;
-  if (!make_map(&tmZ, z, B, Dz, kHM) || !make_map(&tmW1, w1, kHN, Dz, kHN / CM)) return SB_ERR_CUDA;
+  if (!make_map(&tmZ, z, B, Dz, kHM) || !make_map(&tmW1, w1, kHN, Dz, kHN)) return SB_ERR_CUDA;
   HradParams p;
   p.B = B; p.Dz = Dz; p.G = G; p.nkb = Dz / kHK; p.S = hrad_splits(mtiles, p.nkb);
   p.tail_rows = std::max(1, std::min(kTailRowsMax, (B + 127) / 128));
@@ -431,19 +375,8 @@ extern "C" sb_status sb_hrad_predict(int32_t B, int32_t Dz, int32_t G, const voi
   p.b1 = b1; p.w2 = w2; p.b2 = b2; p.w3 = w3; p.b3 = b3; p.stop = stop;
   p.logits = logits; p.s_t = s_t; p.gamma = gamma; p.bpos = branch_pos;
   cudaStream_t s = (cudaStream_t)stream;
-  {
-    cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute at;
-    at.id = cudaLaunchAttributeClusterDimension;
-    at.val.clusterDim.x = 1; at.val.clusterDim.y = CM; at.val.clusterDim.z = 1;
-    cfg.gridDim = dim3(p.S, hrad_tiles(mtiles), 1);
-    cfg.blockDim = dim3(kHThreads, 1, 1);
-    cfg.dynamicSmemBytes = kHradSmem;
-    cfg.stream = s;
-    cfg.attrs = &at;
-    cfg.numAttrs = 1;
-    if (cudaLaunchKernelEx(&cfg, k_hrad, tmZ, tmW1, p) != cudaSuccess) return SB_ERR_CUDA;
-  }
+  k_hrad<<<dim3(p.S, mtiles), kHThreads, kHradSmem, s>>>(tmZ, tmW1, p);
+  if (cudaGetLastError() != cudaSuccess) return SB_ERR_CUDA;
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute at;
   at.id = cudaLaunchAttributeProgrammaticStreamSerialization;

@@ -515,13 +515,6 @@ __device__ __forceinline__ void load_stage(const uint8_t* bp, const uint8_t* bq,
 template <class C, typename T>
 __device__ __forceinline__ void compute_stage(const StageRegs<C>& r, int c, LazyAcc<false, 4>& pa,
                                               LazyAcc<true, 4>& qa) {
-#ifdef SB_EXP_NOCOMPUTE  // experiment builds only: the ring without the arithmetic
-  uint32_t x = 0;
-#pragma unroll
-  for (int j = 0; j < C::VPT; ++j) x ^= r.p[j].x ^ r.q[j].w;
-  pa.z[0] += __uint_as_float(x & 1u);
-  return;
-#endif
   if constexpr (sizeof(T) == 2) {
     acc_vecs_bf16<C::VPT>(pa, r.p, c);
     acc_vecs_bf16<C::VPT>(qa, r.q, c);
