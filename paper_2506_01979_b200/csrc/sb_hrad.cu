@@ -25,6 +25,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "sb_host.h"
 #include "sb_ring.cuh"
@@ -333,7 +334,15 @@ static bool make_map(CUtensorMap* m, const void* base, int rows, int cols, int b
 // Cluster width along the row tiles (W1 multicast) and K splits per tile: as many
 // splits as fill the SMs (one CTA each), <= k-blocks, <= 16 (the tail sums them).
 static int hrad_splits(int mtiles, int nkb) {
-  return std::max(1, std::min(nkb, num_sms() / mtiles));
+  static int force = -1;  // SB_HRAD_SPLITS: experiment override
+  if (force < 0) {
+    const char* e = getenv("SB_HRAD_SPLITS");
+    force = e ? std::max(1, atoi(e)) : 0;
+  }
+  if (force > 0) return std::min(nkb, force);
+  // fill the SMs, but no more than 18 splits: the tail reads S x B x 1 KB of partials
+  // (measured: B = 2048 best at 18; B = 256 at 16 rather than 148)
+  return std::max(1, std::min(std::min(nkb, 18), num_sms() / mtiles));
 }
 
 }  // namespace sb
