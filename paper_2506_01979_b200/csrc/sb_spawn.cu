@@ -196,8 +196,13 @@ __global__ void __launch_bounds__(NT) k_spawn(SpawnParams p, bool vec_ok) {
         float f[E];
         Vec<T>::unpack(x[j], f);
         const bool valid = vb + j * NT < nvec;
-        const float vm = Vec<T>::vmax(f);
-        acc.template add_cm<E>(f, vm, vb + j * NT);
+        float vm;
+        if constexpr (sizeof(T) == 2) {
+          vm = acc_vecs_bf16<1>(acc, x + j, 0);  // packed FFMA2 / FADD2 sums, returns the max
+        } else {
+          vm = Vec<T>::vmax(f);
+          acc.template add_cm<E>(f, vm, vb + j * NT);
+        }
         unsigned cand = __ballot_sync(0xffffffffu, valid && vm >= filt);
         while (cand) {  // rare once warm: one lane's values, broadcast, qualifying ones inserted
           const int src = __ffs(cand) - 1;

@@ -3,6 +3,5 @@ export PYTHONUNBUFFERED=1
 T=${TAG:-x}
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/${T}_build.log 2>&1
-for S in 18 12 9 6 4; do SB_HRAD_SPLITS=$S timeout 300 python bench.py --config hrad --steps 30 --no-cpu-baseline > gpurun_out/${T}_S$S.log 2>&1; done
-for S in 16 8 4; do SB_HRAD_SPLITS=$S timeout 300 python bench.py --config hrad --hrad-batch 256 --steps 30 --no-cpu-baseline > gpurun_out/${T}_b256_S$S.log 2>&1; done
-timeout 300 python bench.py --config hrad --hrad-batch 256 --steps 30 --no-cpu-baseline > gpurun_out/${T}_b256_def.log 2>&1
+timeout 300 python -m pytest tests/test_gpu_next.py -q -x -k spawn 2>&1 | tail -2 > gpurun_out/${T}_tests.log
+for r in 1 2; do timeout 600 python bench.py --config spawn --steps 20 > gpurun_out/${T}_bench_spawn_$r.log 2>&1; done
