@@ -306,7 +306,7 @@ def run_ours(args, rank, world, local_rank):
                      "achieved": round(ver_gbs, 1), "peak": peak, "peak_source": peak_src, "unit": "GB/s",
                      "frac": round(ver_gbs / peak, 4), "traffic": traffic_from_profiles(cfg.name),
                      "algorithmic_bytes_per_launch": rf_bytes, "row_pairs_per_launch": units},
-        "gpu_launches": args.steps * ((1 if adaptive else 0) + (6 if vocab else 2)),
+        "gpu_launches": args.steps * ((1 if adaptive else 0) + (6 if vocab else 3)),  # conf; plan + rows + select (+3 shard kernels)
         "clocks": clk.summary(),
         "generation_s": round(gen_s, 1),
     }
