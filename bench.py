@@ -492,7 +492,8 @@ def run_next(args, rank, world, local_rank):
         "roofline": {"bound": "hbm", "kernel": kern, "achieved": round(gbs, 1), "peak": peak,
                      "peak_source": peak_src, "unit": "GB/s", "frac": round(gbs / peak, 4), "traffic": None,
                      "algorithmic_bytes_per_launch": nbytes},
-        "gpu_launches": args.steps, "clocks": clk.summary(), "generation_s": round(gen_s, 1),
+        "gpu_launches": args.steps * (2 if args.config == "tree" else 1), "clocks": clk.summary(),
+        "generation_s": round(gen_s, 1),
     }
 
 
