@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(cThreads, 1) k_conf_tma(ConfParams p) {
     for (int li = e, unit = blockIdx.x + e * gridDim.x; unit < total; li += cNE, unit += cNE * gridDim.x) {
       const int grp = unit / G, i = unit % G;
       const int stage = li % cNP;
-      mbar_wait(&S.pfull[stage], (uint32_t)(li / cNP) & 1u);
+      mbar_wait_parked(&S.pfull[stage], (uint32_t)(li / cNP) & 1u);
       RowStat r = lane < cCW ? S.part[stage][lane] : rowstat_empty();
       const uint2 cand = lane < cCW ? S.cand[stage][lane] : make_uint2(0xffffffffu, 0u);
       __syncwarp();

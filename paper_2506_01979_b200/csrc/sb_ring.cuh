@@ -44,6 +44,26 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     if (tries > (1u << 24)) __trap();
   }
 }
+// The same with exponential back-off (nanosleep 256 ns .. 2 us between probes), for
+// waits that last whole units (an epilogue warp waiting for the consumers' partials):
+// their spinning took issue slots from the consumer warps (k_rows_tma: 8-13 % of all
+// issued instructions).  Watchdog ~2^22 probes (seconds).
+__device__ __forceinline__ void mbar_wait_parked(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0, ns = 256;
+  for (uint32_t tries = 0;; ++tries) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (ok) break;
+    __nanosleep(ns);
+    ns = ns < 2048 ? 2 * ns : ns;
+    if (tries > (1u << 22)) __trap();
+  }
+}
 // 1-D bulk copy global -> shared, completion (bytes) signalled on bar.
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
                                          uint64_t policy) {

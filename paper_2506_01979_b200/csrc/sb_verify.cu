@@ -609,7 +609,7 @@ __global__ void __launch_bounds__(C::ROWS_THREADS, 1) k_rows_tma(RowsParams p) {
           lpx = lqx = -CUDART_INF_F;
         }
       }
-      mbar_wait(&S.pfull[up.stage], up.phase);
+      mbar_wait_parked(&S.pfull[up.stage], up.phase);
       RowStat ps = lane < C::CW ? S.part[up.stage][0][lane] : rowstat_empty();
       RowStat qs = lane < C::CW ? S.part[up.stage][1][lane] : rowstat_empty();
       const uint2 cand = lane < C::CW ? S.cand[up.stage][lane] : make_uint2(0xffffffffu, 0u);
