@@ -270,6 +270,27 @@ def run_ours(args, rank, world, local_rank):
     if vocab:  # every rank verifies the same tokens: count them once
         toks_all, comm_all = float(toks), float(committed)
 
+    # ---- C1 also has a latency number: one round of batch 1 as its own
+    # dependent step, replayed from a CUDA graph (rotating over 8 distinct rounds)
+    round_lat = None
+    if cfg.name == "c1" and not vocab and world == 1:
+        c1 = synth.config("c1", rounds=1)
+        one = [synth.generate(c1, device=dev, seed=1000 + r) for r in range(8)]
+        d1 = api.dims_for(one[0]["PL"], V=one[0]["V"])
+        b1s = [api.StepBuffers.alloc(d1, dev) for _ in one]
+        gs = [api.CallGraph(lambda s_, x=x, bb=bb: api.verify_step(d1, x, bb, stream=s_)) for x, bb in zip(one, b1s)]
+        for g_ in gs:
+            g_.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        nrep = 200
+        e0.record(torch.cuda.current_stream())
+        for k in range(nrep):
+            gs[k % len(gs)].replay()
+        e1.record(torch.cuda.current_stream())
+        torch.cuda.synchronize()
+        round_lat = round(1e3 * e0.elapsed_time(e1) / nrep, 2)
+
     # ---- e2e through the public API with host buffers (pinned), H2D + D2H inside
     e2e = None
     if not args.no_e2e and not vocab:
@@ -312,6 +333,10 @@ def run_ours(args, rank, world, local_rank):
     }
     if e2e is not None:
         line["e2e"] = e2e
+    if round_lat is not None:
+        line["per_round_latency_us"] = round_lat
+        line["per_round_note"] = ("one C1 round (batch 1, K=2, gamma=8, fp32) as a dependent step: "
+                                  "conf-free verify + select from a CUDA graph; latency-bound (4 MB of rows)")
     if not args.no_cpu_baseline and world == 1 and not vocab:
         line["cpu_baseline"] = cpu_baseline(cfg, inp, adaptive, buf, budget_s=args.cpu_budget)
     return line
