@@ -75,6 +75,7 @@ SMALL = [
     ("K1_vanilla_sd", dict(name="c4", V=20000, B=64, K=1, G=5, layout="mixed"), 0, 0),
     ("bf16_large_V_few_seq", dict(name="c3", B=6, layout="mixed"), 0, 0),
     ("gamma_max_31", dict(name="c2", V=4096, B=16, K=2, G=31, layout="mixed"), 0, 0),
+    ("B1_single_round_f32", dict(name="c1", B=1, rounds=1, layout="fixed"), 0, 0),
 ]
 
 
