@@ -237,6 +237,11 @@ def run_ours(args, rank, world, local_rank):
             d, PLv, QLv, inp["tok"], inp["u"], gam, inp["branch_pos"], buf.lse_p, buf.lse_q,
             buf.p_tok, buf.q_tok, buf.acc_mask, buf.n_acc, buf.top1_q, buf.top1_id_q, buf.entropy_q,
             buf.status, buf.workspace, s, comm),
+        "verify_reuse": (lambda s: api.sb_verify_branches_reuse(
+            d, PLv, QLv, inp["tok"], inp["u"], gam, inp["branch_pos"], buf.lse_p, buf.lse_q,
+            buf.p_tok, buf.q_tok, buf.acc_mask, buf.n_acc, buf.top1_q, buf.top1_id_q, buf.entropy_q,
+            buf.status, buf.conf_workspace, buf.workspace, s))
+        if adaptive and comm is None else None,
         "fused": (lambda s: api.sb_verify_select(
             d, PLv, QLv, inp["tok"], inp["u"], inp["us"], gam, inp["branch_pos"], 0, buf, s))
         if comm is None else None,
@@ -320,6 +325,7 @@ def run_ours(args, rank, world, local_rank):
         "logit_GBps": round(step_gbs, 1), "logit_frac_of_peak": round(step_gbs / world / peak, 4),
         "committed_tokens_per_s": round(comm_all / (ms_step_all * 1e-3), 1),
         "breakdown_ms": {"draft_confidence": round(t_conf, 4), "verify": round(t_ver, 4),
+                         "verify_reusing_confidence_rows": round(kt["verify_reuse"], 4),
                          "select": round(t_sel, 4), "verify_select": round(t_fused, 4),
                          "source": "each call replayed alone from its own CUDA graph, CUDA events"},
         "timing": "CUDA graph replay of the whole step" if not args.no_graph else "eager C-ABI calls",

@@ -194,6 +194,26 @@ sb_status sb_verify_select(const sb_dims* d, const void* p_logits, const void* q
                            size_t workspace_bytes, sb_stream_t stream);
 
 /*
+ * sb_verify_branches_reuse — sb_verify_branches for the adaptive-gamma step (SURVEY §8.4
+ * C2/C3): conf_workspace is the workspace of a preceding sb_draft_confidence call on the
+ * slot-0 view of the same q_logits (K = 1, seq_stride = this call's sequence stride,
+ * same B, G, V, row_stride, dtype; e.g. api.conf_dims(d)).  That call already streamed
+ * draft rows 0..G-1 of slot 0 and left their reduced softmax state in its workspace;
+ * this call reads those states back instead of re-reading the rows (only their p rows
+ * and the token logits are read).  Outputs and errors as sb_verify_branches; the q
+ * statistics of those rows come from the confidence pass (same arithmetic, a
+ * different summation order: within the 1e-5 tolerance, not bit-identical).  Not for
+ * vocabulary shards (SB_ERR_INVALID_ARG).
+ */
+sb_status sb_verify_branches_reuse(const sb_dims* d, const void* p_logits, const void* q_logits,
+                                   const int32_t* tok, const float* u, const int32_t* gamma,
+                                   const int32_t* branch_pos, float* lse_p, float* lse_q, float* p_tok,
+                                   float* q_tok, uint32_t* acc_mask, int32_t* n_acc, float* top1_q,
+                                   int32_t* top1_id_q, float* entropy_q, int32_t* status,
+                                   const void* conf_workspace, void* workspace, size_t workspace_bytes,
+                                   sb_stream_t stream);
+
+/*
  * sb_draft_confidence — the implicit draft-confidence statistic and adaptive gamma.
  *   (§4.2 P170; Eq. 6 P194-202; Eq. 7 P218; Alg. 1 P517; App. E.6 P954/P965)
  *

@@ -17,7 +17,7 @@ SB_ST_GAMMA_CLAMPED, SB_ST_BRANCH_CLAMPED, SB_ST_BAD_TOKEN, SB_ST_NONFINITE, SB_
 
 # every symbol include/specbranch.h declares
 EXPORTS = ("sb_version", "sb_status_string", "sb_workspace_bytes", "sb_verify_branches",
-           "sb_select_branch", "sb_verify_select", "sb_draft_confidence", "sb_spawn_branches", "sb_kv_rollback", "sb_tree_workspace_bytes", "sb_tree_verify", "sb_hrad_workspace_bytes", "sb_hrad_predict", "sb_shard_partial_bytes", "sb_shard_verify_local",
+           "sb_select_branch", "sb_verify_select", "sb_verify_branches_reuse", "sb_draft_confidence", "sb_spawn_branches", "sb_kv_rollback", "sb_tree_workspace_bytes", "sb_tree_verify", "sb_hrad_workspace_bytes", "sb_hrad_predict", "sb_shard_partial_bytes", "sb_shard_verify_local",
            "sb_shard_verify_combine", "sb_shard_select_local", "sb_shard_select_sample",
            "sb_shard_select_commit", "sb_comm_unique_id_bytes", "sb_comm_unique_id", "sb_comm_create",
            "sb_comm_destroy")
@@ -43,6 +43,7 @@ _SIGS = {
     "sb_status_string": ([_I], ctypes.c_char_p),
     "sb_workspace_bytes": ([_D], _S),
     "sb_verify_branches": ([_D] + [_P] * 18 + [_S, _P], _I),
+    "sb_verify_branches_reuse": ([_D] + [_P] * 18 + [_S, _P], _I),
     "sb_select_branch": ([_D] + [_P] * 8 + [_I] + [_P] * 14 + [_S, _P], _I),
     "sb_draft_confidence": ([_D, _P, _P, _I, _F, _F, ctypes.c_int32] + [_P] * 10 + [_S, _P], _I),
     "sb_verify_select": ([_D] + [_P] * 7 + [_I] + [_P] * 22 + [_S, _P], _I),

@@ -80,6 +80,23 @@ def sb_verify_branches(d, p_logits, q_logits, tok, u, gamma, branch_pos, lse_p, 
     L.check(rc, "sb_verify_branches")
 
 
+def sb_verify_branches_reuse(d, p_logits, q_logits, tok, u, gamma, branch_pos, lse_p, lse_q, p_tok,
+                             q_tok, acc_mask, n_acc, top1_q, top1_id_q, entropy_q, status, conf_workspace,
+                             workspace, stream=None):
+    """sb_verify_branches reusing the slot-0 draft-row states of a preceding
+    sb_draft_confidence(conf_dims(d), ...) whose workspace is conf_workspace."""
+    rc = L.lib().sb_verify_branches_reuse(
+        ctypes.byref(d), _ptr(p_logits, LOG, "p_logits"), _ptr(q_logits, LOG, "q_logits"),
+        _ptr(tok, I32, "tok"), _ptr(u, F32, "u"), _ptr(gamma, I32, "gamma"),
+        _ptr(branch_pos, I32, "branch_pos"), _ptr(lse_p, F32, "lse_p"), _ptr(lse_q, F32, "lse_q"),
+        _ptr(p_tok, F32, "p_tok"), _ptr(q_tok, F32, "q_tok"), _ptr(acc_mask, I32, "acc_mask"),
+        _ptr(n_acc, I32, "n_acc"), _ptr(top1_q, F32, "top1_q"), _ptr(top1_id_q, I32, "top1_id_q"),
+        _ptr(entropy_q, F32, "entropy_q"), _ptr(status, I32, "status"),
+        _ptr(conf_workspace, torch.uint8, "conf_workspace"),
+        _ptr(workspace, torch.uint8, "workspace"), workspace.numel(), _stream(stream))
+    L.check(rc, "sb_verify_branches_reuse")
+
+
 def sb_select_branch(d, p_logits, q_logits, tok, u, us, gamma, branch_pos, n_acc, rule, sel_k,
                      commit_len, out_tok, y_tok, y_kind, offsets, packed_tok, path_rolled,
                      branch_discarded, keep_mask, resid_mass, status, workspace, stream=None, comm=None):
@@ -254,8 +271,10 @@ def verify_step(d: L.sb_dims, inp: dict, buf: StepBuffers, rule: int = SB_SELECT
 
     inp: PL, QL, tok, u, us, gamma, branch_pos device tensors (synth.generate layout).
     With adaptive=True gamma_b = max(1, stop_b) of the slot-0 draft rows (Eq. 6, TOP1)
-    replaces inp["gamma"] and s_b = 0.  fused=True runs verify +
-    select as one launch (sb_verify_select); fused=False issues the two calls.
+    replaces inp["gamma"] and s_b = 0, and the verify pass reuses the
+    confidence pass's slot-0 draft-row states (sb_verify_branches_reuse).  Otherwise
+    fused=True runs verify + select through sb_verify_select, fused=False issues the two
+    calls.
     """
     gamma = inp["gamma"]
     if adaptive:
@@ -264,12 +283,18 @@ def verify_step(d: L.sb_dims, inp: dict, buf: StepBuffers, rule: int = SB_SELECT
                             buf.c_knext, buf.c_gamma, buf.conf_workspace, stream)
         gamma = buf.c_gamma.view(-1)
     PL, QL = views if views is not None else (inp["PL"], inp["QL"])
-    if fused and comm is None:
+    if adaptive and comm is None:  # the confidence pass already streamed slot 0's draft rows
+        sb_verify_branches_reuse(d, PL, QL, inp["tok"], inp["u"], gamma, inp["branch_pos"],
+                                 buf.lse_p, buf.lse_q, buf.p_tok, buf.q_tok, buf.acc_mask, buf.n_acc,
+                                 buf.top1_q, buf.top1_id_q, buf.entropy_q, buf.status, buf.conf_workspace,
+                                 buf.workspace, stream)
+    elif fused and comm is None:
         sb_verify_select(d, PL, QL, inp["tok"], inp["u"], inp["us"], gamma, inp["branch_pos"], rule, buf, stream)
         return gamma
-    sb_verify_branches(d, PL, QL, inp["tok"], inp["u"], gamma, inp["branch_pos"],
-                       buf.lse_p, buf.lse_q, buf.p_tok, buf.q_tok, buf.acc_mask, buf.n_acc,
-                       buf.top1_q, buf.top1_id_q, buf.entropy_q, buf.status, buf.workspace, stream, comm)
+    else:
+        sb_verify_branches(d, PL, QL, inp["tok"], inp["u"], gamma, inp["branch_pos"],
+                           buf.lse_p, buf.lse_q, buf.p_tok, buf.q_tok, buf.acc_mask, buf.n_acc,
+                           buf.top1_q, buf.top1_id_q, buf.entropy_q, buf.status, buf.workspace, stream, comm)
     sb_select_branch(d, PL, QL, inp["tok"], inp["u"], inp["us"], gamma,
                      inp["branch_pos"], buf.n_acc, rule, buf.sel_k, buf.commit_len, buf.out_tok,
                      buf.y_tok, buf.y_kind, buf.offsets, buf.packed_tok, buf.path_rolled,

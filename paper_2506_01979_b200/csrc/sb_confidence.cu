@@ -27,6 +27,7 @@ struct ConfParams {
   int* cnt;
   float* ws_stat;
   float* ws_c;
+  RowStat* qrs;  // [B][K][G] this row's reduced state (reuse by sb_verify_branches_reuse)
 };
 
 // Per-row statistic and the group-completion logic shared by both kernels.
@@ -38,6 +39,7 @@ __device__ __forceinline__ void conf_epilogue(const ConfParams& p, int grp, int 
   const int b = grp / d.K, k = grp % d.K;
   const RowOut o = finish(s);
   if (tid == 0) {
+    p.qrs[(int64_t)grp * G + i] = s;
     const int64_t e = (int64_t)grp * G + i;
     double top1 = CUDART_NAN, H = CUDART_NAN, tp = CUDART_NAN, st = CUDART_NAN;
     int id = -1;
@@ -325,7 +327,7 @@ extern "C" sb_status sb_draft_confidence(const sb_dims* dd, const void* q_logits
   p.d = to_dims(dd); p.QL = q_logits; p.tok = tok; p.mode = mode; p.eps = eps; p.lambda = lambda;
   p.k_max = k_max; p.top1_prob = top1_prob; p.entropy = entropy; p.tok_prob = tok_prob;
   p.stat = stat; p.top1_id = top1_id; p.stop = stop; p.k_next = k_next; p.gamma_next = gamma_next;
-  p.cnt = w.conf_cnt; p.ws_stat = w.conf_stat; p.ws_c = w.conf_c;
+  p.cnt = w.conf_cnt; p.ws_stat = w.conf_stat; p.ws_c = w.conf_c; p.qrs = w.qrs;
   const bool vok = vec_ok(dd, q_logits);
   const size_t row_bytes = (size_t)dd->V * elem_size(dd);
   if (vok && row_bytes % 16 == 0 && !tma_disabled())

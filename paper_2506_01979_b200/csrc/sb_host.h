@@ -38,6 +38,8 @@ struct Workspace {
   int4* dec;         // [B] sharded select: decision record
   int* ready;        // [B] fused step: per-sequence phase-1 completion flags
   int* plan;         // [4] fused step: delta, total units
+  RowStat* qrs;      // [B][K][G] row states of the rows sb_draft_confidence streamed
+                     // (read back by sb_verify_branches_reuse instead of the q rows)
   size_t bytes;
 };
 
@@ -69,6 +71,7 @@ inline Workspace carve(const sb_dims& d, void* base) {
   }
   w.ready = (int*)take(sizeof(int) * B);
   w.plan = (int*)take(sizeof(int) * 4);
+  w.qrs = (RowStat*)take(sizeof(RowStat) * B * K * (G ? G : 1));
   w.bytes = off;
   return w;
 }

@@ -31,6 +31,7 @@ struct RowsParams {
   const float* u;
   const SeqInfo* info;
   const int* unit_off;
+  const RowStat* qreuse;  // [B][G] slot-0 q-row states from sb_draft_confidence, or NULL
   int* cnt;
   float4* rowstat;
   uint8_t* pflag;
@@ -171,6 +172,12 @@ __device__ __forceinline__ int4 unit_prefetch(const RowsParams& p, int unit, int
   if (unit >= total) return make_int4(0, 0, 0, 0);
   const Unit u = decode_unit(p, unit);
   return unit_entry(u.b, u.slot, u.i, u.in);
+}
+
+// Slot-0 draft rows i < G were streamed by sb_draft_confidence: with p.qreuse their q
+// state is read back instead of the row (SURVEY §8.4 adaptive configs).
+__device__ __forceinline__ bool q_reused(const RowsParams& p, const Unit& un) {
+  return p.qreuse != nullptr && un.slot == 0 && un.i < p.d.G;
 }
 
 // Everything after a row pair's statistics are known: path-token probabilities and the
@@ -329,6 +336,7 @@ struct RowsSmem {
   uint64_t pfull[C::NP], pempty[C::NP];
   RowStat part[C::NP][2][C::CW];  // [slot][p,q][warp]
   uint2 cand[C::NP][C::CW];       // q-row argmax candidates per warp (tag, lane mask)
+  int ponly[C::NS];               // stage holds only the p chunk (q state reused)
   alignas(128) uint8_t buf[C::NS][2][C::CHUNK];
 };
 
@@ -531,6 +539,29 @@ __device__ __forceinline__ void compute_stage(const StageRegs<C>& r, int c, Lazy
   }
 }
 
+// p-only stage (q state reused): the p vectors and the p arithmetic alone
+template <class C, typename T, bool FULL>
+__device__ __forceinline__ void load_stage_p(const uint8_t* bp, int nvec, StageRegs<C>& r) {
+  const int tid = threadIdx.x;
+#pragma unroll
+  for (int j = 0; j < C::VPT; ++j) {
+    const int v = tid + j * C::CT;
+    r.p[j] = (FULL || v < nvec) ? lds128(bp + v * 16) : neg_inf_vec<T>();
+  }
+}
+template <class C, typename T>
+__device__ __forceinline__ void compute_stage_p(const StageRegs<C>& r, int c, LazyAcc<false, 4>& pa) {
+  if constexpr (sizeof(T) == 2) {
+    acc_vecs_bf16<C::VPT>(pa, r.p, c);
+  } else {
+    constexpr int E = Vec<T>::E;
+    float fp[C::VPT * E];
+#pragma unroll
+    for (int j = 0; j < C::VPT; ++j) Vec<T>::unpack(r.p[j], fp + j * E);
+    pa.template add<C::VPT * E>(fp, c);
+  }
+}
+
 template <class C, typename T>
 __global__ void __launch_bounds__(C::ROWS_THREADS, 1) k_rows_tma(RowsParams p) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -567,12 +598,14 @@ __global__ void __launch_bounds__(C::ROWS_THREADS, 1) k_rows_tma(RowsParams p) {
         nxt = unit_prefetch(p, unit + gridDim.x, total);
         const char* prow = reinterpret_cast<const char*>(PL + row_off(d, un.b, un.slot, un.i));
         const char* qrow = reinterpret_cast<const char*>(QL + row_off(d, un.b, un.slot, un.i));
+        const bool po = q_reused(p, un);
         for (int c = 0; c < nchunks; ++c) {
           const uint32_t bytes = min((uint32_t)C::CHUNK, row_bytes - (uint32_t)c * C::CHUNK);
           mbar_wait(&S.empty[rp.stage], rp.phase ^ 1u);
-          mbar_expect_tx(&S.full[rp.stage], 2 * bytes);
+          S.ponly[rp.stage] = po;  // published by the arrive below (release)
+          mbar_expect_tx(&S.full[rp.stage], (po ? 1 : 2) * bytes);
           bulk_g2s(S.buf[rp.stage][0], prow + (size_t)c * C::CHUNK, bytes, &S.full[rp.stage], pol);
-          bulk_g2s(S.buf[rp.stage][1], qrow + (size_t)c * C::CHUNK, bytes, &S.full[rp.stage], pol);
+          if (!po) bulk_g2s(S.buf[rp.stage][1], qrow + (size_t)c * C::CHUNK, bytes, &S.full[rp.stage], pol);
           rp.advance();
         }
       }
@@ -609,6 +642,9 @@ __global__ void __launch_bounds__(C::ROWS_THREADS, 1) k_rows_tma(RowsParams p) {
           lpx = lqx = -CUDART_INF_F;
         }
       }
+      const bool po = q_reused(p, un);
+      RowStat qr;
+      if (po) qr = p.qreuse[(int64_t)un.b * d.G + un.i];
       mbar_wait_parked(&S.pfull[up.stage], up.phase);
       RowStat ps = lane < C::CW ? S.part[up.stage][0][lane] : rowstat_empty();
       RowStat qs = lane < C::CW ? S.part[up.stage][1][lane] : rowstat_empty();
@@ -622,7 +658,8 @@ __global__ void __launch_bounds__(C::ROWS_THREADS, 1) k_rows_tma(RowsParams p) {
         ps = combine(ps, shfl_xor(ps, o));
         qs = combine(qs, shfl_xor(qs, o));
       }
-      qs.idx = resolve_argmax<C, T>(qmw, cand, qs.m, qrow, nvec_last, nchunks);
+      if (po) qs = qr;
+      else qs.idx = resolve_argmax<C, T>(qmw, cand, qs.m, qrow, nvec_last, nchunks);
       if (p.partial) {  // a7: this shard's state, combined across shards later
         if (lane < ntok && has_tok) p.tokpart[et] = make_float2(lpx, lqx);
         if (lane == 0) {
@@ -651,20 +688,26 @@ __global__ void __launch_bounds__(C::ROWS_THREADS, 1) k_rows_tma(RowsParams p) {
     for (int c = 0; c < nchunks - 1; ++c) {  // full chunks: no guards, no fill
       StageRegs<C> r;
       mbar_wait(&S.full[rp.stage], rp.phase);
-      load_stage<C, T, true>(S.buf[rp.stage][0], S.buf[rp.stage][1], 0, r);
+      const bool po = *reinterpret_cast<volatile int*>(&S.ponly[rp.stage]);
+      if (!po) load_stage<C, T, true>(S.buf[rp.stage][0], S.buf[rp.stage][1], 0, r);
+      else load_stage_p<C, T, true>(S.buf[rp.stage][0], 0, r);
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.empty[rp.stage]);
       rp.advance();
-      compute_stage<C, T>(r, c, pa, qa);
+      if (!po) compute_stage<C, T>(r, c, pa, qa);
+      else compute_stage_p<C, T>(r, c, pa);
     }
     {  // last (possibly partial) chunk
       StageRegs<C> r;
       mbar_wait(&S.full[rp.stage], rp.phase);
-      load_stage<C, T, false>(S.buf[rp.stage][0], S.buf[rp.stage][1], nvec_last, r);
+      const bool po = *reinterpret_cast<volatile int*>(&S.ponly[rp.stage]);
+      if (!po) load_stage<C, T, false>(S.buf[rp.stage][0], S.buf[rp.stage][1], nvec_last, r);
+      else load_stage_p<C, T, false>(S.buf[rp.stage][0], nvec_last, r);
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.empty[rp.stage]);
       rp.advance();
-      compute_stage<C, T>(r, nchunks - 1, pa, qa);
+      if (!po) compute_stage<C, T>(r, nchunks - 1, pa, qa);
+      else compute_stage_p<C, T>(r, nchunks - 1, pa);
     }
     uint2 cand;
     const RowStat ps = warp_part<C, T, false>(pa, nullptr, nvec_last, nchunks);
@@ -723,7 +766,7 @@ static sb_status launch_rows(const RowsParams& p, bool vok, cudaStream_t s) {
 //   epilogue : phase-1 -> token tests / n_k / ready[b]; sample -> locate us*R, re-read
 //              one segment, commit / rollback outputs; the last sequence scans offsets.
 struct StepParams {
-  RowsParams r;
+  RowsParams r{};
   const float* us;
   int rule;
   const int* plan;  // [0] delta, [1] total units
@@ -1214,14 +1257,12 @@ sb_status sb_rows_partial(const sb_dims* dd, const void* p_logits, const void* q
   return dd->dtype == SB_BF16 ? launch_rows_variant<__nv_bfloat16>(p, s) : launch_rows_variant<float>(p, s);
 }
 
-extern "C" sb_status sb_verify_branches(const sb_dims* dd, const void* p_logits,
-                                        const void* q_logits, const int32_t* tok, const float* u,
-                                        const int32_t* gamma, const int32_t* branch_pos,
-                                        float* lse_p, float* lse_q, float* p_tok, float* q_tok,
-                                        uint32_t* acc_mask, int32_t* n_acc, float* top1_q,
-                                        int32_t* top1_id_q, float* entropy_q, int32_t* status,
-                                        void* comm, void* workspace, size_t workspace_bytes,
-                                        sb_stream_t stream) {
+static sb_status verify_impl(const sb_dims* dd, const void* p_logits, const void* q_logits, const int32_t* tok,
+                             const float* u, const int32_t* gamma, const int32_t* branch_pos, float* lse_p,
+                             float* lse_q, float* p_tok, float* q_tok, uint32_t* acc_mask, int32_t* n_acc,
+                             float* top1_q, int32_t* top1_id_q, float* entropy_q, int32_t* status, void* comm,
+                             void* workspace, size_t workspace_bytes, const void* conf_workspace,
+                             sb_stream_t stream) {
   if (!dims_valid(dd)) return SB_ERR_INVALID_ARG;
   if (!p_logits || !q_logits || !tok || !u || !lse_p || !lse_q || !p_tok || !q_tok || !acc_mask ||
       !n_acc || !status || !workspace)
@@ -1248,6 +1289,13 @@ extern "C" sb_status sb_verify_branches(const sb_dims* dd, const void* p_logits,
   p.top1_q = top1_q; p.entropy_q = entropy_q; p.top1_id_q = top1_id_q;
   p.acc_mask = acc_mask; p.n_acc = n_acc; p.status = status;
   p.partial = 0; p.v_offset = 0; p.rowpart = nullptr; p.tokpart = nullptr; p.ready = nullptr;
+  p.qreuse = nullptr;
+  if (conf_workspace && dd->G > 0) {  // slot-0 rows of the same q tensor, as sb_draft_confidence saw them
+    sb_dims cd = *dd;
+    cd.K = 1;
+    cd.seq_stride = d.ss;
+    p.qreuse = carve(cd, const_cast<void*>(conf_workspace)).qrs;
+  }
   const bool vok = vec_ok(dd, p_logits) && vec_ok(dd, q_logits);
   const size_t row_bytes = (size_t)dd->V * elem_size(dd);
   if (vok && row_bytes % 16 == 0 && !tma_disabled())
@@ -1258,6 +1306,32 @@ extern "C" sb_status sb_verify_branches(const sb_dims* dd, const void* p_logits,
   }
   return row_bytes <= 131072 ? launch_rows<float, 128, 4>(p, vok, s)
                              : launch_rows<float, 256, 4>(p, vok, s);
+}
+
+extern "C" sb_status sb_verify_branches(const sb_dims* dd, const void* p_logits,
+                                        const void* q_logits, const int32_t* tok, const float* u,
+                                        const int32_t* gamma, const int32_t* branch_pos,
+                                        float* lse_p, float* lse_q, float* p_tok, float* q_tok,
+                                        uint32_t* acc_mask, int32_t* n_acc, float* top1_q,
+                                        int32_t* top1_id_q, float* entropy_q, int32_t* status,
+                                        void* comm, void* workspace, size_t workspace_bytes,
+                                        sb_stream_t stream) {
+  return verify_impl(dd, p_logits, q_logits, tok, u, gamma, branch_pos, lse_p, lse_q, p_tok, q_tok, acc_mask,
+                     n_acc, top1_q, top1_id_q, entropy_q, status, comm, workspace, workspace_bytes, nullptr,
+                     stream);
+}
+
+extern "C" sb_status sb_verify_branches_reuse(const sb_dims* dd, const void* p_logits, const void* q_logits,
+                                              const int32_t* tok, const float* u, const int32_t* gamma,
+                                              const int32_t* branch_pos, float* lse_p, float* lse_q, float* p_tok,
+                                              float* q_tok, uint32_t* acc_mask, int32_t* n_acc, float* top1_q,
+                                              int32_t* top1_id_q, float* entropy_q, int32_t* status,
+                                              const void* conf_workspace, void* workspace, size_t workspace_bytes,
+                                              sb_stream_t stream) {
+  if (!conf_workspace || sharded(dd)) return SB_ERR_INVALID_ARG;
+  return verify_impl(dd, p_logits, q_logits, tok, u, gamma, branch_pos, lse_p, lse_q, p_tok, q_tok, acc_mask,
+                     n_acc, top1_q, top1_id_q, entropy_q, status, nullptr, workspace, workspace_bytes,
+                     conf_workspace, stream);
 }
 
 // ---------------------------------------------------------------- fused entry point

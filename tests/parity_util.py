@@ -16,6 +16,7 @@ import oracle
 from paper_2506_01979_b200 import api, synth
 
 REL, ABS = 1e-5, 1e-7
+ENT_ABS = 1e-6
 
 
 def gpu_run(inp: dict, rule=0, adaptive=False, eps=0.2, k_max=6, fused=True):
@@ -73,10 +74,14 @@ def compare(g: dict, o: dict, sel=None, strict=True):
             if err.size and err.max() > REL:
                 rep["fail"].append((k + "_tol", float(err.max())))
     for k in ("top1_q", "entropy_q", "p_tok", "q_tok"):
-        ok, relerr = _close(gs[k], o[k])
+        # entropy (nats) also gets an absolute 1e-6: H = ln2 (log2 Z - S1/Z) from fp32 sums,
+        # and the register-staged fallback rebases S1 at every new running maximum
+        # (measured: 4e-7 absolute on an H = 0.018 row); DESIGN reading 30
+        ab = ENT_ABS if k == "entropy_q" else ABS
+        ok, relerr = _close(gs[k], o[k], ab=ab)
         rep[f"max_rel_{k}"] = relerr
         if not ok:
-            bad = ~np.isclose(gs[k].astype(np.float64), o[k], rtol=REL, atol=ABS, equal_nan=True)
+            bad = ~np.isclose(gs[k].astype(np.float64), o[k], rtol=REL, atol=ab, equal_nan=True)
             fail(k, np.where(bad.reshape(len(sel), -1).any(axis=1))[0])
     # discrete
     ok_id = gs["top1_id_q"] == o["top1_id_q"]

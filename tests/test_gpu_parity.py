@@ -209,3 +209,39 @@ def test_baseline_config_full_size(name, adaptive, sample):
     # flagged (|us*R - F| < 1e-6), so only the decision ties are bounded here
     assert rep["ties"]["decision"] <= 0.1 * rep["n"], rep
     print(name, {k: v for k, v in rep.items() if k != "fail"})
+
+
+@pytest.mark.parametrize("name,kw", [("bf16_mixed_V32000", dict(name="c2", B=48, layout="mixed")),
+                                     ("f32_mixed_ragged", dict(name="c1", V=3001, B=40, K=3, G=6, rounds=1,
+                                                                layout="mixed")),
+                                     ("bf16_K8_G16", dict(name="c5", V=9000, B=24, K=8, G=16, layout="mixed"))])
+def test_verify_reuse_of_confidence_states(name, kw):
+    """sb_verify_branches_reuse: slot-0 draft rows i < G are not re-read; their q state
+    comes from the preceding sb_draft_confidence.  Same bars against the oracle on mixed
+    layouts (branch rows s_b > 0, Algorithm-1 form, gamma = 0), with the step's select."""
+    import oracle
+    from paper_2506_01979_b200 import api, synth
+
+    from parity_util import compare, oracle_for
+
+    c = cfg(kw.pop("name"), **kw)
+    inp = synth.generate(c, device="cuda", seed=31)
+    d = api.dims_for(inp["PL"], V=inp["V"])
+    buf = api.StepBuffers.alloc(d, inp["PL"].device)
+    api.sb_draft_confidence(api.conf_dims(d), inp["QL"], None, api.SB_CONF_TOP1, 0.2, 1.0, 6, buf.c_top1, buf.c_id,
+                            buf.c_ent, None, buf.c_stat, buf.c_stop, buf.c_knext, buf.c_gamma, buf.conf_workspace)
+    api.sb_verify_branches_reuse(d, inp["PL"], inp["QL"], inp["tok"], inp["u"], inp["gamma"], inp["branch_pos"],
+                                 buf.lse_p, buf.lse_q, buf.p_tok, buf.q_tok, buf.acc_mask, buf.n_acc, buf.top1_q,
+                                 buf.top1_id_q, buf.entropy_q, buf.status, buf.conf_workspace, buf.workspace)
+    api.sb_select_branch(d, inp["PL"], inp["QL"], inp["tok"], inp["u"], inp["us"], inp["gamma"], inp["branch_pos"],
+                         buf.n_acc, 0, buf.sel_k, buf.commit_len, buf.out_tok, buf.y_tok, buf.y_kind, buf.offsets,
+                         buf.packed_tok, buf.path_rolled, buf.branch_discarded, buf.keep_mask, buf.resid_mass,
+                         buf.status, buf.workspace)
+    torch.cuda.synchronize()
+    g = {k: getattr(buf, k).cpu().numpy() for k in buf.__dataclass_fields__ if k not in ("workspace", "conf_workspace")}
+    g["acc_mask"] = g["acc_mask"].view(np.uint32)
+    g["keep_mask"] = g["keep_mask"].view(np.uint32)
+    inp_np = synth.to_numpy_inputs(inp)
+    o = oracle_for(inp_np, inp_np["gamma"])
+    rep = compare(g, o)
+    assert rep["exact_seq"] >= 0.9 * rep["n"], rep
