@@ -100,3 +100,27 @@ def test_product_path_never_imports_oracle():
     for f in glob.glob(os.path.join(pkg, "**", "*.*"), recursive=True):
         if f.endswith((".py", ".cu", ".cuh", ".h")):
             assert not pat.search(open(f).read()), f
+
+
+def test_invalid_args_rejected_on_host_next_rows(L):
+    """The §8.6 entry points and the reuse variant check their arguments before any
+    launch (fake non-null device pointers never get dereferenced)."""
+    lib = L.lib()
+    d = _dims(L)
+    fake = ctypes.c_void_p(256)
+    # sb_verify_branches_reuse: a conf workspace is required
+    args = [fake] * 16 + [None, fake]
+    assert lib.sb_verify_branches_reuse(ctypes.byref(d), *args, 1 << 30, None) == L.SB_ERR_INVALID_ARG
+    # sb_spawn_branches: k_max in [1, 16]
+    assert lib.sb_spawn_branches(ctypes.byref(d), fake, None, None, 0, 17, fake, fake, None, None,
+                                 None) == L.SB_ERR_INVALID_ARG
+    # sb_kv_rollback: rows must be 16-byte multiples
+    assert lib.sb_kv_rollback(4, 2, 3, fake, 24, 32, None, fake, fake, fake, None, None) == L.SB_ERR_INVALID_ARG
+    # sb_tree_verify: K must be 1
+    assert lib.sb_tree_workspace_bytes(ctypes.byref(d)) == 0  # d has K = 4
+    assert lib.sb_tree_verify(ctypes.byref(d), *[fake] * 15, fake, 1 << 30, None) == L.SB_ERR_INVALID_ARG
+    # sb_hrad_predict: B >= 1, Dz a multiple of 64 (12 tensors, workspace, bytes, stream)
+    hr = [fake] * 12 + [fake, 1 << 30, None]
+    assert lib.sb_hrad_predict(0, 256, 8, *hr) == L.SB_ERR_INVALID_ARG
+    assert lib.sb_hrad_predict(4, 200, 8, *hr) == L.SB_ERR_UNSUPPORTED
+    assert lib.sb_hrad_predict(4, 256, 40, *hr) == L.SB_ERR_INVALID_ARG  # G > 31
