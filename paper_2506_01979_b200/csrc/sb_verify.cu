@@ -13,6 +13,7 @@
 //                         sequence (per-sequence counter) builds acc_mask, n_acc,
 //                         status and the sentinels of untested entries.
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 
@@ -1211,7 +1212,16 @@ using RCF = RC<16, 6, 2, 4>;   // the fused step kernel's geometry
 template <typename T>
 static sb_status launch_rows_variant(const RowsParams& p, cudaStream_t s) {
   const char* e = getenv("SB_ROWS_VARIANT");
-  const int v = e ? atoi(e) : 0;
+  int v = e ? atoi(e) : -1;
+  if (v < 0) {
+    // default: 20 consumer warps (20 KB chunks), unless the padding of a row's last
+    // chunk (lanes that cost instructions, not bytes) wastes > 3 % more of the stages
+    // than with 16 warps (16 KB chunks): C1 / C2's 125 / 62.5 KB rows waste 12 / 28 %
+    // with 20 KB chunks and 2.4 % with 16 KB ones; C3 / C4 stay on 20 warps
+    const double rb = (double)p.d.V * sizeof(T);
+    auto waste = [&](double chunk) { const double n = std::ceil(rb / chunk); return (n * chunk - rb) / (n * chunk); };
+    v = waste(RC0::CHUNK) - waste(RC2::CHUNK) > 0.03 ? 2 : 0;
+  }
   switch (v) {
     case 1: return launch_rows_tma<RC1, T>(p, s);
     case 2: return launch_rows_tma<RC2, T>(p, s);
