@@ -542,7 +542,28 @@ def run_e2e(args, inp, d, buf, adaptive, stream, dev, world):
     from paper_2506_01979_b200 import api
 
     keys = ("PL", "QL", "tok", "u", "us", "gamma", "branch_pos")
-    host = {k: torch.empty(inp[k].shape, dtype=inp[k].dtype, pin_memory=True) for k in keys}
+    need = sum(inp[k].numel() * inp[k].element_size() for k in keys)
+    # every rank pins its own inputs: skip (all ranks alike) rather than exhaust host memory
+    try:
+        import psutil
+
+        avail = psutil.virtual_memory().available
+    except Exception:
+        avail = float("inf")
+    host, ok = None, need * world <= 0.6 * avail
+    if ok:
+        try:
+            host = {k: torch.empty(inp[k].shape, dtype=inp[k].dtype, pin_memory=True) for k in keys}
+        except Exception:
+            host, ok = None, False
+    if world > 1:
+        f = torch.tensor([1 if ok else 0], device=dev)
+        torch.distributed.all_reduce(f, op=torch.distributed.ReduceOp.MIN)
+        ok = bool(f.item())
+    if not ok:
+        del host
+        return {"unavailable": "pinned host copies of %d ranks x %.1f GB of inputs exceed 60 %% of the %.0f GB "
+                               "of available host memory" % (world, need / 1e9, avail / 1e9)}
     for k in keys:
         host[k].copy_(inp[k])
     dv = {k: inp[k] for k in keys}
