@@ -60,11 +60,20 @@ def build(force: bool = False, verbose: bool = False, extra=(), out: str = SO) -
     builds, loaded through SB_LIB_PATH)."""
     if out == SO and not extra and not force and up_to_date():
         return SO
-    cmd = nvcc_cmd(verbose)
-    cmd[cmd.index(SO + ".tmp")] = out + ".tmp"
-    cmd[1:1] = list(extra)
-    subprocess.check_call(cmd)
-    os.replace(out + ".tmp", out)
+    import fcntl
+
+    # several ranks of one torchrun job may get here at once: one builds, the others
+    # wait on the lock and then find the library up to date
+    with open(out + ".lock", "w") as lk:
+        fcntl.flock(lk, fcntl.LOCK_EX)
+        if out == SO and not extra and not force and up_to_date():
+            return SO
+        tmp = f"{out}.{os.getpid()}.tmp"
+        cmd = nvcc_cmd(verbose)
+        cmd[cmd.index(SO + ".tmp")] = tmp
+        cmd[1:1] = list(extra)
+        subprocess.check_call(cmd)
+        os.replace(tmp, out)
     return out
 
 
