@@ -707,12 +707,18 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--ref-seqs", type=int, default=32)
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: test-only multi-rank runs on one GPU (LOCAL_RANK modulo the device count)")
     args = ap.parse_args()
     if args.mode is None:
         args.mode = "vocab" if args.config == "c5" else "seq"
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.dist_backend == "gloo" and args.impl != "reference":
+        import torch
+
+        local_rank %= max(1, torch.cuda.device_count())
     if args.impl == "reference":
         line = run_reference(args, rank, world)
         if line is not None:
@@ -722,7 +728,10 @@ def main():
         import torch
 
         torch.cuda.set_device(local_rank)
-        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if args.dist_backend == "nccl":
+            torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:  # test-only: several ranks sharing one GPU (gloo collectives on CPU tensors)
+            torch.distributed.init_process_group("gloo")
     runner = {"hrad": run_hrad, "spawn": run_next, "kv": run_next, "tree": run_next}.get(args.config, run_ours)
     line = runner(args, rank, world, local_rank)
     if line is not None:
