@@ -1,17 +1,19 @@
 // sb_verify.cu — sb_verify_branches: one streaming pass over every tested (p,q) row
-// pair, fused with the acceptance test and, in the last CTA of each sequence, the
+// pair, fused with the acceptance test and, in the CTA completing each sequence, the
 // first-rejection scan (SURVEY §8.1 rows a1 + a2; PAPER §3 P94, Alg. 1 P523-538).
 //
 // Kernels
-//   k_plan  (1 CTA)       clamp gamma_b / s_b, L_b, tested row pairs per sequence,
-//                         exclusive scan -> unit offsets.
-//   k_rows  (persistent)  one unit = one physical row pair (p row, q row) of V logits,
-//                         streamed once with 16-byte loads, 2 x U loads in flight per
-//                         thread; online max / sum / entropy / top-1 in registers, one
-//                         block reduction, then the row's path tokens: P[x], Q[x] in
-//                         fp64 and acc = u*Q[x] <= P[x].  The CTA that completes a
-//                         sequence (per-sequence counter) builds acc_mask, n_acc,
-//                         status and the sentinels of untested entries.
+//   k_plan      (1 CTA)      clamp gamma_b / s_b, L_b, tested row pairs per sequence,
+//                            exclusive scan -> unit offsets.
+//   k_rows_tma  (persistent, 16-byte aligned rows; the path every benchmark takes)
+//                            producer warp: cp.async.bulk ring of p / q chunks; consumer
+//                            warps: lazy-offset online max / sum / entropy with packed
+//                            FFMA2 / FADD2 bf16 arithmetic; epilogue warps: token tests
+//                            in fp64, row outputs, per-sequence completion -> n_k.
+//                            sb_verify_branches_reuse: slot-0 q rows come back as states
+//                            from the confidence pass (p chunks only for those units).
+//   k_rows      (fallback)   the same arithmetic register-staged, any alignment.
+//   k_step_tma  (opt-in)     verify + sample in one persistent launch (SB_FUSED_STEP=1).
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -325,11 +327,12 @@ __global__ void __launch_bounds__(NT) k_rows(RowsParams p, bool vec_ok) {
 //                             vectors per thread per row per stage), then per unit one
 //                             warp reduction (+ exact first-argmax) -> a partial in
 //                             shared memory (NP slots, mbarrier handshake);
-//   warps CW+1..  epilogue  : (NE warps, alternating units) prefetch the unit's path tokens, uniforms and their two
-//                             logits while the consumers stream, then combines the CW
-//                             partials, runs the token tests in fp64, writes the row
-//                             outputs and the per-sequence completion — concurrently with
-//                             the consumers streaming the next units.
+//   warps CW+1..  epilogue  : NE warps, alternating units: prefetch the unit's path
+//                             tokens, uniforms and their two logits while the consumers
+//                             stream, then combine the CW partials, resolve the q argmax,
+//                             run the token tests in fp64, write the row outputs and the
+//                             per-sequence completion — concurrently with the consumers
+//                             streaming the next units.
 
 template <class C>
 struct RowsSmem {
