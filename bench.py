@@ -611,17 +611,17 @@ def cpu_baseline(cfg, inp, adaptive, buf, budget_s=15.0):
     B = inp["PL"].shape[0]
     gamma_all = (buf.c_gamma.view(-1) if adaptive else inp["gamma"]).cpu().numpy()
 
-    def run(idx):
+    def run(idx, nth=nthreads):
         it = torch.as_tensor(idx, device=inp["PL"].device)
         sub = synth.to_numpy_inputs({k: (v.index_select(0, it) if torch.is_tensor(v) else v) for k, v in inp.items()})
         t0 = time.time()
         if adaptive:
-            c = oracle.confidence(np.ascontiguousarray(sub["QL"][:, :1]), V=sub["V"], nthreads=nthreads)
+            c = oracle.confidence(np.ascontiguousarray(sub["QL"][:, :1]), V=sub["V"], nthreads=nth)
             g = c["gamma_next"][:, 0]
         else:
             g = sub["gamma"]
         oracle.verify(sub["PL"], sub["QL"], sub["tok"], sub["u"], sub["us"], g, sub["branch_pos"],
-                      nthreads=nthreads, V=sub["V"])
+                      nthreads=nth, V=sub["V"])
         return time.time() - t0, verified_tokens(g.tolist(), sub["branch_pos"].tolist(), cfg.K)
 
     n = min(B, nthreads)
@@ -632,9 +632,14 @@ def cpu_baseline(cfg, inp, adaptive, buf, budget_s=15.0):
         if n2 > n:
             dt, tk = run(np.arange(n2))
             n = n2
+    # the same oracle on one core, over a few sequences (SURVEY §8.4 "a 1-thread run")
+    n1 = min(B, 4)
+    dt1, tk1 = run(np.arange(n1), nth=1)
     return {"value": round(tk / dt, 1), "unit": "verified draft tokens/s", "cores": nthreads,
             "kind": "oracle", "sample": f"{n} of {B} sequences of {cfg.name.upper()} (first {n}), {dt:.1f} s, "
-                                        f"OpenMP over sequences, fp64 plain loops"}
+                                        f"OpenMP over sequences, fp64 plain loops",
+            "single_core_value": round(tk1 / dt1, 1),
+            "single_core_sample": f"{n1} sequences on 1 thread, {dt1:.1f} s"}
 
 
 def run_reference(args, rank, world):
