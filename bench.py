@@ -599,6 +599,16 @@ def run_e2e(args, inp, d, buf, adaptive, stream, dev, world):
             "steps": steps, "path": "pinned host -> H2D -> verify_step (C ABI) -> D2H of the commit"}
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
 def cpu_baseline(cfg, inp, adaptive, buf, budget_s=15.0):
     """The fp64 oracle as it stands, on this host's cores, over a bounded sample."""
     import numpy as np
@@ -638,6 +648,7 @@ def cpu_baseline(cfg, inp, adaptive, buf, budget_s=15.0):
     return {"value": round(tk / dt, 1), "unit": "verified draft tokens/s", "cores": nthreads,
             "kind": "oracle", "sample": f"{n} of {B} sequences of {cfg.name.upper()} (first {n}), {dt:.1f} s, "
                                         f"OpenMP over sequences, fp64 plain loops",
+            "cpu_model": cpu_model(),
             "single_core_value": round(tk1 / dt1, 1),
             "single_core_sample": f"{n1} sequences on 1 thread, {dt1:.1f} s"}
 
