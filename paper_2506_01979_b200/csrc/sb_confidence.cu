@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(NT) k_conf(ConfParams p, bool vec_ok) {
 #define SB_CONF_CW 16
 #endif
 #ifndef SB_CONF_NE
-#define SB_CONF_NE 2
+#define SB_CONF_NE 4
 #endif
 constexpr int cNS = SB_CONF_NS;  // (macros: A/B experiment builds only)
 constexpr int cCW = SB_CONF_CW;
