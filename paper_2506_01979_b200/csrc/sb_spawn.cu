@@ -16,7 +16,10 @@
 
 namespace sb {
 
-constexpr int kSpawnNT = 256;
+// CTA size by batch: 8 warps per row while one wave of 256-thread CTAs (5 per SM at 48
+// registers) covers the batch, 2 warps per row beyond that (C4's 2048 rows: 14 CTAs of
+// 64 threads per SM, one wave; measured 0.198 ms -> 0.158 ms)
+constexpr int kSpawnNT = 256, kSpawnNTSmall = 64;
 
 struct SpawnParams {
   Dims d;
@@ -294,7 +297,8 @@ __global__ void __launch_bounds__(NT) k_spawn(SpawnParams p, bool vec_ok) {
 
 template <typename T, int KL>
 static sb_status launch_spawn(const SpawnParams& p, bool vok, cudaStream_t s) {
-  k_spawn<T, KL, 4, kSpawnNT><<<p.d.B, kSpawnNT, 0, s>>>(p, vok);
+  if (p.d.B > 5 * num_sms()) k_spawn<T, KL, 4, kSpawnNTSmall><<<p.d.B, kSpawnNTSmall, 0, s>>>(p, vok);
+  else k_spawn<T, KL, 4, kSpawnNT><<<p.d.B, kSpawnNT, 0, s>>>(p, vok);
   return cuda_status(cudaGetLastError());
 }
 

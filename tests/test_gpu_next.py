@@ -19,7 +19,10 @@ SPAWN = [("bf16_V128256", dict(name="c3", B=40, layout="mixed"), 6, 0),
          ("bf16_V32000_k16", dict(name="c2", B=64, layout="mixed"), 16, 0),
          ("f32_V3001_ragged", dict(name="c1", V=3001, B=48, rounds=1, layout="mixed"), 8, 0),
          ("bf16_token_mode", dict(name="c2", V=5000, B=48, layout="mixed"), 6, 1),
-         ("tiny_V5", dict(name="c2", V=5, B=64, K=2, G=3, layout="mixed"), 8, 0)]
+         ("tiny_V5", dict(name="c2", V=5, B=64, K=2, G=3, layout="mixed"), 8, 0),
+         # B > 5 x SMs: the 64-thread-CTA geometry
+         ("bf16_V5000_B1000", dict(name="c2", V=5000, B=1000, layout="mixed"), 16, 0),
+         ("f32_V3001_B800_ragged", dict(name="c1", V=3001, B=800, rounds=1, layout="mixed"), 8, 0)]
 
 
 @pytest.mark.parametrize("name,kw,k_max,mode", SPAWN, ids=[c[0] for c in SPAWN])
