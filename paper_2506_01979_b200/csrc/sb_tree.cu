@@ -223,7 +223,9 @@ static bool tree_dims_valid(const sb_dims* d) {
 
 template <typename T>
 static sb_status launch_tree(const TreeParams& p, bool vok, cudaStream_t s) {
-  k_tree_rows<T, 256, 4><<<p.d.B * (p.d.G + 1), 256, 0, s>>>(p, vok);
+  // 128-thread CTAs, 4 vectors in flight per thread (measured on 256 dense 30-node
+  // trees, V = 32000: 256 threads 0.135 ms, 128 threads 0.119 ms, 64 threads 0.125 ms)
+  k_tree_rows<T, 128, 4><<<p.d.B * (p.d.G + 1), 128, 0, s>>>(p, vok);
   k_tree_select<T, 256><<<p.d.B, 256, 0, s>>>(p, vok);
   return cuda_status(cudaGetLastError());
 }
