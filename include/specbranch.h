@@ -301,13 +301,13 @@ sb_status sb_tree_verify(const sb_dims* d, const void* p_logits, const void* q_l
  *   from sb_draft_confidence, clamped to [0, G]; NULL stop -> G), (G, G) if s_t = 2.
  * z: [B][Dz] bf16 row-major (features Concat(h^1..h^4, e_t), Eq. 4), w1: [256][Dz] bf16,
  * b1 [256], w2 [64][256], b2 [64], w3 [3][64], b3 [3] fp32 — all device pointers,
- * caller-owned, z / w1 16-byte aligned.  Outputs (device, overwritten): s_t [B];
+ * caller-owned, z / w1 / b1 / w2 16-byte aligned.  Outputs (device, overwritten): s_t [B];
  * logits [B][3], gamma [B], branch_pos [B] may be NULL.  Layer 1 runs on the tensor
  * cores (tcgen05, fp32 accumulation, split along K; the split partials — the
  * workspace, sb_hrad_workspace_bytes(B, Dz) bytes, 16-byte aligned, no initialisation
  * needed — are summed in a fixed order, so results are run-to-run deterministic);
  * layers 2-3 in fp32.  Errors: SB_ERR_INVALID_ARG (B < 1, G outside [0, 31], NULL
- * required pointer), SB_ERR_UNSUPPORTED (Dz not a multiple of 64, misaligned z / w1),
+ * required pointer), SB_ERR_UNSUPPORTED (Dz not a multiple of 64, misaligned z / w1 / b1 / w2),
  * SB_ERR_WORKSPACE (too small), SB_ERR_CUDA (tensor-map encode or launch).
  * Stream-ordered, no host synchronisation.
  */

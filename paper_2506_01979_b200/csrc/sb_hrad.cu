@@ -20,8 +20,8 @@
 //   warps 2-5 epilogue     : tcgen05.ld of each 128 x 256 fp32 partial, staged through
 //                            shared memory and stored coalesced to partial[s] (L2-sized).
 // k_hrad_tail (programmatic dependent launch): sums the S partials of a row in split
-// order (deterministic), + b1, ReLU, layers 2-3 (W2 staged in padded shared memory),
-// argmax, H_t.
+// order (deterministic), + b1, ReLU, layers 2-3 (each thread holds a 32-column slice of
+// one W2 row in registers), argmax, H_t.
 #include <cuda.h>
 
 #include <algorithm>
@@ -226,54 +226,87 @@ __global__ void __launch_bounds__(kHThreads, 1)
 }
 
 // Split-K sum (in split order) + b1, ReLU, layers 2-3, argmax, H_t for p.tail_rows
-// rows per CTA.  A programmatic dependent of k_hrad: W2 is staged (row stride 257,
-// conflict-free for both the coalesced fill and the per-output reads) before
-// griddepcontrol.wait, so it overlaps k_hrad's tail.
-constexpr int kW2Stride = kHN + 1;
-constexpr size_t kTailSmem = (size_t)(kH2 * kW2Stride + kTailRowsMax * kHN + kTailRowsMax * kH2) * 4;
+// rows per CTA.  A programmatic dependent of k_hrad: each thread loads its slice of W2
+// (output j = tid % 64, hidden-1 columns [32 sl, 32 sl + 32), sl = tid / 64) into
+// registers before griddepcontrol.wait, so it overlaps k_hrad's tail.  Layer 2 then
+// costs one broadcast LDS.128 per four FMAs (h1 rows in shared memory); the 8 slice
+// partials of each output are summed in slice order (deterministic).
+constexpr int kSl = kTailThreads / kH2;  // 8 slices of hidden-1
+constexpr int kSw = kHN / kSl;           // 32 columns per slice
+static_assert(kSl * kH2 == kTailThreads && kSw % 4 == 0, "tail geometry");
+constexpr size_t kTailSmem = (size_t)(kTailRowsMax * kHN + kTailRowsMax * kSl * kH2 + kTailRowsMax * kH2) * 4;
 __global__ void __launch_bounds__(kTailThreads, 1) k_hrad_tail(HradParams p) {
   extern __shared__ float tsm[];
-  float* w2s = tsm;                        // [64][257]
-  float* h1s = w2s + kH2 * kW2Stride;      // [R][256]
-  float* h2s = h1s + kTailRowsMax * kHN;   // [R][64]
-  const int tid = threadIdx.x;
+  float* h1s = tsm;                              // [R][256]
+  float* part = h1s + kTailRowsMax * kHN;        // [R][8][64]
+  float* h2s = part + kTailRowsMax * kSl * kH2;  // [R][64]
+  const int tid = threadIdx.x, j = tid % kH2, sl = tid / kH2;
   const int R = p.tail_rows;
   const int r0 = blockIdx.x * R;
   const int rows = min(R, p.B - r0);
-  for (int e = tid; e < kH2 * kHN; e += kTailThreads) w2s[(e / kHN) * kW2Stride + e % kHN] = __ldg(p.w2 + e);
+  float4 w[kSw / 4];
+  const float4* wsrc = reinterpret_cast<const float4*>(p.w2 + j * kHN + sl * kSw);
+#pragma unroll
+  for (int i = 0; i < kSw / 4; ++i) w[i] = __ldg(wsrc + i);
   asm volatile("griddepcontrol.wait;" ::: "memory");  // k_hrad's partials are complete
-  for (int e = tid; e < rows * (kHN / 4); e += kTailThreads) {  // 8 split loads in flight
-    const int rr = e / (kHN / 4), c4 = (e % (kHN / 4)) * 4;
-    const float4* src = reinterpret_cast<const float4*>(p.partial + (int64_t)(r0 + rr) * kHN + c4);
+  // split sum: float4 element e = rr * 64 + c/4 of the CTA's rows (contiguous in each
+  // split's partial), at most two per thread (R <= 16), 2 x 6 split loads in flight
+  static_assert(kTailRowsMax * kHN / 4 <= 2 * kTailThreads, "two split-sum elements per thread");
+  {
+    const int nel = rows * (kHN / 4);
     const int64_t qs = (int64_t)p.B * kHN / 4;
-    float4 s = __ldcg(src);
-    for (int q0 = 1; q0 < p.S; q0 += 8) {
-      float4 v[8];
+    const float4* base = reinterpret_cast<const float4*>(p.partial) + (int64_t)r0 * (kHN / 4);
+    const int e0 = tid, e1 = tid + kTailThreads;
+    const bool has0 = e0 < nel, has1 = e1 < nel;
+    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 s0 = has0 ? __ldcg(base + e0) : z4, s1 = has1 ? __ldcg(base + e1) : z4;
+    for (int q0 = 1; q0 < p.S; q0 += 6) {
+      float4 v0[6], v1[6];
 #pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (q0 + j < p.S) v[j] = __ldcg(src + (q0 + j) * qs);
+      for (int jj = 0; jj < 6; ++jj) {
+        const bool in = q0 + jj < p.S;
+        v0[jj] = (in && has0) ? __ldcg(base + (q0 + jj) * qs + e0) : z4;
+        v1[jj] = (in && has1) ? __ldcg(base + (q0 + jj) * qs + e1) : z4;
+      }
 #pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (q0 + j < p.S) { s.x += v[j].x; s.y += v[j].y; s.z += v[j].z; s.w += v[j].w; }
+      for (int jj = 0; jj < 6; ++jj)
+        if (q0 + jj < p.S) {
+          s0.x += v0[jj].x; s0.y += v0[jj].y; s0.z += v0[jj].z; s0.w += v0[jj].w;
+          s1.x += v1[jj].x; s1.y += v1[jj].y; s1.z += v1[jj].z; s1.w += v1[jj].w;
+        }
     }
-    const float4 bb = __ldg(reinterpret_cast<const float4*>(p.b1 + c4));
-    *reinterpret_cast<float4*>(h1s + rr * kHN + c4) =
-        make_float4(fmaxf(s.x + bb.x, 0.f), fmaxf(s.y + bb.y, 0.f), fmaxf(s.z + bb.z, 0.f), fmaxf(s.w + bb.w, 0.f));
+    if (has0) {
+      const float4 bb = __ldg(reinterpret_cast<const float4*>(p.b1) + e0 % (kHN / 4));
+      reinterpret_cast<float4*>(h1s)[e0] = make_float4(fmaxf(s0.x + bb.x, 0.f), fmaxf(s0.y + bb.y, 0.f),
+                                                       fmaxf(s0.z + bb.z, 0.f), fmaxf(s0.w + bb.w, 0.f));
+    }
+    if (has1) {
+      const float4 bb = __ldg(reinterpret_cast<const float4*>(p.b1) + e1 % (kHN / 4));
+      reinterpret_cast<float4*>(h1s)[e1] = make_float4(fmaxf(s1.x + bb.x, 0.f), fmaxf(s1.y + bb.y, 0.f),
+                                                       fmaxf(s1.z + bb.z, 0.f), fmaxf(s1.w + bb.w, 0.f));
+    }
+  }
+  __syncthreads();
+  for (int rr = 0; rr < rows; ++rr) {
+    const float4* h = reinterpret_cast<const float4*>(h1s + rr * kHN + sl * kSw);
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll
+    for (int i = 0; i < kSw / 4; ++i) {
+      const float4 x = h[i];
+      a0 = fmaf(w[i].x, x.x, a0);
+      a1 = fmaf(w[i].y, x.y, a1);
+      a2 = fmaf(w[i].z, x.z, a2);
+      a3 = fmaf(w[i].w, x.w, a3);
+    }
+    part[(rr * kSl + sl) * kH2 + j] = (a0 + a1) + (a2 + a3);
   }
   __syncthreads();
   for (int e = tid; e < rows * kH2; e += kTailThreads) {
-    const int rr = e / kH2, j = e % kH2;
-    const float* w = w2s + j * kW2Stride;
-    const float* h = h1s + rr * kHN;
-    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-#pragma unroll 4
-    for (int c = 0; c < kHN; c += 4) {
-      a0 = fmaf(w[c], h[c], a0);
-      a1 = fmaf(w[c + 1], h[c + 1], a1);
-      a2 = fmaf(w[c + 2], h[c + 2], a2);
-      a3 = fmaf(w[c + 3], h[c + 3], a3);
-    }
-    h2s[rr * kH2 + j] = fmaxf((a0 + a1) + (a2 + a3) + __ldg(p.b2 + j), 0.f);
+    const int rr = e / kH2, jj = e % kH2;
+    float a = 0.f;
+#pragma unroll
+    for (int q = 0; q < kSl; ++q) a += part[(rr * kSl + q) * kH2 + jj];
+    h2s[rr * kH2 + jj] = fmaxf(a + __ldg(p.b2 + jj), 0.f);
   }
   __syncthreads();
   if (tid < rows) {
@@ -363,7 +396,8 @@ extern "C" sb_status sb_hrad_predict(int32_t B, int32_t Dz, int32_t G, const voi
   if (B < 1 || Dz < 1 || G < 0 || G > kMaxG || !z || !w1 || !b1 || !w2 || !b2 || !w3 || !b3 || !s_t ||
       !workspace)
     return SB_ERR_INVALID_ARG;
-  if (Dz % kHK != 0 || (uintptr_t)z % 16 || (uintptr_t)w1 % 16) return SB_ERR_UNSUPPORTED;
+  if (Dz % kHK != 0 || (uintptr_t)z % 16 || (uintptr_t)w1 % 16 || (uintptr_t)b1 % 16 || (uintptr_t)w2 % 16)
+    return SB_ERR_UNSUPPORTED;
   if ((uintptr_t)workspace % 16) return SB_ERR_INVALID_ARG;
   if (workspace_bytes < sb_hrad_workspace_bytes(B, Dz)) return SB_ERR_WORKSPACE;
   static bool attr = false;
