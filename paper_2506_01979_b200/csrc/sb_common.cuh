@@ -400,6 +400,27 @@ __device__ __forceinline__ RowStat shfl_xor(const RowStat& s, int o) {
   return r;
 }
 
+// Warp reduction of one lane state's (ms, z, s1), m and idx left to the caller: every
+// lane first moves to the warp's largest offset (one ex2, as LazyAcc::rescale), then
+// plain sums — two independent 5-round trees instead of 5 rounds of combine() (5
+// shuffles + 2 ex2 each) on the consumers' per-unit critical path.
+__device__ __forceinline__ RowStat warp_reduce_offsets(RowStat s) {
+  float MS = s.ms;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) MS = fmaxf(MS, __shfl_xor_sync(0xffffffffu, MS, o));
+  const float dd = s.ms - MS, sc = ex2(dd);
+  float z = s.z * sc, s1 = sc * fmaf(s.z, dd, s.s1);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    z += __shfl_xor_sync(0xffffffffu, z, o);
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+  }
+  s.ms = MS;
+  s.z = z;
+  s.s1 = s1;
+  return s;
+}
+
 // Block-wide reduction of RowStat; result valid in every thread.  smem: NT/32 entries.
 template <int NT>
 __device__ __forceinline__ RowStat block_reduce(RowStat s, RowStat* smem) {

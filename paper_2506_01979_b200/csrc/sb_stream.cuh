@@ -31,8 +31,7 @@ __device__ __forceinline__ RowStat warp_part_deferred(const LazyAcc<kQ, 4>& a, u
   const unsigned t = hold ? (unsigned)a.tag : 0xffffffffu;
   const unsigned tmin = __reduce_min_sync(0xffffffffu, t);
   cand = make_uint2(tmin, __ballot_sync(0xffffffffu, hold && t == tmin));
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) s = combine(s, shfl_xor(s, o));
+  s = warp_reduce_offsets(s);
   s.m = mw;
   s.idx = 0x7fffffff;
   return s;

@@ -371,8 +371,7 @@ __device__ __forceinline__ RowStat warp_part(const LazyAcc<kQ, 4>& a, const T* r
       if (have[j]) x[j] = __ldg(cv + v);
     }
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) s = combine(s, shfl_xor(s, o));
+  s = warp_reduce_offsets(s);
   s.m = mw;
   int cand = 0x7fffffff;
   if (need) {
