@@ -421,6 +421,17 @@ __device__ __forceinline__ RowStat warp_reduce_offsets(RowStat s) {
   return s;
 }
 
+// The same with the maximum reduced too (the lanes' idx are not combined: callers
+// resolve the argmax separately).
+__device__ __forceinline__ RowStat warp_reduce_state(RowStat s) {
+  float m = s.m;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  s = warp_reduce_offsets(s);
+  s.m = m;
+  return s;
+}
+
 // Block-wide reduction of RowStat; result valid in every thread.  smem: NT/32 entries.
 template <int NT>
 __device__ __forceinline__ RowStat block_reduce(RowStat s, RowStat* smem) {

@@ -656,11 +656,8 @@ __global__ void __launch_bounds__(C::ROWS_THREADS, 1) k_rows_tma(RowsParams p) {
       if (lane == 0) mbar_arrive(&S.pempty[up.stage]);
       up.advance();
       const float qmw = qs.m;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        ps = combine(ps, shfl_xor(ps, o));
-        qs = combine(qs, shfl_xor(qs, o));
-      }
+      ps = warp_reduce_state(ps);  // idx: p's unused, q's resolved below
+      qs = warp_reduce_state(qs);
       if (po) qs = qr;
       else qs.idx = resolve_argmax<C, T>(qmw, cand, qs.m, qrow, nvec_last, nchunks);
       if (p.partial) {  // a7: this shard's state, combined across shards later
@@ -1019,11 +1016,8 @@ __global__ void __launch_bounds__(C::THREADS, 1) k_step_tma(StepParams sp) {
         if (lane == 0) mbar_arrive(&S.pempty[up.stage]);
         up.advance();
         const float qmw = qs.m;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          ps = combine(ps, shfl_xor(ps, o));
-          qs = combine(qs, shfl_xor(qs, o));
-        }
+        ps = warp_reduce_state(ps);  // idx: p's unused, q's resolved below
+        qs = warp_reduce_state(qs);
         qs.idx = resolve_argmax<C, T>(qmw, cand, qs.m, qrow, nvec_last, nchunks);
         warp_epilogue<T>(p, un, ps, qs, x, lpx, lqx, uu, et);
         continue;
