@@ -189,11 +189,18 @@ __global__ void __launch_bounds__(NT) k_spawn(SpawnParams p, bool vec_ok) {
     const int nvec = d.V / E;
     const uint4* rv = reinterpret_cast<const uint4*>(row);
     const int nv_round = (nvec + 32 * U * NW - 1) / (32 * U * NW) * (32 * U * NW);
+    // register double buffer: the next U vectors are in flight while these are reduced
+    uint4 xn[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) xn[j] = (tid + j * NT < nvec) ? ldg_stream(rv + tid + j * NT) : neg_inf_vec<T>();
     for (int vb = tid; vb < nv_round; vb += U * NT) {  // warp-uniform trip count
       uint4 x[U];
 #pragma unroll
-      for (int j = 0; j < U; ++j)
-        x[j] = (vb + j * NT < nvec) ? ldg_stream(rv + vb + j * NT) : neg_inf_vec<T>();
+      for (int j = 0; j < U; ++j) {
+        x[j] = xn[j];
+        const int vn = vb + U * NT + j * NT;
+        xn[j] = (vn < nvec) ? ldg_stream(rv + vn) : neg_inf_vec<T>();
+      }
 #pragma unroll
       for (int j = 0; j < U; ++j) {
         float f[E];
