@@ -373,9 +373,11 @@ static int hrad_splits(int mtiles, int nkb) {
     force = e ? std::max(1, atoi(e)) : 0;
   }
   if (force > 0) return std::min(nkb, force);
-  // fill the SMs, but no more than 18 splits: the tail reads S x B x 1 KB of partials
-  // (measured: B = 2048 best at 18; B = 256 at 16 rather than 148)
-  return std::max(1, std::min(std::min(nkb, 18), num_sms() / mtiles));
+  // fill the SMs, but no more than 18 splits (32 for a single 256-row block): the tail
+  // reads S x B x 1 KB of partials (measured with the register-sliced tail: B = 2048
+  // 12 / 18 / 24 splits 47.3 / 44.7 / 61.0 us; B = 256 16 / 32 / 64 splits 33.0 / 31.3 / 32.8 us)
+  const int cap = mtiles == 1 ? 32 : 18;
+  return std::max(1, std::min(std::min(nkb, cap), num_sms() / mtiles));
 }
 
 }  // namespace sb

@@ -164,7 +164,7 @@ def test_tree_bad_parent_and_nonfinite():
 
 # ---------------------------------------------------------------- f4: H-RAD MLP (tcgen05)
 HRAD = [("B1_Dz64", 1, 64), ("B100_Dz320", 100, 320), ("B129_Dz256", 129, 256), ("B128_Dz5120", 128, 5120),
-        ("B300_Dz2048", 300, 2048), ("B2048_Dz20480", 2048, 20480)]
+        ("B300_Dz2048", 300, 2048), ("B256_Dz20480", 256, 20480), ("B2048_Dz20480", 2048, 20480)]
 
 
 @pytest.mark.parametrize("name,B,Dz", HRAD, ids=[h[0] for h in HRAD])
