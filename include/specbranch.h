@@ -39,6 +39,16 @@
  *     carries the per-row softmax state between them) and must not be shared by calls
  *     in flight on different streams.
  *   - Functions are stateless apart from `workspace` and thread-safe across streams.
+ *   - Input domain (precondition on every logit row the call reads): the row's maximum
+ *     logit m (NaN entries ignored) is finite with |m| < 2^24 (SB_LOGIT_RANGE).  Entries
+ *     below the maximum are unrestricted: -inf, -FLT_MAX or finfo(bf16).min masks
+ *     contribute exactly 0, as in the plain definition softmax(l)_v = exp(l_v - m) / Z.
+ *     Why: the kernels evaluate every term as 2^(l c - fl(m c)) in fp32 (c = log2 e),
+ *     exact up to the rounding of fl(m c), which stays below one unit of the exponent
+ *     only while |m| < 2^24.  A row outside the domain is not evaluated: its row / path
+ *     outputs are NaN (as for a row with no distribution) and SB_ST_RANGE is set.  A
+ *     row holding +inf, no finite entry (all -inf), or NaN (in-range rows) sets
+ *     SB_ST_NONFINITE instead.  (Real logits lie within a few hundred of 0.)
  */
 #ifndef SPECBRANCH_H
 #define SPECBRANCH_H
@@ -49,6 +59,8 @@
 #ifdef __cplusplus
 extern "C" {
 #endif
+
+#define SB_LOGIT_RANGE 16777216.0f /* 2^24: input domain bound on |row maximum| (above) */
 
 typedef struct CUstream_st* sb_stream_t; /* identical to cudaStream_t; NULL = default */
 
@@ -69,9 +81,12 @@ typedef enum { SB_CONF_TOP1 = 0, SB_CONF_TOKEN = 1, SB_CONF_ENTROPY = 2 } sb_con
 #define SB_ST_GAMMA_CLAMPED 1u  /* gamma_b outside [0,G]: clamped                        */
 #define SB_ST_BRANCH_CLAMPED 2u /* s_b outside [0,gamma_b]: clamped                      */
 #define SB_ST_BAD_TOKEN 4u      /* a path token outside [0,V): that test counts rejected */
-#define SB_ST_NONFINITE 8u      /* a row read holds NaN/+inf or is all -inf              */
+#define SB_ST_NONFINITE 8u      /* a row read holds +inf, no finite entry, or (in-range
+                                   rows) a NaN: it has no distribution                  */
 #define SB_ST_ZERO_RESID 16u    /* residual mass R == 0 after a rejection: sampled from p */
 #define SB_ST_BAD_PARENT 32u    /* tree: parent[j] outside [-1, j): node j counts rejected */
+#define SB_ST_RANGE 64u         /* a row read violates the input domain (below): its
+                                   maximum is finite with |max| >= 2^24; not evaluated  */
 
 typedef struct {
   int32_t B;          /* sequences, >= 1                                              */

@@ -22,6 +22,7 @@ _SRC = os.path.join(_HERE, "oracle.c")
 
 OR_BF16, OR_F32 = 0, 1
 ST_GAMMA_CLAMPED, ST_BRANCH_CLAMPED, ST_BAD_TOKEN, ST_NONFINITE, ST_ZERO_RESID, ST_BAD_PARENT = 1, 2, 4, 8, 16, 32
+ST_RANGE = 64  # row outside the input domain (|row max| >= 2^24), oracle.h
 TIE_ACC_MASK, TIE_ACC_DEC, TIE_SAMPLE, TIE_ILLCOND, TIE_CONF, TIE_EQ7 = 1, 2, 4, 8, 16, 32
 CONF_TOP1, CONF_TOKEN, CONF_ENTROPY = 0, 1, 2
 
@@ -106,6 +107,7 @@ def lib():
         _lib.oracle_verify_f64u.restype = ctypes.c_int
         _lib.oracle_confidence.restype = ctypes.c_int
         _lib.oracle_row_softmax.restype = ctypes.c_double
+        _lib.oracle_row_domain.restype = ctypes.c_uint32
         _lib.oracle_adaptive_k.restype = ctypes.c_int
         _lib.oracle_adaptive_k.argtypes = [ctypes.c_double, ctypes.c_int]
     return _lib
@@ -188,6 +190,15 @@ def row_softmax(L, b, slot, i, V=None):
     P = np.empty(V, dtype=np.float64)
     lse = lib().oracle_row_softmax(ctypes.byref(d), _ptr(L), b, slot, i, _ptr(P))
     return P, lse
+
+
+def row_domain(L, b, slot, i, V=None):
+    """Input-domain validation of one physical row: 0, ST_NONFINITE or ST_RANGE."""
+    B, K, R1, stride = L.shape
+    V = stride if V is None else V
+    d = _dims(L, B, K, R1 - 1, V)
+    d.row_stride = stride
+    return int(lib().oracle_row_domain(ctypes.byref(d), _ptr(L), b, slot, i))
 
 
 def adaptive_k(c: float, k_max: int) -> int:

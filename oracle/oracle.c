@@ -41,9 +41,9 @@ double oracle_logit(const or_dims* d, const void* L, int b, int slot, int i, int
 }
 
 /* Softmax of one row, plain two-pass definition (SURVEY §8.0 "Per-row definitions"):
- * m = max l, Z = sum exp(l - m), lse = m + ln Z, P(v) = exp(l(v) - lse).
- * A row containing NaN or +inf, or one whose entries are all masked (-inf; an entry
- * <= -2^97 counts as masked, reading 34), has no distribution: NaN. */
+ * m = max l, Z = sum exp(l - m), lse = m + ln Z, P(v) = exp(l(v) - m) / Z.
+ * A row containing NaN or +inf, or whose entries are all -inf, has no distribution:
+ * NaN.  (Terms with l = -inf add exp(-inf) = 0, SURVEY reading 20.) */
 double oracle_row_softmax(const or_dims* d, const void* L, int b, int slot, int i, double* P) {
   const int V = d->V;
   double m = -INFINITY;
@@ -52,13 +52,44 @@ double oracle_row_softmax(const or_dims* d, const void* L, int b, int slot, int 
     if (isnan(l) || l == INFINITY) return NAN;
     if (l > m) m = l;
   }
-  if (m <= -0x1p97) return NAN; /* all entries masked (-inf, or <= -2^97: DESIGN reading 34) */
+  if (m == -INFINITY) return NAN; /* all entries -inf */
   double Z = 0.0;
   for (int v = 0; v < V; ++v) Z += exp(oracle_logit(d, L, b, slot, i, v) - m);
   double lse = m + log(Z);
+  /* P = exp(l - m) / Z (not exp(l - lse): at |m| >> 1 the sum m + ln Z rounds ln Z away) */
   if (P)
-    for (int v = 0; v < V; ++v) P[v] = exp(oracle_logit(d, L, b, slot, i, v) - lse);
+    for (int v = 0; v < V; ++v) P[v] = exp(oracle_logit(d, L, b, slot, i, v) - m) / Z;
   return lse;
+}
+
+/* Input-domain validation (include/specbranch.h "Input domain", DESIGN reading 34) — a
+ * precondition of the library, checked here as its own step before the softmax: the
+ * maximum of the non-NaN entries must be finite with |m| < 2^24.  Order of the checks:
+ * +inf entry or no finite entry -> NONFINITE; |m| >= 2^24 -> RANGE; NaN -> NONFINITE. */
+uint32_t oracle_row_domain(const or_dims* d, const void* L, int b, int slot, int i) {
+  double m = -INFINITY;
+  int has_nan = 0, has_pinf = 0;
+  for (int v = 0; v < d->V; ++v) {
+    const double l = oracle_logit(d, L, b, slot, i, v);
+    if (isnan(l)) has_nan = 1;
+    else if (l == INFINITY) has_pinf = 1;
+    else if (l > m) m = l;
+  }
+  if (has_pinf || m == -INFINITY) return OR_ST_NONFINITE;
+  if (fabs(m) >= OR_LOGIT_RANGE) return OR_ST_RANGE;
+  if (has_nan) return OR_ST_NONFINITE;
+  return 0;
+}
+
+/* Validation, then the plain softmax of an in-domain row; NaN lse (and the status bit
+ * in *st) for a row that is not evaluated. */
+static double row_eval(const or_dims* d, const void* L, int b, int slot, int i, double* P, uint32_t* st) {
+  const uint32_t dom = oracle_row_domain(d, L, b, slot, i);
+  if (dom) {
+    if (st) *st |= dom;
+    return NAN;
+  }
+  return oracle_row_softmax(d, L, b, slot, i, P);
 }
 
 /* top-1 probability, smallest argmax id, entropy H = -sum Q ln Q (nats) of a q row
@@ -149,13 +180,13 @@ static void verify_one(const or_dims* d, const void* PL, const void* QL, const i
       const int ts = (i < s) ? 0 : k;  /* own token and uniform from the branch row    */
       const int64_t er = ((int64_t)b * K + ls) * R1 + i; /* physical row entry  */
       const int64_t et = ((int64_t)b * K + ts) * R1 + i; /* token-slot entry    */
-      double lse_p = oracle_row_softmax(d, PL, b, ls, i, P);
-      double lse_q = oracle_row_softmax(d, QL, b, ls, i, Q);
+      double lse_p = row_eval(d, PL, b, ls, i, P, &st);
+      double lse_q = row_eval(d, QL, b, ls, i, Q, &st);
       o->lse_p[er] = lse_p;
       o->lse_q[er] = lse_q;
       int acc = 0;
       if (isnan(lse_p) || isnan(lse_q)) {
-        st |= OR_ST_NONFINITE;
+        /* no distribution on one side: the test fails (reading 25); status set above */
       } else {
         q_row_confidence(d, QL, b, ls, i, Q, &o->top1_q[er], &o->top1_id_q[er], &o->entropy_q[er]);
         int x = tok[et];
@@ -224,10 +255,9 @@ static void verify_one(const or_dims* d, const void* PL, const void* QL, const i
   int y = -1;
   double mass = 0.0;
   if (ykind != 0) {
-    double lp = oracle_row_softmax(d, PL, b, yslot, yrow, P);
-    double lq = (ykind == 1) ? oracle_row_softmax(d, QL, b, yslot, yrow, Q) : 0.0;
+    double lp = row_eval(d, PL, b, yslot, yrow, P, &st);
+    double lq = (ykind == 1) ? row_eval(d, QL, b, yslot, yrow, Q, &st) : 0.0;
     if (isnan(lp) || isnan(lq)) {
-      st |= OR_ST_NONFINITE;
       ykind = 0;
     } else {
       /* norm(max(0, p - q)) at the first rejected position (P94, P554); bonus: p */
@@ -313,7 +343,7 @@ int oracle_confidence(const or_dims* d, const void* QL, const int32_t* tok, int 
     uint32_t ties = 0;
     for (int i = 0; i < G; ++i) {
       const int64_t e = ((int64_t)b * K + k) * G + i;
-      double lse = oracle_row_softmax(d, QL, b, k, i, Q);
+      double lse = row_eval(d, QL, b, k, i, Q, NULL);
       double top1 = NAN, H = NAN, tp = NAN, stat = NAN;
       int32_t id = -1;
       if (!isnan(lse)) {
@@ -366,7 +396,7 @@ int oracle_spawn(const or_dims* d, const void* QL, const int32_t* branch_pos, co
       o->btok[(int64_t)b * k_max + j] = -1;
       o->bprob[(int64_t)b * k_max + j] = NAN;
     }
-    double lse = oracle_row_softmax(d, QL, b, 0, s, Q);
+    double lse = row_eval(d, QL, b, 0, s, Q, NULL);
     uint32_t ties = 0;
     int k = 0;
     double c = NAN;
@@ -423,9 +453,9 @@ static void tree_one(const or_dims* d, const void* PL, const void* QL, const int
     const int pj = par[j];
     if (pj < -1 || pj >= j) { st |= OR_ST_BAD_PARENT; continue; }
     const int row = pj + 1;
-    double lp = oracle_row_softmax(d, PL, b, 0, row, P);
-    double lq = oracle_row_softmax(d, QL, b, 0, row, Q);
-    if (isnan(lp) || isnan(lq)) { st |= OR_ST_NONFINITE; continue; }
+    double lp = row_eval(d, PL, b, 0, row, P, &st);
+    double lq = row_eval(d, QL, b, 0, row, Q, &st);
+    if (isnan(lp) || isnan(lq)) continue;
     const int x = tk[j];
     if (x < 0 || x >= V) { st |= OR_ST_BAD_TOKEN; continue; }
     const double ui = (double)ub[j];
@@ -453,10 +483,9 @@ static void tree_one(const or_dims* d, const void* PL, const void* QL, const int
       /* y from row c+1: residual if c has children (all rejected), else bonus */
       int ykind = has_child ? 1 : 2, y = -1;
       double mass = 0.0;
-      double lp = oracle_row_softmax(d, PL, b, 0, c + 1, P);
-      double lq = ykind == 1 ? oracle_row_softmax(d, QL, b, 0, c + 1, Q) : 0.0;
+      double lp = row_eval(d, PL, b, 0, c + 1, P, &st);
+      double lq = ykind == 1 ? row_eval(d, QL, b, 0, c + 1, Q, &st) : 0.0;
       if (isnan(lp) || isnan(lq)) {
-        st |= OR_ST_NONFINITE;
         ykind = 0;
       } else {
         for (int v = 0; v < V; ++v) r[v] = (ykind == 1) ? fmax(0.0, P[v] - Q[v]) : P[v];

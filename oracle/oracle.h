@@ -37,9 +37,19 @@ extern "C" {
 #define OR_ST_GAMMA_CLAMPED 1u  /* gamma_b > G  -> clamped to G                  */
 #define OR_ST_BRANCH_CLAMPED 2u /* s_b > gamma_b or < 0 -> clamped               */
 #define OR_ST_BAD_TOKEN 4u      /* a path token outside [0, V): counted rejected */
-#define OR_ST_NONFINITE 8u      /* a row read has NaN/+inf, or is all -inf       */
+#define OR_ST_NONFINITE 8u      /* a row read has +inf, no finite entry, or NaN  */
 #define OR_ST_ZERO_RESID 16u    /* residual mass R == 0 after a rejection -> P   */
 #define OR_ST_BAD_PARENT 32u    /* tree: parent[j] outside [-1, j): node rejected */
+#define OR_ST_RANGE 64u         /* a row read is outside the input domain        */
+
+/* Input-domain validation (a separate, explicit step before any softmax; the library's
+ * documented precondition, include/specbranch.h "Input domain"): the maximum m of the
+ * row's non-NaN entries must be finite with |m| < 2^24.  Returns 0 (in domain),
+ * OR_ST_NONFINITE (+inf entry, or no finite entry, or NaN in an in-range row) or
+ * OR_ST_RANGE (finite maximum with |m| >= 2^24).  Rows that fail are not evaluated: the
+ * contract gives them NaN outputs and the status bit; oracle_row_softmax itself is the
+ * plain definition and is never bent to the kernel. */
+#define OR_LOGIT_RANGE 16777216.0 /* 2^24 */
 
 /* near-tie flags (oracle only): the decision is within the fp32 error band */
 #define OR_TIE_ACC_MASK 1u  /* |u - P/Q| < 1e-6 at some tested row             */
@@ -100,8 +110,12 @@ typedef struct {
 double oracle_logit(const or_dims* d, const void* L, int b, int slot, int i, int v);
 
 /* Softmax of one physical row in fp64 (two passes): writes P[V] and returns lse.
- * Returns NaN lse for a non-finite or all -inf row. */
+ * Plain definition: NaN lse for a row holding NaN or +inf, or whose entries are all
+ * -inf (no distribution); every other row, at any magnitude, gets its softmax. */
 double oracle_row_softmax(const or_dims* d, const void* L, int b, int slot, int i, double* P);
+
+/* The input-domain validation above for one row: 0, OR_ST_NONFINITE or OR_ST_RANGE. */
+uint32_t oracle_row_domain(const or_dims* d, const void* L, int b, int slot, int i);
 
 /* One verify-and-branch round for all B sequences; uniforms in fp32
  * (widened exactly).  rule: 0 = Eq. 9 (default), 1 = Algorithm 1 argmax r_b.

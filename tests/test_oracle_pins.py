@@ -101,6 +101,49 @@ def test_bf16_widening_is_exact(orc):
     assert np.allclose(P, ref, atol=1e-16)
 
 
+def test_softmax_is_plain_at_any_magnitude(orc):
+    """oracle_row_softmax is the plain definition for every finite row, whatever its
+    magnitude (the library's input domain is a separate validation step, DESIGN reading
+    34): a row at -2^98 with one entry 2^91 above the rest is a point mass; a row whose
+    entries are all equal is uniform; finfo(bf16).min masks contribute exactly 0."""
+    V = 6
+    L = np.full((1, 1, 2, V), -(2.0 ** 98), np.float32)
+    P, lse = orc.row_softmax(L, 0, 0, 0)
+    assert np.allclose(P, 1.0 / V, atol=1e-15) and lse == -(2.0 ** 98) + math.log(V)
+    L[0, 0, 0, 3] = -(2.0 ** 98) + 2.0 ** 91
+    P, _ = orc.row_softmax(L, 0, 0, 0)
+    assert P.tolist() == [0, 0, 0, 1.0, 0, 0]
+    assert orc.row_domain(L, 0, 0, 0) == orc.ST_RANGE
+    bmin = np.float32(-3.3895313892515355e38)  # finfo(bfloat16).min, exact in fp32
+    L2 = np.full((1, 1, 2, V), bmin, np.float32)
+    a = float(np.float32(math.log(3.0)))  # exactly the stored fp32 value
+    L2[0, 0, 0, :2] = [0.0, a]
+    P, lse = orc.row_softmax(L2, 0, 0, 0)
+    ea = math.exp(a)
+    assert np.allclose(P, [1 / (1 + ea), ea / (1 + ea), 0, 0, 0, 0], atol=1e-15)
+    assert abs(lse - math.log1p(ea)) < 1e-15
+    assert orc.row_domain(L2, 0, 0, 0) == 0
+
+
+def test_row_domain_classes(orc):
+    """The validation step's classes, in its stated order (oracle.h)."""
+    V = 4
+
+    def dom(vals):
+        L = np.zeros((1, 1, 1, V), np.float32)
+        L[0, 0, 0] = vals
+        return orc.row_domain(L, 0, 0, 0)
+
+    assert dom([0.0, 1.0, -np.inf, 2.0 ** 24 - 2]) == 0
+    assert dom([0.0, 1.0, 2.0 ** 24, 3.0]) == orc.ST_RANGE
+    assert dom([-(2.0 ** 24), -(2.0 ** 25), -np.inf, -np.inf]) == orc.ST_RANGE
+    assert dom([-np.inf] * 4) == orc.ST_NONFINITE
+    assert dom([0.0, np.inf, 1.0, 2.0]) == orc.ST_NONFINITE
+    assert dom([0.0, np.nan, 1.0, 2.0]) == orc.ST_NONFINITE
+    assert dom([np.nan, -(2.0 ** 30), 1e30, 2.0]) == orc.ST_RANGE  # range checked before NaN
+    assert dom([np.nan] * 4) == orc.ST_NONFINITE
+
+
 # ---------------------------------------------------------------- accept test (P94, S123-149)
 @pytest.mark.parametrize("case", GOLD["accept_prob"])
 def test_accept_prob_examples(orc, case):
@@ -487,16 +530,20 @@ def test_status_flags(orc):
     o = orc.verify(PL, PL, np.zeros((1, 1, 2), np.int32), np.zeros((1, 1, 2)), np.array([0.5]),
                    gamma=[1], branch_pos=[0])
     assert o["status"][0] & orc.ST_NONFINITE
-    # a row whose entries are all <= -2^97 is masked (DESIGN reading 34); one finite
-    # entry above it is a point mass
+    # input domain (DESIGN reading 34): a finite row whose maximum has |m| >= 2^24 is
+    # not evaluated (ST_RANGE, NaN outputs); masks below an in-range maximum are exact
     M = np.full_like(PL, -(2.0 ** 98))
     o = orc.verify(M, M, np.zeros((1, 1, 2), np.int32), np.zeros((1, 1, 2)), np.array([0.5]),
                    gamma=[1], branch_pos=[0])
-    assert o["status"][0] & orc.ST_NONFINITE
+    assert o["status"][0] == orc.ST_RANGE and np.isnan(o["lse_p"][0, 0, 0])
     M[..., 1] = -3.0
     o = orc.verify(M, M, np.ones((1, 1, 2), np.int32), np.zeros((1, 1, 2)), np.array([0.5]),
                    gamma=[1], branch_pos=[0])
-    assert not o["status"][0] & orc.ST_NONFINITE and o["n_acc"][0, 0] == 1
+    assert o["status"][0] == 0 and o["n_acc"][0, 0] == 1 and o["lse_p"][0, 0, 0] == -3.0
+    A = np.full_like(PL, -np.inf)
+    o = orc.verify(A, A, np.zeros((1, 1, 2), np.int32), np.zeros((1, 1, 2)), np.array([0.5]),
+                   gamma=[1], branch_pos=[0])
+    assert o["status"][0] == orc.ST_NONFINITE
     o = orc.verify(PL * 0, PL * 0, np.zeros((1, 1, 2), np.int32), np.zeros((1, 1, 2)), np.array([0.5]),
                    gamma=[5], branch_pos=[9])
     assert o["status"][0] & orc.ST_GAMMA_CLAMPED and o["status"][0] & orc.ST_BRANCH_CLAMPED
