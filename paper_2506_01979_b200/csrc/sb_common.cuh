@@ -6,6 +6,11 @@
 // so the rounding of ms cancels between a row's normaliser Z = sum e_v and any single
 // probability 2^(l_x c - MS) / Z evaluated later in fp64 with the same MS.  The
 // entropy uses S1 = sum e_v * a_v (a_v the exponent), H = ln2 * (log2 Z - S1 / Z).
+// Per-thread sums are fp32; every reduction across threads, warps and shards is fp64
+// (RowStat), and q rows keep the element that set the current offset out of the fp32
+// accumulators (LazyAcc / RowAcc "frozen" part), so the small terms of a peaked row are
+// never rounded against its dominant term: H of a near one-hot row stays within
+// 1e-5 |H| + 1e-7 nats (SURVEY §8.4 pass band).
 // All reductions are fixed-order trees (no float atomics): bit-reproducible.
 #pragma once
 #include <cuda_bf16.h>
@@ -27,10 +32,15 @@ constexpr float kMsEmpty = -1e30f;  // exponent offset of a state that has seen 
 constexpr float kRescaleP = 20.f;
 constexpr float kRescaleQ = 6.f;
 constexpr int kMaxG = 31;
-// Masked logits (DESIGN reading 34): an entry <= -2^97 counts as -inf.  The bf16 q-row
-// path clamps its inputs to -2^97 (one HMNMX2.NAN per two values, NaN kept) so the
-// entropy sum e*a never meets 0 * -inf; a row whose maximum is <= -2^97 has no
-// distribution (finish()).
+// Input domain (include/specbranch.h "Input domain"; DESIGN reading 34): a row is
+// evaluated iff its maximum logit m (NaN entries ignored) is finite with |m| < 2^24,
+// where the fp32 offset ms = fl(m c) is exact to within one unit of the exponent; other
+// entries are unrestricted (-inf, -FLT_MAX, finfo(bf16).min masks contribute exactly 0).
+constexpr float kLogitRange = 16777216.f;  // 2^24
+// The bf16 q-row path clamps its inputs to -2^97 (one HMNMX2.NAN per two values, NaN
+// kept) so the entropy sum e*a never meets 0 * -inf.  For any row with m > -2^97 this is
+// exact (the clamped entries contribute 0 either way); a row whose clamped maximum is
+// -2^97 is outside the domain or all -inf, told apart by row_has_finite() (rare path).
 constexpr float kMaskedLogit = -1.5845632502852868e29f;  // -2^97, exact in bf16 (0xf000)
 constexpr uint32_t kMaskedBf16x2 = 0xf000f000u;
 
@@ -119,14 +129,30 @@ struct Vec<float> {
 };
 
 // ------------------------------------------------------------------ online row state
-// Per-thread running state of one row.  NA independent accumulators for ILP and a
-// shorter fp32 summation chain.  kQ adds S1 (entropy) and the top-1 index.
+// Offset bookkeeping shared by the accumulators: the new offset clamped to the fp32
+// range (a maximum beyond 2.36e38 overflows m*c; such a row is outside the input domain
+// anyway) and the rescale exponent clamped to [-256, 0] (0 only when leaving the empty
+// state, whose sums are 0), so no 0 * inf can poison a finite row.
+__device__ __forceinline__ float offset_of(float m) {
+  return fminf(fmaxf(m * kC, -3.4028234663852886e38f), 3.4028234663852886e38f);
+}
+__device__ __forceinline__ float rescale_exp(float ms, float nms) {
+  return fminf(fmaxf(ms - nms, -256.f), 0.f);
+}
+
+// Per-thread running state of one row with the exact running maximum as offset.
+// NA independent accumulators for ILP and a shorter fp32 summation chain.  kQ adds S1
+// (entropy), the top-1 index and the frozen part: the element(s) equal to the current
+// maximum are kept in (zf, s1f) instead of z[] (their e = 2^(m c - ms) from an accurate
+// exp2 of the exactly representable residual m c - fl(m c)), and join z[] only when a
+// larger maximum arrives.
 template <bool kQ, int NA>
 struct RowAcc {
   float m;       // running max (raw logit units), -inf until the first finite value
   float ms;      // m * c (fp32), the exponent offset used by every term
   float z[NA];   // sum of 2^(l c - ms)
   float s1[kQ ? NA : 1];
+  float zf, s1f;  // kQ: frozen e and e*a of the maximum's element(s)
   int idx;       // smallest index attaining m (kQ only)
 
   __device__ __forceinline__ void init() {
@@ -136,34 +162,50 @@ struct RowAcc {
     for (int j = 0; j < NA; ++j) z[j] = 0.f;
 #pragma unroll
     for (int j = 0; j < (kQ ? NA : 1); ++j) s1[j] = 0.f;
+    zf = s1f = 0.f;
     idx = 0x7fffffff;
   }
 
   // raise the running max to nm (> m); rare after the first few vectors
   __device__ __forceinline__ void rescale(float nm) {
-    const float nms = nm * kC;
-    const float sc = ex2(ms - nms);  // 0 from the kMsEmpty sentinel
-    const float dd = ms - nms;
+    const float nms = offset_of(nm);
+    const float dd = rescale_exp(ms, nms);
+    const float sc = ex2(dd);  // 0 from the kMsEmpty sentinel
 #pragma unroll
     for (int j = 0; j < NA; ++j) {
-      if (kQ) s1[j] = sc * (s1[j] + z[j] * dd);
+      if (kQ) s1[j] = sc * fmaf(z[j], dd, s1[j]);
       z[j] *= sc;
+    }
+    if (kQ) {  // the previous maximum's element(s) become ordinary terms
+      s1[0] = fmaf(sc, fmaf(zf, dd, s1f), s1[0]);
+      z[0] = fmaf(sc, zf, z[0]);
     }
     m = nm;
     ms = nms;
   }
+  // kQ: move the n elements equal to the new maximum into the frozen part
+  __device__ __forceinline__ void freeze(int n) {
+    const float a = fmaf(m, kC, -ms);  // exact: the rounding residual of ms
+    const float e = exp2f(a);
+    zf = (float)n * e;
+    s1f = zf * a;
+  }
 
   // accumulate E values f[] whose first element has index base
   template <int E>
-  __device__ __forceinline__ void add(const float* f, float vmax, int base) {
+  __device__ __forceinline__ void add(const float* fin, float vmax, int base) {
+    float f[E];
+#pragma unroll
+    for (int j = 0; j < E; ++j) f[j] = fin[j];
     if (vmax > m) {
       rescale(vmax);
       if (kQ) {
-        int first = E;
+        int first = E, n = 0;
 #pragma unroll
         for (int j = E - 1; j >= 0; --j)
-          if (f[j] == vmax) first = j;
+          if (f[j] == vmax) { first = j; ++n; f[j] = kMaskedLogit; }
         idx = base + first;
+        freeze(n);
       }
     }
 #pragma unroll
@@ -178,7 +220,11 @@ struct RowAcc {
   __device__ __forceinline__ void add1(float f, int index) {
     if (f > m) {
       rescale(f);
-      if (kQ) idx = index;
+      if (kQ) {
+        idx = index;
+        freeze(1);
+        return;
+      }
     }
     const float a = fmaf(f, kC, -ms);
     const float e = ex2(a);
@@ -189,15 +235,18 @@ struct RowAcc {
 
 // Lazy-offset accumulator for the streaming (TMA) kernels.  Per group of N values:
 // the exact running max m (one FMNMX), the group tag of its first occurrence (Q rows;
-// one FSETP + SEL), and the exponent offset ms raised only when max*c - ms > 20, a
-// warp-uniform rare branch, so the hot path is unpack, FFMA, MUFU.EX2, FADD (+ FMNMX,
-// FFMA for the entropy sum of q rows).
+// one FSETP + SEL), and the exponent offset ms raised only when max*c - ms > 20 (p) / 6
+// (q), a warp-uniform rare branch, so the hot path is unpack, FFMA, MUFU.EX2, FADD (+
+// FMNMX, FFMA for the entropy sum of q rows).  q rows freeze the element(s) that raise
+// the offset (see RowAcc): for a peaked row that is its dominant element, so the fp32
+// sums z[] only ever hold terms far below it.
 template <bool kQ, int NA>
 struct LazyAcc {
   float m;
   float ms;
   float z[NA];
   float s1[kQ ? NA : 1];
+  float zf, s1f;
   int tag;
 
   __device__ __forceinline__ void init() {
@@ -207,20 +256,38 @@ struct LazyAcc {
     for (int j = 0; j < NA; ++j) z[j] = 0.f;
 #pragma unroll
     for (int j = 0; j < (kQ ? NA : 1); ++j) s1[j] = 0.f;
+    zf = s1f = 0.f;
     tag = -1;
   }
   __device__ __forceinline__ void rescale(float nms) {
-    const float dd = ms - nms;
+    const float dd = rescale_exp(ms, nms);
     const float sc = ex2(dd);
 #pragma unroll
     for (int j = 0; j < NA; ++j) {
       if (kQ) s1[j] = sc * fmaf(z[j], dd, s1[j]);
       z[j] *= sc;
     }
+    if (kQ) {
+      s1[0] = fmaf(sc, fmaf(zf, dd, s1f), s1[0]);
+      z[0] = fmaf(sc, zf, z[0]);
+    }
     ms = nms;
   }
+  // kQ, inside the rescale branch: the group's elements equal to its maximum cm (which
+  // set the new offset) leave f[] for the frozen part
   template <int N>
-  __device__ __forceinline__ void add(const float* f, int t) {
+  __device__ __forceinline__ void freeze(float* f, float cm) {
+    int n = 0;
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+      if (f[j] == cm) { f[j] = kMaskedLogit; ++n; }
+    const float a = fmaf(cm, kC, -ms);  // exact residual of ms = fl(cm c)
+    const float e = exp2f(a);
+    zf = (float)n * e;
+    s1f = zf * a;
+  }
+  template <int N>
+  __device__ __forceinline__ void add(float* f, int t) {
     float cm = f[0];
 #pragma unroll
     for (int j = 1; j + 1 < N; j += 2) cm = fmax3(cm, f[j], f[j + 1]);
@@ -229,12 +296,16 @@ struct LazyAcc {
   }
   // the same with the group maximum cm = max(f[0..N)) already known
   template <int N>
-  __device__ __forceinline__ void add_cm(const float* f, float cm, int t) {
+  __device__ __forceinline__ void add_cm(float* f, float cm, int t) {
     if (kQ) tag = (cm > m) ? t : tag;
     m = fmaxf(m, cm);
-    const bool up = cm * kC - ms > (kQ ? kRescaleQ : kRescaleP);
-    if (__any_sync(0xffffffffu, up)) {
-      if (up) rescale(cm * kC);
+    bool up = cm * kC - ms > (kQ ? kRescaleQ : kRescaleP);
+    while (__builtin_expect(__any_sync(0xffffffffu, up), 0)) {
+      if (up) {
+        rescale(offset_of(cm));
+        if (kQ) freeze<N>(f, cm);
+      }
+      up = false;
     }
 #pragma unroll
     for (int j = 0; j < N; ++j) {
@@ -271,7 +342,10 @@ struct LazyAcc {
     // rare; written as a loop so the compiler keeps it a branch instead of predicating
     // the rescale into every iteration
     while (__builtin_expect(__any_sync(0xffffffffu, up), 0)) {
-      if (up) rescale(cm * kC);
+      if (up) {
+        rescale(offset_of(cm));
+        if (kQ) freeze<N>(f, cm);
+      }
       up = false;
     }
     const float2 c2 = make_float2(kC, kC), n2 = make_float2(-ms, -ms);
@@ -320,8 +394,11 @@ __device__ __forceinline__ float acc_vecs_bf16(LazyAcc<kQ, 4>& a, const uint4* x
 }
 
 // Reduced row state (one per thread after folding accumulators, then across threads).
+// The sums are fp64 from here on: a row's dominant term (the frozen part of the thread
+// holding it) and everything else meet only in fp64 adds.
 struct RowStat {
-  float m, ms, z, s1;
+  float m, ms;
+  double z, s1;
   int idx;
 };
 
@@ -337,8 +414,8 @@ __device__ __forceinline__ RowStat fold_lazy(const LazyAcc<kQ, NA>& a) {
 #pragma unroll
     for (int j = 0; j < NA; ++j) s += a.s1[j];
   }
-  r.z = z;
-  r.s1 = s;
+  r.z = (double)z + (double)a.zf;
+  r.s1 = kQ ? (double)s + (double)a.s1f : 0.0;
   r.idx = 0x7fffffff;
   return r;
 }
@@ -348,8 +425,8 @@ __device__ __forceinline__ RowStat rowstat_empty() {
   RowStat r;
   r.m = -CUDART_INF_F;
   r.ms = kMsEmpty;
-  r.z = 0.f;
-  r.s1 = 0.f;
+  r.z = 0.0;
+  r.s1 = 0.0;
   r.idx = 0x7fffffff;
   return r;
 }
@@ -366,26 +443,36 @@ __device__ __forceinline__ RowStat fold(const RowAcc<kQ, NA>& a) {
 #pragma unroll
     for (int j = 0; j < NA; ++j) s += a.s1[j];
   }
-  r.z = z;
-  r.s1 = s;
+  r.z = (double)z + (double)a.zf;
+  r.s1 = kQ ? (double)s + (double)a.s1f : 0.0;
   r.idx = kQ ? a.idx : 0;
   return r;
+}
+
+// Bring a state's sums to the offset MS >= s.ms (fp64; the scale 2^(s.ms - MS) is 1
+// exactly for the state that holds MS).
+__device__ __forceinline__ void shift_to(RowStat& s, float MS) {
+  const float dd = rescale_exp(s.ms, MS);
+  const double sc = (double)ex2(dd);
+  s.s1 = sc * fma(s.z, (double)dd, s.s1);
+  s.z = sc * s.z;
+  s.ms = MS;
 }
 
 // Combine two states (called in a fixed tree order).  The exact max / first index
 // follow the larger value (ties: smaller index); the sums are brought to the larger
 // exponent offset.  Works for any offsets (lazy or exact), for empty states (kMsEmpty,
 // z = 0) and keeps NaN poison (z = NaN) of non-finite rows.
-__device__ __forceinline__ RowStat combine(const RowStat& a, const RowStat& b) {
+__device__ __forceinline__ RowStat combine(RowStat a, RowStat b) {
   RowStat r;
   const bool bw = b.m > a.m || (b.m == a.m && b.idx < a.idx);
   r.m = bw ? b.m : a.m;
   r.idx = bw ? b.idx : a.idx;
   const float MS = fmaxf(a.ms, b.ms);
-  const float da = a.ms - MS, db = b.ms - MS;
-  const float sa = ex2(da), sb = ex2(db);
-  r.z = a.z * sa + b.z * sb;
-  r.s1 = sa * fmaf(a.z, da, a.s1) + sb * fmaf(b.z, db, b.s1);
+  shift_to(a, MS);
+  shift_to(b, MS);
+  r.z = a.z + b.z;
+  r.s1 = a.s1 + b.s1;
   r.ms = MS;
   return r;
 }
@@ -402,20 +489,19 @@ __device__ __forceinline__ RowStat shfl_xor(const RowStat& s, int o) {
 
 // Warp reduction of one lane state's (ms, z, s1), m and idx left to the caller: every
 // lane first moves to the warp's largest offset (one ex2, as LazyAcc::rescale), then
-// plain sums — two independent 5-round trees instead of 5 rounds of combine() (5
-// shuffles + 2 ex2 each) on the consumers' per-unit critical path.
+// plain fp64 sums — two independent 5-round trees instead of 5 rounds of combine() on
+// the consumers' per-unit critical path.
 __device__ __forceinline__ RowStat warp_reduce_offsets(RowStat s) {
   float MS = s.ms;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) MS = fmaxf(MS, __shfl_xor_sync(0xffffffffu, MS, o));
-  const float dd = s.ms - MS, sc = ex2(dd);
-  float z = s.z * sc, s1 = sc * fmaf(s.z, dd, s.s1);
+  shift_to(s, MS);
+  double z = s.z, s1 = s.s1;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     z += __shfl_xor_sync(0xffffffffu, z, o);
     s1 += __shfl_xor_sync(0xffffffffu, s1, o);
   }
-  s.ms = MS;
   s.z = z;
   s.s1 = s1;
   return s;
@@ -524,25 +610,65 @@ __device__ __forceinline__ void stream_pair(const T* __restrict__ prow, const T*
   }
 }
 
-// Final per-row quantities from a reduced state.
+// Final per-row quantities from a reduced state.  st classifies the row (include/
+// specbranch.h "Input domain"): SB_ST_NONFINITE for a +inf entry or no finite entry
+// (m = +-inf), SB_ST_RANGE for a finite maximum with |m| >= 2^24, SB_ST_NONFINITE for a
+// NaN entry of an in-range row (z poisoned); only st == 0 rows have a distribution.
+// (bf16 q rows: a clamped maximum of exactly -2^97 is reported SB_ST_RANGE here; the
+// caller tells "all -inf" apart with row_has_finite().)
 struct RowOut {
   float MS;     // exponent offset (log2 units) of Z
-  float Z;      // sum 2^(l c - MS)
-  bool finite;  // row had a distribution (no NaN / +inf, not all -inf)
+  double Z;     // sum 2^(l c - MS)
+  int st;       // 0, SB_ST_NONFINITE or SB_ST_RANGE
+  bool finite;  // st == 0: the row has a distribution
 };
+__device__ __forceinline__ int row_class(float m, double z) {
+  if (m == CUDART_INF_F || m == -CUDART_INF_F) return SB_ST_NONFINITE;
+  if (!(fabsf(m) < kLogitRange)) return m == m ? SB_ST_RANGE : SB_ST_NONFINITE;
+  if (!(z > 0.0) || z == CUDART_INF) return SB_ST_NONFINITE;  // NaN entry (or no mass)
+  return 0;
+}
 __device__ __forceinline__ RowOut finish(const RowStat& r) {
   RowOut o;
   o.MS = r.ms;
   o.Z = r.z;
-  o.finite = (r.m > kMaskedLogit) && (r.m != CUDART_INF_F) && (r.z == r.z) && (r.z > 0.f) &&
-             (r.z != CUDART_INF_F);
+  o.st = row_class(r.m, r.z);
+  o.finite = (o.st == 0);
   return o;
 }
 
+// The normaliser as stored in the float4 row-state records (MS_p, Z_p, MS_q, Z_q): Z of
+// an evaluated row, NaN for SB_ST_NONFINITE, -1 for SB_ST_RANGE; z_class() reads it back.
+__device__ __forceinline__ float z_store(const RowOut& o) {
+  return o.finite ? (float)o.Z : (o.st == SB_ST_RANGE ? -1.f : CUDART_NAN_F);
+}
+__device__ __forceinline__ int z_class(float z) {
+  return z > 0.f ? 0 : (z == -1.f ? (int)SB_ST_RANGE : (int)SB_ST_NONFINITE);
+}
+// Per-token flag bits (workspace pflag): 1 accepted, 2 bad token, 4 / 8 the rows'
+// SB_ST_NONFINITE / SB_ST_RANGE.
+__device__ __forceinline__ uint8_t st_flags(int st) {
+  return (uint8_t)(((st & SB_ST_NONFINITE) ? 4 : 0) | ((st & SB_ST_RANGE) ? 8 : 0));
+}
+__device__ __forceinline__ int flags_st(uint32_t f) {
+  return ((f & 2u) ? (int)SB_ST_BAD_TOKEN : 0) | ((f & 4u) ? (int)SB_ST_NONFINITE : 0) |
+         ((f & 8u) ? (int)SB_ST_RANGE : 0);
+}
+
 // Probability of one token from the row state, in fp64: 2^(l_x c - MS) / Z.
-__device__ __forceinline__ double tok_prob(float lx, float MS, float Z) {
+__device__ __forceinline__ double tok_prob(float lx, float MS, double Z) {
   const double arg = (double)lx * (double)kC - (double)MS;  // exact product in fp64
-  return exp2(arg) / (double)Z;
+  return exp2(arg) / Z;
+}
+
+// Does a bf16 row hold any finite entry?  (The rare tie-break of a q row whose clamped
+// maximum is -2^97: out of the input domain if so, all -inf otherwise.)  One warp, any
+// alignment; returns the answer in every lane.
+__device__ __forceinline__ bool row_has_finite_bf16(const __nv_bfloat16* row, int V) {
+  const unsigned short* r = reinterpret_cast<const unsigned short*>(row);
+  bool any = false;
+  for (int v = threadIdx.x & 31; v < V && !any; v += 32) any = (__ldg(r + v) & 0x7f80u) != 0x7f80u;
+  return __any_sync(0xffffffffu, any);
 }
 
 // Warp-level inclusive scan (Kogge-Stone), fixed order.

@@ -17,9 +17,12 @@ struct SeqInfo {
 
 // Per physical row partial state of one vocabulary shard (sharded mode, a7).
 struct ShardRow {
-  float pm, pms, pz;        // p: max, exponent offset, sum
-  float qm, qms, qz, qs1;   // q: max, offset, sum, entropy sum
+  float pm, pms;            // p: max, exponent offset
+  double pz;                // p: sum
+  float qm, qms;            // q: max, offset
+  double qz, qs1;           // q: sum, entropy sum
   int qidx;                 // q: first global index of the shard max
+  int qfin;                 // q: the slice holds a finite entry (clamped-row tie-break)
 };
 
 // Workspace carve-up (all offsets 256-byte aligned).

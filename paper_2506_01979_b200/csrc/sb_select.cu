@@ -97,20 +97,20 @@ __global__ void __launch_bounds__(NT) k_select(SelParams p, bool vec_ok) {
     smp.qrow = QL + row_off(d, b, sh_slot, sh_row);
     smp.V = d.V;
     smp.vec_ok = vec_ok;
-    bool finite;
+    int cls;
     float MSp, Zp, MSq = 0.f, Zq = 1.f;
     if (kind == 2) {
       float m;
       const RowOut o = block_row_stats<T, NT>(smp.prow, d.V, vec_ok, red, &m);
-      MSp = o.MS; Zp = o.Z; finite = o.finite;
+      MSp = o.MS; Zp = (float)o.Z; cls = o.st;
     } else {
       const float4 rs = p.rowstat[ent(d, b, sh_slot, sh_row)];
       MSp = rs.x; Zp = rs.y; MSq = rs.z; Zq = rs.w;
-      finite = (Zp == Zp) && (Zq == Zq);
+      cls = z_class(Zp) | z_class(Zq);
     }
-    if (!finite) {
+    if (cls) {
       kind = 0;
-      if (tid == 0) sh_st |= SB_ST_NONFINITE;
+      if (tid == 0) sh_st |= cls;
     } else {
       smp.MSp = MSp; smp.iZp = 1.f / Zp; smp.MSq = MSq; smp.iZq = 1.f / Zq;
       smp.resid = (kind == 1);
@@ -216,7 +216,7 @@ struct SelSmem {
   uint64_t dfull[sNQ], dempty[sNQ], sfull[sNQ];
   Dec dec[sNQ];
   float rs[sNQ][4];
-  int ok[sNQ];
+  int ok[sNQ];  // row class of the sampled row(s): 0, SB_ST_NONFINITE, SB_ST_RANGE
   RowStat red[sCW];
   float seg[sNQ][sSegMax];
   int s_last;
@@ -403,9 +403,9 @@ __global__ void __launch_bounds__(sThreads, 1) k_select_tma(SelParams p) {
       double mass = 0.0;
       if (kind != 0) {
         const float MSp = S.rs[q][0], Zp = S.rs[q][1], MSq = S.rs[q][2], Zq = S.rs[q][3];
-        if (!S.ok[q]) {
+        if (S.ok[q]) {
           kind = 0;
-          st |= SB_ST_NONFINITE;
+          st |= S.ok[q];
         } else {
           const T* prow = PL + row_off(d, b, D.slot, D.row);
           const T* qrow = QL + row_off(d, b, D.slot, D.row);
@@ -576,17 +576,17 @@ __global__ void __launch_bounds__(sThreads, 1) k_select_tma(SelParams p) {
         for (int j = 1; j < sCW; ++j) r = combine(r, S.red[j]);
         const RowOut o = finish(r);
         S.rs[q][0] = o.MS; S.rs[q][1] = o.Z; S.rs[q][2] = 0.f; S.rs[q][3] = 1.f;
-        S.ok[q] = o.finite;
+        S.ok[q] = o.st;
       }
       consumer_sync(sCT);
     } else if (D.kind == 1 && tid == 0) {  // the epilogue reads the same state from S.rs
       S.rs[q][0] = D.rs.x; S.rs[q][1] = D.rs.y; S.rs[q][2] = D.rs.z; S.rs[q][3] = D.rs.w;
-      S.ok[q] = (D.rs.y == D.rs.y) && (D.rs.w == D.rs.w);
+      S.ok[q] = z_class(D.rs.y) | z_class(D.rs.w);
     }
     if (D.kind != 0) {
       const bool resid = (D.kind == 1);
       const float4 rsv = resid ? D.rs : make_float4(S.rs[q][0], S.rs[q][1], S.rs[q][2], S.rs[q][3]);
-      const bool ok = resid ? ((rsv.y == rsv.y) && (rsv.w == rsv.w)) : (S.ok[q] != 0);
+      const bool ok = resid ? (z_class(rsv.y) | z_class(rsv.w)) == 0 : (S.ok[q] == 0);
       const float MSp = rsv.x, MSq = rsv.z, kq = rsv.y / rsv.w;
       if (resid)
         seg_pass<T, true>(S, rp, q, nchunks, nvec_last, ok, MSp, MSq, kq);

@@ -70,16 +70,20 @@ __global__ void __launch_bounds__(128) k_shard_combine(ShardCombineParams p) {
     const bool tested = (k == 0) ? (r < in.L) : (r > in.s && r < in.L);
     if (read) {
       RowStat P = rowstat_empty(), Q = rowstat_empty();
+      int qfin = 0;
       for (int g = 0; g < p.nranks; ++g) {
         const ShardRow sr = reinterpret_cast<const ShardRow*>(p.gathered + g * p.rank_bytes)[e];
         RowStat a, c;
-        a.m = sr.pm; a.ms = sr.pms; a.z = sr.pz; a.s1 = 0.f; a.idx = 0;
+        a.m = sr.pm; a.ms = sr.pms; a.z = sr.pz; a.s1 = 0.0; a.idx = 0;
         c.m = sr.qm; c.ms = sr.qms; c.z = sr.qz; c.s1 = sr.qs1; c.idx = sr.qidx;
+        qfin |= sr.qfin;
         P = combine(P, a);
         Q = combine(Q, c);
       }
-      const RowOut po = finish(P), qo = finish(Q);
-      p.rowstat[e] = make_float4(po.MS, po.finite ? po.Z : CUDART_NAN_F, qo.MS, qo.finite ? qo.Z : CUDART_NAN_F);
+      const RowOut po = finish(P);
+      RowOut qo = finish(Q);
+      if (d.dtype == SB_BF16 && Q.m == kMaskedLogit && !qfin) qo.st = SB_ST_NONFINITE;  // all -inf (finish_q)
+      p.rowstat[e] = make_float4(po.MS, z_store(po), qo.MS, z_store(qo));
       if (tested) {
         p.lse_p[e] = po.finite ? (float)(((double)po.MS + log2((double)po.Z)) * LN2) : CUDART_NAN_F;
         p.lse_q[e] = qo.finite ? (float)(((double)qo.MS + log2((double)qo.Z)) * LN2) : CUDART_NAN_F;
@@ -117,9 +121,9 @@ __global__ void __launch_bounds__(128) k_shard_combine(ShardCombineParams p) {
     uint8_t fl = 0;
     float pt = CUDART_NAN_F, qt = CUDART_NAN_F, key = CUDART_NAN_F;
     const float4 rs = p.rowstat[ent(d, b, (r <= in.s) ? 0 : k, r)];
-    const bool finite = (rs.y == rs.y) && (rs.w == rs.w);
-    if (!finite) {
-      fl |= 4;
+    const int cls = z_class(rs.y) | z_class(rs.w);
+    if (cls) {
+      fl |= st_flags(cls);
     } else if (x < 0 || x >= p.v_total) {
       fl |= 2;
     } else {
@@ -157,12 +161,7 @@ __global__ void __launch_bounds__(128) k_shard_combine(ShardCombineParams p) {
     }
   }
   anyf = __reduce_or_sync(0xffffffffu, anyf);
-  if (lane == 0) {
-    int st = in.st;
-    if (anyf & 2u) st |= SB_ST_BAD_TOKEN;
-    if (anyf & 4u) st |= SB_ST_NONFINITE;
-    p.status[b] = st;
-  }
+  if (lane == 0) p.status[b] = in.st | flags_st(anyf);
 }
 
 // ---------------------------------------------------------------- select, local
@@ -273,7 +272,7 @@ __global__ void __launch_bounds__(256) k_shard_select_local(ShardSelParams p) {
   const int4 D = sdec;
   const int kind = D.z;
   const float4 rs = srs;
-  const bool ok = (rs.y == rs.y) && (rs.w == rs.w);
+  const bool ok = (z_class(rs.y) | (kind == 1 ? z_class(rs.w) : 0)) == 0;  // a bonus reads p only
   if (kind == 0 || !ok) {
     if (tid == 0) p.mass[b] = make_double2(0.0, 0.0);
     return;
@@ -322,9 +321,10 @@ __global__ void __launch_bounds__(128) k_shard_sample(ShardSelParams p) {
   int y = -1;
   double mass = 0.0;
   const float4 rs = kind ? p.rowstat[ent(d, b, D.w >> 16, D.w & 0xffff)] : make_float4(0.f, 1.f, 0.f, 1.f);
-  if (kind != 0 && !((rs.y == rs.y) && (rs.w == rs.w))) {
+  const int cls = kind ? (z_class(rs.y) | (kind == 1 ? z_class(rs.w) : 0)) : 0;  // a bonus reads p only
+  if (cls) {
     kind = 0;
-    st |= SB_ST_NONFINITE;
+    st |= cls;
   }
   if (kind != 0) {
     bool resid = (kind == 1);

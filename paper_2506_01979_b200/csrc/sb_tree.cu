@@ -89,8 +89,7 @@ __global__ void __launch_bounds__(NT) k_tree_rows(TreeParams p, bool vec_ok) {
   }
   if (threadIdx.x == 0) {
     const RowOut op = finish(sp), oq = finish(sq);
-    p.rowstat[(int64_t)b * R1 + r] = (op.finite && oq.finite) ? make_float4(op.MS, op.Z, oq.MS, oq.Z)
-                                                              : make_float4(0.f, CUDART_NAN_F, 0.f, CUDART_NAN_F);
+    p.rowstat[(int64_t)b * R1 + r] = make_float4(op.MS, z_store(op), oq.MS, z_store(oq));
   }
 }
 
@@ -123,8 +122,9 @@ __global__ void __launch_bounds__(NT) k_tree_select(TreeParams p, bool vec_ok) {
         pj = -3;  // never anybody's child
       } else {
         const float4 rs = p.rowstat[(int64_t)b * R1 + pj + 1];
-        if (!(rs.y == rs.y) || !(rs.w == rs.w)) {
-          st |= SB_ST_NONFINITE;
+        const int cls = z_class(rs.y) | z_class(rs.w);
+        if (cls) {
+          st |= cls;
         } else if (x < 0 || x >= d.V) {
           st |= SB_ST_BAD_TOKEN;
         } else {
@@ -176,19 +176,19 @@ __global__ void __launch_bounds__(NT) k_tree_select(TreeParams p, bool vec_ok) {
     smp.V = d.V;
     smp.vec_ok = vec_ok;
     float MSp, Zp, MSq = 0.f, Zq = 1.f;
-    bool finite;
+    int cls;
     if (kind == 2) {  // a leaf's p row: never streamed by k_tree_rows
       float m;
       const RowOut o = block_row_stats<T, NT>(smp.prow, d.V, vec_ok, sm.red, &m);
-      MSp = o.MS; Zp = o.Z; finite = o.finite;
+      MSp = o.MS; Zp = (float)o.Z; cls = o.st;
     } else {
       const float4 rs = p.rowstat[(int64_t)b * R1 + c + 1];
       MSp = rs.x; Zp = rs.y; MSq = rs.z; Zq = rs.w;
-      finite = (Zp == Zp) && (Zq == Zq);
+      cls = z_class(Zp) | z_class(Zq);
     }
-    if (!finite) {
+    if (cls) {
       kind = 0;
-      if (tid == 0) sh_st |= SB_ST_NONFINITE;
+      if (tid == 0) sh_st |= cls;
     } else {
       smp.MSp = MSp; smp.iZp = 1.f / Zp; smp.MSq = MSq; smp.iZq = 1.f / Zq;
       smp.resid = (kind == 1);

@@ -204,7 +204,7 @@ __device__ __forceinline__ void unit_epilogue(const RowsParams& p, const Unit& u
     uint8_t fl = 0;
     float pt = CUDART_NAN_F, qt = CUDART_NAN_F;
     if (!(po.finite && qo.finite)) {
-      fl |= 4;
+      fl |= st_flags(po.st | qo.st);
     } else if (x < 0 || x >= d.V) {
       fl |= 2;
     } else {
@@ -231,8 +231,7 @@ __device__ __forceinline__ void unit_epilogue(const RowsParams& p, const Unit& u
       const double Z = qo.Z;
       p.entropy_q[e] = conf_ok ? (float)(LN2 * (log2(Z) - (double)qs.s1 / Z)) : CUDART_NAN_F;
     }
-    p.rowstat[e] = make_float4(po.MS, po.finite ? po.Z : CUDART_NAN_F, qo.MS,
-                               qo.finite ? qo.Z : CUDART_NAN_F);
+    p.rowstat[e] = make_float4(po.MS, z_store(po), qo.MS, z_store(qo));
   }
   // completion: the CTA finishing the sequence decides n_k (first zero bit)
   sync();
@@ -255,8 +254,7 @@ __device__ __forceinline__ void unit_epilogue(const RowsParams& p, const Unit& u
         const int ts = (r < in.s) ? 0 : k;
         const uint8_t fl = __ldcg(p.pflag + ent(d, b, ts, r));
         if (fl & 1) mask |= 1u << r;
-        if (fl & 2) st |= SB_ST_BAD_TOKEN;
-        if (fl & 4) st |= SB_ST_NONFINITE;
+        st |= flags_st(fl);
       }
       const uint32_t rej = ~mask & (in.L >= 32 ? 0xffffffffu : ((1u << in.L) - 1));
       p.acc_mask[(int64_t)b * d.K + k] = mask;
@@ -390,22 +388,35 @@ __device__ __forceinline__ RowStat warp_part(const LazyAcc<kQ, 4>& a, const T* r
 }
 
 // Epilogue of one unit by one warp, with the token data already prefetched.
+// The class of a q row reduced from clamped bf16 inputs (LazyAcc::add_bf16): a clamped
+// maximum of exactly -2^97 means "outside the input domain" if the row holds a finite
+// entry and "all -inf" otherwise (one warp re-reads the row; never on a real row).
+template <typename T>
+__device__ __forceinline__ RowOut finish_q(const RowStat& qs, const T* qrow, int V) {
+  RowOut qo = finish(qs);
+  if constexpr (sizeof(T) == 2) {
+    if (qs.m == kMaskedLogit && !row_has_finite_bf16(reinterpret_cast<const __nv_bfloat16*>(qrow), V))
+      qo.st = SB_ST_NONFINITE;
+  }
+  return qo;
+}
+
 template <typename T>
 __device__ __forceinline__ void warp_epilogue(const RowsParams& p, const Unit& un, const RowStat& ps,
-                                              const RowStat& qs, int x, float lpx, float lqx, float uu,
-                                              int64_t et) {
+                                              const RowStat& qs, const T* qrow, int x, float lpx, float lqx,
+                                              float uu, int64_t et) {
   const Dims& d = p.d;
   const int lane = threadIdx.x & 31;
   const int b = un.b, slot = un.slot, i = un.i;
   const SeqInfo& in = un.in;
-  const RowOut po = finish(ps), qo = finish(qs);
+  const RowOut po = finish(ps), qo = finish_q<T>(qs, qrow, d.V);
   const bool branch_row = (slot == 0 && i == in.s);
   const int ntok = branch_row ? d.K : 1;
   if (lane < ntok) {
     uint8_t fl = 0;
     float pt = CUDART_NAN_F, qt = CUDART_NAN_F;
     if (!(po.finite && qo.finite)) {
-      fl |= 4;
+      fl |= st_flags(po.st | qo.st);
     } else if (x < 0 || x >= d.V) {
       fl |= 2;
     } else {
@@ -432,8 +443,7 @@ __device__ __forceinline__ void warp_epilogue(const RowsParams& p, const Unit& u
       const double Z = qo.Z;
       p.entropy_q[e] = conf_ok ? (float)(LN2 * (log2(Z) - (double)qs.s1 / Z)) : CUDART_NAN_F;
     }
-    p.rowstat[e] = make_float4(po.MS, po.finite ? po.Z : CUDART_NAN_F, qo.MS,
-                               qo.finite ? qo.Z : CUDART_NAN_F);
+    p.rowstat[e] = make_float4(po.MS, z_store(po), qo.MS, z_store(qo));
   }
   __syncwarp();
   int last = 0;
@@ -448,18 +458,18 @@ __device__ __forceinline__ void warp_epilogue(const RowsParams& p, const Unit& u
   __threadfence();
   // first rejection per branch: lane r holds row r's flags for every branch (loads
   // issued back to back), then one ballot per branch
-  uint32_t fw[4] = {0u, 0u, 0u, 0u};  // 3 bits per branch, 10 branches per word
+  uint32_t fw[4] = {0u, 0u, 0u, 0u};  // 4 flag bits per branch, 8 branches per word
   if (lane < in.L) {
 #pragma unroll 8
     for (int k = 0; k < d.K; ++k) {
       const uint32_t f = __ldcg(p.pflag + ent(d, b, (lane < in.s) ? 0 : k, lane));
-      fw[k / 10] |= (f & 7u) << (3 * (k % 10));
+      fw[k / 8] |= (f & 15u) << (4 * (k % 8));
     }
   }
   const uint32_t rowmask = in.L >= 32 ? 0xffffffffu : ((1u << in.L) - 1u);
   uint32_t anyf = 0;
   for (int k = 0; k < d.K; ++k) {
-    const uint32_t f = (fw[k / 10] >> (3 * (k % 10))) & 7u;
+    const uint32_t f = (fw[k / 8] >> (4 * (k % 8))) & 15u;
     const uint32_t mask = __ballot_sync(0xffffffffu, f & 1u) & rowmask;
     anyf |= f;
     if (lane == 0) {
@@ -489,10 +499,7 @@ __device__ __forceinline__ void warp_epilogue(const RowsParams& p, const Unit& u
     }
   }
   if (lane == 0) {
-    int st = in.st;
-    if (anyf & 2u) st |= SB_ST_BAD_TOKEN;
-    if (anyf & 4u) st |= SB_ST_NONFINITE;
-    p.status[b] = st;
+    p.status[b] = in.st | flags_st(anyf);
     p.cnt[b] = 0;  // leave the workspace re-usable
     if (p.ready) {  // fused step: the sequence's sample unit may start
       __threadfence();
@@ -662,16 +669,27 @@ __global__ void __launch_bounds__(C::ROWS_THREADS, 1) k_rows_tma(RowsParams p) {
       else qs.idx = resolve_argmax<C, T>(qmw, cand, qs.m, qrow, nvec_last, nchunks);
       if (p.partial) {  // a7: this shard's state, combined across shards later
         if (lane < ntok && has_tok) p.tokpart[et] = make_float2(lpx, lqx);
+        ShardRow r;
         if (lane == 0) {
-          ShardRow r;
           r.pm = ps.m; r.pms = ps.ms; r.pz = ps.z;
           r.qm = qs.m; r.qms = qs.ms; r.qz = qs.z; r.qs1 = qs.s1;
           r.qidx = (qs.idx == 0x7fffffff) ? qs.idx : qs.idx + p.v_offset;
-          p.rowpart[ent(d, un.b, un.slot, un.i)] = r;
+        }
+        {
+          // a clamped q maximum of -2^97 leaves "finite entry or all -inf" open (finish_q)
+          bool fin = qs.m > kMaskedLogit && qs.m < CUDART_INF_F;
+          if (sizeof(T) == 2 && qs.m == kMaskedLogit)
+            fin = row_has_finite_bf16(reinterpret_cast<const __nv_bfloat16*>(qrow), d.V);
+          else if (sizeof(T) == 4)
+            fin = qs.m > -CUDART_INF_F && qs.m < CUDART_INF_F;
+          if (lane == 0) {
+            r.qfin = fin;
+            p.rowpart[ent(d, un.b, un.slot, un.i)] = r;
+          }
         }
         continue;
       }
-      warp_epilogue<T>(p, un, ps, qs, x, lpx, lqx, uu, et);
+      warp_epilogue<T>(p, un, ps, qs, qrow, x, lpx, lqx, uu, et);
     }
     return;
   }
@@ -1019,7 +1037,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) k_step_tma(StepParams sp) {
         ps = warp_reduce_state(ps);  // idx: p's unused, q's resolved below
         qs = warp_reduce_state(qs);
         qs.idx = resolve_argmax<C, T>(qmw, cand, qs.m, qrow, nvec_last, nchunks);
-        warp_epilogue<T>(p, un, ps, qs, x, lpx, lqx, uu, et);
+        warp_epilogue<T>(p, un, ps, qs, qrow, x, lpx, lqx, uu, et);
         continue;
       }
       // ---- sample unit
@@ -1032,9 +1050,10 @@ __global__ void __launch_bounds__(C::THREADS, 1) k_step_tma(StepParams sp) {
       double mass = 0.0;
       if (kind != 0) {
         const float4 rs = (kind == 1) ? D.rs : S.brs[dq.stage];
-        if (!((rs.y == rs.y) && (rs.w == rs.w))) {
+        const int cls = z_class(rs.y) | z_class(rs.w);
+        if (cls) {
           kind = 0;
-          st |= SB_ST_NONFINITE;
+          st |= cls;
         } else {
           const T* prow = PL + row_off(d, b, D.slot, D.row);
           const T* qrow = QL + row_off(d, b, D.slot, D.row);
@@ -1170,11 +1189,11 @@ __global__ void __launch_bounds__(C::THREADS, 1) k_step_tma(StepParams sp) {
 #pragma unroll
       for (int j = 1; j < C::CW; ++j) r = combine(r, S.red[j]);
       const RowOut o = finish(r);
-      if (tid == 0) S.brs[dq.stage] = make_float4(o.MS, o.finite ? o.Z : CUDART_NAN_F, 0.f, 1.f);
+      if (tid == 0) S.brs[dq.stage] = make_float4(o.MS, z_store(o), 0.f, 1.f);
       consumer_sync(C::CT);
       step_seg_pass<C, T, false>(S, rp, seg, nchunks, nvec_last, o.finite, o.MS, 0.f, 0.f);
     } else if (D.kind == 1) {
-      const bool ok = (D.rs.y == D.rs.y) && (D.rs.w == D.rs.w);
+      const bool ok = (z_class(D.rs.y) | z_class(D.rs.w)) == 0;
       step_seg_pass<C, T, true>(S, rp, seg, nchunks, nvec_last, ok, D.rs.x, D.rs.z, D.rs.y / D.rs.w);
     }
     __syncwarp();

@@ -16,7 +16,6 @@ import oracle
 from paper_2506_01979_b200 import api, synth
 
 REL, ABS = 1e-5, 1e-7
-ENT_ABS = 1e-6
 
 
 def gpu_run(inp: dict, rule=0, adaptive=False, eps=0.2, k_max=6, fused=True):
@@ -41,6 +40,16 @@ def _close(g, r, rel=REL, ab=ABS):
     ok = bool(np.all(err <= rel * np.abs(r[m]) + ab)) if m.any() else True
     relerr = float(np.max(err / np.maximum(np.abs(r[m]), 1e-30))) if m.any() else 0.0
     return nan_ok and ok, relerr
+
+
+def _band(g, r):
+    """max |gpu - ref| / (1e-5 |ref| + 1e-7): <= 1 means inside the pass band."""
+    g = np.asarray(g, np.float64)
+    r = np.asarray(r, np.float64)
+    m = ~np.isnan(r) & ~np.isnan(g)
+    if not m.any():
+        return 0.0
+    return float(np.max(np.abs(g[m] - r[m]) / (REL * np.abs(r[m]) + ABS)))
 
 
 def compare(g: dict, o: dict, sel=None, strict=True):
@@ -74,14 +83,11 @@ def compare(g: dict, o: dict, sel=None, strict=True):
             if err.size and err.max() > REL:
                 rep["fail"].append((k + "_tol", float(err.max())))
     for k in ("top1_q", "entropy_q", "p_tok", "q_tok"):
-        # entropy (nats) also gets an absolute 1e-6: H = ln2 (log2 Z - S1/Z) from fp32 sums,
-        # and the register-staged fallback rebases S1 at every new running maximum
-        # (measured: 4e-7 absolute on an H = 0.018 row); DESIGN reading 30
-        ab = ENT_ABS if k == "entropy_q" else ABS
-        ok, relerr = _close(gs[k], o[k], ab=ab)
+        ok, relerr = _close(gs[k], o[k])
         rep[f"max_rel_{k}"] = relerr
+        rep[f"max_band_{k}"] = _band(gs[k], o[k])
         if not ok:
-            bad = ~np.isclose(gs[k].astype(np.float64), o[k], rtol=REL, atol=ab, equal_nan=True)
+            bad = ~np.isclose(gs[k].astype(np.float64), o[k], rtol=REL, atol=ABS, equal_nan=True)
             fail(k, np.where(bad.reshape(len(sel), -1).any(axis=1))[0])
     # discrete
     ok_id = gs["top1_id_q"] == o["top1_id_q"]
@@ -98,8 +104,9 @@ def compare(g: dict, o: dict, sel=None, strict=True):
     ot = (gs["out_tok"] != o["out_tok"]).any(axis=1) & ~t_dec & ~t_samp
     fail("out_tok", np.where(ot)[0])
     same = (gs["y_kind"] == o["y_kind"]) & ~t_dec & ~t_samp
-    ok, relerr = _close(gs["resid_mass"][same], o["resid_mass"][same], REL, 1e-6)
+    ok, relerr = _close(gs["resid_mass"][same], o["resid_mass"][same])
     rep["max_rel_resid_mass"] = relerr
+    rep["max_band_resid_mass"] = _band(gs["resid_mass"][same], o["resid_mass"][same])
     if not ok:
         rep["fail"].append(("resid_mass", relerr))
     rep["exact_seq"] = int((~t_dec & ~t_samp).sum())

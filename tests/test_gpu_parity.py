@@ -169,7 +169,7 @@ def test_special_values_and_status():
 
     from parity_util import compare, gpu_run, oracle_for
 
-    c = cfg("c2", V=3000, B=12, K=2, G=4, layout="fixed")
+    c = cfg("c2", V=3000, B=16, K=2, G=4, layout="fixed")
     inp = synth.generate(c, device="cuda", seed=9)
     inp["PL"][0, 0, 1, 17] = float("nan")
     inp["QL"][1, 0, 0, 5] = float("inf")
@@ -183,16 +183,24 @@ def test_special_values_and_status():
     inp["branch_pos"][7] = 3
     inp["gamma"][7] = 2
     inp["QL"][8, 0, 2, :100] = float("-inf")  # masked draft logits
-    inp["QL"][9, 0, 1, :] = -(2.0 ** 98)  # finite but all <= -2^97: masked (reading 34)
+    inp["QL"][9, 0, 1, :] = -(2.0 ** 98)  # finite, max outside the input domain (reading 34)
     inp["PL"][10, 0, 0, ::2] = float("-inf")  # half-masked target and draft rows
     inp["QL"][10, 0, 0, 1::3] = float("-inf")
-    inp["QL"][11, 0, 1, 3:] = -(2.0 ** 97)  # masked tail at exactly -2^97
+    inp["QL"][11, 0, 1, 3:] = -(2.0 ** 97)  # masked tail at exactly -2^97 (in domain)
+    bmin = torch.finfo(torch.bfloat16).min
+    inp["QL"][12, 1, 2, :] = float("-inf")  # an all -inf draft row (bf16 clamp tie-break)
+    inp["QL"][13, 1, 2, :] = bmin  # a draft row fully masked with finfo(bf16).min: RANGE
+    inp["PL"][14, 0, 3, 5::2] = bmin  # finfo.min masks under an in-range maximum: exact
+    inp["QL"][14, 0, 3, 7::3] = bmin
+    inp["PL"][15, 0, 2, :] = 3.0e7  # a target row whose maximum is >= 2^24: RANGE
     g, _, _ = gpu_run(inp)
     inp_np = synth.to_numpy_inputs(inp)
     o = oracle_for(inp_np, inp_np["gamma"])
     compare(g, o)
-    assert g["status"][0] & 8 and g["status"][4] & 4 and g["status"][6] & 1 and g["status"][7] & 2
-    assert g["status"][9] & 8 and not g["status"][10] & 8 and not g["status"][11] & 8
+    st = g["status"]
+    assert st[0] & 8 and st[4] & 4 and st[6] & 1 and st[7] & 2
+    assert st[9] & 64 and not st[10] & 72 and not st[11] & 72
+    assert st[12] == 8 and st[13] == 64 and st[14] == 0 and st[15] == 64
 
 
 @pytest.mark.slow
