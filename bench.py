@@ -476,7 +476,13 @@ def run_next(args, rank, world, local_rank):
         cl = torch.randint(1, G + 2, (B,), generator=g, dtype=torch.int32).to(dev)
         yk = torch.ones(B, dtype=torch.int32, device=dev)
         bpos = torch.zeros(B, dtype=torch.int32, device=dev)
-        fn = lambda s_: api.sb_kv_rollback(kv, bpos, sel, cl, yk, out_kv=out, stream=s_)  # noqa: E731
+        # keep mask of the round (as sb_select_branch writes it): slot 0 below s_b = 0 is
+        # empty, the selected slot (0 on rollback) keeps positions i < n_b
+        n_b = (cl - yk.ne(0).to(torch.int32)).clamp(min=0)
+        bits = ((1 << n_b.to(torch.int64)) - 1).to(torch.int32)
+        keep = torch.zeros((B, K), dtype=torch.int32, device=dev)
+        keep[torch.arange(B, device=dev), sel.clamp(min=0).long()] = bits
+        fn = lambda s_: api.sb_kv_rollback(kv, keep, out_kv=out, stream=s_)  # noqa: E731
         moved = int((cl - 1).clamp(min=0).sum())
         nbytes, units, unit = 2 * moved * row, moved, "KV positions kept/s"
         work = f"f2 KV rollback, batch {B}, K = {K}, gamma = {G}, {row} B per position (out of place)"

@@ -267,16 +267,17 @@ sb_status sb_spawn_branches(const sb_dims* d, const void* q_logits, const int32_
  * sb_kv_rollback — keep the surviving branch's draft KV rows (P241,
  * shared-prefix KV P220).  kv: the draft KV of the round, [B][K][G+1] positions of
  * row_bytes each (16-byte multiple) at row_stride_bytes, token-slot layout (as tok).
- * With the decisions of sb_select_branch (sel_k, commit_len, y_kind) and branch_pos
- * (NULL -> 0): the committed draft positions i < n_b = commit_len[b] - [y_kind[b] != 0]
- * come from slot ts(k*, i) = (i < s_b ? 0 : k*) (slot 0 when k* = -1).
- *   out_kv != NULL: out_kv[b][i] (layout [B][G+1] at row_stride_bytes) = that row, i < n_b;
- *   out_kv == NULL: in place, rows i in [s_b, n_b) of slot k* are moved into slot 0.
- * Rows at i >= n_b are not touched (they are the rolled-back positions).
+ * keep_mask [B][K] (device, from sb_select_branch): bit i of keep_mask[b][k] set iff the
+ * draft token at slot k, position i is committed; at most one slot per position (the
+ * slot ts(k*, i) = (i < s_b ? 0 : k*) of the clamped layout, slot 0 when k* = -1).
+ *   out_kv != NULL: out_kv[b][i] (layout [B][G+1] at row_stride_bytes) = that row;
+ *   out_kv == NULL: in place, kept rows of slots k > 0 are moved into slot 0.
+ * Positions with no kept bit are not touched (the rolled-back positions).
+ * Errors: SB_ERR_INVALID_ARG (dims, NULL kv / keep_mask, row sizes or pointers not
+ * 16-byte multiples / aligned), SB_ERR_CUDA (launch).
  */
 sb_status sb_kv_rollback(int32_t B, int32_t K, int32_t G, const void* kv, int64_t row_bytes,
-                         int64_t row_stride_bytes, const int32_t* branch_pos, const int32_t* sel_k,
-                         const int32_t* commit_len, const int32_t* y_kind, void* out_kv,
+                         int64_t row_stride_bytes, const uint32_t* keep_mask, void* out_kv,
                          sb_stream_t stream);
 
 /*

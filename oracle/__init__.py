@@ -248,16 +248,19 @@ def tree_verify(PL, QL, parent, tok, u, us, nthreads=0, V=None):
     return out
 
 
-def kv_rollback(kv, branch_pos, sel_k, commit_len, y_kind):
+def kv_rollback(kv, branch_pos, gamma, sel_k, commit_len, y_kind):
     """Plain gather of the committed draft KV rows: out[b][i] =
-    kv[b][ts(k*, i)][i] for i < commit_len - [y sampled], ts(k, i) = (i < s_b ? 0 : k).
-    Rows past n_b are left as NaN-free zeros in the returned array."""
+    kv[b][ts(k*, i)][i] for i < n_b = commit_len - [y sampled], ts(k, i) = (i < s_b ? 0
+    : k), with gamma_b and s_b clamped as the verify contract clamps them (SURVEY §8.0
+    Shapes: gamma_b to [0, G], s_b to [0, gamma_b]).  Rows past n_b are zeros."""
     B, K, R1 = kv.shape[:3]
+    G = R1 - 1
     out = np.zeros((B, R1) + kv.shape[3:], dtype=kv.dtype)
     for b in range(B):
         n = int(commit_len[b]) - (1 if y_kind[b] != 0 else 0)
         ks = int(sel_k[b])
-        s = int(branch_pos[b])
+        g = G if gamma is None else min(max(int(gamma[b]), 0), G)
+        s = min(max(int(branch_pos[b]), 0), g)
         for i in range(n):
             slot = 0 if (i < s or ks < 0) else ks
             out[b, i] = kv[b, slot, i]

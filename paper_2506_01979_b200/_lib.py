@@ -48,7 +48,7 @@ _SIGS = {
     "sb_draft_confidence": ([_D, _P, _P, _I, _F, _F, ctypes.c_int32] + [_P] * 10 + [_S, _P], _I),
     "sb_verify_select": ([_D] + [_P] * 7 + [_I] + [_P] * 22 + [_S, _P], _I),
     "sb_spawn_branches": ([_D, _P, _P, _P, _I, ctypes.c_int32] + [_P] * 4 + [_P], _I),
-    "sb_kv_rollback": ([_I, _I, _I, _P, ctypes.c_int64, ctypes.c_int64] + [_P] * 5 + [_P], _I),
+    "sb_kv_rollback": ([_I, _I, _I, _P, ctypes.c_int64, ctypes.c_int64, _P, _P, _P], _I),
     "sb_tree_workspace_bytes": ([_D], _S),
     "sb_hrad_workspace_bytes": ([_I, _I], _S),
     "sb_hrad_predict": ([_I, _I, _I] + [_P] * 12 + [_P, _S, _P], _I),

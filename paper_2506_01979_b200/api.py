@@ -151,13 +151,26 @@ def sb_spawn_branches(d, q_logits, branch_pos, tok, mode, k_max, k_out, branch_t
         _ptr(branch_prob, F32, "branch_prob"), _ptr(conf, F32, "conf"), _stream(stream)), "sb_spawn_branches")
 
 
-def sb_kv_rollback(kv: torch.Tensor, branch_pos, sel_k, commit_len, y_kind, out_kv=None, stream=None):
-    """kv: [B][K][G+1][...] (any dtype, row = the trailing dims, contiguous)."""
+def sb_kv_rollback(kv: torch.Tensor, keep_mask, out_kv=None, stream=None):
+    """kv: [B][K][G+1][...] device tensor (any dtype); the trailing dims of a position
+    must be contiguous, positions may be strided (e.g. a slice of a larger cache).
+    keep_mask: int32 [B][K] from sb_select_branch.  out_kv: [B][G+1][...] or None."""
+    if kv.dim() < 4:
+        raise ValueError("kv must be [B][K][G+1][...]")
     B, K, R1 = kv.shape[:3]
+    _ptr(kv[0, 0, 0], None, "kv position")  # device + contiguous trailing dims
+    if not kv.is_cuda or kv.stride(1) != R1 * kv.stride(2) or kv.stride(0) != K * kv.stride(1):
+        raise ValueError("kv: expected [B][K][G+1] positions at a uniform stride on the device")
     row = kv[0, 0, 0].numel() * kv.element_size()
+    stride = kv.stride(2) * kv.element_size()
+    if out_kv is not None:
+        if tuple(out_kv.shape) != (B, R1) + tuple(kv.shape[3:]) or out_kv.dtype != kv.dtype:
+            raise ValueError("out_kv must be [B][G+1][...] of kv's dtype")
+        _ptr(out_kv[0, 0], None, "out_kv position")
+        if out_kv.stride(1) * out_kv.element_size() != stride or out_kv.stride(0) != R1 * out_kv.stride(1):
+            raise ValueError("out_kv: positions must use kv's position stride")
     L.check(L.lib().sb_kv_rollback(
-        B, K, R1 - 1, ctypes.c_void_p(kv.data_ptr()), row, row, _ptr(branch_pos, I32, "branch_pos"),
-        _ptr(sel_k, I32, "sel_k"), _ptr(commit_len, I32, "commit_len"), _ptr(y_kind, I32, "y_kind"),
+        B, K, R1 - 1, ctypes.c_void_p(kv.data_ptr()), row, stride, _ptr(keep_mask, I32, "keep_mask"),
         None if out_kv is None else ctypes.c_void_p(out_kv.data_ptr()), _stream(stream)), "sb_kv_rollback")
 
 
@@ -259,7 +272,10 @@ class StepBuffers:
 
 
 def conf_dims(d: L.sb_dims) -> L.sb_dims:
-    """Slot-0 view of a [B][K][G+1] draft tensor (the drafted path before branching)."""
+    """Slot-0 view of a [B][K][G+1] draft tensor (the drafted path before branching).
+    Unsharded dims only (verify_step rejects adaptive gamma on vocabulary shards)."""
+    if d.v_total and d.v_total != d.V:
+        raise ValueError("conf_dims: vocabulary-shard dims (the confidence pass is unsharded)")
     return L.sb_dims(d.B, 1, d.G, d.V, 0, d.V, d.row_stride,
                      d.seq_stride or d.K * (d.G + 1) * d.row_stride, d.dtype, 0)
 
@@ -277,6 +293,10 @@ def verify_step(d: L.sb_dims, inp: dict, buf: StepBuffers, rule: int = SB_SELECT
     calls.
     """
     gamma = inp["gamma"]
+    if adaptive and (comm is not None or (d.v_total and d.v_total != d.V)):
+        # sb_draft_confidence scores whole draft rows; a vocabulary shard would score its
+        # slice only and every rank would take a different gamma (ADVICE r1)
+        raise ValueError("adaptive gamma is not supported on vocabulary shards (sb_draft_confidence is unsharded)")
     if adaptive:
         sb_draft_confidence(conf_dims(d), inp["QL"], None, SB_CONF_TOP1, eps, 1.0, k_max,
                             buf.c_top1, buf.c_id, buf.c_ent, None, buf.c_stat, buf.c_stop,

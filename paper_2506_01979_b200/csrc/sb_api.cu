@@ -5,15 +5,16 @@
 #include "sb_host.h"
 
 namespace sb {
+int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev;
+}
+// queried per call (the driver caches device attributes): a process may drive several GPUs
 int num_sms() {
-  static int n = 0;
-  if (n == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
+  int n = 0;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, current_device());
+  return n > 0 ? n : 148;
 }
 bool tma_disabled() {
   const char* e = getenv("SB_DISABLE_TMA");

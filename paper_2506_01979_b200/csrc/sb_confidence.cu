@@ -270,12 +270,7 @@ __global__ void k_conf_empty(int n, int* stop, int* k_next, int* gamma_next) {
 
 template <typename T, int NT, int U>
 static sb_status launch_conf(const ConfParams& p, bool vok, cudaStream_t s) {
-  static int g = 0;
-  if (g == 0) {
-    int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_conf<T, NT, U>, NT, 0);
-    g = std::max(1, occ) * num_sms();
-  }
+  const int g = full_grid<k_conf<T, NT, U>>(NT);
   const int64_t units = (int64_t)p.d.B * p.d.K * p.d.G;
   const int grid = (int)std::min<int64_t>(g, units);
   k_conf<T, NT, U><<<grid, NT, 0, s>>>(p, vok);
@@ -284,14 +279,8 @@ static sb_status launch_conf(const ConfParams& p, bool vok, cudaStream_t s) {
 
 template <typename T>
 static sb_status launch_conf_tma(const ConfParams& p, cudaStream_t s) {
-  static bool attr = false;
   const int smem = (int)sizeof(ConfSmem);
-  if (!attr) {
-    if (cudaFuncSetAttribute(k_conf_tma<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
-        cudaSuccess)
-      return SB_ERR_CUDA;
-    attr = true;
-  }
+  if (ensure_smem<k_conf_tma<T>>(smem) != cudaSuccess) return SB_ERR_CUDA;
   const int64_t units = (int64_t)p.d.B * p.d.K * p.d.G;
   const int grid = (int)std::min<int64_t>(num_sms(), units);
   return cuda_status(launch_pdl(k_conf_tma<T>, dim3(grid), dim3(cThreads), smem, s, p));

@@ -5,6 +5,8 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "sb_common.cuh"
 
 namespace sb {
@@ -135,7 +137,29 @@ inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t
   return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
 }
 
-int num_sms();        // cached cudaDevAttrMultiProcessorCount of the current device
+int num_sms();        // cudaDevAttrMultiProcessorCount of the current device
 bool tma_disabled();  // SB_DISABLE_TMA=1 forces the register-staged kernels (tests)
+int current_device();
+
+// Dynamic shared memory opt-in of kernel K on the current device.  Function attributes
+// are per device, so the "done" record is a per-kernel bitmask of devices (atomic: the
+// entry points are callable from several host threads); a race only repeats the call.
+template <auto K>
+inline cudaError_t ensure_smem(int bytes) {
+  static std::atomic<uint64_t> done{0};
+  const uint64_t bit = 1ull << (current_device() & 63);
+  if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_release);
+  return e;
+}
+
+// Resident CTAs per SM x SMs for a static-smem kernel on the current device.
+template <auto K>
+inline int full_grid(int threads) {
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, K, threads, 0);
+  return (occ > 0 ? occ : 1) * num_sms();
+}
 
 }  // namespace sb

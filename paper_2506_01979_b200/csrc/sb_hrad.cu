@@ -367,11 +367,8 @@ static bool make_map(CUtensorMap* m, const void* base, int rows, int cols, int b
 // Cluster width along the row tiles (W1 multicast) and K splits per tile: as many
 // splits as fill the SMs (one CTA each), <= k-blocks, <= 16 (the tail sums them).
 static int hrad_splits(int mtiles, int nkb) {
-  static int force = -1;  // SB_HRAD_SPLITS: experiment override
-  if (force < 0) {
-    const char* e = getenv("SB_HRAD_SPLITS");
-    force = e ? std::max(1, atoi(e)) : 0;
-  }
+  const char* e = getenv("SB_HRAD_SPLITS");  // experiment override
+  const int force = e ? std::max(1, atoi(e)) : 0;
   if (force > 0) return std::min(nkb, force);
   // fill the SMs, but no more than 18 splits (32 for a single 256-row block): the tail
   // reads S x B x 1 KB of partials (measured with the register-sliced tail: B = 2048
@@ -402,14 +399,8 @@ extern "C" sb_status sb_hrad_predict(int32_t B, int32_t Dz, int32_t G, const voi
     return SB_ERR_UNSUPPORTED;
   if ((uintptr_t)workspace % 16) return SB_ERR_INVALID_ARG;
   if (workspace_bytes < sb_hrad_workspace_bytes(B, Dz)) return SB_ERR_WORKSPACE;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(k_hrad, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kHradSmem) != cudaSuccess ||
-        cudaFuncSetAttribute(k_hrad_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTailSmem) !=
-            cudaSuccess)
-      return SB_ERR_CUDA;
-    attr = true;
-  }
+  if (ensure_smem<k_hrad>((int)kHradSmem) != cudaSuccess || ensure_smem<k_hrad_tail>((int)kTailSmem) != cudaSuccess)
+    return SB_ERR_CUDA;
   const int mtiles = (B + kTP * kHM - 1) / (kTP * kHM);
   CUtensorMap tmZ, tmW1;
   if (!make_map(&tmZ, z, B, Dz, kHM) || !make_map(&tmW1, w1, kHN, Dz, kHN)) return SB_ERR_CUDA;

@@ -1,10 +1,11 @@
 // sb_kv.cu — sb_kv_rollback: keep the surviving branch's draft KV rows and drop the
 // rest (PAPER P241 "discarding all non-selected branches and their
-// associated KV-Cache", shared-prefix KV P220).  A pure HBM gather: for sequence b the
-// committed draft positions i < n_b (n_b = commit_len - [y sampled]) live in token slot
-// ts(k*, i) = (i < s_b ? 0 : k*); they are copied to out[b][i] (out-of-place), or into
-// slot 0 in place (out = NULL: rows i >= s_b of slot k* move to slot 0, the shared
-// prefix already is slot 0).  16-byte vectors, 4 in flight per thread.
+// associated KV-Cache", shared-prefix KV P220).  A pure HBM gather driven by the keep
+// mask of sb_select_branch (bit i of keep_mask[b][k] set iff the draft token at slot k,
+// position i is committed — at most one slot per position, already reflecting the
+// clamped gamma_b / s_b layout): the kept row of position i is copied to out[b][i]
+// (out-of-place), or into slot 0 in place (out = NULL; rows already in slot 0 stay).
+// 16-byte vectors, 4 in flight per thread.
 #include <algorithm>
 
 #include "sb_host.h"
@@ -18,10 +19,7 @@ struct KvParams {
   int64_t row_bytes, stride;  // bytes per position, bytes between positions
   const char* kv;
   char* out;
-  const int* bpos;
-  const int* sel_k;
-  const int* commit_len;
-  const int* y_kind;
+  const uint32_t* keep;       // [B][K] keep mask of sb_select_branch
 };
 
 // one CTA per (sequence, position), sized so every thread has its U vectors of the row
@@ -29,12 +27,10 @@ struct KvParams {
 template <int U>
 __global__ void __launch_bounds__(256) k_kv_rollback(KvParams p) {
   const int b = blockIdx.x / p.R1, i = blockIdx.x % p.R1;
-  const int ks = __ldg(p.sel_k + b);
-  const int n = __ldg(p.commit_len + b) - (__ldg(p.y_kind + b) != 0 ? 1 : 0);
-  int s = p.bpos ? __ldg(p.bpos + b) : 0;
-  s = max(0, s);
-  if (i >= n) return;
-  const int slot = (i < s || ks < 0) ? 0 : ks;
+  int slot = -1;
+  for (int k = 0; k < p.K; ++k)
+    if ((__ldg(p.keep + (int64_t)b * p.K + k) >> i) & 1u) slot = k;
+  if (slot < 0) return;  // not committed: a rolled-back position
   const char* src = p.kv + (((int64_t)b * p.K + slot) * p.R1 + i) * p.stride;
   char* dst;
   if (p.out) {
@@ -62,16 +58,14 @@ __global__ void __launch_bounds__(256) k_kv_rollback(KvParams p) {
 using namespace sb;
 
 extern "C" sb_status sb_kv_rollback(int32_t B, int32_t K, int32_t G, const void* kv, int64_t row_bytes,
-                                    int64_t row_stride_bytes, const int32_t* branch_pos, const int32_t* sel_k,
-                                    const int32_t* commit_len, const int32_t* y_kind, void* out_kv,
+                                    int64_t row_stride_bytes, const uint32_t* keep_mask, void* out_kv,
                                     sb_stream_t stream) {
-  if (B < 1 || K < 1 || G < 0 || G > kMaxG || !kv || !sel_k || !commit_len || !y_kind) return SB_ERR_INVALID_ARG;
+  if (B < 1 || K < 1 || K > kMaxK || G < 0 || G > kMaxG || !kv || !keep_mask) return SB_ERR_INVALID_ARG;
   if (row_bytes <= 0 || row_bytes % 16 || row_stride_bytes < row_bytes || row_stride_bytes % 16) return SB_ERR_INVALID_ARG;
   if ((uintptr_t)kv % 16 || (uintptr_t)out_kv % 16) return SB_ERR_INVALID_ARG;
   KvParams p;
   p.B = B; p.K = K; p.R1 = G + 1; p.row_bytes = row_bytes; p.stride = row_stride_bytes;
-  p.kv = static_cast<const char*>(kv); p.out = static_cast<char*>(out_kv); p.bpos = branch_pos;
-  p.sel_k = sel_k; p.commit_len = commit_len; p.y_kind = y_kind;
+  p.kv = static_cast<const char*>(kv); p.out = static_cast<char*>(out_kv); p.keep = keep_mask;
   // 4 vectors in flight per thread (8 KB rows: 128-thread CTAs).  Measured on the
   // C4-shaped rollback: 2 / 4 / 8 / 16 vectors per thread 35.1 / 26.2 / 29.0 / 29.0 us
   constexpr int U = kKvU;

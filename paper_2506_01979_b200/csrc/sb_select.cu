@@ -609,14 +609,8 @@ __global__ void __launch_bounds__(sThreads, 1) k_select_tma(SelParams p) {
 
 template <typename T>
 static sb_status launch_select_tma(const SelParams& p, cudaStream_t s) {
-  static bool attr = false;
   const int smem = (int)sizeof(SelSmem);
-  if (!attr) {
-    if (cudaFuncSetAttribute(k_select_tma<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
-        cudaSuccess)
-      return SB_ERR_CUDA;
-    attr = true;
-  }
+  if (ensure_smem<k_select_tma<T>>(smem) != cudaSuccess) return SB_ERR_CUDA;
   const int grid = std::min(num_sms(), p.d.B);
   return cuda_status(launch_pdl(k_select_tma<T>, dim3(grid), dim3(sThreads), smem, s, p));
 }

@@ -744,14 +744,8 @@ __global__ void __launch_bounds__(C::ROWS_THREADS, 1) k_rows_tma(RowsParams p) {
 
 template <class C, typename T>
 static sb_status launch_rows_tma(const RowsParams& p, cudaStream_t s) {
-  static bool attr = false;
   const int smem = (int)sizeof(RowsSmem<C>);
-  if (!attr) {
-    if (cudaFuncSetAttribute(k_rows_tma<C, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
-        cudaSuccess)
-      return SB_ERR_CUDA;
-    attr = true;
-  }
+  if (ensure_smem<k_rows_tma<C, T>>(smem) != cudaSuccess) return SB_ERR_CUDA;
   const int64_t max_units = (int64_t)p.d.B * p.d.K * (p.d.G + 1);
   const int grid = (int)std::min<int64_t>(num_sms(), max_units);
   return cuda_status(launch_pdl(k_rows_tma<C, T>, dim3(grid), dim3(C::ROWS_THREADS), smem, s, p));
@@ -759,12 +753,7 @@ static sb_status launch_rows_tma(const RowsParams& p, cudaStream_t s) {
 
 template <typename T, int NT, int U>
 static sb_status launch_rows(const RowsParams& p, bool vok, cudaStream_t s) {
-  static int g = 0;
-  if (g == 0) {
-    int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_rows<T, NT, U>, NT, 0);
-    g = std::max(1, occ) * num_sms();
-  }
+  const int g = full_grid<k_rows<T, NT, U>>(NT);
   const int64_t max_units = (int64_t)p.d.B * p.d.K * (p.d.G + 1);
   const int grid = (int)std::min<int64_t>(g, max_units);
   k_rows<T, NT, U><<<grid, NT, 0, s>>>(p, vok);
@@ -1205,13 +1194,8 @@ __global__ void __launch_bounds__(C::THREADS, 1) k_step_tma(StepParams sp) {
 
 template <class C, typename T>
 static sb_status launch_step_tma(const StepParams& sp, cudaStream_t s) {
-  static bool attr = false;
   const int smem = (int)sizeof(StepSmem<C>);
-  if (!attr) {
-    if (cudaFuncSetAttribute(k_step_tma<C, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
-      return SB_ERR_CUDA;
-    attr = true;
-  }
+  if (ensure_smem<k_step_tma<C, T>>(smem) != cudaSuccess) return SB_ERR_CUDA;
   k_step_tma<C, T><<<num_sms(), C::THREADS, smem, s>>>(sp);
   return cuda_status(cudaGetLastError());
 }

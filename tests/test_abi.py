@@ -115,7 +115,8 @@ def test_invalid_args_rejected_on_host_next_rows(L):
     assert lib.sb_spawn_branches(ctypes.byref(d), fake, None, None, 0, 17, fake, fake, None, None,
                                  None) == L.SB_ERR_INVALID_ARG
     # sb_kv_rollback: rows must be 16-byte multiples
-    assert lib.sb_kv_rollback(4, 2, 3, fake, 24, 32, None, fake, fake, fake, None, None) == L.SB_ERR_INVALID_ARG
+    assert lib.sb_kv_rollback(4, 2, 3, fake, 24, 32, fake, None, None) == L.SB_ERR_INVALID_ARG
+    assert lib.sb_kv_rollback(4, 2, 3, fake, 32, 32, None, None, None) == L.SB_ERR_INVALID_ARG  # keep_mask
     # sb_tree_verify: K must be 1
     assert lib.sb_tree_workspace_bytes(ctypes.byref(d)) == 0  # d has K = 4
     assert lib.sb_tree_verify(ctypes.byref(d), *[fake] * 15, fake, 1 << 30, None) == L.SB_ERR_INVALID_ARG

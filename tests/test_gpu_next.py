@@ -62,12 +62,15 @@ def test_kv_rollback_matches_oracle(inplace):
 
     c = synth.config("c2", V=2048, B=48, K=4, G=8, layout="mixed")
     inp = synth.generate(c, device="cpu", seed=23)
+    inp["gamma"][:3] = torch.tensor([11, 5, 4], dtype=torch.int32)  # clamped layouts
+    inp["branch_pos"][:3] = torch.tensor([2, 7, -1], dtype=torch.int32)
     inp_np = synth.to_numpy_inputs(inp)
     o = oracle.verify(inp_np["PL"], inp_np["QL"], inp_np["tok"], inp_np["u"], inp_np["us"], inp_np["gamma"],
                       inp_np["branch_pos"])
     g = torch.Generator().manual_seed(5)
     kv = torch.randint(-30000, 30000, (c.B, c.K, c.G + 1, 2, 8, 64), generator=g, dtype=torch.int16)
-    ref = oracle.kv_rollback(kv.numpy(), inp_np["branch_pos"], o["sel_k"], o["commit_len"], o["y_kind"])
+    ref = oracle.kv_rollback(kv.numpy(), inp_np["branch_pos"], inp_np["gamma"], o["sel_k"], o["commit_len"],
+                             o["y_kind"])
     # the kept set is the oracle's keep_mask, an independent statement of the same decision
     for b in range(c.B):
         for k in range(c.K):
@@ -76,7 +79,7 @@ def test_kv_rollback_matches_oracle(inplace):
                     assert np.array_equal(ref[b, i], kv.numpy()[b, k, i])
     dev = lambda a: torch.as_tensor(np.ascontiguousarray(a), device="cuda")  # noqa: E731
     kvd = kv.cuda()
-    args = (dev(inp_np["branch_pos"]), dev(o["sel_k"]), dev(o["commit_len"]), dev(o["y_kind"]))
+    args = (dev(o["keep_mask"].view(np.int32)),)
     n = o["commit_len"] - (o["y_kind"] != 0)
     if inplace:
         api.sb_kv_rollback(kvd, *args)

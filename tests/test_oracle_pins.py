@@ -416,6 +416,13 @@ def test_branch_eq9_ties_smaller_token_then_k(orc):
     assert o["sel_k"][0] == 0
 
 
+def test_branch_alg1_ties_smaller_k(orc):
+    """Alg. 1 argmax r_b (P540) with equal uniforms: the smaller branch index wins
+    (DESIGN reading 36), whatever the tokens' ids."""
+    o = _branch_round(orc, [0.3, 0.3], [0.3, 0.3], rule=1, u_branch=[0.25, 0.25], toks=(3, 1))
+    assert o["n_acc"][0].tolist() == [1, 1] and o["sel_k"][0] == 0
+
+
 def test_k1_branch_coupling_equals_single_token_test(orc):
     """K=1 at the branch row (s=gamma) makes the same accept decision as the plain test
     with the same uniform (S438)."""
@@ -600,10 +607,12 @@ def test_kv_rollback_rows_are_keep_mask(orc):
 
     c = synth.config("c2", V=512, B=32, K=3, G=6, layout="mixed")
     inp_np = synth.to_numpy_inputs(synth.generate(c, device="cpu", seed=41))
+    inp_np["gamma"][:3] = [9, 4, 3]  # clamped layouts: gamma > G, s > gamma, s < 0
+    inp_np["branch_pos"][:3] = [1, 6, -2]
     o = oracle.verify(inp_np["PL"], inp_np["QL"], inp_np["tok"], inp_np["u"], inp_np["us"], inp_np["gamma"],
                       inp_np["branch_pos"])
     kv = np.arange(c.B * c.K * (c.G + 1) * 4, dtype=np.int64).reshape(c.B, c.K, c.G + 1, 4)
-    out = oracle.kv_rollback(kv, inp_np["branch_pos"], o["sel_k"], o["commit_len"], o["y_kind"])
+    out = oracle.kv_rollback(kv, inp_np["branch_pos"], inp_np["gamma"], o["sel_k"], o["commit_len"], o["y_kind"])
     for b in range(c.B):
         n = int(o["commit_len"][b]) - int(o["y_kind"][b] != 0)
         kept = [(k, i) for k in range(c.K) for i in range(c.G + 1) if (int(o["keep_mask"][b, k]) >> i) & 1]
