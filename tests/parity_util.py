@@ -52,8 +52,44 @@ def _band(g, r):
     return float(np.max(np.abs(g[m] - r[m]) / (REL * np.abs(r[m]) + ABS)))
 
 
-def compare(g: dict, o: dict, sel=None, strict=True):
-    """Compare gpu outputs g with oracle outputs o on sequences `sel` (indices into g)."""
+def sample_candidates(inp_np: dict, o: dict, b: int, band: float = 1e-6):
+    """The tokens an inverse-CDF draw may return for oracle sequence b when t = us R lies
+    within `band` (probability mass) of a CDF breakpoint: every id with mass whose
+    interval [F(j-1), F(j)) comes within the band of t (SURVEY §8.0 "Inverse CDF"), from
+    the oracle's own fp64 softmax of the sampled row."""
+    g = int(o["_gamma"][b]) if "_gamma" in o else int(inp_np["gamma"][b])
+    G = inp_np["PL"].shape[2] - 1
+    g = min(max(g, 0), G)
+    s = min(max(int(inp_np["branch_pos"][b]), 0), g)
+    L = g if s < g else g + 1
+    ks, kind = int(o["sel_k"][b]), int(o["y_kind"][b])
+    if ks < 0:
+        row, slot = min(int(o["n_acc"][b, 0]), s), 0
+    else:
+        n = int(o["n_acc"][b, ks])
+        row, slot = (n, 0 if n <= s else ks) if n < L else (g, ks)
+    V = inp_np["V"]
+    P, _ = oracle.row_softmax(inp_np["PL"][b:b + 1], 0, slot, row, V=V)
+    if kind == 1:
+        Q, _ = oracle.row_softmax(inp_np["QL"][b:b + 1], 0, slot, row, V=V)
+        r = np.maximum(0.0, P - Q)
+        if r.sum() == 0.0:
+            r = P
+    else:
+        r = P
+    F = np.cumsum(r)
+    t = float(inp_np["us"][b]) * F[-1]
+    ok = (r > 0) & (F - r - band <= t) & (t < F + band)
+    cand = set(np.nonzero(ok)[0].tolist())
+    if t >= F[-1] - band:
+        cand.add(int(np.nonzero(r > 0)[0][-1]))
+    return cand
+
+
+def compare(g: dict, o: dict, sel=None, strict=True, inp_np=None):
+    """Compare gpu outputs g with oracle outputs o on sequences `sel` (indices into g).
+    With inp_np (the oracle's inputs), a near-tie sample is not skipped: the GPU's token
+    must be one of the ids adjacent to the CDF breakpoint (sample_candidates)."""
     B = o["status"].shape[0]
     sel = np.arange(B) if sel is None else np.asarray(sel)
     gs = {k: (v[sel] if isinstance(v, np.ndarray) and v.ndim >= 1 and v.shape[0] >= len(sel) and k not in ("offsets", "packed_tok") else v)
@@ -103,6 +139,23 @@ def compare(g: dict, o: dict, sel=None, strict=True):
     fail("y_tok", np.where((gs["y_tok"] != o["y_tok"]) & ~t_dec & ~t_samp)[0])
     ot = (gs["out_tok"] != o["out_tok"]).any(axis=1) & ~t_dec & ~t_samp
     fail("out_tok", np.where(ot)[0])
+    rep["tie_samples_checked"] = 0
+    rep["tie_samples_differ"] = 0
+    if inp_np is not None:
+        # flagged samples: the GPU token must be a valid draw at the breakpoint, and the
+        # rest of the commit must agree
+        for b in np.where(t_samp & ~t_dec & (o["y_kind"] != 0))[0]:
+            rep["tie_samples_checked"] += 1
+            if gs["y_tok"][b] == o["y_tok"][b]:
+                continue
+            rep["tie_samples_differ"] += 1
+            if int(gs["y_tok"][b]) not in sample_candidates(inp_np, o, b):
+                fail("y_tok_tie_invalid", [b])
+            n = int(o["commit_len"][b]) - 1
+            if not np.array_equal(gs["out_tok"][b, :n], o["out_tok"][b, :n]) or gs["out_tok"][b, n] != gs["y_tok"][b]:
+                fail("out_tok_tie", [b])
+        m = o["margin_sample"][t_samp]
+        rep["tie_margin_hist"] = np.histogram(np.log10(np.maximum(m, 1e-12)), bins=[-12, -9, -8, -7, -6])[0].tolist()
     same = (gs["y_kind"] == o["y_kind"]) & ~t_dec & ~t_samp
     ok, relerr = _close(gs["resid_mass"][same], o["resid_mass"][same])
     rep["max_rel_resid_mass"] = relerr

@@ -18,27 +18,22 @@ def _built():
     build()
 
 
-def _run(cfg, row_pad=0, rule=0, seed=None, adaptive=False, sample=None, nthreads=0, fused=True):
+def _check_chunk(inp, g, idx, adaptive, rule, nthreads):
+    """Oracle on sequences idx of the GPU run g (same bytes), compared element by element."""
     import oracle
     from paper_2506_01979_b200 import synth
 
-    from parity_util import compare, gpu_run, internal_consistency, oracle_for
+    from parity_util import compare, oracle_for
 
-    inp = synth.generate(cfg, device="cuda", seed=seed, row_pad=row_pad)
-    g, d, _ = gpu_run(inp, rule=rule, adaptive=adaptive, fused=fused)
-    internal_consistency(g, cfg.G)
-    B = inp["PL"].shape[0]
-    idx = np.arange(B) if sample is None else np.unique(np.r_[0, B - 1, np.random.default_rng(1).choice(B, sample - 2, replace=False)])
-    it = torch.as_tensor(idx, device="cuda")
+    it = torch.as_tensor(idx, device=inp["PL"].device)
     sub = synth.to_numpy_inputs({k: (v.index_select(0, it) if torch.is_tensor(v) else v) for k, v in inp.items()})
-    inp_np = sub
     if adaptive:
         c = oracle.confidence(np.ascontiguousarray(sub["QL"][:, :1]), mode=oracle.CONF_TOP1, eps=0.2,
-                              k_max=6, V=inp_np["V"], nthreads=nthreads)
+                              k_max=6, V=sub["V"], nthreads=nthreads)
         tie = (c["ties"][:, 0] & oracle.TIE_CONF) != 0
         assert np.array_equal(c["stop"][:, 0][~tie], g["c_stop"][idx, 0][~tie])
         assert np.array_equal(c["k_next"][:, 0][~tie], g["c_knext"][idx, 0][~tie]) or (c["ties"][:, 0] & oracle.TIE_EQ7).any()
-        G = cfg.G
+        G = sub["PL"].shape[2] - 1
         for key, gk in (("top1_prob", "c_top1"), ("entropy", "c_ent"), ("stat", "c_stat")):
             ref = c[key][:, 0, :G]
             got = g[gk][idx, 0, :G].astype(np.float64)
@@ -50,11 +45,43 @@ def _run(cfg, row_pad=0, rule=0, seed=None, adaptive=False, sample=None, nthread
         gamma = sub["gamma"]
         keep = np.ones(len(idx), bool)
     o = oracle_for(sub, gamma, rule=rule, nthreads=nthreads)
+    o["_gamma"] = np.asarray(gamma)
     keep_idx = np.where(keep)[0]
     osub = {k: (v[keep_idx] if isinstance(v, np.ndarray) and v.ndim >= 1 and v.shape[0] == len(idx) else v)
             for k, v in o.items()}
-    rep = compare(g, osub, sel=idx[keep_idx])
-    return rep, g
+    isub = {k: (v[keep_idx] if isinstance(v, np.ndarray) and v.ndim >= 1 and v.shape[0] == len(idx) else v)
+            for k, v in sub.items()}
+    return compare(g, osub, sel=idx[keep_idx], inp_np=isub)
+
+
+def _merge(reps):
+    out = {"n": 0, "ties": {"acc_mask": 0, "decision": 0, "sample": 0}, "exact_seq": 0, "y_compared": 0,
+           "tie_samples_checked": 0, "tie_samples_differ": 0, "tie_margin_hist": [0, 0, 0, 0]}
+    for r in reps:
+        for k in ("n", "exact_seq", "y_compared", "tie_samples_checked", "tie_samples_differ"):
+            out[k] += r[k]
+        for k in out["ties"]:
+            out["ties"][k] += r["ties"][k]
+        out["tie_margin_hist"] = [a + b for a, b in zip(out["tie_margin_hist"], r.get("tie_margin_hist", [0] * 4))]
+        for k, v in r.items():
+            if k.startswith("max_"):
+                out[k] = max(out.get(k, 0.0), v)
+    return out
+
+
+def _run(cfg, row_pad=0, rule=0, seed=None, adaptive=False, sample=None, nthreads=0, fused=True, chunk=None):
+    from paper_2506_01979_b200 import synth
+
+    from parity_util import gpu_run, internal_consistency
+
+    inp = synth.generate(cfg, device="cuda", seed=seed, row_pad=row_pad)
+    g, d, _ = gpu_run(inp, rule=rule, adaptive=adaptive, fused=fused)
+    internal_consistency(g, cfg.G)
+    B = inp["PL"].shape[0]
+    idx = np.arange(B) if sample is None else np.unique(np.r_[0, B - 1, np.random.default_rng(1).choice(B, sample - 2, replace=False)])
+    step = len(idx) if chunk is None else chunk
+    reps = [_check_chunk(inp, g, idx[j:j + step], adaptive, rule, nthreads) for j in range(0, len(idx), step)]
+    return _merge(reps), g
 
 
 def cfg(name, **kw):
@@ -204,19 +231,17 @@ def test_special_values_and_status():
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("name,adaptive,sample", [("c1", False, None), ("c2", True, None),
-                                                  ("c3", True, 48), ("c4", False, 32),
-                                                  ("c5", False, 16)])
-def test_baseline_config_full_size(name, adaptive, sample):
-    """Full BASELINE sizes in bench.py's launch configuration; the oracle checks every
-    sequence of C1/C2 and a sampled subset (first, last, random) of C3-C5."""
+@pytest.mark.parametrize("name,adaptive,chunk", [("c1", False, 256), ("c2", True, 64), ("c3", True, 64),
+                                                 ("c4", False, 256), ("c5", False, 64)])
+def test_baseline_config_full_size(name, adaptive, chunk):
+    """Full BASELINE sizes in bench.py's launch configuration; the oracle checks EVERY
+    sequence (in chunks that bound host memory), SURVEY §8.4 "Parity coverage".  Near-tie
+    samples are not skipped: the GPU's token must be a valid draw at the breakpoint."""
     c = cfg(name)
-    rep, g = _run(c, adaptive=adaptive, sample=sample, nthreads=0)
-    # discrete decisions must be near-tie-free for almost all sequences; samples that land
-    # in the bulk of a large vocabulary sit on ~1e-7-mass tokens and are legitimately
-    # flagged (|us*R - F| < 1e-6), so only the decision ties are bounded here
+    rep, g = _run(c, adaptive=adaptive, nthreads=0, chunk=chunk)
+    assert rep["n"] == c.B * c.rounds or adaptive, rep
     assert rep["ties"]["decision"] <= 0.1 * rep["n"], rep
-    print(name, {k: v for k, v in rep.items() if k != "fail"})
+    print(name, rep)
 
 
 @pytest.mark.parametrize("name,kw", [("bf16_mixed_V32000", dict(name="c2", B=48, layout="mixed")),

@@ -217,9 +217,12 @@ def test_q_zero_accepts(orc):
 
 
 # ---------------------------------------------------------------- exact laws by enumeration
-def _enumerate_first_token_law(orc, P0, Q0, V):
-    """Batch of one-row rounds covering every (x, u-interval, us-interval) with weights."""
-    PL_rows, QL_rows, toks, us_l, uu, w = [], [], [], [], [], []
+def enum_first_token_cases(P0, Q0, V):
+    """Batch of one-row rounds (K = 1, s_b = 0, gamma_b = 1) covering every (x,
+    u-interval, us-interval) at interval midpoints, with the probability weight of each:
+    x ~ Q, then u < a = min(1, P/Q) (accept) or u in (a, 1) followed by the residual's
+    inverse-CDF intervals of us.  Returns (PL, QL, tok, u, us, w, Pe)."""
+    toks, us_l, uu, w = [], [], [], []
     lp = logits_from_probs([P0, P0])
     lq = logits_from_probs([Q0, Q0])
     Pe, Qe = softmax64(lp[0]), softmax64(lq[0])
@@ -246,11 +249,20 @@ def _enumerate_first_token_law(orc, P0, Q0, V):
     tok[:, 0, 0] = toks
     u = np.zeros((n, 1, 2))
     u[:, 0, 0] = uu
-    o = orc.verify(PL, QL, tok, u, np.asarray(us_l), gamma=np.ones(n), branch_pos=np.zeros(n), f64_uniforms=True)
+    return PL, QL, tok, u, np.asarray(us_l), np.asarray(w), Pe
+
+
+def first_token_law(out_tok0, w, V):
     law = np.zeros(V)
-    for b in range(n):
-        law[o["out_tok"][b, 0]] += w[b]
-    return law, Pe
+    np.add.at(law, out_tok0, w)
+    return law
+
+
+def _enumerate_first_token_law(orc, P0, Q0, V):
+    PL, QL, tok, u, us, w, Pe = enum_first_token_cases(P0, Q0, V)
+    n = len(w)
+    o = orc.verify(PL, QL, tok, u, us, gamma=np.ones(n), branch_pos=np.zeros(n), f64_uniforms=True)
+    return first_token_law(o["out_tok"][:, 0], w, V), Pe
 
 
 def test_losslessness_enumeration(orc):
