@@ -5,10 +5,12 @@
 
 One step = one pass of the whole hot path over one batch of synthetic input
 ([draft confidence ->] sb_verify_branches -> sb_select_branch, through the C ABI).
-Default workload: BASELINE config C4 (Qwen V=151936, 2048 sequences per GPU, K=4,
-gamma=8, bf16) — the configuration the metric's "1/2/4/8 GPUs" is quoted on.
-Sequences shard across ranks with no data-path collective (weak scaling: each rank
-owns 2048 sequences).  Rank 0 prints one JSON line.
+Default workload: BASELINE config C4 (Qwen V=151936, 2048 sequences, K=4, gamma=8,
+bf16) — the configuration the metric's "1/2/4/8 GPUs" is quoted on.  Sequences shard
+across ranks with no data-path collective: by default the 2048 sequences are split over
+the N ranks (strong scaling; --scaling weak gives every rank 2048).
+`python bench.py --gpus N` without torchrun re-launches itself as N ranks.  Rank 0 prints
+one JSON line.
 """
 from __future__ import annotations
 
@@ -107,11 +109,15 @@ def bytes_model(gamma, bpos, y_kind, K, V, es, G, conf_rows=0, bonus_rows=False)
     return a1, a4, a6, small, units
 
 
-def rank_slice(cfg, rank, world):
-    """Sequences [b0, b1) a rank owns: weak scaling, each rank a full per-GPU batch with
-    global sequence keys rank*B .. (rank+1)*B - 1 (no data-path collective)."""
+def rank_slice(cfg, rank, world, scaling="strong"):
+    """Sequences [b0, b1) a rank owns (global sequence keys; no data-path collective).
+    strong (default): the configuration's batch split contiguously, rank g
+    owns [g B / N, (g + 1) B / N) (C4 at 8 GPUs: 256 each); weak: every rank a full
+    per-GPU batch with keys rank * B .. (rank + 1) * B - 1."""
     Bl = cfg.B * cfg.rounds
-    return rank * Bl, (rank + 1) * Bl
+    if scaling == "weak":
+        return rank * Bl, (rank + 1) * Bl
+    return rank * Bl // world, (rank + 1) * Bl // world
 
 
 def reduce_over_ranks(ms_step, toks, committed, nbytes, device, world):
@@ -139,11 +145,12 @@ def run_ours(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     cfg = synth.config(args.config, **({"delta": args.delta} if args.delta is not None else {}))
-    Bl = cfg.B * cfg.rounds
-    b0, b1 = rank_slice(cfg, rank, world)
+    Btot = cfg.B * cfg.rounds
+    b0, b1 = rank_slice(cfg, rank, world, args.scaling)
     vocab = args.mode == "vocab"
     if vocab:  # every rank sees all sequences and owns a vocabulary slice (a7)
-        b0, b1 = 0, Bl
+        b0, b1 = 0, Btot
+    Bl = b1 - b0  # this rank's sequences
     t0 = time.time()
     inp = synth.generate(cfg, device=dev, b0=b0, b1=b1)
     gen_s = time.time() - t0
@@ -315,10 +322,11 @@ def run_ours(args, rank, world, local_rank):
         "metric": METRIC, "value": round(value, 1), "unit": "verified draft tokens/s",
         "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
         "ms_per_step": round(ms_step_all, 4), "higher_is_better": True,
-        "scaling": "strong" if vocab else "weak",
+        "scaling": "strong" if vocab else args.scaling,
         "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic (seeded, DESIGN.md §Input recipe)",
         "config": {"workload": f"{cfg.name.upper()}: {cfg.note}", "V": cfg.V, "K": cfg.K, "G": cfg.G,
-                   "per_rank_batch": Bl, "global_batch": Bl if vocab else Bl * world, "layout": cfg.layout,
+                   "per_rank_batch": Bl, "global_batch": Btot if (vocab or args.scaling == "strong") else Btot * world,
+                   "layout": cfg.layout,
                    "parallelism": (f"vocabulary-sharded x{world} (NCCL all-gather / all-reduce, sb_comm)"
                                    if vocab else f"sequence-sharded x{world} (no data-path collective)"),
                    "l2": "inputs larger than L2 (%.1f GB per step vs 126 MB)" % (bytes_all / 1e9 / world)},
@@ -595,11 +603,13 @@ def run_e2e(args, inp, d, buf, adaptive, stream, dev, world):
     ms = s.elapsed_time(e) / steps
     gamma = (buf.c_gamma.view(-1) if adaptive else inp["gamma"]).cpu().tolist()
     toks = verified_tokens(gamma, inp["branch_pos"].cpu().tolist(), d.K)
-    if world > 1:
+    if world > 1:  # time = max over ranks, tokens = sum over ranks
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t[0])
-        toks *= world
+        n = torch.tensor([float(toks)], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(n, op=torch.distributed.ReduceOp.SUM)
+        toks = float(n[0])
     return {"value": round(toks / (ms * 1e-3), 1), "unit": "verified draft tokens/s",
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "ms_per_step": round(ms, 3),
             "steps": steps, "path": "pinned host -> H2D -> verify_step (C ABI) -> D2H of the commit"}
@@ -729,14 +739,29 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--ref-seqs", type=int, default=32)
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="sequence-sharded configs: strong = the config's batch split over the ranks "
+                         "(SURVEY §8.5, default); weak = a full batch per rank")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: test-only multi-rank runs on one GPU (LOCAL_RANK modulo the device count)")
     args = ap.parse_args()
     if args.mode is None:
         args.mode = "vocab" if args.config == "c5" else "seq"
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl != "reference":
+        # launched as `python bench.py --gpus N`: become N ranks (one process per GPU)
+        import socket
+
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+        os.execv(sys.executable, cmd)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl != "reference" and world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.dist_backend == "gloo" and args.impl != "reference":
         import torch
 

@@ -43,6 +43,7 @@ struct Workspace {
   int4* dec;         // [B] sharded select: decision record
   int* ready;        // [B] fused step: per-sequence phase-1 completion flags
   int* plan;         // [4] fused step: delta, total units
+  int* seqpk;        // [B] packed layout of each sequence (k_plan): s | g<<5 | L<<10 | Lr<<16 | st<<22
   RowStat* qrs;      // [B][K][G] row states of the rows sb_draft_confidence streamed
                      // (read back by sb_verify_branches_reuse instead of the q rows)
   size_t bytes;
@@ -76,6 +77,7 @@ inline Workspace carve(const sb_dims& d, void* base) {
   }
   w.ready = (int*)take(sizeof(int) * B);
   w.plan = (int*)take(sizeof(int) * 4);
+  w.seqpk = (int*)take(sizeof(int) * B);
   w.qrs = (RowStat*)take(sizeof(RowStat) * B * K * (G ? G : 1));
   w.bytes = off;
   return w;

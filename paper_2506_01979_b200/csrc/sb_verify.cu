@@ -34,6 +34,7 @@ struct RowsParams {
   const float* u;
   const SeqInfo* info;
   const int* unit_off;
+  const int* seqpk;       // [B] packed layout (k_plan), read by the warp-cooperative decode
   const RowStat* qreuse;  // [B][G] slot-0 q-row states from sb_draft_confidence, or NULL
   int* cnt;
   float4* rowstat;
@@ -59,7 +60,7 @@ __host__ __device__ inline int4 unit_entry(int b, int slot, int i, const SeqInfo
 __global__ void __launch_bounds__(1024) k_plan(Dims d, const int* __restrict__ gamma,
                                                const int* __restrict__ bpos, SeqInfo* info,
                                                int* unit_off, int with_bonus, int fused_grid, int* plan,
-                                               int* ready) {
+                                               int* ready, int* seqpk) {
   __shared__ int wsum[32];
   pdl_wait();
   const int tid = threadIdx.x, NT = blockDim.x;
@@ -77,6 +78,7 @@ __global__ void __launch_bounds__(1024) k_plan(Dims d, const int* __restrict__ g
     const int L = (s < g) ? g : g + 1;
     const int Lr = with_bonus ? g + 1 : L;  // sharded mode also reads every bonus row
     info[b] = SeqInfo{g, s, L, st, Lr, {0, 0, 0}};
+    if (seqpk) seqpk[b] = s | (g << 5) | (L << 10) | (Lr << 16) | (st << 22);
     local += Lr + (d.K - 1) * (Lr - 1 - s);  // slot 0: rows 0..Lr-1; slots k>0: s+1..Lr-1
   }
   // block exclusive scan of the per-thread sums
@@ -174,6 +176,60 @@ __device__ __forceinline__ Unit unit_from(int4 e) {
 __device__ __forceinline__ int4 unit_prefetch(const RowsParams& p, int unit, int total) {
   if (unit >= total) return make_int4(0, 0, 0, 0);
   const Unit u = decode_unit(p, unit);
+  return unit_entry(u.b, u.slot, u.i, u.in);
+}
+
+// Warp-cooperative decode of a unit (the streaming kernels' producer and epilogue warps):
+// a CTA walks its units in increasing order, so the sequence of the next unit is at or
+// after the current one; lane l probes sequence base + l (unit offset + packed layout,
+// two independent loads, one round trip), one ballot finds it.  Against the binary
+// search's log2(B) dependent loads per unit this keeps a short unit's producer from
+// stalling (C2: 668 units of 125 KB).
+struct Probe {
+  int off, pk;
+};
+__device__ __forceinline__ Probe probe_load(const RowsParams& p, int base) {
+  const int bb = base + (threadIdx.x & 31);
+  Probe r;
+  r.off = bb <= p.d.B ? __ldg(p.unit_off + bb) : 0x7fffffff;
+  r.pk = bb < p.d.B ? __ldg(p.seqpk + bb) : 0;
+  return r;
+}
+// The packed geometry of `unit` (zeros past the end); base <= the unit's sequence on
+// entry, its sequence on return.  Warp-uniform arguments.
+__device__ __forceinline__ int4 probe_resolve(const RowsParams& p, Probe pr, int& base, int unit, int total) {
+  if (unit >= total) return make_int4(0, 0, 0, 0);
+  unsigned le = __ballot_sync(0xffffffffu, pr.off <= unit);
+  while (le == 0xffffffffu) {  // more than 32 sequences ahead (only the first decode)
+    base += 32;
+    pr = probe_load(p, base);
+    le = __ballot_sync(0xffffffffu, pr.off <= unit);
+  }
+  if (le == 0u) {  // not reachable from a valid base; keep the binary search as a guard
+    const Unit u = decode_unit(p, unit);
+    base = u.b;
+    return unit_entry(u.b, u.slot, u.i, u.in);
+  }
+  const int src = __popc(le) - 1;
+  const int off = __shfl_sync(0xffffffffu, pr.off, src);
+  const int pk = __shfl_sync(0xffffffffu, pr.pk, src);
+  base += src;
+  Unit u;
+  u.b = base;
+  u.in.s = pk & 31;
+  u.in.g = (pk >> 5) & 31;
+  u.in.L = (pk >> 10) & 63;
+  u.in.Lr = (pk >> 16) & 63;
+  u.in.st = pk >> 22;
+  const int j = unit - off;
+  if (j < u.in.Lr) {
+    u.slot = 0;
+    u.i = j;
+  } else {
+    const int per = u.in.Lr - 1 - u.in.s, jj = j - u.in.Lr;
+    u.slot = 1 + jj / per;
+    u.i = u.in.s + 1 + jj % per;
+  }
   return unit_entry(u.b, u.slot, u.i, u.in);
 }
 
@@ -598,14 +654,15 @@ __global__ void __launch_bounds__(C::ROWS_THREADS, 1) k_rows_tma(RowsParams p) {
   const int nchunks = (row_bytes + C::CHUNK - 1) / C::CHUNK;
   const int nvec_last = (int)(row_bytes - (uint32_t)(nchunks - 1) * C::CHUNK) / 16;
 
-  if (warp == C::CW) {  // ---------------- producer
-    if (lane == 0) {
-      const uint64_t pol = policy_evict_first();
-      RingPos<C::NS> rp;
-      int4 nxt = unit_prefetch(p, blockIdx.x, total);
-      for (int unit = blockIdx.x; unit < total; unit += gridDim.x) {
-        const Unit un = unit_from(nxt);
-        nxt = unit_prefetch(p, unit + gridDim.x, total);
+  if (warp == C::CW) {  // ---------------- producer (lane 0 issues, the warp decodes)
+    const uint64_t pol = policy_evict_first();
+    RingPos<C::NS> rp;
+    int base = 0;
+    int4 cur = probe_resolve(p, probe_load(p, 0), base, blockIdx.x, total);
+    for (int unit = blockIdx.x; unit < total; unit += gridDim.x) {
+      const Unit un = unit_from(cur);
+      const Probe pr = probe_load(p, base);  // the next unit's probe, in flight during the copies
+      if (lane == 0) {
         const char* prow = reinterpret_cast<const char*>(PL + row_off(d, un.b, un.slot, un.i));
         const char* qrow = reinterpret_cast<const char*>(QL + row_off(d, un.b, un.slot, un.i));
         const bool po = q_reused(p, un);
@@ -619,18 +676,21 @@ __global__ void __launch_bounds__(C::ROWS_THREADS, 1) k_rows_tma(RowsParams p) {
           rp.advance();
         }
       }
+      __syncwarp();
+      cur = probe_resolve(p, pr, base, unit + gridDim.x, total);
     }
     return;
   }
   if (warp > C::CW) {  // ---------------- epilogue warps: warp e takes local units e, e+NE, ...
     const int e = warp - C::CW - 1;
-    int4 nxt = unit_prefetch(p, blockIdx.x + e * gridDim.x, total);
+    int base = 0;
+    int4 nxt = probe_resolve(p, probe_load(p, 0), base, blockIdx.x + e * gridDim.x, total);
     for (int li = e, unit = blockIdx.x + e * gridDim.x; unit < total; li += C::NE, unit += C::NE * gridDim.x) {
       RingPos<C::NP> up;
       up.stage = li % C::NP;
       up.phase = (uint32_t)(li / C::NP) & 1u;
       const Unit un = unit_from(nxt);
-      nxt = unit_prefetch(p, unit + C::NE * gridDim.x, total);
+      nxt = probe_resolve(p, probe_load(p, base), base, unit + C::NE * gridDim.x, total);
       const T* prow = PL + row_off(d, un.b, un.slot, un.i);
       const T* qrow = QL + row_off(d, un.b, un.slot, un.i);
       // prefetch the path tokens through this row, their uniforms and logits
@@ -1253,11 +1313,12 @@ sb_status sb_rows_partial(const sb_dims* dd, const void* p_logits, const void* q
   if (!vok || ((size_t)dd->V * elem_size(dd)) % 16) return SB_ERR_UNSUPPORTED;
   const Dims d = to_dims(dd);
   if (launch_pdl(k_plan, dim3(1), dim3(1024), 0, s, d, gamma, branch_pos, w.info, w.unit_off, 1, 0,
-                 (int*)nullptr, (int*)nullptr) != cudaSuccess)
+                 (int*)nullptr, (int*)nullptr, w.seqpk) != cudaSuccess)
     return SB_ERR_CUDA;
   RowsParams p{};
   p.d = d; p.PL = p_logits; p.QL = q_logits; p.tok = tok; p.u = u;
-  p.info = w.info; p.unit_off = w.unit_off; p.cnt = w.cnt; p.rowstat = w.rowstat; p.pflag = w.pflag;
+  p.info = w.info; p.unit_off = w.unit_off; p.seqpk = w.seqpk; p.cnt = w.cnt; p.rowstat = w.rowstat;
+  p.pflag = w.pflag;
   p.partial = 1;
   p.v_offset = dd->v_offset;
   const size_t per = (size_t)dd->B * dd->K * (dd->G + 1);
@@ -1288,12 +1349,13 @@ static sb_status verify_impl(const sb_dims* dd, const void* p_logits, const void
   cudaStream_t s = (cudaStream_t)stream;
 
   if (launch_pdl(k_plan, dim3(1), dim3(1024), 0, s, d, gamma, branch_pos, w.info, w.unit_off, 0, 0,
-                 (int*)nullptr, (int*)nullptr) != cudaSuccess)
+                 (int*)nullptr, (int*)nullptr, w.seqpk) != cudaSuccess)
     return SB_ERR_CUDA;
 
   RowsParams p;
   p.d = d; p.PL = p_logits; p.QL = q_logits; p.tok = tok; p.u = u;
-  p.info = w.info; p.unit_off = w.unit_off; p.cnt = w.cnt; p.rowstat = w.rowstat; p.pflag = w.pflag;
+  p.info = w.info; p.unit_off = w.unit_off; p.seqpk = w.seqpk; p.cnt = w.cnt; p.rowstat = w.rowstat;
+  p.pflag = w.pflag;
   p.lse_p = lse_p; p.lse_q = lse_q; p.p_tok = p_tok; p.q_tok = q_tok;
   p.top1_q = top1_q; p.entropy_q = entropy_q; p.top1_id_q = top1_id_q;
   p.acc_mask = acc_mask; p.n_acc = n_acc; p.status = status;
@@ -1381,12 +1443,13 @@ extern "C" sb_status sb_verify_select(const sb_dims* dd, const void* p_logits, c
   }
   const Dims d = to_dims(dd);
   cudaStream_t s = (cudaStream_t)stream;
-  k_plan<<<1, 1024, 0, s>>>(d, gamma, branch_pos, w.info, w.unit_off, 0, num_sms(), w.plan, w.ready);
+  k_plan<<<1, 1024, 0, s>>>(d, gamma, branch_pos, w.info, w.unit_off, 0, num_sms(), w.plan, w.ready, w.seqpk);
   if (cudaGetLastError() != cudaSuccess) return SB_ERR_CUDA;
   StepParams sp{};
   RowsParams& p = sp.r;
   p.d = d; p.PL = p_logits; p.QL = q_logits; p.tok = tok; p.u = u;
-  p.info = w.info; p.unit_off = w.unit_off; p.cnt = w.cnt; p.rowstat = w.rowstat; p.pflag = w.pflag;
+  p.info = w.info; p.unit_off = w.unit_off; p.seqpk = w.seqpk; p.cnt = w.cnt; p.rowstat = w.rowstat;
+  p.pflag = w.pflag;
   p.lse_p = lse_p; p.lse_q = lse_q; p.p_tok = p_tok; p.q_tok = q_tok;
   p.top1_q = top1_q; p.entropy_q = entropy_q; p.top1_id_q = top1_id_q;
   p.acc_mask = acc_mask; p.n_acc = n_acc; p.status = status; p.ready = w.ready;

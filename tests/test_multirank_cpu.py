@@ -23,7 +23,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, out_dir):
+def _worker(rank, world, port, out_dir, scaling):
     sys.path.insert(0, ROOT)
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -33,7 +33,7 @@ def _worker(rank, world, port, out_dir):
     from paper_2506_01979_b200 import synth
 
     cfg = synth.config("c2", V=256, B=6, K=3, G=5, layout="mixed")
-    b0, b1 = bench.rank_slice(cfg, rank, world)
+    b0, b1 = bench.rank_slice(cfg, rank, world, scaling)
     inp = synth.to_numpy_inputs(synth.generate(cfg, device="cpu", b0=b0, b1=b1))
     o = oracle.verify(inp["PL"], inp["QL"], inp["tok"], inp["u"], inp["us"], inp["gamma"], inp["branch_pos"],
                       nthreads=1, V=inp["V"])
@@ -53,16 +53,21 @@ def _worker(rank, world, port, out_dir):
     dist.destroy_process_group()
 
 
-def test_sequence_sharding_world2_gloo(tmp_path):
+@pytest.mark.parametrize("scaling", ["strong", "weak"])
+def test_sequence_sharding_world2_gloo(tmp_path, scaling):
+    """strong (bench default, SURVEY §8.5): the 6 sequences split 3 + 3 over the ranks;
+    weak: every rank 6 sequences with global keys rank*6 ...  Either way the shards are
+    the same bytes and results as the unsharded batch."""
     world = 2
-    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path), scaling), nprocs=world, join=True)
     r = np.load(tmp_path / "res.npz")
     sys.path.insert(0, ROOT)
     import oracle
     from paper_2506_01979_b200 import synth
 
     cfg = synth.config("c2", V=256, B=6, K=3, G=5, layout="mixed")
-    full = synth.to_numpy_inputs(synth.generate(cfg, device="cpu", b0=0, b1=world * cfg.B))
+    n = cfg.B if scaling == "strong" else world * cfg.B
+    full = synth.to_numpy_inputs(synth.generate(cfg, device="cpu", b0=0, b1=n))
     # shard bytes == the same sequences of the unsharded batch (counter-keyed generator)
     assert np.array_equal(r["PL"], full["PL"]) and np.array_equal(r["tok"], full["tok"])
     o = oracle.verify(full["PL"], full["QL"], full["tok"], full["u"], full["us"], full["gamma"],
