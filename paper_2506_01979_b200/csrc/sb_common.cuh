@@ -152,7 +152,8 @@ struct RowAcc {
   float ms;      // m * c (fp32), the exponent offset used by every term
   float z[NA];   // sum of 2^(l c - ms)
   float s1[kQ ? NA : 1];
-  float zf, s1f;  // kQ: frozen e and e*a of the maximum's element(s)
+  float fa;      // kQ: exponent a = m c - ms of the frozen maximum element(s) ...
+  int fn;        // ... and their count (0: none); their e = 2^a is evaluated in fp64
   int idx;       // smallest index attaining m (kQ only)
 
   __device__ __forceinline__ void init() {
@@ -162,7 +163,8 @@ struct RowAcc {
     for (int j = 0; j < NA; ++j) z[j] = 0.f;
 #pragma unroll
     for (int j = 0; j < (kQ ? NA : 1); ++j) s1[j] = 0.f;
-    zf = s1f = 0.f;
+    fa = 0.f;
+    fn = 0;
     idx = 0x7fffffff;
   }
 
@@ -176,19 +178,18 @@ struct RowAcc {
       if (kQ) s1[j] = sc * fmaf(z[j], dd, s1[j]);
       z[j] *= sc;
     }
-    if (kQ) {  // the previous maximum's element(s) become ordinary terms
-      s1[0] = fmaf(sc, fmaf(zf, dd, s1f), s1[0]);
-      z[0] = fmaf(sc, zf, z[0]);
+    if (kQ && fn) {  // the previous maximum's element(s) become ordinary terms
+      const float ef = (float)fn * exp2f(fa);
+      s1[0] = fmaf(sc, ef * (fa + dd), s1[0]);
+      z[0] = fmaf(sc, ef, z[0]);
     }
     m = nm;
     ms = nms;
   }
   // kQ: move the n elements equal to the new maximum into the frozen part
   __device__ __forceinline__ void freeze(int n) {
-    const float a = fmaf(m, kC, -ms);  // exact: the rounding residual of ms
-    const float e = exp2f(a);
-    zf = (float)n * e;
-    s1f = zf * a;
+    fa = fmaf(m, kC, -ms);  // exact: the rounding residual of ms
+    fn = n;
   }
 
   // accumulate E values f[] whose first element has index base
@@ -246,7 +247,8 @@ struct LazyAcc {
   float ms;
   float z[NA];
   float s1[kQ ? NA : 1];
-  float zf, s1f;
+  float fa;  // kQ: frozen element(s): exponent and count (see RowAcc)
+  int fn;
   int tag;
 
   __device__ __forceinline__ void init() {
@@ -256,7 +258,8 @@ struct LazyAcc {
     for (int j = 0; j < NA; ++j) z[j] = 0.f;
 #pragma unroll
     for (int j = 0; j < (kQ ? NA : 1); ++j) s1[j] = 0.f;
-    zf = s1f = 0.f;
+    fa = 0.f;
+    fn = 0;
     tag = -1;
   }
   __device__ __forceinline__ void rescale(float nms) {
@@ -267,9 +270,10 @@ struct LazyAcc {
       if (kQ) s1[j] = sc * fmaf(z[j], dd, s1[j]);
       z[j] *= sc;
     }
-    if (kQ) {
-      s1[0] = fmaf(sc, fmaf(zf, dd, s1f), s1[0]);
-      z[0] = fmaf(sc, zf, z[0]);
+    if (kQ && fn) {
+      const float ef = (float)fn * exp2f(fa);
+      s1[0] = fmaf(sc, ef * (fa + dd), s1[0]);
+      z[0] = fmaf(sc, ef, z[0]);
     }
     ms = nms;
   }
@@ -281,10 +285,8 @@ struct LazyAcc {
 #pragma unroll
     for (int j = 0; j < N; ++j)
       if (f[j] == cm) { f[j] = kMaskedLogit; ++n; }
-    const float a = fmaf(cm, kC, -ms);  // exact residual of ms = fl(cm c)
-    const float e = exp2f(a);
-    zf = (float)n * e;
-    s1f = zf * a;
+    fa = fmaf(cm, kC, -ms);  // exact residual of ms = fl(cm c)
+    fn = n;
   }
   template <int N>
   __device__ __forceinline__ void add(float* f, int t) {
@@ -402,6 +404,16 @@ struct RowStat {
   int idx;
 };
 
+// The frozen element(s) of a q row, n * 2^a and their entropy term n * 2^a * a, in fp64
+// (a is the exact rounding residual of the offset: a one-hot row gets H = 0 exactly).
+__device__ __forceinline__ void add_frozen(RowStat& r, int n, float a) {
+  if (n) {
+    const double e = (double)n * exp2((double)a);
+    r.z += e;
+    r.s1 += e * (double)a;
+  }
+}
+
 template <bool kQ, int NA>
 __device__ __forceinline__ RowStat fold_lazy(const LazyAcc<kQ, NA>& a) {
   RowStat r;
@@ -414,8 +426,9 @@ __device__ __forceinline__ RowStat fold_lazy(const LazyAcc<kQ, NA>& a) {
 #pragma unroll
     for (int j = 0; j < NA; ++j) s += a.s1[j];
   }
-  r.z = (double)z + (double)a.zf;
-  r.s1 = kQ ? (double)s + (double)a.s1f : 0.0;
+  r.z = (double)z;
+  r.s1 = (double)s;
+  if (kQ) add_frozen(r, a.fn, a.fa);
   r.idx = 0x7fffffff;
   return r;
 }
@@ -443,8 +456,9 @@ __device__ __forceinline__ RowStat fold(const RowAcc<kQ, NA>& a) {
 #pragma unroll
     for (int j = 0; j < NA; ++j) s += a.s1[j];
   }
-  r.z = (double)z + (double)a.zf;
-  r.s1 = kQ ? (double)s + (double)a.s1f : 0.0;
+  r.z = (double)z;
+  r.s1 = (double)s;
+  if (kQ) add_frozen(r, a.fn, a.fa);
   r.idx = kQ ? a.idx : 0;
   return r;
 }
