@@ -194,13 +194,20 @@ __device__ __forceinline__ void seg_values(const T* prow, const T* qrow, uint32_
   uint4 vp = sizeof(T) == 2 ? make_uint4(0xff80ff80u, 0xff80ff80u, 0xff80ff80u, 0xff80ff80u)
                             : make_uint4(0xff800000u, 0xff800000u, 0xff800000u, 0xff800000u);
   uint4 vq = vp;
-  if (off < row_bytes) {
+  float lp[E], lq[E];
+  if (off + 16 <= row_bytes) {
     vp = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(prow) + off));
     if (resid) vq = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(qrow) + off));
+    Vec<T>::unpack(vp, lp);
+    Vec<T>::unpack(vq, lq);
+  } else {  // the ragged end of a shard row (length not a multiple of 16 bytes): scalar, -inf past V
+    const int v0 = (int)(off / sizeof(T)), V = (int)(row_bytes / sizeof(T));
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      lp[e] = v0 + e < V ? ld_scalar(prow + v0 + e) : -CUDART_INF_F;
+      lq[e] = (resid && v0 + e < V) ? ld_scalar(qrow + v0 + e) : -CUDART_INF_F;
+    }
   }
-  float lp[E], lq[E];
-  Vec<T>::unpack(vp, lp);
-  Vec<T>::unpack(vq, lq);
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const float P = __fmul_rn(ex2(__fmaf_rn(lp[e], kC, -MSp)), iZp);
@@ -555,8 +562,8 @@ extern "C" sb_status sb_shard_select_local(const sb_dims* dd, const void* p_logi
   if (!dims_valid(dd)) return SB_ERR_INVALID_ARG;
   if (!p_logits || !q_logits || !tok || !u || !n_acc || !mass || !workspace) return SB_ERR_INVALID_ARG;
   if (rule != SB_SELECT_EQ9 && rule != SB_SELECT_ALG1) return SB_ERR_INVALID_ARG;
-  if (!vec_ok(dd, p_logits) || !vec_ok(dd, q_logits) || ((size_t)dd->V * elem_size(dd)) % 16)
-    return SB_ERR_UNSUPPORTED;
+  // 16-byte aligned row starts and strides (shard_bounds aligns slice starts); any length
+  if (!vec_ok(dd, p_logits) || !vec_ok(dd, q_logits)) return SB_ERR_UNSUPPORTED;
   const Workspace w = carve(*dd, workspace);
   if (workspace_bytes < w.bytes) return SB_ERR_WORKSPACE;
   ShardSelParams p{};

@@ -369,6 +369,27 @@ __global__ void __launch_bounds__(NT) k_rows(RowsParams p, bool vec_ok) {
     stream_pair<T, NA, NT, U>(prow, qrow, d.V, vec_ok, pa, qa);
     const RowStat ps = block_reduce<NT>(fold(pa), red);
     const RowStat qs = block_reduce<NT>(fold(qa), red);
+    if (p.partial) {  // a7: this shard's row states and token logits (any row length)
+      const bool branch_row = (un.slot == 0 && un.i == un.in.s);
+      const int ntok = branch_row ? d.K : 1;
+      if (tid < ntok && un.i < un.in.L) {
+        const int64_t et = ent(d, un.b, branch_row ? tid : un.slot, un.i);
+        const int xl = __ldg(p.tok + et) - p.v_offset;
+        const bool mine = xl >= 0 && xl < d.V;
+        p.tokpart[et] = make_float2(mine ? ld_scalar(prow + xl) : -CUDART_INF_F,
+                                    mine ? ld_scalar(qrow + xl) : -CUDART_INF_F);
+      }
+      if (tid == 0) {
+        ShardRow r;
+        r.pm = ps.m; r.pms = ps.ms; r.pz = ps.z;
+        r.qm = qs.m; r.qms = qs.ms; r.qz = qs.z; r.qs1 = qs.s1;
+        r.qidx = (qs.idx == 0x7fffffff) ? qs.idx : qs.idx + p.v_offset;
+        r.qfin = qs.m > -CUDART_INF_F && qs.m < CUDART_INF_F;  // unclamped inputs: the true maximum
+        p.rowpart[ent(d, un.b, un.slot, un.i)] = r;
+      }
+      __syncthreads();
+      continue;
+    }
     unit_epilogue(p, un, prow, qrow, ps, qs, tid, NT, &s_last, &s_st, [] { __syncthreads(); });
   }
 }
@@ -1310,7 +1331,7 @@ sb_status sb_rows_partial(const sb_dims* dd, const void* p_logits, const void* q
   const Workspace w = carve(*dd, workspace);
   if (workspace_bytes < w.bytes) return SB_ERR_WORKSPACE;
   const bool vok = vec_ok(dd, p_logits) && vec_ok(dd, q_logits);
-  if (!vok || ((size_t)dd->V * elem_size(dd)) % 16) return SB_ERR_UNSUPPORTED;
+  const size_t row_bytes = (size_t)dd->V * elem_size(dd);
   const Dims d = to_dims(dd);
   if (launch_pdl(k_plan, dim3(1), dim3(1024), 0, s, d, gamma, branch_pos, w.info, w.unit_off, 1, 0,
                  (int*)nullptr, (int*)nullptr, w.seqpk) != cudaSuccess)
@@ -1324,7 +1345,14 @@ sb_status sb_rows_partial(const sb_dims* dd, const void* p_logits, const void* q
   const size_t per = (size_t)dd->B * dd->K * (dd->G + 1);
   p.rowpart = reinterpret_cast<ShardRow*>(partial);
   p.tokpart = reinterpret_cast<float2*>(reinterpret_cast<char*>(partial) + per * sizeof(ShardRow));
-  return dd->dtype == SB_BF16 ? launch_rows_variant<__nv_bfloat16>(p, s) : launch_rows_variant<float>(p, s);
+  if (vok && row_bytes % 16 == 0 && !tma_disabled())
+    return dd->dtype == SB_BF16 ? launch_rows_variant<__nv_bfloat16>(p, s) : launch_rows_variant<float>(p, s);
+  // a ragged shard (row length not a 16-byte multiple, e.g. the last slice) or a
+  // misaligned one: the register-staged kernel, any alignment
+  if (dd->dtype == SB_BF16)
+    return row_bytes <= 131072 ? launch_rows<__nv_bfloat16, 128, 4>(p, vok, s)
+                               : launch_rows<__nv_bfloat16, 256, 4>(p, vok, s);
+  return row_bytes <= 131072 ? launch_rows<float, 128, 4>(p, vok, s) : launch_rows<float, 256, 4>(p, vok, s);
 }
 
 static sb_status verify_impl(const sb_dims* dd, const void* p_logits, const void* q_logits, const int32_t* tok,

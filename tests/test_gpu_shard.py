@@ -30,6 +30,9 @@ CASES = [
     ("bf16_V32000_alg1", dict(name="c2", V=32000, B=24, layout="mixed"), (2, 8), 1),
     ("f32_V4096", dict(name="c1", V=4096, B=32, rounds=1, K=3, G=6, layout="mixed"), (2, 4), 0),
     ("bf16_uneven_V5000", dict(name="c4", V=5000, B=16, K=2, G=5, layout="mixed"), (3,), 0),
+    # ragged last slices (row lengths not 16-byte multiples): register-staged partial pass
+    ("f32_ragged_V3001", dict(name="c1", V=3001, B=24, rounds=1, K=3, G=6, layout="mixed"), (2, 3, 8), 0),
+    ("bf16_ragged_V5003", dict(name="c2", V=5003, B=24, K=3, G=7, layout="mixed"), (2, 4), 1),
 ]
 
 
