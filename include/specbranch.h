@@ -191,11 +191,11 @@ sb_status sb_select_branch(const sb_dims* d, const void* p_logits, const void* q
 
 /*
  * sb_verify_select — sb_verify_branches followed by sb_select_branch: every output of
- * both calls, with the same meaning, in one call (one workspace, one stream).  By default
- * the two kernels run back to back; with SB_FUSED_STEP=1 in the environment a single
- * persistent launch interleaves each sequence's sample unit a few waves of row pairs
- * behind its last row pair (correct, but measured slower on B200).
- * Unsharded only.
+ * both calls, with the same meaning, in one call (one workspace, one stream).  Small
+ * problems (as sb_step_adaptive) run as one persistent launch with V-split rows
+ * (sb_flow.cu); otherwise the two streaming kernels run back to back (with
+ * SB_FUSED_STEP=1 in the environment a single persistent TMA-ring launch instead; correct,
+ * measured slower on B200).  Unsharded only.
  */
 sb_status sb_verify_select(const sb_dims* d, const void* p_logits, const void* q_logits,
                            const int32_t* tok, const float* u, const float* us,
@@ -206,6 +206,31 @@ sb_status sb_verify_select(const sb_dims* d, const void* p_logits, const void* q
                            int32_t* out_tok, int32_t* y_tok, int32_t* y_kind, int32_t* offsets,
                            int32_t* packed_tok, int32_t* path_rolled, int32_t* branch_discarded,
                            uint32_t* keep_mask, float* resid_mass, void* workspace,
+                           size_t workspace_bytes, sb_stream_t stream);
+
+/*
+ * sb_step_adaptive — the whole adaptive-gamma step in one call:
+ * sb_draft_confidence on the slot-0 draft rows (SB_CONF_TOP1, lambda unused, Eq. 6 stop
+ * with eps, Eq. 7 k with k_max), gamma_b = max(1, stop_b) (written to c_gamma_next), then
+ * sb_verify_branches and sb_select_branch with that gamma and branch_pos.  Every output
+ * has the meaning of the corresponding call (c_* arrays [B][G] / [B] as sb_draft_confidence
+ * with K = 1).  Small problems (unsharded, 16-byte aligned rows of 16-byte multiples,
+ * B <= 1024, <= ~1 GB of rows) run as ONE persistent launch that splits every row into
+ * V-segments (sb_flow.cu); larger ones as the three streaming kernels, the verify reusing
+ * the confidence pass's row states.  conf_workspace: sb_workspace_bytes of the slot-0
+ * dims (K = 1, seq_stride of d), zero-filled once; workspace: sb_workspace_bytes(d).
+ * Errors as the three calls; G must be >= 1.
+ */
+sb_status sb_step_adaptive(const sb_dims* d, const void* p_logits, const void* q_logits, const int32_t* tok,
+                           const float* u, const float* us, const int32_t* branch_pos, sb_select_rule rule,
+                           float eps, int32_t k_max, float* c_top1_prob, int32_t* c_top1_id, float* c_entropy,
+                           float* c_stat, int32_t* c_stop, int32_t* c_k_next, int32_t* c_gamma_next, float* lse_p,
+                           float* lse_q, float* p_tok, float* q_tok, uint32_t* acc_mask, int32_t* n_acc,
+                           float* top1_q, int32_t* top1_id_q, float* entropy_q, int32_t* status, int32_t* sel_k,
+                           int32_t* commit_len, int32_t* out_tok, int32_t* y_tok, int32_t* y_kind,
+                           int32_t* offsets, int32_t* packed_tok, int32_t* path_rolled,
+                           int32_t* branch_discarded, uint32_t* keep_mask, float* resid_mass,
+                           void* conf_workspace, size_t conf_workspace_bytes, void* workspace,
                            size_t workspace_bytes, sb_stream_t stream);
 
 /*

@@ -14,10 +14,11 @@ SB_BF16, SB_F32 = 0, 1
 SB_SELECT_EQ9, SB_SELECT_ALG1 = 0, 1
 SB_CONF_TOP1, SB_CONF_TOKEN, SB_CONF_ENTROPY = 0, 1, 2
 SB_ST_GAMMA_CLAMPED, SB_ST_BRANCH_CLAMPED, SB_ST_BAD_TOKEN, SB_ST_NONFINITE, SB_ST_ZERO_RESID = 1, 2, 4, 8, 16
+SB_ST_BAD_PARENT, SB_ST_RANGE = 32, 64
 
 # every symbol include/specbranch.h declares
 EXPORTS = ("sb_version", "sb_status_string", "sb_workspace_bytes", "sb_verify_branches",
-           "sb_select_branch", "sb_verify_select", "sb_verify_branches_reuse", "sb_draft_confidence", "sb_spawn_branches", "sb_kv_rollback", "sb_tree_workspace_bytes", "sb_tree_verify", "sb_hrad_workspace_bytes", "sb_hrad_predict", "sb_shard_partial_bytes", "sb_shard_verify_local",
+           "sb_select_branch", "sb_verify_select", "sb_step_adaptive", "sb_verify_branches_reuse", "sb_draft_confidence", "sb_spawn_branches", "sb_kv_rollback", "sb_tree_workspace_bytes", "sb_tree_verify", "sb_hrad_workspace_bytes", "sb_hrad_predict", "sb_shard_partial_bytes", "sb_shard_verify_local",
            "sb_shard_verify_combine", "sb_shard_select_local", "sb_shard_select_sample",
            "sb_shard_select_commit", "sb_comm_unique_id_bytes", "sb_comm_unique_id", "sb_comm_create",
            "sb_comm_destroy")
@@ -47,6 +48,7 @@ _SIGS = {
     "sb_select_branch": ([_D] + [_P] * 8 + [_I] + [_P] * 14 + [_S, _P], _I),
     "sb_draft_confidence": ([_D, _P, _P, _I, _F, _F, ctypes.c_int32] + [_P] * 10 + [_S, _P], _I),
     "sb_verify_select": ([_D] + [_P] * 7 + [_I] + [_P] * 22 + [_S, _P], _I),
+    "sb_step_adaptive": ([_D] + [_P] * 6 + [_I, _F, ctypes.c_int32] + [_P] * 7 + [_P] * 21 + [_P, _S, _P, _S, _P], _I),
     "sb_spawn_branches": ([_D, _P, _P, _P, _I, ctypes.c_int32] + [_P] * 4 + [_P], _I),
     "sb_kv_rollback": ([_I, _I, _I, _P, ctypes.c_int64, ctypes.c_int64, _P, _P, _P], _I),
     "sb_tree_workspace_bytes": ([_D], _S),

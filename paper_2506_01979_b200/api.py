@@ -131,6 +131,28 @@ def sb_verify_select(d, p_logits, q_logits, tok, u, us, gamma, branch_pos, rule,
     L.check(rc, "sb_verify_select")
 
 
+def sb_step_adaptive(d, p_logits, q_logits, tok, u, us, branch_pos, rule, eps, k_max, buf: "StepBuffers",
+                     stream=None):
+    """The adaptive-gamma step ([confidence -> gamma] -> verify -> select) in one C-ABI call;
+    confidence outputs into buf.c_* (slot-0 view, K = 1), the rest as sb_verify_select."""
+    rc = L.lib().sb_step_adaptive(
+        ctypes.byref(d), _ptr(p_logits, LOG, "p_logits"), _ptr(q_logits, LOG, "q_logits"), _ptr(tok, I32, "tok"),
+        _ptr(u, F32, "u"), _ptr(us, F32, "us"), _ptr(branch_pos, I32, "branch_pos"), int(rule), float(eps),
+        int(k_max), _ptr(buf.c_top1, F32, "c_top1"), _ptr(buf.c_id, I32, "c_id"), _ptr(buf.c_ent, F32, "c_ent"),
+        _ptr(buf.c_stat, F32, "c_stat"), _ptr(buf.c_stop, I32, "c_stop"), _ptr(buf.c_knext, I32, "c_knext"),
+        _ptr(buf.c_gamma, I32, "c_gamma"), _ptr(buf.lse_p, F32, "lse_p"), _ptr(buf.lse_q, F32, "lse_q"),
+        _ptr(buf.p_tok, F32, "p_tok"), _ptr(buf.q_tok, F32, "q_tok"), _ptr(buf.acc_mask, I32, "acc_mask"),
+        _ptr(buf.n_acc, I32, "n_acc"), _ptr(buf.top1_q, F32, "top1_q"), _ptr(buf.top1_id_q, I32, "top1_id_q"),
+        _ptr(buf.entropy_q, F32, "entropy_q"), _ptr(buf.status, I32, "status"), _ptr(buf.sel_k, I32, "sel_k"),
+        _ptr(buf.commit_len, I32, "commit_len"), _ptr(buf.out_tok, I32, "out_tok"), _ptr(buf.y_tok, I32, "y_tok"),
+        _ptr(buf.y_kind, I32, "y_kind"), _ptr(buf.offsets, I32, "offsets"), _ptr(buf.packed_tok, I32, "packed_tok"),
+        _ptr(buf.path_rolled, I32, "path_rolled"), _ptr(buf.branch_discarded, I32, "branch_discarded"),
+        _ptr(buf.keep_mask, I32, "keep_mask"), _ptr(buf.resid_mass, F32, "resid_mass"),
+        _ptr(buf.conf_workspace, torch.uint8, "conf_workspace"), buf.conf_workspace.numel(),
+        _ptr(buf.workspace, torch.uint8, "workspace"), buf.workspace.numel(), _stream(stream))
+    L.check(rc, "sb_step_adaptive")
+
+
 def sb_draft_confidence(d, q_logits, tok, mode, eps, lam, k_max, top1_prob, top1_id, entropy,
                         tok_prob, stat, stop, k_next, gamma_next, workspace, stream=None):
     rc = L.lib().sb_draft_confidence(
@@ -287,22 +309,27 @@ def verify_step(d: L.sb_dims, inp: dict, buf: StepBuffers, rule: int = SB_SELECT
 
     inp: PL, QL, tok, u, us, gamma, branch_pos device tensors (synth.generate layout).
     With adaptive=True gamma_b = max(1, stop_b) of the slot-0 draft rows (Eq. 6, TOP1)
-    replaces inp["gamma"] and s_b = 0, and the verify pass reuses the
-    confidence pass's slot-0 draft-row states (sb_verify_branches_reuse).  Otherwise
-    fused=True runs verify + select through sb_verify_select, fused=False issues the two
-    calls.
+    replaces inp["gamma"]: with fused=True through sb_step_adaptive
+    (one call; one launch for small batches), with fused=False as sb_draft_confidence ->
+    sb_verify_branches_reuse (the confidence pass's slot-0 draft-row states) ->
+    sb_select_branch.  Otherwise fused=True runs verify + select through sb_verify_select,
+    fused=False issues the two calls.
     """
     gamma = inp["gamma"]
     if adaptive and (comm is not None or (d.v_total and d.v_total != d.V)):
         # sb_draft_confidence scores whole draft rows; a vocabulary shard would score its
         # slice only and every rank would take a different gamma (ADVICE r1)
         raise ValueError("adaptive gamma is not supported on vocabulary shards (sb_draft_confidence is unsharded)")
+    PL, QL = views if views is not None else (inp["PL"], inp["QL"])
+    if adaptive and fused and comm is None:  # the whole adaptive step in one call
+        sb_step_adaptive(d, PL, QL, inp["tok"], inp["u"], inp["us"], inp["branch_pos"], rule, eps, k_max, buf,
+                         stream)
+        return buf.c_gamma.view(-1)
     if adaptive:
         sb_draft_confidence(conf_dims(d), inp["QL"], None, SB_CONF_TOP1, eps, 1.0, k_max,
                             buf.c_top1, buf.c_id, buf.c_ent, None, buf.c_stat, buf.c_stop,
                             buf.c_knext, buf.c_gamma, buf.conf_workspace, stream)
         gamma = buf.c_gamma.view(-1)
-    PL, QL = views if views is not None else (inp["PL"], inp["QL"])
     if adaptive and comm is None:  # the confidence pass already streamed slot 0's draft rows
         sb_verify_branches_reuse(d, PL, QL, inp["tok"], inp["u"], gamma, inp["branch_pos"],
                                  buf.lse_p, buf.lse_q, buf.p_tok, buf.q_tok, buf.acc_mask, buf.n_acc,

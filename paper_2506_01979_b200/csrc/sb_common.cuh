@@ -685,6 +685,22 @@ __device__ __forceinline__ bool row_has_finite_bf16(const __nv_bfloat16* row, in
   return __any_sync(0xffffffffu, any);
 }
 
+// The class of a q row reduced from clamped bf16 inputs (LazyAcc::add_bf16): a clamped
+// maximum of exactly -2^97 means "outside the input domain" if the row holds a finite
+// entry and "all -inf" otherwise (one warp re-reads the row; never on a real row).
+// Warp-uniform call.
+template <typename T>
+__device__ __forceinline__ RowOut finish_q(const RowStat& qs, const T* qrow, int V) {
+  RowOut qo = finish(qs);
+  if constexpr (sizeof(T) == 2) {
+    if (qs.m == kMaskedLogit && !row_has_finite_bf16(reinterpret_cast<const __nv_bfloat16*>(qrow), V)) {
+      qo.st = SB_ST_NONFINITE;
+      qo.finite = false;
+    }
+  }
+  return qo;
+}
+
 // Warp-level inclusive scan (Kogge-Stone), fixed order.
 __device__ __forceinline__ float warp_incl_scan(float x) {
   const int lane = threadIdx.x & 31;

@@ -465,19 +465,6 @@ __device__ __forceinline__ RowStat warp_part(const LazyAcc<kQ, 4>& a, const T* r
 }
 
 // Epilogue of one unit by one warp, with the token data already prefetched.
-// The class of a q row reduced from clamped bf16 inputs (LazyAcc::add_bf16): a clamped
-// maximum of exactly -2^97 means "outside the input domain" if the row holds a finite
-// entry and "all -inf" otherwise (one warp re-reads the row; never on a real row).
-template <typename T>
-__device__ __forceinline__ RowOut finish_q(const RowStat& qs, const T* qrow, int V) {
-  RowOut qo = finish(qs);
-  if constexpr (sizeof(T) == 2) {
-    if (qs.m == kMaskedLogit && !row_has_finite_bf16(reinterpret_cast<const __nv_bfloat16*>(qrow), V))
-      qo.st = SB_ST_NONFINITE;
-  }
-  return qo;
-}
-
 template <typename T>
 __device__ __forceinline__ void warp_epilogue(const RowsParams& p, const Unit& un, const RowStat& ps,
                                               const RowStat& qs, const T* qrow, int x, float lpx, float lqx,
@@ -1315,6 +1302,18 @@ static sb_status launch_rows_variant(const RowsParams& p, cudaStream_t s) {
 
 using namespace sb;
 
+namespace sb {
+bool flow_eligible(const sb_dims* dd, const void* PL, const void* QL);
+}
+sb_status sb_flow_verify_select(const sb_dims* dd, const void* p_logits, const void* q_logits, const int32_t* tok,
+                                const float* u, const float* us, const int32_t* gamma, const int32_t* branch_pos,
+                                sb_select_rule rule, float* lse_p, float* lse_q, float* p_tok, float* q_tok,
+                                uint32_t* acc_mask, int32_t* n_acc, float* top1_q, int32_t* top1_id_q,
+                                float* entropy_q, int32_t* status, int32_t* sel_k, int32_t* commit_len,
+                                int32_t* out_tok, int32_t* y_tok, int32_t* y_kind, int32_t* offsets,
+                                int32_t* packed_tok, int32_t* path_rolled, int32_t* branch_discarded,
+                                uint32_t* keep_mask, float* resid_mass, void* workspace, cudaStream_t s);
+
 struct sb_comm;
 sb_status sb_shard_verify_nccl(const sb_dims* d, const void* p_logits, const void* q_logits, const int32_t* tok,
                                const float* u, const int32_t* gamma, const int32_t* branch_pos, float* lse_p,
@@ -1455,6 +1454,11 @@ extern "C" sb_status sb_verify_select(const sb_dims* dd, const void* p_logits, c
   if (workspace_bytes < w.bytes) return SB_ERR_WORKSPACE;
   const bool vok = vec_ok(dd, p_logits) && vec_ok(dd, q_logits);
   const size_t row_bytes = (size_t)dd->V * elem_size(dd);
+  if (flow_eligible(dd, p_logits, q_logits))  // small batches: one launch (sb_flow.cu)
+    return sb_flow_verify_select(dd, p_logits, q_logits, tok, u, us, gamma, branch_pos, rule, lse_p, lse_q, p_tok,
+                                 q_tok, acc_mask, n_acc, top1_q, top1_id_q, entropy_q, status, sel_k, commit_len,
+                                 out_tok, y_tok, y_kind, offsets, packed_tok, path_rolled, branch_discarded,
+                                 keep_mask, resid_mass, workspace, (cudaStream_t)stream);
   // The single-launch fused kernel (k_step_tma) is correct but measured slower than the
   // two launches on B200 (C4: 6.88 vs 6.70 ms), so it is opt-in.
   const char* fz = getenv("SB_FUSED_STEP");
