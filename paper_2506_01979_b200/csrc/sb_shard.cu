@@ -168,6 +168,7 @@ __global__ void __launch_bounds__(128) k_shard_combine(ShardCombineParams p) {
 struct ShardSelParams {
   Dims d;
   int v_offset, v_total, rule, nseg;
+  bool vec;  // 16-byte aligned rows: vector loads (else scalar)
   const void* PL;
   const void* QL;
   const int* tok;
@@ -187,7 +188,8 @@ struct ShardSelParams {
 
 template <typename T>
 __device__ __forceinline__ void seg_values(const T* prow, const T* qrow, uint32_t row_bytes, int sI,
-                                           bool resid, float MSp, float iZp, float MSq, float iZq, float* r) {
+                                           bool resid, float MSp, float iZp, float MSq, float iZq, float* r,
+                                           bool vec) {
   constexpr int E = Vec<T>::E;
   const int lane = threadIdx.x & 31;
   const uint32_t off = (uint32_t)sI * 512 + lane * 16;
@@ -195,12 +197,12 @@ __device__ __forceinline__ void seg_values(const T* prow, const T* qrow, uint32_
                             : make_uint4(0xff800000u, 0xff800000u, 0xff800000u, 0xff800000u);
   uint4 vq = vp;
   float lp[E], lq[E];
-  if (off + 16 <= row_bytes) {
+  if (vec && off + 16 <= row_bytes) {
     vp = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(prow) + off));
     if (resid) vq = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(qrow) + off));
     Vec<T>::unpack(vp, lp);
     Vec<T>::unpack(vq, lq);
-  } else {  // the ragged end of a shard row (length not a multiple of 16 bytes): scalar, -inf past V
+  } else {  // unaligned rows, or the ragged end of a shard row: scalar, -inf past V
     const int v0 = (int)(off / sizeof(T)), V = (int)(row_bytes / sizeof(T));
 #pragma unroll
     for (int e = 0; e < E; ++e) {
@@ -294,13 +296,13 @@ __global__ void __launch_bounds__(256) k_shard_select_local(ShardSelParams p) {
   for (int sI = warp; sI < p.nseg; sI += 8) {
     float r[E];
     if (kind == 1) {
-      seg_values<T>(prow, qrow, row_bytes, sI, true, rs.x, iZp, rs.z, iZq, r);
+      seg_values<T>(prow, qrow, row_bytes, sI, true, rs.x, iZp, rs.z, iZq, r, p.vec);
       const float incl = warp_scan_rn2(seq_sum_rn<E>(r));
       if (lane == 31) segR[sI] = incl;
     } else if (lane == 31) {
       segR[sI] = 0.f;
     }
-    seg_values<T>(prow, qrow, row_bytes, sI, false, rs.x, iZp, rs.z, iZq, r);
+    seg_values<T>(prow, qrow, row_bytes, sI, false, rs.x, iZp, rs.z, iZq, r, p.vec);
     const float inclp = warp_scan_rn2(seq_sum_rn<E>(r));
     if (lane == 31) segP[sI] = inclp;
   }
@@ -400,7 +402,7 @@ __global__ void __launch_bounds__(128) k_shard_sample(ShardSelParams p) {
         const T* qrow = static_cast<const T*>(p.QL) + row_off(d, b, slot, row);
         float r[E];
         seg_values<T>(prow, qrow, (uint32_t)d.V * sizeof(T), sStar, resid, rs.x, 1.f / rs.y, rs.z,
-                      1.f / rs.w, r);
+                      1.f / rs.w, r, p.vec);
         const float inc = warp_scan_rn2(seq_sum_rn<E>(r));
         float Fv = __shfl_up_sync(0xffffffffu, inc, 1);
         if (lane == 0) Fv = 0.f;
@@ -562,11 +564,10 @@ extern "C" sb_status sb_shard_select_local(const sb_dims* dd, const void* p_logi
   if (!dims_valid(dd)) return SB_ERR_INVALID_ARG;
   if (!p_logits || !q_logits || !tok || !u || !n_acc || !mass || !workspace) return SB_ERR_INVALID_ARG;
   if (rule != SB_SELECT_EQ9 && rule != SB_SELECT_ALG1) return SB_ERR_INVALID_ARG;
-  // 16-byte aligned row starts and strides (shard_bounds aligns slice starts); any length
-  if (!vec_ok(dd, p_logits) || !vec_ok(dd, q_logits)) return SB_ERR_UNSUPPORTED;
   const Workspace w = carve(*dd, workspace);
   if (workspace_bytes < w.bytes) return SB_ERR_WORKSPACE;
   ShardSelParams p{};
+  p.vec = vec_ok(dd, p_logits) && vec_ok(dd, q_logits);  // else scalar loads (any alignment / length)
   p.d = to_dims(dd); p.v_offset = dd->v_offset; p.v_total = dd->v_total; p.rule = rule; p.nseg = nseg_of(dd);
   p.PL = p_logits; p.QL = q_logits; p.tok = tok; p.u = u; p.n_acc = n_acc; p.info = w.info;
   p.rowstat = w.rowstat; p.tok_lp = w.tok_lp; p.dec = w.dec; p.segs = w.segs;
@@ -585,6 +586,7 @@ extern "C" sb_status sb_shard_select_sample(const sb_dims* dd, const double* gat
   const Workspace w = carve(*dd, workspace);
   if (workspace_bytes < w.bytes) return SB_ERR_WORKSPACE;
   ShardSelParams p{};
+  p.vec = vec_ok(dd, p_logits) && vec_ok(dd, q_logits);
   p.d = to_dims(dd); p.v_offset = dd->v_offset; p.v_total = dd->v_total; p.nseg = nseg_of(dd);
   p.PL = p_logits; p.QL = q_logits; p.us = us; p.info = w.info; p.rowstat = w.rowstat; p.dec = w.dec;
   p.segs = w.segs; p.gmass = reinterpret_cast<const double2*>(gathered_mass); p.nranks = nranks; p.rank = rank;
