@@ -29,12 +29,17 @@
 #include <cstdlib>
 
 #include "sb_host.h"
+#include "sb_ring.cuh"
 #include "sb_sample.cuh"
 
 namespace sb {
 
 constexpr int kFT = 256;  // threads per CTA
 constexpr int kFW = kFT / 32;
+constexpr int kSW = 6;          // stream warps (0..5): load, accumulate, warp-reduce
+constexpr int kST = kSW * 32;
+constexpr int kEW = kFW - kSW;  // finalizer warps (6, 7): combine, global partials, epilogues
+constexpr int kNSlot = 4;       // items in flight between the two roles
 constexpr int kFU = 4;  // 16-byte vectors per thread per row in flight
 constexpr int kFlowMaxB = 1024;
 constexpr int kMinSegBytes = 8192;
@@ -95,17 +100,17 @@ __device__ __forceinline__ void seg_stream(const T* prow, const T* qrow, int v0,
   constexpr int E = Vec<T>::E;
   const uint4* pv = reinterpret_cast<const uint4*>(prow);
   const uint4* qv = reinterpret_cast<const uint4*>(qrow);
-  for (int base = v0 + (int)threadIdx.x; base - (int)threadIdx.x < v1; base += kFT * kFU) {
+  for (int base = v0 + (int)threadIdx.x; base - (int)threadIdx.x < v1; base += kST * kFU) {
     uint4 xp[kFU], xq[kFU];
 #pragma unroll
     for (int j = 0; j < kFU; ++j) {
-      const int v = base + j * kFT;
+      const int v = base + j * kST;
       if (HASP) xp[j] = v < v1 ? ldg_stream(pv + v) : neg_inf_vec<T>();
       if (HASQ) xq[j] = v < v1 ? ldg_stream(qv + v) : neg_inf_vec<T>();
     }
 #pragma unroll
     for (int j = 0; j < kFU; ++j) {
-      const int v = base + j * kFT;
+      const int v = base + j * kST;
       if constexpr (sizeof(T) == 2) {
         if (HASP) acc_vecs_bf16<1>(pa, &xp[j], v);
         if (HASQ) {
@@ -147,15 +152,12 @@ __device__ __forceinline__ void seg_stream(const T* prow, const T* qrow, int v0,
   }
 }
 
-// Both states block-reduced (fp64 sums, exact max / first index); valid in every thread.
-__device__ __forceinline__ void block_pair(const LazyAcc<false, 4>& pa, const LazyAcc<true, 4>& qa, int qidx,
-                                           RowStat* red, RowStat& ps, RowStat& qs, bool hasp, bool hasq) {
-  if (hasp) ps = block_reduce<kFT>(fold_lazy(pa), red);
-  if (hasq) {
-    RowStat s = fold_lazy(qa);
-    s.idx = qidx;
-    qs = block_reduce<kFT>(s, red);
-  }
+// A stream warp's state (fp64 sums, exact max / first index) reduced over its 32 lanes
+// (fixed tree order).
+__device__ __forceinline__ RowStat warp_state(RowStat s) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s = combine(s, shfl_xor(s, o));
+  return s;
 }
 
 __device__ __forceinline__ RowStat ldcg_rowstat(const RowStat* src) {
@@ -165,34 +167,44 @@ __device__ __forceinline__ RowStat ldcg_rowstat(const RowStat* src) {
   return x;
 }
 
-// Segment partials -> the last arriving CTA (returns true there, with the combined
-// states of all S segments in segment order, in thread 0).
-__device__ __forceinline__ bool last_segment(RowStat* part, int base, int S, int nst, int* cnt, RowStat* st,
-                                             int* s_flag) {
-  if (S == 1) {
-    __syncthreads();  // st (shared) written by thread 0
-    return true;
-  }
-  if (threadIdx.x == 0) {
+// Finalizer warp: publish this CTA's segment state(s) st[0..nst) of item `base` (segment
+// base % S of a row) and, on the last arriving CTA, return true with the states of all S
+// segments combined (lanes load the partials in parallel, fixed tree order) in st.
+__device__ __forceinline__ bool warp_last_segment(RowStat* part, int base, int S, int nst, int* cnt, RowStat* st) {
+  if (S == 1) return true;
+  const int lane = threadIdx.x & 31;
+  int last = 0;
+  if (lane == 0) {
     for (int k = 0; k < nst; ++k) part[(int64_t)base * nst + k] = st[k];
     __threadfence();
-    s_flag[0] = (atomicAdd(cnt, 1) == S - 1);
+    last = (atomicAdd(cnt, 1) == S - 1);
   }
-  __syncthreads();
-  const bool last = s_flag[0] != 0;
-  if (last && threadIdx.x == 0) {
-    __threadfence();
-    const int first = base - base % S;
-    for (int k = 0; k < nst; ++k) {
-      RowStat r = rowstat_empty();
-      for (int j = 0; j < S; ++j) r = combine(r, ldcg_rowstat(part + (int64_t)(first + j) * nst + k));
-      st[k] = r;
-    }
-    *cnt = 0;  // leave the workspace re-usable
+  last = __shfl_sync(0xffffffffu, last, 0);
+  if (!last) return false;
+  __threadfence();
+  const int first = base - base % S;
+  for (int k = 0; k < nst; ++k) {
+    RowStat r = rowstat_empty();
+    for (int j = lane; j < S; j += 32) r = combine(r, ldcg_rowstat(part + (int64_t)(first + j) * nst + k));
+    st[k] = warp_state(r);
   }
-  __syncthreads();
-  return last;
+  if (lane == 0) *cnt = 0;  // leave the workspace re-usable
+  return true;
 }
+
+// Stream-warp -> finalizer-warp handoff of one item (the shared-memory slot ring).
+struct FSlot {
+  RowStat part[kSW][2];
+};
+struct FlowSmem {
+  uint64_t full[kNSlot], empty[kNSlot];
+  FSlot slot[kNSlot];
+  int off[kFlowMaxB + 1];
+  int pk[kFlowMaxB];
+  int w[kFW];
+  float fred[kSW];
+  double scale[kEW][kFlowMaxScale];
+};
 
 // ---------------------------------------------------------------- phase C epilogue
 template <typename T>
@@ -573,49 +585,92 @@ __device__ void sample_final(const FlowParams& p, int b, int4 D, int s, int L, d
 }
 
 // ---------------------------------------------------------------- the kernel
+// Warp roles: warps 0..kSW-1 stream item segments (register-staged 16-byte loads, kFU
+// vectors per row per thread in flight) and hand each warp's reduced state to a
+// finalizer warp through a shared-memory slot (mbarrier full / empty); the kEW finalizer
+// warps (items alternate between them) combine the states, publish segment partials,
+// and run the epilogues (token tests, n_k, the decision, the sample, the commit) while
+// the stream warps already load the next items.
+template <typename T>
+__device__ __forceinline__ void flow_handoff(FlowSmem& S, int li, const RowStat& a, const RowStat& b) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int sl = li % kNSlot;
+  const uint32_t ph = (uint32_t)(li / kNSlot) & 1u;
+  if (lane == 0) {
+    mbar_wait(&S.empty[sl], ph ^ 1u);
+    S.slot[sl].part[warp][0] = a;
+    S.slot[sl].part[warp][1] = b;
+    mbar_arrive(&S.full[sl]);
+  }
+  __syncwarp();
+}
+// Finalizer side: the kSW warp states of item li combined (lane-parallel, fixed order).
+__device__ __forceinline__ void flow_take(FlowSmem& S, int li, RowStat& a, RowStat& b) {
+  const int lane = threadIdx.x & 31;
+  const int sl = li % kNSlot;
+  const uint32_t ph = (uint32_t)(li / kNSlot) & 1u;
+  mbar_wait_parked(&S.full[sl], ph);
+  RowStat x = lane < kSW ? S.slot[sl].part[lane][0] : rowstat_empty();
+  RowStat y = lane < kSW ? S.slot[sl].part[lane][1] : rowstat_empty();
+  __syncwarp();
+  if (lane == 0) mbar_arrive(&S.empty[sl]);
+  a = warp_state(x);
+  b = warp_state(y);
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kFT, 4) k_flow(FlowParams p) {
-  __shared__ int s_off[kFlowMaxB + 1];
-  __shared__ int s_pk[kFlowMaxB];
-  __shared__ RowStat s_red[kFW];
-  __shared__ RowStat s_st[2];
-  __shared__ int s_flag[4];
-  __shared__ float s_fred[kFW];
-  __shared__ double s_scale[kFlowMaxScale];
-  __shared__ int s_w[kFW];
+  extern __shared__ __align__(16) uint8_t flow_smem[];
+  FlowSmem& S = *reinterpret_cast<FlowSmem*>(flow_smem);
   const Dims& d = p.d;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool streamer = warp < kSW;
+  const int fe = warp - kSW;  // finalizer index (streamers: < 0)
   const T* PL = static_cast<const T*>(p.PL);
   const T* QL = static_cast<const T*>(p.QL);
   const uint32_t rb = (uint32_t)d.V * sizeof(T);
   const int nv = (int)(rb / 16);
+  if (tid == 0) {
+    for (int k = 0; k < kNSlot; ++k) {
+      mbar_init(&S.full[k], kSW);
+      mbar_init(&S.empty[k], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
   pdl_wait();
+  int li = 0;  // this CTA's running item count (the slot ring position)
 
   // ---- phase C: confidence rows (slot 0, rows 0..G-1), adaptive only
   if (p.adaptive) {
     const int items = d.B * d.G * p.Sc;
-    for (int it = blockIdx.x; it < items; it += gridDim.x) {
+    for (int it = blockIdx.x; it < items; it += gridDim.x, ++li) {
       const int r = it / p.Sc, sg = it % p.Sc, b = r / d.G, i = r % d.G;
       const T* qrow = QL + row_off(d, b, 0, i);
-      const int v0 = (int)((int64_t)nv * sg / p.Sc), v1 = (int)((int64_t)nv * (sg + 1) / p.Sc);
-      LazyAcc<false, 4> pa;
-      LazyAcc<true, 4> qa;
-      qa.init();
-      int qidx = 0x7fffffff;
-      seg_stream<T, false, true>(nullptr, qrow, v0, v1, pa, qa, qidx);
-      RowStat ps, qs;
-      block_pair(pa, qa, qidx, s_red, ps, qs, false, true);
-      if (tid == 0) s_st[0] = qs;
-      if (last_segment(p.cpart, it, p.Sc, 1, p.ccnt + r, s_st, s_flag) && tid == 0)
-        conf_row_final<T>(p, b, i, s_st[0]);
-      __syncthreads();
+      if (streamer) {
+        const int v0 = (int)((int64_t)nv * sg / p.Sc), v1 = (int)((int64_t)nv * (sg + 1) / p.Sc);
+        LazyAcc<false, 4> pa;
+        LazyAcc<true, 4> qa;
+        qa.init();
+        int qidx = 0x7fffffff;
+        seg_stream<T, false, true>(nullptr, qrow, v0, v1, pa, qa, qidx);
+        RowStat qs = fold_lazy(qa);
+        qs.idx = qidx;
+        flow_handoff<T>(S, li, warp_state(qs), rowstat_empty());
+      } else if (li % kEW == fe) {
+        RowStat st[2];
+        flow_take(S, li, st[0], st[1]);
+        if (warp_last_segment(p.cpart, it, p.Sc, 1, p.ccnt + r, st) && lane == 0) conf_row_final<T>(p, b, i, st[0]);
+        __syncwarp();
+      }
     }
-    if (tid == 0)  // grid barrier: every gamma_b known
+    if (lane == 0)  // grid barrier: every gamma_b known
       while (ld_acquire(p.ctr + FC_CONF_DONE) < d.B) __nanosleep(128);
-    __syncthreads();
+    __syncwarp();
   }
 
   // ---- plan (every CTA, shared memory): clamped layout, units per sequence, scan
+  __syncthreads();
   {
     int carry = 0;
     for (int b0 = 0; b0 < d.B; b0 += kFT) {
@@ -630,7 +685,7 @@ __global__ void __launch_bounds__(kFT, 4) k_flow(FlowParams p) {
         if (s > g) { s = g; st |= SB_ST_BRANCH_CLAMPED; }
         if (s < 0) { s = 0; st |= SB_ST_BRANCH_CLAMPED; }
         const int L = (s < g) ? g : g + 1;
-        s_pk[b] = s | (g << 5) | (L << 10) | (st << 16);
+        S.pk[b] = s | (g << 5) | (L << 10) | (st << 16);
         nu = L + (d.K - 1) * (L - 1 - s);
       }
       int incl = nu;
@@ -639,35 +694,37 @@ __global__ void __launch_bounds__(kFT, 4) k_flow(FlowParams p) {
         const int yv = __shfl_up_sync(0xffffffffu, incl, o);
         if (lane >= o) incl += yv;
       }
-      if (lane == 31) s_w[warp] = incl;
+      if (lane == 31) S.w[warp] = incl;
       __syncthreads();
-      int wo = 0;
-      for (int w = 0; w < warp; ++w) wo += s_w[w];
-      if (b < d.B) s_off[b] = carry + wo + incl - nu;
-      int tot = 0;
-      for (int w = 0; w < kFW; ++w) tot += s_w[w];
+      int wo = 0, tot = 0;
+      for (int w = 0; w < kFW; ++w) {
+        if (w < warp) wo += S.w[w];
+        tot += S.w[w];
+      }
+      if (b < d.B) S.off[b] = carry + wo + incl - nu;
       carry += tot;
       __syncthreads();
     }
-    if (tid == 0) s_off[d.B] = carry;
+    if (tid == 0) S.off[d.B] = carry;
     __syncthreads();
   }
-  const int U = s_off[d.B];
+  const int U = S.off[d.B];
   const int Smax = max(1, (int)(rb / kMinSegBytes));
   const int Sr = min(Smax, max(1, (kFlowTarget + U - 1) / max(U, 1)));
 
   // ---- phase R: (row pair, segment)
-  for (int it = blockIdx.x; it < U * Sr; it += gridDim.x) {
+  for (int it = blockIdx.x; it < U * Sr; it += gridDim.x, ++li) {
+    if (!streamer && li % kEW != fe) continue;
     const int u = it / Sr, sg = it % Sr;
     int lo = 0, hi = d.B;  // sequence of unit u (binary search in shared memory)
     while (hi - lo > 1) {
       const int mid = (lo + hi) >> 1;
-      if (s_off[mid] <= u) lo = mid; else hi = mid;
+      if (S.off[mid] <= u) lo = mid; else hi = mid;
     }
-    const int b = lo, pk = s_pk[b];
+    const int b = lo, pk = S.pk[b];
     FUnit un;
     un.b = b; un.s = pk & 31; un.g = (pk >> 5) & 31; un.L = (pk >> 10) & 63; un.st = pk >> 16;
-    const int j = u - s_off[b];
+    const int j = u - S.off[b];
     if (j < un.L) { un.slot = 0; un.i = j; }
     else {
       const int per = un.L - 1 - un.s, jj = j - un.L;
@@ -677,100 +734,111 @@ __global__ void __launch_bounds__(kFT, 4) k_flow(FlowParams p) {
     const T* prow = PL + row_off(d, b, un.slot, un.i);
     const T* qrow = QL + row_off(d, b, un.slot, un.i);
     const bool reuse = p.adaptive && un.slot == 0 && un.i < d.G;  // q state from phase C
-    const int v0 = (int)((int64_t)nv * sg / Sr), v1 = (int)((int64_t)nv * (sg + 1) / Sr);
-    LazyAcc<false, 4> pa;
-    LazyAcc<true, 4> qa;
-    pa.init();
-    qa.init();
-    int qidx = 0x7fffffff;
-    if (reuse) seg_stream<T, true, false>(prow, nullptr, v0, v1, pa, qa, qidx);
-    else seg_stream<T, true, true>(prow, qrow, v0, v1, pa, qa, qidx);
-    RowStat ps, qs;
-    block_pair(pa, qa, qidx, s_red, ps, qs, true, !reuse);
-    if (tid == 0) {
-      s_st[0] = ps;
-      s_st[1] = reuse ? rowstat_empty() : qs;
+    if (streamer) {
+      const int v0 = (int)((int64_t)nv * sg / Sr), v1 = (int)((int64_t)nv * (sg + 1) / Sr);
+      LazyAcc<false, 4> pa;
+      LazyAcc<true, 4> qa;
+      pa.init();
+      qa.init();
+      int qidx = 0x7fffffff;
+      if (reuse) seg_stream<T, true, false>(prow, nullptr, v0, v1, pa, qa, qidx);
+      else seg_stream<T, true, true>(prow, qrow, v0, v1, pa, qa, qidx);
+      RowStat qs = fold_lazy(qa);
+      qs.idx = qidx;
+      flow_handoff<T>(S, li, warp_state(fold_lazy(pa)), reuse ? rowstat_empty() : warp_state(qs));
+    } else {
+      RowStat st[2];
+      flow_take(S, li, st[0], st[1]);
+      if (warp_last_segment(p.rpart, it, Sr, 2, p.rcnt + ent(d, b, un.slot, un.i), st)) {
+        const RowStat qf = reuse ? ldcg_rowstat(p.qstate + (int64_t)b * d.G + un.i) : st[1];
+        unit_final<T>(p, un, st[0], qf, prow, qrow, un.L + (d.K - 1) * (un.L - 1 - un.s));
+      }
+      __syncwarp();
     }
-    const bool last = last_segment(p.rpart, it, Sr, 2, p.rcnt + ent(d, b, un.slot, un.i), s_st, s_flag);
-    if (last && warp == 0) {
-      const RowStat qf = reuse ? ldcg_rowstat(p.qstate + (int64_t)b * d.G + un.i) : s_st[1];
-      unit_final<T>(p, un, s_st[0], qf, prow, qrow, un.L + (d.K - 1) * (un.L - 1 - un.s));
-    }
-    __syncthreads();
   }
 
   // ---- phase S: (sequence, segment) of the sampled row (pair)
   const int Ss = p.Ss, nsub = p.nsub;
-  for (int it = blockIdx.x; it < d.B * Ss; it += gridDim.x) {
+  for (int it = blockIdx.x; it < d.B * Ss; it += gridDim.x, ++li) {
+    if (!streamer && li % kEW != fe) continue;
     const int b = it / Ss, sg = it % Ss;
-    if (tid == 0)
-      while (ld_acquire(p.ready + b) == 0) __nanosleep(64);
-    __syncthreads();
-    const int4 D = __ldcg(p.dec + b);
-    const int kind = D.z, row = D.w & 0xff, sl = D.w >> 8;
-    const int s0 = (int)((int64_t)nsub * sg / Ss), s1 = (int)((int64_t)nsub * (sg + 1) / Ss);
-    float* subR = p.subs + (int64_t)b * 2 * p.sub_stride;
-    float* subP = subR + p.sub_stride;
-    if (kind != 0) {
-      const T* prow = PL + row_off(d, b, sl, row);
-      const T* qrow = QL + row_off(d, b, sl, row);
-      float MSp, MSq = 0.f, kq = 0.f;
-      if (kind == 1) {
-        const float4 rs = p.rowstat[ent(d, b, sl, row)];
-        MSp = rs.x; MSq = rs.z; kq = rs.y / rs.w;
-      } else {  // bonus row: this segment's exact maximum sets its own offset
-        float m = -CUDART_INF_F;
-        const int e0 = s0 * (kSegBytes / 16), e1 = min(s1 * (kSegBytes / 16), nv);
-        for (int v = e0 + tid; v < e1; v += kFT) {
-          float f[Vec<T>::E];
-          Vec<T>::unpack(ldg_stream(reinterpret_cast<const uint4*>(prow) + v), f);
-          m = fmaxf(m, Vec<T>::vmax(f));
-        }
+    if (streamer) {
+      if (lane == 0)
+        while (ld_acquire(p.ready + b) == 0) __nanosleep(64);
+      __syncwarp();
+      const int4 D = __ldcg(p.dec + b);
+      const int kind = D.z, row = D.w & 0xff, sl = D.w >> 8;
+      const int s0 = (int)((int64_t)nsub * sg / Ss), s1 = (int)((int64_t)nsub * (sg + 1) / Ss);
+      float* subR = p.subs + (int64_t)b * 2 * p.sub_stride;
+      float* subP = subR + p.sub_stride;
+      if (kind != 0) {
+        const T* prow = PL + row_off(d, b, sl, row);
+        const T* qrow = QL + row_off(d, b, sl, row);
+        float MSp, MSq = 0.f, kq = 0.f;
+        if (kind == 1) {
+          const float4 rs = __ldcg(p.rowstat + ent(d, b, sl, row));
+          MSp = rs.x; MSq = rs.z; kq = rs.y / rs.w;
+        } else {  // bonus row: this segment's exact maximum sets its own offset
+          float m = -CUDART_INF_F;
+          const int e0 = s0 * (kSegBytes / 16), e1 = min(s1 * (kSegBytes / 16), nv);
+          for (int v = e0 + tid; v < e1; v += kST) {
+            float f[Vec<T>::E];
+            Vec<T>::unpack(ldg_stream(reinterpret_cast<const uint4*>(prow) + v), f);
+            m = fmaxf(m, Vec<T>::vmax(f));
+          }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-        if (lane == 0) s_fred[warp] = m;
-        __syncthreads();
-        m = s_fred[0];
-        for (int w = 1; w < kFW; ++w) m = fmaxf(m, s_fred[w]);
-        if (tid == 0) p.segmax[(int64_t)b * p.segmax_stride + sg] = m;
-        MSp = offset_of(m);
-      }
-      for (int sI = s0 + warp; sI < s1; sI += kFW) {
-        float sr, sp;
-        sub_sums<T>(prow, qrow, rb, sI, kind == 1, MSp, MSq, kq, sr, sp);
-        if (lane == 0) {
-          subR[sI] = sr;
-          subP[sI] = sp;
+          for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+          if (lane == 0) S.fred[warp] = m;
+          consumer_sync(kST);
+          m = S.fred[0];
+          for (int w = 1; w < kSW; ++w) m = fmaxf(m, S.fred[w]);
+          consumer_sync(kST);  // fred reusable
+          if (tid == 0) p.segmax[(int64_t)b * p.segmax_stride + sg] = m;
+          MSp = offset_of(m);
         }
+        for (int sI = s0 + warp; sI < s1; sI += kSW) {
+          float sr, sp;
+          sub_sums<T>(prow, qrow, rb, sI, kind == 1, MSp, MSq, kq, sr, sp);
+          if (lane == 0) {
+            subR[sI] = sr;
+            subP[sI] = sp;
+          }
+        }
+        __threadfence();  // the sums (and segment max) before the handoff: read by another CTA
       }
-    }
-    __syncthreads();
-    if (tid == 0) {
-      __threadfence();
-      s_flag[0] = (atomicAdd(p.scnt + b, 1) == Ss - 1);
-    }
-    __syncthreads();
-    if (s_flag[0]) {
-      if (warp == 0) {
+      flow_handoff<T>(S, li, rowstat_empty(), rowstat_empty());
+    } else {
+      RowStat st0, st1;
+      flow_take(S, li, st0, st1);  // every stream warp's sums are written
+      int last = 0;
+      if (lane == 0) {
         __threadfence();
-        const int pk = s_pk[b];
-        sample_final<T>(p, b, D, pk & 31, (pk >> 10) & 63, s_scale);
+        last = (atomicAdd(p.scnt + b, 1) == Ss - 1);
+      }
+      last = __shfl_sync(0xffffffffu, last, 0);
+      if (last) {
+        __threadfence();
+        const int4 D = __ldcg(p.dec + b);
+        const int pk = S.pk[b];
+        sample_final<T>(p, b, D, pk & 31, (pk >> 10) & 63, S.scale[fe]);
+        int lastseq = 0;
         if (lane == 0) {
           p.scnt[b] = 0;
           p.ready[b] = 0;  // every segment of b has passed its wait
           __threadfence();
-          s_flag[1] = (atomicAdd(p.ctr + FC_SEQ_DONE, 1) == d.B - 1);
+          lastseq = (atomicAdd(p.ctr + FC_SEQ_DONE, 1) == d.B - 1);
+        }
+        lastseq = __shfl_sync(0xffffffffu, lastseq, 0);
+        if (lastseq) {  // the last sequence: offsets and the packed stream
+          __threadfence();
+          warp_offsets(d.B, d.G, p.commit_len, p.out_tok, p.offsets, p.packed_tok);
         }
       }
-      __syncthreads();
-      if (s_flag[1]) {  // the last sequence: offsets and the packed stream, whole CTA
-        __threadfence();
-        block_offsets<kFT>(d.B, d.G, p.commit_len, p.out_tok, p.offsets, p.packed_tok, s_off);
-      }
+      __syncwarp();
     }
-    __syncthreads();
   }
   // ---- the last CTA to leave resets the grid counters
+  __syncthreads();
   if (tid == 0) {
     __threadfence();
     if (atomicAdd(p.ctr + FC_EXIT, 1) == (int)gridDim.x - 1) {
@@ -820,8 +888,12 @@ FlowParams flow_params(const sb_dims* dd, const Workspace& w) {
 
 template <typename T>
 static sb_status launch_flow(const FlowParams& p, cudaStream_t s) {
-  const int grid = full_grid<k_flow<T>>(kFT);
-  return cuda_status(launch_pdl(k_flow<T>, dim3(grid), dim3(kFT), 0, s, p));
+  const int smem = (int)sizeof(FlowSmem);
+  if (ensure_smem<k_flow<T>>(smem) != cudaSuccess) return SB_ERR_CUDA;
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_flow<T>, kFT, smem);
+  const int grid = std::max(1, occ) * num_sms();  // all co-resident (the S phase spins)
+  return cuda_status(launch_pdl(k_flow<T>, dim3(grid), dim3(kFT), smem, s, p));
 }
 
 sb_status flow_run(const FlowParams& p, int dtype, cudaStream_t s) {
