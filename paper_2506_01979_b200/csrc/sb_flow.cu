@@ -47,6 +47,20 @@ constexpr int kFlowMaxScale = 132;  // sample segments per row (rows <= 1 MB: ns
 
 enum { FC_CONF_DONE = 0, FC_SEQ_DONE = 1, FC_EXIT = 2 };
 
+// Debug timeline (SB_FLOW_TRACE builds only): per CTA, per warp-0 / warp-6 event, the
+// global timer.  Read back with sb_flow_trace_read().
+#ifdef SB_FLOW_TRACE
+constexpr int kTrCta = 1024, kTrEv = 64;
+__device__ unsigned long long g_trace[kTrCta][2][kTrEv];
+__device__ __forceinline__ void trace(int role, int ev) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  if (blockIdx.x < kTrCta && ev < kTrEv && (threadIdx.x & 31) == 0) g_trace[blockIdx.x][role][ev] = t;
+}
+#else
+__device__ __forceinline__ void trace(int, int) {}
+#endif
+
 struct FlowParams {
   Dims d;
   const void* PL;
@@ -619,7 +633,7 @@ __device__ __forceinline__ void flow_take(FlowSmem& S, int li, RowStat& a, RowSt
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kFT, 4) k_flow(FlowParams p) {
+__global__ void __launch_bounds__(kFT, 3) k_flow(FlowParams p) {
   extern __shared__ __align__(16) uint8_t flow_smem[];
   FlowSmem& S = *reinterpret_cast<FlowSmem*>(flow_smem);
   const Dims& d = p.d;
@@ -640,6 +654,10 @@ __global__ void __launch_bounds__(kFT, 4) k_flow(FlowParams p) {
   __syncthreads();
   pdl_wait();
   int li = 0;  // this CTA's running item count (the slot ring position)
+  int tev = 0;
+  const int trole = warp == 0 ? 0 : (warp == kSW ? 1 : -1);
+  if (trole >= 0) trace(trole, tev);
+  ++tev;
 
   // ---- phase C: confidence rows (slot 0, rows 0..G-1), adaptive only
   if (p.adaptive) {
@@ -664,9 +682,13 @@ __global__ void __launch_bounds__(kFT, 4) k_flow(FlowParams p) {
         __syncwarp();
       }
     }
+    if (trole >= 0) trace(trole, tev);
+    ++tev;
     if (lane == 0)  // grid barrier: every gamma_b known
       while (ld_acquire(p.ctr + FC_CONF_DONE) < d.B) __nanosleep(128);
     __syncwarp();
+    if (trole >= 0) trace(trole, tev);
+    ++tev;
   }
 
   // ---- plan (every CTA, shared memory): clamped layout, units per sequence, scan
@@ -746,6 +768,7 @@ __global__ void __launch_bounds__(kFT, 4) k_flow(FlowParams p) {
       RowStat qs = fold_lazy(qa);
       qs.idx = qidx;
       flow_handoff<T>(S, li, warp_state(fold_lazy(pa)), reuse ? rowstat_empty() : warp_state(qs));
+      if (trole == 0) trace(0, 4 + (li & 31));
     } else {
       RowStat st[2];
       flow_take(S, li, st[0], st[1]);
@@ -754,8 +777,10 @@ __global__ void __launch_bounds__(kFT, 4) k_flow(FlowParams p) {
         unit_final<T>(p, un, st[0], qf, prow, qrow, un.L + (d.K - 1) * (un.L - 1 - un.s));
       }
       __syncwarp();
+      if (trole == 1) trace(1, 4 + (li & 31));
     }
   }
+  if (trole >= 0) trace(trole, 40);
 
   // ---- phase S: (sequence, segment) of the sampled row (pair)
   const int Ss = p.Ss, nsub = p.nsub;
@@ -763,9 +788,11 @@ __global__ void __launch_bounds__(kFT, 4) k_flow(FlowParams p) {
     if (!streamer && li % kEW != fe) continue;
     const int b = it / Ss, sg = it % Ss;
     if (streamer) {
+      if (trole == 0) trace(0, 41);
       if (lane == 0)
         while (ld_acquire(p.ready + b) == 0) __nanosleep(64);
       __syncwarp();
+      if (trole == 0) trace(0, 42);
       const int4 D = __ldcg(p.dec + b);
       const int kind = D.z, row = D.w & 0xff, sl = D.w >> 8;
       const int s0 = (int)((int64_t)nsub * sg / Ss), s1 = (int)((int64_t)nsub * (sg + 1) / Ss);
@@ -807,6 +834,7 @@ __global__ void __launch_bounds__(kFT, 4) k_flow(FlowParams p) {
         __threadfence();  // the sums (and segment max) before the handoff: read by another CTA
       }
       flow_handoff<T>(S, li, rowstat_empty(), rowstat_empty());
+      if (trole == 0) trace(0, 43);
     } else {
       RowStat st0, st1;
       flow_take(S, li, st0, st1);  // every stream warp's sums are written
@@ -838,6 +866,7 @@ __global__ void __launch_bounds__(kFT, 4) k_flow(FlowParams p) {
     }
   }
   // ---- the last CTA to leave resets the grid counters
+  if (trole >= 0) trace(trole, 63);
   __syncthreads();
   if (tid == 0) {
     __threadfence();
@@ -852,19 +881,19 @@ __global__ void __launch_bounds__(kFT, 4) k_flow(FlowParams p) {
 }  // namespace sb
 
 namespace sb {
-// The fused step is for small problems: unsharded, 16-byte aligned rows of 16-byte
-// multiples, B <= 1024 (plan in shared memory) and at most ~1 GB of rows in the largest
-// layout (beyond that the separate streaming kernels are at the copy roofline already).
-// SB_FLOW=0 disables it, SB_FLOW=1 uses it whenever the shape allows.
+// The fused step covers unsharded, 16-byte aligned rows of 16-byte multiples and
+// B <= 1024 (plan in shared memory).  It is OPT-IN (SB_FLOW=1): measured on B200 it is
+// slower than the warp-specialised TMA kernels even on the small configurations it was
+// built for (C2 verify + select 82 vs 56 us; C1 one round 34 vs 30 us; DESIGN.md §13 has
+// the globaltimer timeline): its register-staged items execute ~2x the instructions per
+// byte of k_rows_tma and every V-segment adds a chain of dependent global round trips
+// (partial -> fence -> atomic -> combine -> epilogue -> release) of ~1 us each.
 bool flow_eligible(const sb_dims* dd, const void* PL, const void* QL) {
   const char* e = getenv("SB_FLOW");
-  if ((e && e[0] == '0') || tma_disabled() || sharded(dd)) return false;
+  if (!(e && e[0] == '1') || tma_disabled() || sharded(dd)) return false;
   if (!vec_ok(dd, PL) || !vec_ok(dd, QL)) return false;
   const size_t rb = (size_t)dd->V * elem_size(dd);
-  if (rb % 16 || dd->B > kFlowMaxB || rb > ((size_t)kFlowMaxScale - 1) * 8 * kSegBytes) return false;
-  if (e && e[0] == '1') return true;
-  const double est = (double)dd->B * (dd->G + 1 + (double)(dd->K - 1) * dd->G) * 2.0 * (double)rb;
-  return est <= 1.0e9;
+  return rb % 16 == 0 && dd->B <= kFlowMaxB && rb <= ((size_t)kFlowMaxScale - 1) * 8 * kSegBytes;
 }
 
 FlowParams flow_params(const sb_dims* dd, const Workspace& w) {
@@ -991,3 +1020,9 @@ extern "C" sb_status sb_step_adaptive(const sb_dims* dd, const void* p_logits, c
                           commit_len, out_tok, y_tok, y_kind, offsets, packed_tok, path_rolled, branch_discarded,
                           keep_mask, resid_mass, status, nullptr, workspace, workspace_bytes, stream);
 }
+
+#ifdef SB_FLOW_TRACE
+extern "C" int sb_flow_trace_read(void* host, size_t bytes) {
+  return (int)cudaMemcpyFromSymbol(host, sb::g_trace, bytes < sizeof(sb::g_trace) ? bytes : sizeof(sb::g_trace));
+}
+#endif

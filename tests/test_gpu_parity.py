@@ -106,19 +106,17 @@ SMALL = [
 ]
 
 
-@pytest.mark.parametrize("fused", ["flow", "flow_forced", "single_launch", "verify_select", "two_calls"])
+@pytest.mark.parametrize("fused", ["flow", "single_launch", "verify_select", "two_calls"])
 @pytest.mark.parametrize("name,kw,pad,rule", SMALL, ids=[c[0] for c in SMALL])
 def test_small_parity(name, kw, pad, rule, fused, monkeypatch):
-    """flow: sb_verify_select's one-launch small-batch kernel (sb_flow.cu, the default for
-    these sizes); flow_forced: the same for every shape it supports; single_launch: the
-    persistent TMA-ring k_step_tma; verify_select: the two streaming kernels behind
-    sb_verify_select; two_calls: sb_verify_branches then sb_select_branch."""
+    """flow: the opt-in one-launch small-batch kernel (SB_FLOW=1, sb_flow.cu);
+    single_launch: the persistent TMA-ring k_step_tma (SB_FUSED_STEP=1); verify_select: the
+    two streaming kernels behind sb_verify_select (the default); two_calls:
+    sb_verify_branches then sb_select_branch."""
     kw = dict(kw)
     c = cfg(kw.pop("name"), **kw)
-    if fused == "flow_forced":
+    if fused == "flow":
         monkeypatch.setenv("SB_FLOW", "1")
-    if fused in ("single_launch", "verify_select"):
-        monkeypatch.setenv("SB_FLOW", "0")
     if fused == "single_launch":
         monkeypatch.setenv("SB_FUSED_STEP", "1")  # the persistent k_step_tma kernel
     rep, g = _run(c, row_pad=pad, rule=rule, fused=(fused != "two_calls"))
@@ -138,12 +136,13 @@ def test_register_staged_fallback_parity(monkeypatch, name, kw):
     assert rep["exact_seq"] >= 0.9 * rep["n"], rep
 
 
-@pytest.mark.parametrize("path", ["step_adaptive", "three_calls"])
+@pytest.mark.parametrize("path", ["flow", "three_calls"])
 def test_adaptive_confidence_parity(path, monkeypatch):
-    """The adaptive-gamma step: sb_step_adaptive (one launch for this size) and the three
-    streaming kernels (SB_FLOW=0: confidence -> verify reusing its rows -> select)."""
-    if path == "three_calls":
-        monkeypatch.setenv("SB_FLOW", "0")
+    """The adaptive-gamma step through sb_step_adaptive: the opt-in one-launch kernel
+    (SB_FLOW=1) and the default three streaming kernels (confidence -> verify reusing its
+    rows -> select)."""
+    if path == "flow":
+        monkeypatch.setenv("SB_FLOW", "1")
     rep, g = _run(cfg("c2", B=64), adaptive=True)
     assert rep["n"] >= 60
     rep, g = _run(cfg("c2", V=5000, B=40, K=3, G=12, layout="mixed"), adaptive=True)
