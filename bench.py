@@ -637,6 +637,8 @@ def cpu_baseline(cfg, inp, adaptive, buf, budget_s=15.0):
     B = inp["PL"].shape[0]
     gamma_all = (buf.c_gamma.view(-1) if adaptive else inp["gamma"]).cpu().numpy()
 
+    last = {}
+
     def run(idx, nth=nthreads):
         it = torch.as_tensor(idx, device=inp["PL"].device)
         sub = synth.to_numpy_inputs({k: (v.index_select(0, it) if torch.is_tensor(v) else v) for k, v in inp.items()})
@@ -646,9 +648,11 @@ def cpu_baseline(cfg, inp, adaptive, buf, budget_s=15.0):
             g = c["gamma_next"][:, 0]
         else:
             g = sub["gamma"]
-        oracle.verify(sub["PL"], sub["QL"], sub["tok"], sub["u"], sub["us"], g, sub["branch_pos"],
-                      nthreads=nth, V=sub["V"])
-        return time.time() - t0, verified_tokens(g.tolist(), sub["branch_pos"].tolist(), cfg.K)
+        o = oracle.verify(sub["PL"], sub["QL"], sub["tok"], sub["u"], sub["us"], g, sub["branch_pos"],
+                          nthreads=nth, V=sub["V"])
+        dt_ = time.time() - t0
+        last.update(idx=np.asarray(idx), o=o, gamma=np.asarray(g))
+        return dt_, verified_tokens(g.tolist(), sub["branch_pos"].tolist(), cfg.K)
 
     n = min(B, nthreads)
     dt, tk = run(np.arange(n))
@@ -658,6 +662,7 @@ def cpu_baseline(cfg, inp, adaptive, buf, budget_s=15.0):
         if n2 > n:
             dt, tk = run(np.arange(n2))
             n = n2
+    parity = parity_stats(last["o"], buf, last["idx"], last["gamma"], gamma_all)
     # the same oracle on one core, over a few sequences (SURVEY §8.4 "a 1-thread run")
     n1 = min(B, 4)
     dt1, tk1 = run(np.arange(n1), nth=1)
@@ -666,7 +671,49 @@ def cpu_baseline(cfg, inp, adaptive, buf, budget_s=15.0):
                                         f"OpenMP over sequences, fp64 plain loops",
             "cpu_model": cpu_model(),
             "single_core_value": round(tk1 / dt1, 1),
-            "single_core_sample": f"{n1} sequences on 1 thread, {dt1:.1f} s"}
+            "single_core_sample": f"{n1} sequences on 1 thread, {dt1:.1f} s",
+            "parity": parity}
+
+
+def parity_stats(o, buf, idx, gamma_o, gamma_gpu):
+    """The bench's own outputs against the oracle on the cpu_baseline sample (SURVEY §5
+    run record): discrete mismatches outside the oracle's near-tie flags, flagged
+    sequences, and the largest continuous error in units of the pass band
+    |gpu - ref| <= 1e-5 |ref| + 1e-7 (lse: relative to max(1, |lse|))."""
+    import numpy as np
+
+    import oracle
+
+    g = {k: getattr(buf, k)[idx].cpu().numpy() for k in ("n_acc", "sel_k", "commit_len", "y_tok", "y_kind",
+                                                          "out_tok", "lse_p", "lse_q", "p_tok", "q_tok",
+                                                          "top1_q", "entropy_q", "resid_mass")}
+    same_gamma = np.asarray(gamma_o) == np.asarray(gamma_gpu)[idx]
+    ties = o["ties"]
+    dec = (ties & oracle.TIE_ACC_DEC) != 0
+    samp = (ties & (oracle.TIE_SAMPLE | oracle.TIE_ILLCOND)) != 0
+    ok = same_gamma & ~dec
+    mism = np.zeros(len(idx), bool)
+    for k in ("n_acc", "out_tok"):
+        mism |= (g[k] != o[k]).reshape(len(idx), -1).any(axis=1)
+    for k in ("sel_k", "commit_len", "y_kind"):
+        mism |= g[k] != o[k]
+    mism |= (g["y_tok"] != o["y_tok"]) & ~samp
+    band = 0.0
+    for k in ("lse_p", "lse_q"):
+        r, x = o[k][ok], g[k][ok].astype(np.float64)
+        m = ~np.isnan(r) & ~np.isnan(x)
+        if m.any():
+            band = max(band, float(np.max(np.abs(x[m] - r[m]) / (1e-5 * np.maximum(1.0, np.abs(r[m]))))))
+    for k in ("p_tok", "q_tok", "top1_q", "entropy_q", "resid_mass"):
+        r, x = o[k][ok], g[k][ok].astype(np.float64)
+        m = ~np.isnan(r) & ~np.isnan(x)
+        if k == "resid_mass":
+            m &= (g["y_kind"][ok] == o["y_kind"][ok]) & ~samp[ok]
+        if m.any():
+            band = max(band, float(np.max(np.abs(x[m] - r[m]) / (1e-5 * np.abs(r[m]) + 1e-7))))
+    return {"sequences": int(ok.sum()), "discrete_mismatch": int((mism & ok).sum()),
+            "flagged_ties": int((dec | samp).sum()), "max_continuous_band": round(band, 4),
+            "note": "GPU outputs of the timed step vs the oracle on the cpu_baseline sample; band <= 1 passes"}
 
 
 def run_reference(args, rank, world):
@@ -720,6 +767,19 @@ def run_reference(args, rank, world):
     }
 
 
+def emit(line, args):
+    """Print the bench line; with --record also append it to a JSONL run record."""
+    print(json.dumps(line), flush=True)
+    if args.record:
+        import socket
+
+        rec = dict(line, recorded_at=time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime()), host=socket.gethostname(),
+                   argv=sys.argv[1:])
+        os.makedirs(os.path.dirname(os.path.abspath(args.record)), exist_ok=True)
+        with open(args.record, "a") as fh:
+            fh.write(json.dumps(rec) + "\n")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -742,6 +802,8 @@ def main():
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
                     help="sequence-sharded configs: strong = the config's batch split over the ranks "
                          "(SURVEY §8.5, default); weak = a full batch per rank")
+    ap.add_argument("--record", default=os.environ.get("SB_RUN_RECORD"),
+                    help="append the JSON line (plus time and host) to this JSONL run record (SURVEY §5)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: test-only multi-rank runs on one GPU (LOCAL_RANK modulo the device count)")
     args = ap.parse_args()
@@ -769,7 +831,7 @@ def main():
     if args.impl == "reference":
         line = run_reference(args, rank, world)
         if line is not None:
-            print(json.dumps(line), flush=True)
+            emit(line, args)
         return
     if world > 1:
         import torch
@@ -782,7 +844,7 @@ def main():
     runner = {"hrad": run_hrad, "spawn": run_next, "kv": run_next, "tree": run_next}.get(args.config, run_ours)
     line = runner(args, rank, world, local_rank)
     if line is not None:
-        print(json.dumps(line), flush=True)
+        emit(line, args)
     if world > 1:
         import torch
 

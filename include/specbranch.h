@@ -417,6 +417,14 @@ sb_status sb_comm_unique_id(void* unique_id_out);
 sb_status sb_comm_create(const void* unique_id, int32_t nranks, int32_t rank,
                          const sb_dims* max_dims, sb_comm** out);
 sb_status sb_comm_destroy(sb_comm* comm);
+/* Failure detection: SB_ERR_NCCL if the communicator has recorded an
+ * asynchronous NCCL error (ncclCommGetAsyncError; a failed peer or link), SB_OK
+ * otherwise.  Host-only, never blocks.  The sharded calls perform the same check before
+ * enqueueing their collectives.  After SB_ERR_NCCL the communicator is unusable:
+ * sb_comm_abort (ncclCommAbort) releases it without waiting for pending collectives,
+ * which sb_comm_destroy would. */
+sb_status sb_comm_check(sb_comm* comm);
+sb_status sb_comm_abort(sb_comm* comm);
 
 #ifdef __cplusplus
 }

@@ -21,7 +21,7 @@ EXPORTS = ("sb_version", "sb_status_string", "sb_workspace_bytes", "sb_verify_br
            "sb_select_branch", "sb_verify_select", "sb_step_adaptive", "sb_verify_branches_reuse", "sb_draft_confidence", "sb_spawn_branches", "sb_kv_rollback", "sb_tree_workspace_bytes", "sb_tree_verify", "sb_hrad_workspace_bytes", "sb_hrad_predict", "sb_shard_partial_bytes", "sb_shard_verify_local",
            "sb_shard_verify_combine", "sb_shard_select_local", "sb_shard_select_sample",
            "sb_shard_select_commit", "sb_comm_unique_id_bytes", "sb_comm_unique_id", "sb_comm_create",
-           "sb_comm_destroy")
+           "sb_comm_destroy", "sb_comm_check", "sb_comm_abort")
 
 
 class sb_dims(ctypes.Structure):
@@ -65,6 +65,8 @@ _SIGS = {
     "sb_comm_unique_id": ([_P], _I),
     "sb_comm_create": ([_P, _I, _I, _D, ctypes.POINTER(ctypes.c_void_p)], _I),
     "sb_comm_destroy": ([_P], _I),
+    "sb_comm_check": ([_P], _I),
+    "sb_comm_abort": ([_P], _I),
 }
 
 _lib = None

@@ -498,6 +498,16 @@ class Comm:
         L.check(L.lib().sb_comm_create(ctypes.create_string_buffer(unique_id, n), int(nranks), int(rank),
                                        ctypes.byref(max_dims), ctypes.byref(self.handle)), "sb_comm_create")
 
+    def check(self):
+        """Raise if NCCL has recorded an asynchronous error on this communicator."""
+        L.check(L.lib().sb_comm_check(self.handle), "sb_comm_check")
+
+    def abort(self):
+        """Release a failed communicator without waiting for its pending collectives."""
+        if self.handle:
+            L.check(L.lib().sb_comm_abort(self.handle), "sb_comm_abort")
+            self.handle = ctypes.c_void_p()
+
     def close(self):
         if self.handle:
             L.check(L.lib().sb_comm_destroy(self.handle), "sb_comm_destroy")

@@ -32,7 +32,7 @@ def sources():
 
 
 def deps():
-    return sources() + glob.glob(os.path.join(HERE, "csrc", "*.h*")) + [
+    return sources() + glob.glob(os.path.join(HERE, "csrc", "*.h")) + glob.glob(os.path.join(HERE, "csrc", "*.cuh")) + [
         os.path.join(ROOT, "include", "specbranch.h")]
 
 

@@ -26,10 +26,19 @@ constexpr float kC = 1.4426950408889634f;  // fp32(log2 e)
 constexpr float kLn2 = 0.69314718055994531f;
 constexpr int kMaxK = 32;
 constexpr float kMsEmpty = -1e30f;  // exponent offset of a state that has seen no finite value
-// Lazy offset: rescale only when max*c - ms exceeds the threshold.  p rows need only
-// Z, so 2^20 of headroom is free; q rows also sum S1 = sum e*a, whose fp32 rounding
-// grows with the offset lag |a| of the largest terms, so they keep the lag <= 6.
-constexpr float kRescaleP = 20.f;
+// Lazy offset: rescale only when max*c - ms exceeds the threshold.  q rows also sum
+// S1 = sum e*a, whose fp32 rounding grows with the offset lag |a| of the largest terms,
+// so they keep the lag <= 6.  p rows keep it <= 10 so that a peaked row's dominant
+// element (p >= ~0.05: 2^10 above a thread's first-group maximum) raises the offset and
+// is frozen (kept out of the fp32 sums, see RowAcc): with 2^20 of headroom it was
+// summed in fp32 and every later small term rounded against it (Z off by up to ~1e-6
+// relative, residual mass R by ~1e-6 absolute).  10 rather than 6: a bulk N(0, 2^2)
+// logit exceeds its thread's first-group maximum by 10 / c only with probability ~2e-4,
+// so the rescale branch (~150 instructions per warp) stays off the hot path.
+#ifndef SB_RESCALE_P
+#define SB_RESCALE_P 10.f
+#endif
+constexpr float kRescaleP = SB_RESCALE_P;
 constexpr float kRescaleQ = 6.f;
 constexpr int kMaxG = 31;
 // Input domain (include/specbranch.h "Input domain"; DESIGN reading 34): a row is
@@ -71,6 +80,44 @@ __device__ __forceinline__ float ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+__device__ __forceinline__ float fmax_nan(float a, float b) {  // NaN-propagating max
+  float r;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+// 2^a for two values on the FMA pipe (FFMA2), as a stand-in for MUFU.EX2 on a share of
+// the p-row elements: the streaming kernels issue one MUFU per element and the MUFU
+// pipe (16 lanes / clk / SM) co-limits them at full HBM bandwidth.  a <= 2^7 (the lazy
+// offsets keep a <= kRescale); a = round(a) + f, f in [-1/2, 1/2]; 2^f by a degree-5
+// polynomial with p(0) = 1 (fit for relative error on [-1/2, 1/2]: max 1.7e-7, mean
+// -2e-8 with fp32 Horner, about the accuracy of ex2.approx); 2^round(a) built in the
+// exponent field (one IMAD: bits(a + 1.5 2^23) * 2^23 + bits(1.0)) and applied with
+// one FMUL2, so NaN propagates.  Below 2^-126 it returns tiny normals instead of 0
+// (a clamped at -126; masked -inf entries contribute <= 2^-125 each, far below the
+// row's own maximum term 2^-kRescale).
+__device__ __forceinline__ float2 ex2_poly2(float2 a) {
+  a.x = fmax_nan(a.x, -126.f);
+  a.y = fmax_nan(a.y, -126.f);
+  const float2 M = make_float2(12582912.f, 12582912.f);  // 1.5 * 2^23
+  const float2 t = __fadd2_rn(a, M);
+  const float2 j = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = __ffma2_rn(j, make_float2(-1.f, -1.f), a);  // exact
+  float2 q = make_float2(1.3264661e-3f, 1.3264661e-3f);
+  q = __ffma2_rn(q, f, make_float2(9.6714906e-3f, 9.6714906e-3f));
+  q = __ffma2_rn(q, f, make_float2(5.5507336e-2f, 5.5507336e-2f));
+  q = __ffma2_rn(q, f, make_float2(2.4022242e-1f, 2.4022242e-1f));
+  q = __ffma2_rn(q, f, make_float2(6.9314700e-1f, 6.9314700e-1f));
+  q = __ffma2_rn(q, f, make_float2(1.f, 1.f));
+  const float2 sc = make_float2(__int_as_float(__float_as_int(t.x) * 8388608 + 0x3f800000),
+                                __int_as_float(__float_as_int(t.y) * 8388608 + 0x3f800000));
+  return __fmul2_rn(q, sc);
+}
+// p-row exponentials (experiment builds: SB_POLY_P = n routes every n-th packed pair
+// of a p row through ex2_poly2; 0 = all on MUFU.EX2)
+#ifndef SB_POLY_P
+#define SB_POLY_P 0
+#endif
+constexpr int kPolyP = SB_POLY_P;
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
   float r;
   asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
@@ -152,7 +199,7 @@ struct RowAcc {
   float ms;      // m * c (fp32), the exponent offset used by every term
   float z[NA];   // sum of 2^(l c - ms)
   float s1[kQ ? NA : 1];
-  float fa;      // kQ: exponent a = m c - ms of the frozen maximum element(s) ...
+  float fa;      // exponent a = m c - ms of the frozen maximum element(s) ...
   int fn;        // ... and their count (0: none); their e = 2^a is evaluated in fp64
   int idx;       // smallest index attaining m (kQ only)
 
@@ -178,15 +225,15 @@ struct RowAcc {
       if (kQ) s1[j] = sc * fmaf(z[j], dd, s1[j]);
       z[j] *= sc;
     }
-    if (kQ && fn) {  // the previous maximum's element(s) become ordinary terms
+    if (fn) {  // the previous maximum's element(s) become ordinary terms
       const float ef = (float)fn * exp2f(fa);
-      s1[0] = fmaf(sc, ef * (fa + dd), s1[0]);
+      if (kQ) s1[0] = fmaf(sc, ef * (fa + dd), s1[0]);
       z[0] = fmaf(sc, ef, z[0]);
     }
     m = nm;
     ms = nms;
   }
-  // kQ: move the n elements equal to the new maximum into the frozen part
+  // move the n elements equal to the new maximum into the frozen part
   __device__ __forceinline__ void freeze(int n) {
     fa = fmaf(m, kC, -ms);  // exact: the rounding residual of ms
     fn = n;
@@ -200,14 +247,12 @@ struct RowAcc {
     for (int j = 0; j < E; ++j) f[j] = fin[j];
     if (vmax > m) {
       rescale(vmax);
-      if (kQ) {
-        int first = E, n = 0;
+      int first = E, n = 0;
 #pragma unroll
-        for (int j = E - 1; j >= 0; --j)
-          if (f[j] == vmax) { first = j; ++n; f[j] = kMaskedLogit; }
-        idx = base + first;
-        freeze(n);
-      }
+      for (int j = E - 1; j >= 0; --j)
+        if (f[j] == vmax) { first = j; ++n; f[j] = kMaskedLogit; }
+      if (kQ) idx = base + first;
+      freeze(n);
     }
 #pragma unroll
     for (int j = 0; j < E; ++j) {
@@ -221,11 +266,9 @@ struct RowAcc {
   __device__ __forceinline__ void add1(float f, int index) {
     if (f > m) {
       rescale(f);
-      if (kQ) {
-        idx = index;
-        freeze(1);
-        return;
-      }
+      if (kQ) idx = index;
+      freeze(1);
+      return;
     }
     const float a = fmaf(f, kC, -ms);
     const float e = ex2(a);
@@ -247,7 +290,7 @@ struct LazyAcc {
   float ms;
   float z[NA];
   float s1[kQ ? NA : 1];
-  float fa;  // kQ: frozen element(s): exponent and count (see RowAcc)
+  float fa;  // frozen element(s): exponent and count (see RowAcc)
   int fn;
   int tag;
 
@@ -270,14 +313,14 @@ struct LazyAcc {
       if (kQ) s1[j] = sc * fmaf(z[j], dd, s1[j]);
       z[j] *= sc;
     }
-    if (kQ && fn) {
+    if (fn) {
       const float ef = (float)fn * exp2f(fa);
-      s1[0] = fmaf(sc, ef * (fa + dd), s1[0]);
+      if (kQ) s1[0] = fmaf(sc, ef * (fa + dd), s1[0]);
       z[0] = fmaf(sc, ef, z[0]);
     }
     ms = nms;
   }
-  // kQ, inside the rescale branch: the group's elements equal to its maximum cm (which
+  // inside the rescale branch: the group's elements equal to its maximum cm (which
   // set the new offset) leave f[] for the frozen part
   template <int N>
   __device__ __forceinline__ void freeze(float* f, float cm) {
@@ -305,7 +348,7 @@ struct LazyAcc {
     while (__builtin_expect(__any_sync(0xffffffffu, up), 0)) {
       if (up) {
         rescale(offset_of(cm));
-        if (kQ) freeze<N>(f, cm);
+        freeze<N>(f, cm);
       }
       up = false;
     }
@@ -346,7 +389,7 @@ struct LazyAcc {
     while (__builtin_expect(__any_sync(0xffffffffu, up), 0)) {
       if (up) {
         rescale(offset_of(cm));
-        if (kQ) freeze<N>(f, cm);
+        freeze<N>(f, cm);
       }
       up = false;
     }
@@ -360,7 +403,14 @@ struct LazyAcc {
 #pragma unroll
     for (int j = 0; j < NW; ++j) {
       const float2 a = __ffma2_rn(make_float2(f[2 * j], f[2 * j + 1]), c2, n2);
-      const float2 e = make_float2(ex2(a.x), ex2(a.y));
+      float2 e;
+#ifdef SB_P_NOEXP  // bandwidth-ceiling experiment only: p rows skip the exponential (wrong sums)
+      if (!kQ) e = a; else
+#endif
+      if (!kQ && kPolyP > 0 && j % (kPolyP > 0 ? kPolyP : 1) == (kPolyP > 0 ? kPolyP : 1) - 1)
+        e = ex2_poly2(a);
+      else
+        e = make_float2(ex2(a.x), ex2(a.y));
       if (j % 2 == 0) {
         za = __fadd2_rn(za, e);
         if (kQ) sa = __ffma2_rn(e, a, sa);
@@ -406,11 +456,12 @@ struct RowStat {
 
 // The frozen element(s) of a q row, n * 2^a and their entropy term n * 2^a * a, in fp64
 // (a is the exact rounding residual of the offset: a one-hot row gets H = 0 exactly).
+template <bool kQ>
 __device__ __forceinline__ void add_frozen(RowStat& r, int n, float a) {
   if (n) {
     const double e = (double)n * exp2((double)a);
     r.z += e;
-    r.s1 += e * (double)a;
+    if (kQ) r.s1 += e * (double)a;
   }
 }
 
@@ -428,7 +479,7 @@ __device__ __forceinline__ RowStat fold_lazy(const LazyAcc<kQ, NA>& a) {
   }
   r.z = (double)z;
   r.s1 = (double)s;
-  if (kQ) add_frozen(r, a.fn, a.fa);
+  add_frozen<kQ>(r, a.fn, a.fa);
   r.idx = 0x7fffffff;
   return r;
 }
@@ -458,7 +509,7 @@ __device__ __forceinline__ RowStat fold(const RowAcc<kQ, NA>& a) {
   }
   r.z = (double)z;
   r.s1 = (double)s;
-  if (kQ) add_frozen(r, a.fn, a.fa);
+  add_frozen<kQ>(r, a.fn, a.fa);
   r.idx = kQ ? a.idx : 0;
   return r;
 }

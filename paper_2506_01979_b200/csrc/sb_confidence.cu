@@ -297,6 +297,7 @@ extern "C" sb_status sb_draft_confidence(const sb_dims* dd, const void* q_logits
                                          float* stat, int32_t* stop, int32_t* k_next,
                                          int32_t* gamma_next, void* comm, void* workspace,
                                          size_t workspace_bytes, sb_stream_t stream) {
+  SB_NVTX("sb_draft_confidence");
   if (!dims_valid(dd) || !q_logits || !stop || !workspace) return SB_ERR_INVALID_ARG;
   if (mode != SB_CONF_TOP1 && mode != SB_CONF_TOKEN && mode != SB_CONF_ENTROPY)
     return SB_ERR_INVALID_ARG;

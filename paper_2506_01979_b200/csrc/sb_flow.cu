@@ -978,6 +978,7 @@ extern "C" sb_status sb_step_adaptive(const sb_dims* dd, const void* p_logits, c
                                       int32_t* branch_discarded, uint32_t* keep_mask, float* resid_mass,
                                       void* conf_workspace, size_t conf_workspace_bytes, void* workspace,
                                       size_t workspace_bytes, sb_stream_t stream) {
+  SB_NVTX("sb_step_adaptive");
   if (!dims_valid(dd) || sharded(dd) || dd->G < 1) return SB_ERR_INVALID_ARG;
   if (!p_logits || !q_logits || !tok || !u || !us || !c_top1_prob || !c_top1_id || !c_entropy || !c_stat ||
       !c_stop || !c_k_next || !c_gamma_next || !lse_p || !lse_q || !p_tok || !q_tok || !acc_mask || !n_acc ||

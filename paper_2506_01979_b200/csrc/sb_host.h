@@ -7,9 +7,21 @@
 
 #include <atomic>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "sb_common.cuh"
 
 namespace sb {
+
+// One NVTX range per C-ABI call (SURVEY §5 tracing): a push / pop pair, no-ops unless a
+// profiler (nsys, ncu --nvtx) has injected itself.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#define SB_NVTX(name) ::sb::NvtxRange sb_nvtx_range_(name)
 
 struct SeqInfo {
   int g, s, L, st;  // clamped gamma_b, branch row s_b, path length L_b, clamp bits

@@ -392,6 +392,7 @@ extern "C" sb_status sb_hrad_predict(int32_t B, int32_t Dz, int32_t G, const voi
                                      const float* b3, const int32_t* stop, float* logits, int32_t* s_t,
                                      int32_t* gamma, int32_t* branch_pos, void* workspace,
                                      size_t workspace_bytes, sb_stream_t stream) {
+  SB_NVTX("sb_hrad_predict");
   if (B < 1 || Dz < 1 || G < 0 || G > kMaxG || !z || !w1 || !b1 || !w2 || !b2 || !w3 || !b3 || !s_t ||
       !workspace)
     return SB_ERR_INVALID_ARG;

@@ -60,6 +60,7 @@ using namespace sb;
 extern "C" sb_status sb_kv_rollback(int32_t B, int32_t K, int32_t G, const void* kv, int64_t row_bytes,
                                     int64_t row_stride_bytes, const uint32_t* keep_mask, void* out_kv,
                                     sb_stream_t stream) {
+  SB_NVTX("sb_kv_rollback");
   if (B < 1 || K < 1 || K > kMaxK || G < 0 || G > kMaxG || !kv || !keep_mask) return SB_ERR_INVALID_ARG;
   if (row_bytes <= 0 || row_bytes % 16 || row_stride_bytes < row_bytes || row_stride_bytes % 16) return SB_ERR_INVALID_ARG;
   if ((uintptr_t)kv % 16 || (uintptr_t)out_kv % 16) return SB_ERR_INVALID_ARG;

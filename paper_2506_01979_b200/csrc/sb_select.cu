@@ -643,6 +643,7 @@ extern "C" sb_status sb_select_branch(const sb_dims* dd, const void* p_logits, c
                                       uint32_t* keep_mask, float* resid_mass, int32_t* status,
                                       void* comm, void* workspace, size_t workspace_bytes,
                                       sb_stream_t stream) {
+  SB_NVTX("sb_select_branch");
   (void)gamma;
   (void)branch_pos;  // the clamped layout comes from the workspace (sb_verify_branches)
   if (!dims_valid(dd)) return SB_ERR_INVALID_ARG;

@@ -524,6 +524,7 @@ extern "C" sb_status sb_shard_verify_local(const sb_dims* d, const void* p_logit
                                            const int32_t* tok, const float* u, const int32_t* gamma,
                                            const int32_t* branch_pos, void* partial, void* workspace,
                                            size_t workspace_bytes, sb_stream_t stream) {
+  SB_NVTX("sb_shard_verify_local");
   if (!dims_valid(d)) return SB_ERR_INVALID_ARG;
   if (!p_logits || !q_logits || !tok || !u || !partial || !workspace) return SB_ERR_INVALID_ARG;
   return sb_rows_partial(d, p_logits, q_logits, tok, u, gamma, branch_pos, partial, workspace,
@@ -536,6 +537,7 @@ extern "C" sb_status sb_shard_verify_combine(const sb_dims* dd, const void* gath
                                              float* top1_q, int32_t* top1_id_q, float* entropy_q,
                                              int32_t* status, void* workspace, size_t workspace_bytes,
                                              sb_stream_t stream) {
+  SB_NVTX("sb_shard_verify_combine");
   if (!dims_valid(dd) || nranks < 1) return SB_ERR_INVALID_ARG;
   if (!gathered || !tok || !u || !lse_p || !lse_q || !p_tok || !q_tok || !acc_mask || !n_acc || !status ||
       !workspace)
@@ -561,6 +563,7 @@ extern "C" sb_status sb_shard_select_local(const sb_dims* dd, const void* p_logi
                                            const int32_t* tok, const float* u, const int32_t* n_acc,
                                            sb_select_rule rule, double* mass, void* workspace,
                                            size_t workspace_bytes, sb_stream_t stream) {
+  SB_NVTX("sb_shard_select_local");
   if (!dims_valid(dd)) return SB_ERR_INVALID_ARG;
   if (!p_logits || !q_logits || !tok || !u || !n_acc || !mass || !workspace) return SB_ERR_INVALID_ARG;
   if (rule != SB_SELECT_EQ9 && rule != SB_SELECT_ALG1) return SB_ERR_INVALID_ARG;
@@ -581,6 +584,7 @@ extern "C" sb_status sb_shard_select_sample(const sb_dims* dd, const double* gat
                                             int32_t rank, const void* p_logits, const void* q_logits,
                                             const float* us, int32_t* ycand, void* workspace,
                                             size_t workspace_bytes, sb_stream_t stream) {
+  SB_NVTX("sb_shard_select_sample");
   if (!dims_valid(dd) || nranks < 1 || rank < 0 || rank >= nranks) return SB_ERR_INVALID_ARG;
   if (!gathered_mass || !p_logits || !q_logits || !us || !ycand || !workspace) return SB_ERR_INVALID_ARG;
   const Workspace w = carve(*dd, workspace);
@@ -602,6 +606,7 @@ extern "C" sb_status sb_shard_select_commit(const sb_dims* dd, const int32_t* y,
                                             int32_t* path_rolled, int32_t* branch_discarded, uint32_t* keep_mask,
                                             float* resid_mass, int32_t* status, void* workspace,
                                             size_t workspace_bytes, sb_stream_t stream) {
+  SB_NVTX("sb_shard_select_commit");
   if (!dims_valid(dd)) return SB_ERR_INVALID_ARG;
   if (!y || !tok || !sel_k || !commit_len || !out_tok || !y_tok || !y_kind || !offsets || !path_rolled ||
       !branch_discarded || !keep_mask || !status || !workspace)
@@ -633,12 +638,14 @@ struct sb_comm {
 extern "C" size_t sb_comm_unique_id_bytes(void) { return sizeof(ncclUniqueId); }
 
 extern "C" sb_status sb_comm_unique_id(void* out) {
+  SB_NVTX("sb_comm_unique_id");
   if (!out) return SB_ERR_INVALID_ARG;
   return ncclGetUniqueId(reinterpret_cast<ncclUniqueId*>(out)) == ncclSuccess ? SB_OK : SB_ERR_NCCL;
 }
 
 extern "C" sb_status sb_comm_create(const void* unique_id, int32_t nranks, int32_t rank, const sb_dims* max_dims,
                                     sb_comm** out) {
+  SB_NVTX("sb_comm_create");
   if (!unique_id || !out || nranks < 1 || rank < 0 || rank >= nranks || !dims_valid(max_dims))
     return SB_ERR_INVALID_ARG;
   sb_comm* c = new sb_comm();
@@ -666,7 +673,35 @@ extern "C" sb_status sb_comm_create(const void* unique_id, int32_t nranks, int32
   return SB_OK;
 }
 
+// Asynchronous NCCL errors (a peer died, a network error inside a collective) surface
+// through ncclCommGetAsyncError only; every sharded call checks it before enqueueing
+// more work on the communicator (SURVEY §5 failure detection).
+static sb_status comm_health(sb_comm* c) {
+  ncclResult_t e = ncclSuccess;
+  if (ncclCommGetAsyncError(c->nccl, &e) != ncclSuccess) return SB_ERR_NCCL;
+  return (e == ncclSuccess || e == ncclInProgress) ? SB_OK : SB_ERR_NCCL;
+}
+
+extern "C" sb_status sb_comm_check(sb_comm* c) {
+  if (!c) return SB_ERR_INVALID_ARG;
+  return comm_health(c);
+}
+
+extern "C" sb_status sb_comm_abort(sb_comm* c) {
+  SB_NVTX("sb_comm_abort");
+  if (!c) return SB_ERR_INVALID_ARG;
+  const bool ok = ncclCommAbort(c->nccl) == ncclSuccess;
+  cudaFree(c->gather);
+  cudaFree(c->mine);
+  cudaFree(c->gmass);
+  cudaFree(c->mass);
+  cudaFree(c->y);
+  delete c;
+  return ok ? SB_OK : SB_ERR_NCCL;
+}
+
 extern "C" sb_status sb_comm_destroy(sb_comm* c) {
+  SB_NVTX("sb_comm_destroy");
   if (!c) return SB_ERR_INVALID_ARG;
   cudaFree(c->gather);
   cudaFree(c->mine);
@@ -687,6 +722,7 @@ sb_status sb_shard_verify_nccl(const sb_dims* d, const void* p_logits, const voi
                                void* workspace, size_t workspace_bytes, cudaStream_t s) {
   const size_t pb = sb_shard_partial_bytes(d);
   if (pb > c->cap_partial) return SB_ERR_INVALID_ARG;
+  if (comm_health(c) != SB_OK) return SB_ERR_NCCL;
   sb_status st = sb_shard_verify_local(d, p_logits, q_logits, tok, u, gamma, branch_pos, c->mine, workspace,
                                        workspace_bytes, (sb_stream_t)s);
   if (st != SB_OK) return st;
@@ -702,6 +738,7 @@ sb_status sb_shard_select_nccl(const sb_dims* d, const void* p_logits, const voi
                                int32_t* branch_discarded, uint32_t* keep_mask, float* resid_mass, int32_t* status,
                                sb_comm* c, void* workspace, size_t workspace_bytes, cudaStream_t s) {
   if (d->B > c->cap_B) return SB_ERR_INVALID_ARG;
+  if (comm_health(c) != SB_OK) return SB_ERR_NCCL;
   sb_status st = sb_shard_select_local(d, p_logits, q_logits, tok, u, n_acc, rule, c->mass, workspace,
                                        workspace_bytes, (sb_stream_t)s);
   if (st != SB_OK) return st;

@@ -316,6 +316,7 @@ using namespace sb;
 extern "C" sb_status sb_spawn_branches(const sb_dims* dd, const void* q_logits, const int32_t* branch_pos,
                                        const int32_t* tok, sb_conf_mode mode, int32_t k_max, int32_t* k_out,
                                        int32_t* branch_tok, float* branch_prob, float* conf, sb_stream_t stream) {
+  SB_NVTX("sb_spawn_branches");
   if (!dims_valid(dd) || sharded(dd) || !q_logits || !k_out || !branch_tok) return SB_ERR_INVALID_ARG;
   if (mode != SB_CONF_TOP1 && mode != SB_CONF_TOKEN) return SB_ERR_INVALID_ARG;
   if (mode == SB_CONF_TOKEN && !tok) return SB_ERR_INVALID_ARG;

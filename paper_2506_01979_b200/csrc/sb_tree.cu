@@ -245,6 +245,7 @@ extern "C" sb_status sb_tree_verify(const sb_dims* dd, const void* p_logits, con
                                     int32_t* commit_len, int32_t* out_tok, int32_t* y_tok, int32_t* y_kind,
                                     float* resid_mass, int32_t* status, void* workspace, size_t workspace_bytes,
                                     sb_stream_t stream) {
+  SB_NVTX("sb_tree_verify");
   if (!tree_dims_valid(dd) || !p_logits || !q_logits || !parent || !tok || !u || !us || !acc_mask || !keep_mask ||
       !stop_node || !commit_len || !out_tok || !y_tok || !y_kind || !status || !workspace)
     return SB_ERR_INVALID_ARG;

@@ -1414,6 +1414,7 @@ extern "C" sb_status sb_verify_branches(const sb_dims* dd, const void* p_logits,
                                         int32_t* top1_id_q, float* entropy_q, int32_t* status,
                                         void* comm, void* workspace, size_t workspace_bytes,
                                         sb_stream_t stream) {
+  SB_NVTX("sb_verify_branches");
   return verify_impl(dd, p_logits, q_logits, tok, u, gamma, branch_pos, lse_p, lse_q, p_tok, q_tok, acc_mask,
                      n_acc, top1_q, top1_id_q, entropy_q, status, comm, workspace, workspace_bytes, nullptr,
                      stream);
@@ -1426,6 +1427,7 @@ extern "C" sb_status sb_verify_branches_reuse(const sb_dims* dd, const void* p_l
                                               int32_t* top1_id_q, float* entropy_q, int32_t* status,
                                               const void* conf_workspace, void* workspace, size_t workspace_bytes,
                                               sb_stream_t stream) {
+  SB_NVTX("sb_verify_branches_reuse");
   if (!conf_workspace || sharded(dd)) return SB_ERR_INVALID_ARG;
   return verify_impl(dd, p_logits, q_logits, tok, u, gamma, branch_pos, lse_p, lse_q, p_tok, q_tok, acc_mask,
                      n_acc, top1_q, top1_id_q, entropy_q, status, nullptr, workspace, workspace_bytes,
@@ -1443,6 +1445,7 @@ extern "C" sb_status sb_verify_select(const sb_dims* dd, const void* p_logits, c
                                       int32_t* path_rolled, int32_t* branch_discarded, uint32_t* keep_mask,
                                       float* resid_mass, void* workspace, size_t workspace_bytes,
                                       sb_stream_t stream) {
+  SB_NVTX("sb_verify_select");
   if (!dims_valid(dd) || sharded(dd)) return SB_ERR_INVALID_ARG;
   if (!p_logits || !q_logits || !tok || !u || !us || !lse_p || !lse_q || !p_tok || !q_tok || !acc_mask ||
       !n_acc || !status || !sel_k || !commit_len || !out_tok || !y_tok || !y_kind || !offsets || !path_rolled ||

@@ -1,0 +1,8 @@
+set -u
+export PYTHONUNBUFFERED=1
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/r2d_build.log 2>&1
+bash scripts/r2_variants.sh r2d c4 "default r6 r8 r20" > gpurun_out/r2d_variants.txt 2>&1
+timeout 1500 python -m pytest tests -m "gpu and slow" -q -s -p no:cacheprovider 2>&1 | grep -v "^\s*$" | tail -12 > gpurun_out/r2d_slow.log
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_rows_tma" -s 6 -c 1 -o gpurun_out/r2d_c4_rows \
+    python bench.py --config c4 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-graph > gpurun_out/r2d_ncu_rows.log 2>&1

@@ -76,8 +76,20 @@ def test_nccl_comm_single_rank():
         torch.cuda.synchronize()
         inp_np = synth.to_numpy_inputs(inp)
         compare(_np(buf), oracle_for(inp_np, inp_np["gamma"]))
+        comm.check()  # no asynchronous NCCL error recorded
     finally:
         comm.close()
+
+
+def test_nccl_comm_abort():
+    """sb_comm_abort releases a communicator (the failure path's teardown)."""
+    from paper_2506_01979_b200 import api
+
+    d = api.L.sb_dims(4, 2, 4, 1024, 0, 1024, 1024, 0, api.L.SB_BF16, 0)
+    comm = api.Comm(1, 0, d)
+    comm.check()
+    comm.abort()
+    assert not comm.handle
 
 
 def test_sharded_dims_without_comm_rejected():
