@@ -24,6 +24,7 @@ namespace sb {
 
 constexpr float kC = 1.4426950408889634f;  // fp32(log2 e)
 constexpr float kLn2 = 0.69314718055994531f;
+constexpr float kInvC = 0.69314718055994531f;  // 1 / log2 e (the rescale test only)
 constexpr int kMaxK = 32;
 constexpr float kMsEmpty = -1e30f;  // exponent offset of a state that has seen no finite value
 // Lazy offset: rescale only when max*c - ms exceeds the threshold.  q rows also sum
@@ -286,17 +287,24 @@ struct RowAcc {
 // sums z[] only ever hold terms far below it.
 template <bool kQ, int NA>
 struct LazyAcc {
+  static constexpr float kT = kQ ? kRescaleQ : kRescaleP;
   float m;
   float ms;
+  float lim;  // raw-logit form of the rescale test: a group maximum cm > lim ~ (ms + kT) / c
   float z[NA];
   float s1[kQ ? NA : 1];
   float fa;  // frozen element(s): exponent and count (see RowAcc)
   int fn;
   int tag;
 
+  __device__ __forceinline__ void set_offset(float nms) {
+    ms = nms;
+    lim = (nms + kT) * kInvC;
+  }
   __device__ __forceinline__ void init() {
     m = -CUDART_INF_F;
     ms = kMsEmpty;
+    lim = -CUDART_INF_F;  // the empty state takes any finite maximum
 #pragma unroll
     for (int j = 0; j < NA; ++j) z[j] = 0.f;
 #pragma unroll
@@ -318,7 +326,7 @@ struct LazyAcc {
       if (kQ) s1[0] = fmaf(sc, ef * (fa + dd), s1[0]);
       z[0] = fmaf(sc, ef, z[0]);
     }
-    ms = nms;
+    set_offset(nms);
   }
   // inside the rescale branch: the group's elements equal to its maximum cm (which
   // set the new offset) leave f[] for the frozen part
@@ -326,25 +334,28 @@ struct LazyAcc {
   __device__ __forceinline__ void freeze(float* f, float cm) {
     int n = 0;
 #pragma unroll
-    for (int j = 0; j < N; ++j)
-      if (f[j] == cm) { f[j] = kMaskedLogit; ++n; }
+    for (int j = 0; j < N; ++j) {
+      const bool eq = f[j] == cm;
+      f[j] = eq ? kMaskedLogit : f[j];
+      n += eq;
+    }
     fa = fmaf(cm, kC, -ms);  // exact residual of ms = fl(cm c)
     fn = n;
   }
-  template <int N>
-  __device__ __forceinline__ void add(float* f, int t) {
-    float cm = f[0];
-#pragma unroll
-    for (int j = 1; j + 1 < N; j += 2) cm = fmax3(cm, f[j], f[j + 1]);
-    if (N % 2 == 0) cm = fmaxf(cm, f[N - 1]);
-    add_cm<N>(f, cm, t);
-  }
-  // the same with the group maximum cm = max(f[0..N)) already known
-  template <int N>
-  __device__ __forceinline__ void add_cm(float* f, float cm, int t) {
-    if (kQ) tag = (cm > m) ? t : tag;
-    m = fmaxf(m, cm);
-    bool up = cm * kC - ms > (kQ ? kRescaleQ : kRescaleP);
+  // The rescale test of one group.  FIRST: the first group after init() (every lane
+  // takes it together, so no vote, and an empty state needs no rescaling of its sums).
+  template <int N, bool FIRST>
+  __device__ __forceinline__ void raise(float* f, float cm) {
+    if (FIRST) {
+      if (cm > lim) {
+        set_offset(offset_of(cm));
+        freeze<N>(f, cm);
+      }
+      return;
+    }
+    bool up = cm > lim;
+    // rare; written as a loop so the compiler keeps it a branch instead of predicating
+    // the rescale into every iteration
     while (__builtin_expect(__any_sync(0xffffffffu, up), 0)) {
       if (up) {
         rescale(offset_of(cm));
@@ -352,6 +363,21 @@ struct LazyAcc {
       }
       up = false;
     }
+  }
+  template <int N, bool FIRST = false>
+  __device__ __forceinline__ void add(float* f, int t) {
+    float cm = f[0];
+#pragma unroll
+    for (int j = 1; j + 1 < N; j += 2) cm = fmax3(cm, f[j], f[j + 1]);
+    if (N % 2 == 0) cm = fmaxf(cm, f[N - 1]);
+    add_cm<N, FIRST>(f, cm, t);
+  }
+  // the same with the group maximum cm = max(f[0..N)) already known
+  template <int N, bool FIRST = false>
+  __device__ __forceinline__ void add_cm(float* f, float cm, int t) {
+    if (kQ) tag = (cm > m) ? t : tag;
+    m = fmaxf(m, cm);
+    raise<N, FIRST>(f, cm);
 #pragma unroll
     for (int j = 0; j < N; ++j) {
       const float a = fmaf(f[j], kC, -ms);
@@ -366,7 +392,7 @@ struct LazyAcc {
   // goes to z[j % 4]).  q rows clamp their inputs at -2^97 instead of clamping the
   // exponent: identical results for every logit > -2^97, since ex2.approx.ftz is 0
   // below 2^-126 either way.
-  template <int NW>
+  template <int NW, bool FIRST = false>
   __device__ __forceinline__ float add_bf16(const uint32_t* win, int t) {
     static_assert(NA == 4 && NW % 2 == 0, "pairs map to (z0,z1), (z2,z3)");
     constexpr int N = 2 * NW;
@@ -383,16 +409,7 @@ struct LazyAcc {
     cm = fmaxf(cm, f[N - 1]);
     if (kQ) tag = (cm > m) ? t : tag;
     m = fmaxf(m, cm);
-    bool up = cm * kC - ms > (kQ ? kRescaleQ : kRescaleP);
-    // rare; written as a loop so the compiler keeps it a branch instead of predicating
-    // the rescale into every iteration
-    while (__builtin_expect(__any_sync(0xffffffffu, up), 0)) {
-      if (up) {
-        rescale(offset_of(cm));
-        freeze<N>(f, cm);
-      }
-      up = false;
-    }
+    raise<N, FIRST>(f, cm);
     const float2 c2 = make_float2(kC, kC), n2 = make_float2(-ms, -ms);
     float2 za = make_float2(z[0], z[1]), zb = make_float2(z[2], z[3]);
     float2 sa = make_float2(0.f, 0.f), sb = sa;
@@ -435,14 +452,14 @@ __device__ __forceinline__ uint4 neg_inf_vec() {
 }
 
 // Accumulate NV 16-byte bf16 vectors of one row chunk (tag t) into a LazyAcc.
-template <int NV, bool kQ>
+template <int NV, bool kQ, bool FIRST = false>
 __device__ __forceinline__ float acc_vecs_bf16(LazyAcc<kQ, 4>& a, const uint4* x, int t) {
   uint32_t w[4 * NV];
 #pragma unroll
   for (int j = 0; j < NV; ++j) {
     w[4 * j] = x[j].x; w[4 * j + 1] = x[j].y; w[4 * j + 2] = x[j].z; w[4 * j + 3] = x[j].w;
   }
-  return a.template add_bf16<4 * NV>(w, t);
+  return a.template add_bf16<4 * NV, FIRST>(w, t);
 }
 
 // Reduced row state (one per thread after folding accumulators, then across threads).
@@ -456,10 +473,18 @@ struct RowStat {
 
 // The frozen element(s) of a q row, n * 2^a and their entropy term n * 2^a * a, in fp64
 // (a is the exact rounding residual of the offset: a one-hot row gets H = 0 exactly).
+// 2^a for the frozen residual a = fl(m c) rounding error: |a| <= ulp(m c) / 2, tiny
+// for every in-domain row (|m| < 2^24), so a cubic Taylor series is exact to ~1e-16
+// there (the library exp2 costs ~40 fp64 instructions per lane per row).
+__device__ __forceinline__ double exp2_small(float a) {
+  const double x = (double)a * 0.69314718055994530942;
+  if (fabs(x) > 0x1p-12) return exp2((double)a);
+  return fma(x, fma(x, fma(x, 1.0 / 6.0, 0.5), 1.0), 1.0);
+}
 template <bool kQ>
 __device__ __forceinline__ void add_frozen(RowStat& r, int n, float a) {
   if (n) {
-    const double e = (double)n * exp2((double)a);
+    const double e = (double)n * exp2_small(a);
     r.z += e;
     if (kQ) r.s1 += e * (double)a;
   }

@@ -140,9 +140,25 @@ struct ConfSmem {
   alignas(128) uint8_t buf[cNS][cChunk];
 };
 
+// One chunk of a q row into the accumulator; first: the row's first chunk (the peeled
+// rescale test of LazyAcc, warp-uniform).
+template <typename T>
+__device__ __forceinline__ void conf_acc(LazyAcc<true, 4>& a, const uint4* x, int c, bool first) {
+  constexpr int E = Vec<T>::E;
+  if constexpr (sizeof(T) == 2) {
+    if (first) acc_vecs_bf16<cVPT, true, true>(a, x, c);
+    else acc_vecs_bf16<cVPT, true, false>(a, x, c);
+  } else {
+    float f[cVPT * E];
+#pragma unroll
+    for (int j = 0; j < cVPT; ++j) Vec<T>::unpack(x[j], f + j * E);
+    if (first) a.template add<cVPT * E, true>(f, c);
+    else a.template add<cVPT * E, false>(f, c);
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(cThreads, 1) k_conf_tma(ConfParams p) {
-  constexpr int E = Vec<T>::E;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   ConfSmem& S = *reinterpret_cast<ConfSmem*>(smem_raw);
   const Dims& d = p.d;
@@ -216,14 +232,7 @@ __global__ void __launch_bounds__(cThreads, 1) k_conf_tma(ConfParams p) {
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.empty[rp.stage]);
       rp.advance();
-      if constexpr (sizeof(T) == 2) {
-        acc_vecs_bf16<cVPT>(a, x, c);
-      } else {
-        float f[cVPT * E];
-#pragma unroll
-        for (int j = 0; j < cVPT; ++j) Vec<T>::unpack(x[j], f + j * E);
-        a.template add<cVPT * E>(f, c);
-      }
+      conf_acc<T>(a, x, c, c == 0);
     }
     {
       const int c = nchunks - 1;
@@ -237,14 +246,7 @@ __global__ void __launch_bounds__(cThreads, 1) k_conf_tma(ConfParams p) {
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.empty[rp.stage]);
       rp.advance();
-      if constexpr (sizeof(T) == 2) {
-        acc_vecs_bf16<cVPT>(a, x, c);
-      } else {
-        float f[cVPT * E];
-#pragma unroll
-        for (int j = 0; j < cVPT; ++j) Vec<T>::unpack(x[j], f + j * E);
-        a.template add<cVPT * E>(f, c);
-      }
+      conf_acc<T>(a, x, c, nchunks == 1);
     }
     uint2 cand;
     const RowStat s = warp_part_deferred(a, cand);

@@ -28,42 +28,40 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-// Blocking wait on a phase.  A watchdog traps after ~2^24 failed probes (seconds): a
+// One probe of a phase with a suspend-time hint: the warp sleeps in hardware until the
+// phase completes (woken ~60 cycles after the last arrive) or the hint expires, so a
+// waiting warp issues a few instructions per wait instead of polling (with the
+// system-default limit the consumers' and epilogue warps' probe loops were ~20 % of
+// k_rows_tma's issued instructions).
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+      " selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
+      : "memory");
+  return ok != 0;
+}
+// Blocking wait on a phase.  A watchdog traps after ~2^12 expired probes (seconds): a
 // protocol bug then surfaces as a launch error instead of a hung GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t ok = 0;
-  for (uint32_t tries = 0;; ++tries) {
-    asm volatile(
-        "{\n .reg .pred p;\n"
-        " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-        " selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-    if (ok) break;
-    if (tries > (1u << 24)) __trap();
-  }
+#ifdef SB_WAIT_NOWATCHDOG  // experiment: two instructions per retry, no watchdog
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
+      : "memory");
+#else
+  for (uint32_t tries = 0; !mbar_try(bar, parity); ++tries)
+    if (tries > (1u << 12)) __trap();
+#endif
 }
-// The same with exponential back-off (nanosleep 256 ns .. 2 us between probes), for
-// waits that last whole units (an epilogue warp waiting for the consumers' partials):
-// their spinning took issue slots from the consumer warps (k_rows_tma: 8-13 % of all
-// issued instructions).  Watchdog ~2^22 probes (seconds).
-__device__ __forceinline__ void mbar_wait_parked(uint64_t* bar, uint32_t parity) {
-  uint32_t ok = 0, ns = 256;
-  for (uint32_t tries = 0;; ++tries) {
-    asm volatile(
-        "{\n .reg .pred p;\n"
-        " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-        " selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-    if (ok) break;
-    __nanosleep(ns);
-    ns = ns < 2048 ? 2 * ns : ns;
-    if (tries > (1u << 22)) __trap();
-  }
-}
+// Waits that last whole units (an epilogue warp waiting for the consumers' partials):
+// the same hardware sleep.
+__device__ __forceinline__ void mbar_wait_parked(uint64_t* bar, uint32_t parity) { mbar_wait(bar, parity); }
 // 1-D bulk copy global -> shared, completion (bytes) signalled on bar.
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
                                          uint64_t policy) {

@@ -211,7 +211,10 @@ __global__ void __launch_bounds__(NT) k_spawn(SpawnParams p, bool vec_ok) {
           vm = acc_vecs_bf16<1>(acc, x + j, 0);  // packed FFMA2 / FADD2 sums, returns the max
         } else {
           vm = Vec<T>::vmax(f);
-          acc.template add_cm<E>(f, vm, vb + j * NT);
+          float g[E];  // the accumulator freezes (masks) its maximum in place; f feeds the top-K
+#pragma unroll
+          for (int e = 0; e < E; ++e) g[e] = f[e];
+          acc.template add_cm<E>(g, vm, vb + j * NT);
         }
         unsigned cand = __ballot_sync(0xffffffffu, valid && vm >= filt);
         while (cand) {  // rare once warm: one lane's values, broadcast, qualifying ones inserted
@@ -234,7 +237,12 @@ __global__ void __launch_bounds__(NT) k_spawn(SpawnParams p, bool vec_ok) {
     f[0] = v < d.V ? ld_scalar(row + v) : -CUDART_INF_F;
 #pragma unroll
     for (int e = 1; e < E; ++e) f[e] = -CUDART_INF_F;
-    acc.template add<E>(f, 0);
+    {
+      float g[E];  // (add() masks the frozen maximum in place)
+#pragma unroll
+      for (int e = 0; e < E; ++e) g[e] = f[e];
+      acc.template add<E>(g, 0);
+    }
     unsigned cand = __ballot_sync(0xffffffffu, v < d.V && f[0] >= filt);
     while (cand) {
       const int src = __ffs(cand) - 1;

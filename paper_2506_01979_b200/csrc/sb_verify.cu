@@ -594,12 +594,12 @@ __device__ __forceinline__ void load_stage(const uint8_t* bp, const uint8_t* bq,
   }
 }
 
-template <class C, typename T>
+template <class C, typename T, bool FIRST = false>
 __device__ __forceinline__ void compute_stage(const StageRegs<C>& r, int c, LazyAcc<false, 4>& pa,
                                               LazyAcc<true, 4>& qa) {
   if constexpr (sizeof(T) == 2) {
-    acc_vecs_bf16<C::VPT>(pa, r.p, c);
-    acc_vecs_bf16<C::VPT>(qa, r.q, c);
+    acc_vecs_bf16<C::VPT, false, FIRST>(pa, r.p, c);
+    acc_vecs_bf16<C::VPT, true, FIRST>(qa, r.q, c);
   } else {
     constexpr int E = Vec<T>::E;
     float fp[C::VPT * E], fq[C::VPT * E];
@@ -608,8 +608,8 @@ __device__ __forceinline__ void compute_stage(const StageRegs<C>& r, int c, Lazy
       Vec<T>::unpack(r.p[j], fp + j * E);
       Vec<T>::unpack(r.q[j], fq + j * E);
     }
-    pa.template add<C::VPT * E>(fp, c);
-    qa.template add<C::VPT * E>(fq, c);
+    pa.template add<C::VPT * E, FIRST>(fp, c);
+    qa.template add<C::VPT * E, FIRST>(fq, c);
   }
 }
 
@@ -623,20 +623,39 @@ __device__ __forceinline__ void load_stage_p(const uint8_t* bp, int nvec, StageR
     r.p[j] = (FULL || v < nvec) ? lds128(bp + v * 16) : neg_inf_vec<T>();
   }
 }
-template <class C, typename T>
+template <class C, typename T, bool FIRST = false>
 __device__ __forceinline__ void compute_stage_p(const StageRegs<C>& r, int c, LazyAcc<false, 4>& pa) {
   if constexpr (sizeof(T) == 2) {
-    acc_vecs_bf16<C::VPT>(pa, r.p, c);
+    acc_vecs_bf16<C::VPT, false, FIRST>(pa, r.p, c);
   } else {
     constexpr int E = Vec<T>::E;
     float fp[C::VPT * E];
 #pragma unroll
     for (int j = 0; j < C::VPT; ++j) Vec<T>::unpack(r.p[j], fp + j * E);
-    pa.template add<C::VPT * E>(fp, c);
+    pa.template add<C::VPT * E, FIRST>(fp, c);
   }
 }
 
-template <class C, typename T>
+// One ring stage of a unit by the consumer warps: wait -> 16-byte LDS of this thread's
+// vectors -> release the stage -> math, so the producer refills the slot while the
+// consumers compute.  FIRST: the unit's first chunk (peeled rescale test, see LazyAcc);
+// FULL: a whole chunk (no guards, no fill); REUSE: the stage may carry p only.
+template <class C, typename T, bool FIRST, bool FULL, bool REUSE>
+__device__ __forceinline__ void consume_chunk(RowsSmem<C>& S, RingPos<C::NS>& rp, int c, int nvec,
+                                              LazyAcc<false, 4>& pa, LazyAcc<true, 4>& qa) {
+  StageRegs<C> r;
+  mbar_wait(&S.full[rp.stage], rp.phase);
+  const bool po = REUSE && *reinterpret_cast<volatile int*>(&S.ponly[rp.stage]);
+  if (!po) load_stage<C, T, FULL>(S.buf[rp.stage][0], S.buf[rp.stage][1], nvec, r);
+  else load_stage_p<C, T, FULL>(S.buf[rp.stage][0], nvec, r);
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive(&S.empty[rp.stage]);
+  rp.advance();
+  if (!po) compute_stage<C, T, FIRST>(r, c, pa, qa);
+  else compute_stage_p<C, T, FIRST>(r, c, pa);
+}
+
+template <class C, typename T, bool REUSE>
 __global__ void __launch_bounds__(C::ROWS_THREADS, 1) k_rows_tma(RowsParams p) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   RowsSmem<C>& S = *reinterpret_cast<RowsSmem<C>*>(smem_raw);
@@ -769,31 +788,12 @@ __global__ void __launch_bounds__(C::ROWS_THREADS, 1) k_rows_tma(RowsParams p) {
     LazyAcc<true, 4> qa;
     pa.init();
     qa.init();
-    // wait -> 16-byte LDS of this thread's vectors -> release the stage -> math, so the
-    // producer refills the slot while the consumers compute
-    for (int c = 0; c < nchunks - 1; ++c) {  // full chunks: no guards, no fill
-      StageRegs<C> r;
-      mbar_wait(&S.full[rp.stage], rp.phase);
-      const bool po = *reinterpret_cast<volatile int*>(&S.ponly[rp.stage]);
-      if (!po) load_stage<C, T, true>(S.buf[rp.stage][0], S.buf[rp.stage][1], 0, r);
-      else load_stage_p<C, T, true>(S.buf[rp.stage][0], 0, r);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&S.empty[rp.stage]);
-      rp.advance();
-      if (!po) compute_stage<C, T>(r, c, pa, qa);
-      else compute_stage_p<C, T>(r, c, pa);
-    }
-    {  // last (possibly partial) chunk
-      StageRegs<C> r;
-      mbar_wait(&S.full[rp.stage], rp.phase);
-      const bool po = *reinterpret_cast<volatile int*>(&S.ponly[rp.stage]);
-      if (!po) load_stage<C, T, false>(S.buf[rp.stage][0], S.buf[rp.stage][1], nvec_last, r);
-      else load_stage_p<C, T, false>(S.buf[rp.stage][0], nvec_last, r);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&S.empty[rp.stage]);
-      rp.advance();
-      if (!po) compute_stage<C, T>(r, nchunks - 1, pa, qa);
-      else compute_stage_p<C, T>(r, nchunks - 1, pa);
+    if (nchunks == 1) {
+      consume_chunk<C, T, true, false, REUSE>(S, rp, 0, nvec_last, pa, qa);
+    } else {
+      consume_chunk<C, T, true, true, REUSE>(S, rp, 0, 0, pa, qa);
+      for (int c = 1; c < nchunks - 1; ++c) consume_chunk<C, T, false, true, REUSE>(S, rp, c, 0, pa, qa);
+      consume_chunk<C, T, false, false, REUSE>(S, rp, nchunks - 1, nvec_last, pa, qa);
     }
     uint2 cand;
     const RowStat ps = warp_part<C, T, false>(pa, nullptr, nvec_last, nchunks);
@@ -810,13 +810,17 @@ __global__ void __launch_bounds__(C::ROWS_THREADS, 1) k_rows_tma(RowsParams p) {
   }
 }
 
-template <class C, typename T>
-static sb_status launch_rows_tma(const RowsParams& p, cudaStream_t s) {
+template <class C, typename T, bool REUSE>
+static sb_status launch_rows_tma_k(const RowsParams& p, cudaStream_t s) {
   const int smem = (int)sizeof(RowsSmem<C>);
-  if (ensure_smem<k_rows_tma<C, T>>(smem) != cudaSuccess) return SB_ERR_CUDA;
+  if (ensure_smem<k_rows_tma<C, T, REUSE>>(smem) != cudaSuccess) return SB_ERR_CUDA;
   const int64_t max_units = (int64_t)p.d.B * p.d.K * (p.d.G + 1);
   const int grid = (int)std::min<int64_t>(num_sms(), max_units);
-  return cuda_status(launch_pdl(k_rows_tma<C, T>, dim3(grid), dim3(C::ROWS_THREADS), smem, s, p));
+  return cuda_status(launch_pdl(k_rows_tma<C, T, REUSE>, dim3(grid), dim3(C::ROWS_THREADS), smem, s, p));
+}
+template <class C, typename T>
+static sb_status launch_rows_tma(const RowsParams& p, cudaStream_t s) {
+  return p.qreuse ? launch_rows_tma_k<C, T, true>(p, s) : launch_rows_tma_k<C, T, false>(p, s);
 }
 
 template <typename T, int NT, int U>
@@ -1268,12 +1272,12 @@ static sb_status launch_step_tma(const StepParams& sp, cudaStream_t s) {
   return cuda_status(cudaGetLastError());
 }
 
-// Geometry variants (SB_ROWS_VARIANT selects one for experiments; 0 = default).
+// Geometry (SB_ROWS_VARIANT=0 / 2 forces one).  Round 1 also measured 24 consumer warps
+// x 4 x 48 KB stages and 1-vector-per-row stages (24 x 8 x 24 KB, 16 x 12 x 16 KB):
+// none beat these two.
 using RC0 = RC<20, 5, 2, 4, 4>;  // 20 consumer warps, 5 x 40 KB stages, 4 epilogue warps
-using RC1 = RC<24, 4, 2, 4, 4>;  // 24 consumer warps, 4 x 48 KB stages
 using RC2 = RC<16, 6, 2, 4, 4>;  // 16 consumer warps, 6 x 32 KB stages
-using RC3 = RC<24, 8, 1, 4, 4>;  // 24 consumer warps, 1 vector per row per stage, 8 x 24 KB stages
-using RC4 = RC<16, 12, 1, 4, 4>; // 16 consumer warps, 12 x 16 KB stages
+using RC5 = RC<16, 3, 4, 4, 4>;  // experiment: 16 consumer warps, 4 vectors per row per stage, 3 x 64 KB
 using RCF = RC<16, 6, 2, 4>;   // the fused step kernel's geometry
 
 template <typename T>
@@ -1289,13 +1293,8 @@ static sb_status launch_rows_variant(const RowsParams& p, cudaStream_t s) {
     auto waste = [&](double chunk) { const double n = std::ceil(rb / chunk); return (n * chunk - rb) / (n * chunk); };
     v = waste(RC0::CHUNK) - waste(RC2::CHUNK) > 0.03 ? 2 : 0;
   }
-  switch (v) {
-    case 1: return launch_rows_tma<RC1, T>(p, s);
-    case 2: return launch_rows_tma<RC2, T>(p, s);
-    case 3: return launch_rows_tma<RC3, T>(p, s);
-    case 4: return launch_rows_tma<RC4, T>(p, s);
-    default: return launch_rows_tma<RC0, T>(p, s);
-  }
+  if (v == 5) return launch_rows_tma<RC5, T>(p, s);
+  return v == 2 ? launch_rows_tma<RC2, T>(p, s) : launch_rows_tma<RC0, T>(p, s);
 }
 
 }  // namespace sb

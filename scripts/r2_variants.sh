@@ -6,7 +6,12 @@ TAG=$1; CFG=$2; VARS=$3; PAR=${4:-}
 export PYTHONUNBUFFERED=1
 mkdir -p gpurun_out
 for v in $VARS; do
-  if [ "$v" = default ]; then unset SB_LIB_PATH; else export SB_LIB_PATH=$PWD/build/lib_$v.so; fi
+  unset SB_LIB_PATH SB_ROWS_VARIANT
+  case $v in
+    default) ;;
+    rv*) export SB_ROWS_VARIANT=${v#rv} ;;   # geometry variant of the default library
+    *) export SB_LIB_PATH=$PWD/build/lib_$v.so ;;
+  esac
   for rep in 1 2; do
     timeout 600 python bench.py --config $CFG --steps 20 --no-e2e --no-cpu-baseline > gpurun_out/${TAG}_${CFG}_${v}_$rep.log 2>&1
   done
@@ -14,7 +19,7 @@ for v in $VARS; do
     timeout 600 python -m pytest tests/test_gpu_parity.py -q -x -p no:cacheprovider -k "small or special or identical" > gpurun_out/${TAG}_par_${v}.log 2>&1
   fi
 done
-unset SB_LIB_PATH
+unset SB_LIB_PATH SB_ROWS_VARIANT
 python - <<'PY'
 import glob, json, re, os
 tag = os.environ.get("TAG_", "")
