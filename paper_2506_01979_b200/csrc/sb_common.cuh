@@ -68,6 +68,28 @@ __host__ __device__ inline int64_t ent(const Dims& d, int b, int k, int i) {  //
   return ((int64_t)b * d.K + k) * (d.G + 1) + i;
 }
 
+// ------------------------------------------------------------------ timeline tracing
+// SB_TRACE builds only (diagnostics, scripts/step_trace.py): per CTA and role, the
+// global timer at numbered events of the streaming kernels.  Each translation unit
+// defines its own table (SB_TRACE_TABLE) and a C reader.
+#ifdef SB_TRACE
+constexpr int kTrCtas = 160, kTrRoles = 4, kTrEvents = 64;
+#define SB_TRACE_TABLE(name)                                                              \
+  __device__ unsigned long long name[::sb::kTrCtas][::sb::kTrRoles][::sb::kTrEvents];     \
+  extern "C" int name##_read(void* host, size_t bytes) {                                  \
+    return (int)cudaMemcpyFromSymbol(host, name, bytes < sizeof(name) ? bytes : sizeof(name)); \
+  }
+#define SB_TRACE_AT(table, role, ev)                                                      \
+  do {                                                                                    \
+    unsigned long long t_;                                                                \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                \
+    if (blockIdx.x < ::sb::kTrCtas && (ev) < ::sb::kTrEvents && (ev) >= 0)                \
+      table[blockIdx.x][role][ev] = t_;                                                   \
+  } while (0)
+#else
+#define SB_TRACE_AT(table, role, ev) do {} while (0)
+#endif
+
 // ------------------------------------------------------------------ small PTX helpers
 // Programmatic dependent launch (launch_pdl): wait for the predecessor grid's memory,
 // then let the next grid be scheduled.

@@ -12,6 +12,10 @@
 #include "sb_ring.cuh"
 #include "sb_stream.cuh"
 
+#ifdef SB_TRACE
+SB_TRACE_TABLE(sb_trace_conf)
+#endif
+
 namespace sb {
 
 struct ConfParams {
@@ -175,7 +179,9 @@ __global__ void __launch_bounds__(cThreads, 1) k_conf_tma(ConfParams p) {
     fence_mbar_init();
   }
   __syncthreads();
+  if (tid == 0) SB_TRACE_AT(sb_trace_conf, 0, 0);
   pdl_wait();
+  if (tid == 0) SB_TRACE_AT(sb_trace_conf, 0, 1);
   const int total = d.B * d.K * G;
   const T* QL = static_cast<const T*>(p.QL);
   const uint32_t row_bytes = (uint32_t)d.V * sizeof(T);
@@ -216,7 +222,9 @@ __global__ void __launch_bounds__(cThreads, 1) k_conf_tma(ConfParams p) {
       const T* row = QL + row_off(d, grp / d.K, grp % d.K, i);
       r.idx = resolve_argmax<ConfGeo, T>(mw, cand, r.m, row, nvec_last, nchunks);
       conf_epilogue(p, grp, i, row, r, lane, &S.s_last[e], [] { __syncwarp(); });
+      if (lane == 0) SB_TRACE_AT(sb_trace_conf, 2, 2 + li);
     }
+    if (lane == 0) SB_TRACE_AT(sb_trace_conf, 2, 63);
     return;
   }
   RingPos<cNS> rp;

@@ -44,19 +44,21 @@ __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
-// Blocking wait on a phase.  A watchdog traps after ~2^12 expired probes (seconds): a
-// protocol bug then surfaces as a launch error instead of a hung GPU.
+// Blocking wait on a phase: try_wait + branch per probe (two instructions; the waits of
+// the consumer warps are on the issue-bound critical path: a counted watchdog loop cost
+// ~2 % of the C4 verify time).  SB_WATCHDOG builds trap after ~2^12 expired probes
+// (seconds) so that a protocol bug surfaces as a launch error instead of a hung GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-#ifdef SB_WAIT_NOWATCHDOG  // experiment: two instructions per retry, no watchdog
+#ifdef SB_WATCHDOG
+  for (uint32_t tries = 0; !mbar_try(bar, parity); ++tries)
+    if (tries > (1u << 12)) __trap();
+#else
   asm volatile(
       "{\n .reg .pred p;\n"
       "WAIT_%=:\n"
       " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
       " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
       : "memory");
-#else
-  for (uint32_t tries = 0; !mbar_try(bar, parity); ++tries)
-    if (tries > (1u << 12)) __trap();
 #endif
 }
 // Waits that last whole units (an epilogue warp waiting for the consumers' partials):

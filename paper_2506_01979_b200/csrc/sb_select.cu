@@ -21,6 +21,10 @@
 #include "sb_block_sample.cuh"
 #include "sb_sample.cuh"
 
+#ifdef SB_TRACE
+SB_TRACE_TABLE(sb_trace_select)
+#endif
+
 namespace sb {
 
 struct SelParams {
@@ -282,7 +286,9 @@ __global__ void __launch_bounds__(sThreads, 1) k_select_tma(SelParams p) {
     fence_mbar_init();
   }
   __syncthreads();
+  if (tid == 0) SB_TRACE_AT(sb_trace_select, 0, 0);
   pdl_wait();
+  if (tid == 0) SB_TRACE_AT(sb_trace_select, 0, 1);
   const T* PL = static_cast<const T*>(p.PL);
   const T* QL = static_cast<const T*>(p.QL);
   const uint32_t row_bytes = (uint32_t)d.V * sizeof(T);
@@ -526,6 +532,7 @@ __global__ void __launch_bounds__(sThreads, 1) k_select_tma(SelParams p) {
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.dempty[dq.stage]);
+      if (lane == 0) SB_TRACE_AT(sb_trace_select, 2, 2 + (b / gridDim.x));
       dq.advance();
       // global completion -> the last sequence's epilogue scans the offsets
       int last = 0;
@@ -600,6 +607,7 @@ __global__ void __launch_bounds__(sThreads, 1) k_select_tma(SelParams p) {
   }
   // ---------------- the CTA that finished the last sequence: offsets + packed stream
   __syncthreads();
+  if (tid == 0) SB_TRACE_AT(sb_trace_select, 2, 62);
   if (S.s_last) {
     __threadfence();
     block_offsets<sThreads>(d.B, d.G, p.commit_len, p.out_tok, p.offsets, p.packed_tok, S.scan);

@@ -26,6 +26,12 @@
 
 namespace sb {
 
+#ifdef SB_TRACE
+}  // namespace sb
+SB_TRACE_TABLE(sb_trace_rows)
+namespace sb {
+#endif
+
 struct RowsParams {
   Dims d;
   const void* PL;
@@ -673,7 +679,9 @@ __global__ void __launch_bounds__(C::ROWS_THREADS, 1) k_rows_tma(RowsParams p) {
     fence_mbar_init();
   }
   __syncthreads();
+  if (tid == 0) SB_TRACE_AT(sb_trace_rows, 0, 0);
   pdl_wait();
+  if (tid == 0) SB_TRACE_AT(sb_trace_rows, 0, 1);
   const int total = __ldg(p.unit_off + d.B);
   const T* PL = static_cast<const T*>(p.PL);
   const T* QL = static_cast<const T*>(p.QL);
@@ -682,6 +690,7 @@ __global__ void __launch_bounds__(C::ROWS_THREADS, 1) k_rows_tma(RowsParams p) {
   const int nvec_last = (int)(row_bytes - (uint32_t)(nchunks - 1) * C::CHUNK) / 16;
 
   if (warp == C::CW) {  // ---------------- producer (lane 0 issues, the warp decodes)
+    int tli = 0;
     const uint64_t pol = policy_evict_first();
     RingPos<C::NS> rp;
     int base = 0;
@@ -689,6 +698,8 @@ __global__ void __launch_bounds__(C::ROWS_THREADS, 1) k_rows_tma(RowsParams p) {
     for (int unit = blockIdx.x; unit < total; unit += gridDim.x) {
       const Unit un = unit_from(cur);
       const Probe pr = probe_load(p, base);  // the next unit's probe, in flight during the copies
+      if (lane == 0) SB_TRACE_AT(sb_trace_rows, 1, 2 + tli);
+      ++tli;
       if (lane == 0) {
         const char* prow = reinterpret_cast<const char*>(PL + row_off(d, un.b, un.slot, un.i));
         const char* qrow = reinterpret_cast<const char*>(QL + row_off(d, un.b, un.slot, un.i));
@@ -706,6 +717,7 @@ __global__ void __launch_bounds__(C::ROWS_THREADS, 1) k_rows_tma(RowsParams p) {
       __syncwarp();
       cur = probe_resolve(p, pr, base, unit + gridDim.x, total);
     }
+    if (lane == 0) SB_TRACE_AT(sb_trace_rows, 1, 63);
     return;
   }
   if (warp > C::CW) {  // ---------------- epilogue warps: warp e takes local units e, e+NE, ...
@@ -777,17 +789,21 @@ __global__ void __launch_bounds__(C::ROWS_THREADS, 1) k_rows_tma(RowsParams p) {
         continue;
       }
       warp_epilogue<T>(p, un, ps, qs, qrow, x, lpx, lqx, uu, et);
+      if (lane == 0) SB_TRACE_AT(sb_trace_rows, 2, 2 + li);
     }
+    if (lane == 0) SB_TRACE_AT(sb_trace_rows, 2, 63);
     return;
   }
   // ---------------- consumers
   RingPos<C::NS> rp;
   RingPos<C::NP> up;
+  int tli = 0;
   for (int unit = blockIdx.x; unit < total; unit += gridDim.x) {
     LazyAcc<false, 4> pa;
     LazyAcc<true, 4> qa;
     pa.init();
     qa.init();
+    if (tid == 0) SB_TRACE_AT(sb_trace_rows, 3, 2 + tli);
     if (nchunks == 1) {
       consume_chunk<C, T, true, false, REUSE>(S, rp, 0, nvec_last, pa, qa);
     } else {
@@ -807,6 +823,8 @@ __global__ void __launch_bounds__(C::ROWS_THREADS, 1) k_rows_tma(RowsParams p) {
     }
     __syncwarp();
     up.advance();
+    if (tid == 0) SB_TRACE_AT(sb_trace_rows, 3, 32 + tli);
+    ++tli;
   }
 }
 
@@ -1272,12 +1290,12 @@ static sb_status launch_step_tma(const StepParams& sp, cudaStream_t s) {
   return cuda_status(cudaGetLastError());
 }
 
-// Geometry (SB_ROWS_VARIANT=0 / 2 forces one).  Round 1 also measured 24 consumer warps
-// x 4 x 48 KB stages and 1-vector-per-row stages (24 x 8 x 24 KB, 16 x 12 x 16 KB):
-// none beat these two.
+// Geometry (SB_ROWS_VARIANT=0 / 2 forces one).  Also measured: 24 consumer warps x 4 x
+// 48 KB stages, 1-vector-per-row stages (24 x 8 x 24 KB, 16 x 12 x 16 KB; round 1) and
+// 4 vectors per row per stage (16 x 3 x 64 KB; round 2: C4 verify +10 %, C3 +6 %): none
+// beat these two.
 using RC0 = RC<20, 5, 2, 4, 4>;  // 20 consumer warps, 5 x 40 KB stages, 4 epilogue warps
 using RC2 = RC<16, 6, 2, 4, 4>;  // 16 consumer warps, 6 x 32 KB stages
-using RC5 = RC<16, 3, 4, 4, 4>;  // experiment: 16 consumer warps, 4 vectors per row per stage, 3 x 64 KB
 using RCF = RC<16, 6, 2, 4>;   // the fused step kernel's geometry
 
 template <typename T>
@@ -1293,7 +1311,6 @@ static sb_status launch_rows_variant(const RowsParams& p, cudaStream_t s) {
     auto waste = [&](double chunk) { const double n = std::ceil(rb / chunk); return (n * chunk - rb) / (n * chunk); };
     v = waste(RC0::CHUNK) - waste(RC2::CHUNK) > 0.03 ? 2 : 0;
   }
-  if (v == 5) return launch_rows_tma<RC5, T>(p, s);
   return v == 2 ? launch_rows_tma<RC2, T>(p, s) : launch_rows_tma<RC0, T>(p, s);
 }
 
