@@ -56,26 +56,18 @@ struct Workspace {
   int* ready;        // [B] fused step: per-sequence phase-1 completion flags
   int* plan;         // [4] fused step: delta, total units
   int* seqpk;        // [B] packed layout of each sequence (k_plan): s | g<<5 | L<<10 | Lr<<16 | st<<22
-  // small-batch fused step (sb_flow.cu): counters, segment partials, sample segment maxima
-  int* fctr;         // [16] queue / barrier / completion counters (self-resetting)
-  int* frcnt;        // [B][K][G+1] segment arrivals per row pair
-  int* fccnt;        // [B][G] segment arrivals per confidence row
-  int* fcgrp;        // [B] confidence rows done per sequence
-  int* fscnt;        // [B] sample segments done per sequence
-  int* fgam;         // [B] adaptive gamma_b
-  RowStat* frpart;   // [kFlowTarget + B*K*(G+1)][2] row-pair segment partials (p, q)
-  RowStat* fcpart;   // [kFlowTarget + B*G] confidence-row segment partials
-  float* fsegmax;    // [B][nsub/8 + 1] sample-segment maxima (bonus rows)
   RowStat* qrs;      // [B][K][G] row states of the rows sb_draft_confidence streamed
                      // (read back by sb_verify_branches_reuse instead of the q rows)
+  // adaptive single-launch step (k_astep): grab / queue counters, verify entries, sample queue
+  int* actr;         // [8]
+  int4* aqv;         // [B][K][G+1] verify entries (b, slot, i)
+  int* aqv_pub;      // [B][K][G+1] entry published
+  int* asq;          // [B] sample queue
+  int* asq_pub;      // [B]
   size_t bytes;
 };
 
 inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
-
-// Work items the fused small-batch step aims for (2 per flow CTA at 4 CTAs per SM on
-// 148 SMs); also bounds its partial buffers.
-constexpr int kFlowTarget = 1184;
 
 inline Workspace carve(const sb_dims& d, void* base) {
   Workspace w{};
@@ -104,19 +96,12 @@ inline Workspace carve(const sb_dims& d, void* base) {
   w.ready = (int*)take(sizeof(int) * B);
   w.plan = (int*)take(sizeof(int) * 4);
   w.seqpk = (int*)take(sizeof(int) * B);
-  {
-    const size_t rb = (size_t)d.V * (d.dtype == SB_BF16 ? 2 : 4), nsub = (rb + 1023) / 1024;
-    w.fctr = (int*)take(sizeof(int) * 16);
-    w.frcnt = (int*)take(sizeof(int) * B * K * R1);
-    w.fccnt = (int*)take(sizeof(int) * B * (G ? G : 1));
-    w.fcgrp = (int*)take(sizeof(int) * B);
-    w.fscnt = (int*)take(sizeof(int) * B);
-    w.fgam = (int*)take(sizeof(int) * B);
-    w.frpart = (RowStat*)take(sizeof(RowStat) * 2 * (kFlowTarget + B * K * R1));
-    w.fcpart = (RowStat*)take(sizeof(RowStat) * (kFlowTarget + B * (G ? G : 1)));
-    w.fsegmax = (float*)take(sizeof(float) * B * (nsub / 8 + 1));
-  }
   w.qrs = (RowStat*)take(sizeof(RowStat) * B * K * (G ? G : 1));
+  w.actr = (int*)take(sizeof(int) * 8);
+  w.aqv = (int4*)take(sizeof(int4) * B * K * R1);
+  w.aqv_pub = (int*)take(sizeof(int) * B * K * R1);
+  w.asq = (int*)take(sizeof(int) * B);
+  w.asq_pub = (int*)take(sizeof(int) * B);
   w.bytes = off;
   return w;
 }

@@ -28,36 +28,48 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-// One probe of a phase with a suspend-time hint: the warp sleeps in hardware until the
-// phase completes (woken ~60 cycles after the last arrive) or the hint expires, so a
-// waiting warp issues a few instructions per wait instead of polling (with the
-// system-default limit the consumers' and epilogue warps' probe loops were ~20 % of
-// k_rows_tma's issued instructions).
+// One probe of a phase (the warp sleeps in hardware until the phase completes or a
+// system-dependent limit expires).  SB_WAIT_HINT=ns builds pass a suspend-time hint: it
+// did not shorten k_rows_tma's waits measurably and doubled k_select_tma's time (its
+// waits on thread arrivals woke late), so the default passes none.
+#ifdef SB_WAIT_HINT
+#define SB_TRYWAIT_ASM " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, " SB_STR(SB_WAIT_HINT) ";\n"
+#define SB_STR(x) SB_STR2(x)
+#define SB_STR2(x) #x
+#else
+#define SB_TRYWAIT_ASM " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+#endif
 __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
-      "{\n .reg .pred p;\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+      "{\n .reg .pred p;\n" SB_TRYWAIT_ASM
       " selp.u32 %0, 1, 0, p;\n}\n"
       : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
+      : "r"(smem_u32(bar)), "r"(parity)
       : "memory");
   return ok != 0;
 }
-// Blocking wait on a phase: try_wait + branch per probe (two instructions; the waits of
-// the consumer warps are on the issue-bound critical path: a counted watchdog loop cost
-// ~2 % of the C4 verify time).  SB_WATCHDOG builds trap after ~2^12 expired probes
-// (seconds) so that a protocol bug surfaces as a launch error instead of a hung GPU.
+// Blocking wait on a phase.  A watchdog traps after ~2^24 expired probes (seconds): a
+// protocol bug then surfaces as a launch error instead of a hung GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  for (uint32_t tries = 0;; ++tries) {
+    if (mbar_try(bar, parity)) break;
+    if (tries > (1u << 24)) __trap();
+  }
+}
+// The consumer warps' waits for a filled stage of the streaming kernels (k_rows_tma,
+// k_conf_tma, k_astep): try_wait + branch per probe, no watchdog (two instructions; these
+// waits sit on the issue-bound critical path, where the counted loop cost ~2 % of the C4
+// verify time).  Only there: in k_select_tma the same tight loop doubled the kernel time
+// (0.25 -> 0.45 ms on C4), so every other wait keeps mbar_wait.
+__device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
 #ifdef SB_WATCHDOG
-  for (uint32_t tries = 0; !mbar_try(bar, parity); ++tries)
-    if (tries > (1u << 12)) __trap();
+  mbar_wait(bar, parity);
 #else
   asm volatile(
       "{\n .reg .pred p;\n"
-      "WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
-      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
+      "WAIT_%=:\n" SB_TRYWAIT_ASM
+      " @!p bra WAIT_%=;\n}\n" ::"r"(0), "r"(smem_u32(bar)), "r"(parity)
       : "memory");
 #endif
 }

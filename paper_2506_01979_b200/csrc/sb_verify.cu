@@ -22,6 +22,7 @@
 #include "sb_host.h"
 #include "sb_ring.cuh"
 #include "sb_sample.cuh"
+#include "sb_conf.cuh"
 #include "sb_stream.cuh"
 
 namespace sb {
@@ -29,6 +30,7 @@ namespace sb {
 #ifdef SB_TRACE
 }  // namespace sb
 SB_TRACE_TABLE(sb_trace_rows)
+SB_TRACE_TABLE(sb_trace_astep)
 namespace sb {
 #endif
 
@@ -51,6 +53,9 @@ struct RowsParams {
   int* n_acc;
   int* status;
   int* ready;  // fused step: per-sequence "n_k known" flags (NULL otherwise)
+  // adaptive single-launch step (k_astep): the sequence whose n_k is known is appended to
+  // the sample queue (sq[atomicAdd(sq_ctr)] = b, then sq_pub[slot] released); NULL otherwise
+  int *sq_ctr, *sq, *sq_pub;
   // vocabulary-shard partial mode (a7): write the shard's row states / token logits
   int partial, v_offset;
   ShardRow* rowpart;  // [B][K][G+1] physical rows
@@ -575,6 +580,12 @@ __device__ __forceinline__ void warp_epilogue(const RowsParams& p, const Unit& u
       __threadfence();
       asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p.ready + b), "r"(1) : "memory");
     }
+    if (p.sq) {  // adaptive single-launch step: queue the sequence's sample item
+      const int slot = atomicAdd(p.sq_ctr, 1);
+      p.sq[slot] = b;
+      __threadfence();
+      asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p.sq_pub + slot), "r"(1) : "memory");
+    }
   }
 }
 
@@ -650,7 +661,7 @@ template <class C, typename T, bool FIRST, bool FULL, bool REUSE>
 __device__ __forceinline__ void consume_chunk(RowsSmem<C>& S, RingPos<C::NS>& rp, int c, int nvec,
                                               LazyAcc<false, 4>& pa, LazyAcc<true, 4>& qa) {
   StageRegs<C> r;
-  mbar_wait(&S.full[rp.stage], rp.phase);
+  mbar_wait_spin(&S.full[rp.stage], rp.phase);
   const bool po = REUSE && *reinterpret_cast<volatile int*>(&S.ponly[rp.stage]);
   if (!po) load_stage<C, T, FULL>(S.buf[rp.stage][0], S.buf[rp.stage][1], nvec, r);
   else load_stage_p<C, T, FULL>(S.buf[rp.stage][0], nvec, r);
@@ -939,8 +950,8 @@ __device__ __forceinline__ FUnit decode_fused(const RowsParams& p, const int* pl
   return f;
 }
 
-template <class C, typename T, bool RESID>
-__device__ __forceinline__ void step_seg_pass(StepSmem<C>& S, RingPos<C::NS>& rp, float* seg, int nchunks,
+template <class SM, class C, typename T, bool RESID>
+__device__ __forceinline__ void step_seg_pass(SM& S, RingPos<C::NS>& rp, float* seg, int nchunks,
                                               int nvec_last, bool ok, float MSp, float MSq, float kq) {
   constexpr int E = Vec<T>::E;
   constexpr int SPC = C::CHUNK / kSegBytes;  // segments per chunk (= consumer warps)
@@ -1270,10 +1281,10 @@ __global__ void __launch_bounds__(C::THREADS, 1) k_step_tma(StepParams sp) {
       const RowOut o = finish(r);
       if (tid == 0) S.brs[dq.stage] = make_float4(o.MS, z_store(o), 0.f, 1.f);
       consumer_sync(C::CT);
-      step_seg_pass<C, T, false>(S, rp, seg, nchunks, nvec_last, o.finite, o.MS, 0.f, 0.f);
+      step_seg_pass<StepSmem<C>, C, T, false>(S, rp, seg, nchunks, nvec_last, o.finite, o.MS, 0.f, 0.f);
     } else if (D.kind == 1) {
       const bool ok = (z_class(D.rs.y) | z_class(D.rs.w)) == 0;
-      step_seg_pass<C, T, true>(S, rp, seg, nchunks, nvec_last, ok, D.rs.x, D.rs.z, D.rs.y / D.rs.w);
+      step_seg_pass<StepSmem<C>, C, T, true>(S, rp, seg, nchunks, nvec_last, ok, D.rs.x, D.rs.z, D.rs.y / D.rs.w);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&S.pfull[up.stage]);
@@ -1288,6 +1299,557 @@ static sb_status launch_step_tma(const StepParams& sp, cudaStream_t s) {
   if (ensure_smem<k_step_tma<C, T>>(smem) != cudaSuccess) return SB_ERR_CUDA;
   k_step_tma<C, T><<<num_sms(), C::THREADS, smem, s>>>(sp);
   return cuda_status(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------- adaptive step in one launch
+// k_astep: [draft confidence -> adaptive gamma] -> verify -> select for small batches
+// (PAPER Eq. 6-7 P194-220, §3 P94, Alg. 1 P523-557, Eq. 9
+// P236-241).  One persistent CTA per SM with k_rows_tma's warp roles (TMA bulk ring,
+// consumer warps, epilogue warps); work items are grabbed in one global order
+// (atomicAdd on ctr[0]):
+//   [0, B G)            confidence items: slot-0 draft row (b, i), q only;
+//   then queue entries  verify items (b, slot, i), appended by the CTA that completes
+//                       the last confidence row of b (gamma_b = max(1, stop_b) known);
+//   then B sample items appended by the CTA that completes b's last verify item (n_k).
+// A producer waits for the entry it grabbed to be published; every entry depends only
+// on items grabbed before it (whose pipelines never wait on later items), so with all
+// CTAs co-resident the waits end.  The three phases overlap across sequences instead of
+// each ending with a grid-wide drain, and the confidence pass's q-row states replace the
+// slot-0 draft rows in the verify items (sb_verify_branches_reuse).  Every arithmetic
+// step is the separate kernels' (LazyAcc, warp_part*, resolve_argmax, conf_epilogue,
+// warp_epilogue, step_seg_pass, sample_segments), so results agree with them bit for bit.
+struct AItem {
+  int type;  // 0 confidence, 1 verify, 2 sample, -1 exit
+  int b, slot, i;
+  int po;                        // verify: p only (q state from the confidence pass)
+  int ksel, npath, kind;         // sample: Eq. 9 / Alg. 1 decision (as P2Desc)
+  float4 rs;                     // sample: row state of the residual row
+};
+constexpr int kAI = 8;  // items in flight between the producer and the other roles
+
+struct AStepParams {
+  RowsParams r;       // verify outputs and workspace (r.qreuse = confidence row states)
+  ConfParams c;       // confidence outputs, K = 1 slot-0 view
+  const float* us;
+  const int* bpos;
+  int rule;
+  int *ctr;           // [0] grab, [1] verify entries reserved, [2] sequences planned, [3] samples queued,
+                      // [4] exit count, [5] committed sequences
+  int4* qv;           // verify entries (b, slot, i)
+  int* qv_pub;
+  int* sq;            // sample queue: sequences
+  int* sq_pub;
+  int *sel_k, *commit_len, *out_tok, *y_tok, *y_kind, *offsets, *packed_tok, *path_rolled, *branch_discarded;
+  uint32_t* keep_mask;
+  float* resid_mass;
+};
+
+template <class C>
+struct AStepSmem {
+  uint64_t full[C::NS], empty[C::NS];
+  uint64_t pfull[C::NP], pempty[C::NP];
+  uint64_t ifull[kAI], iempty[kAI];
+  AItem item[kAI];
+  RowStat part[C::NP][2][C::CW];
+  uint2 cand[C::NP][C::CW];
+  float4 brs[C::NP];  // bonus-row softmax state computed by the consumers
+  RowStat red[C::CW];
+  int s_last[C::NE];
+  float seg[C::NP][kSegMax];
+  alignas(128) uint8_t buf[C::NS][2][C::CHUNK];
+};
+
+// Records written by other CTAs during this launch are read through L2 (ld.global.cg):
+// a line of neighbouring records may sit in this SM's L1 from before they were written.
+__device__ __forceinline__ SeqInfo ldcg_seqinfo(const SeqInfo* src) {
+  static_assert(sizeof(SeqInfo) == 32, "two 16-byte loads");
+  const int4 a = __ldcg(reinterpret_cast<const int4*>(src)), b = __ldcg(reinterpret_cast<const int4*>(src) + 1);
+  SeqInfo r;
+  r.g = a.x; r.s = a.y; r.L = a.z; r.st = a.w; r.Lr = b.x;
+  r.pad_[0] = b.y; r.pad_[1] = b.z; r.pad_[2] = b.w;
+  return r;
+}
+__device__ __forceinline__ RowStat ldcg_rowstat(const RowStat* src) {
+  static_assert(sizeof(RowStat) == 32, "two 16-byte loads");
+  const int4 a = __ldcg(reinterpret_cast<const int4*>(src)), b = __ldcg(reinterpret_cast<const int4*>(src) + 1);
+  RowStat r;
+  int4 w[2] = {a, b};
+  memcpy(&r, w, sizeof(r));
+  return r;
+}
+__device__ __forceinline__ int ld_acq(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_rel(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Geometry of sequence b once gamma_b is known (k_plan's clamps, unsharded): its SeqInfo.
+__device__ __forceinline__ SeqInfo astep_seqinfo(int g, int s, int G) {
+  int st = 0;
+  if (g > G) { g = G; st |= SB_ST_GAMMA_CLAMPED; }
+  if (g < 0) { g = 0; st |= SB_ST_GAMMA_CLAMPED; }
+  if (s > g) { s = g; st |= SB_ST_BRANCH_CLAMPED; }
+  if (s < 0) { s = 0; st |= SB_ST_BRANCH_CLAMPED; }
+  const int L = (s < g) ? g : g + 1;
+  return SeqInfo{g, s, L, st, L, {0, 0, 0}};
+}
+
+template <class C, typename T>
+__global__ void __launch_bounds__(C::ROWS_THREADS, 1) k_astep(AStepParams ap) {
+  constexpr int E = Vec<T>::E;
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  AStepSmem<C>& S = *reinterpret_cast<AStepSmem<C>*>(smem_raw);
+  const RowsParams& p = ap.r;
+  const Dims& d = p.d;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < C::NS; ++s) {
+      mbar_init(&S.full[s], 1);
+      mbar_init(&S.empty[s], C::CW);
+    }
+    for (int s = 0; s < C::NP; ++s) {
+      mbar_init(&S.pfull[s], C::CW);
+      mbar_init(&S.pempty[s], 1);
+    }
+    for (int s = 0; s < kAI; ++s) {
+      mbar_init(&S.ifull[s], 1);
+      mbar_init(&S.iempty[s], C::CW + 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0) SB_TRACE_AT(sb_trace_astep, 0, 0);
+  pdl_wait();
+  if (tid == 0) SB_TRACE_AT(sb_trace_astep, 0, 1);
+  const int G = d.G, nconf = d.B * G;
+  const T* PL = static_cast<const T*>(p.PL);
+  const T* QL = static_cast<const T*>(p.QL);
+  const uint32_t row_bytes = (uint32_t)d.V * sizeof(T);
+  const int nchunks = (row_bytes + C::CHUNK - 1) / C::CHUNK;
+  const int nvec_last = (int)(row_bytes - (uint32_t)(nchunks - 1) * C::CHUNK) / 16;
+  const int nseg = nchunks * (C::CHUNK / kSegBytes);
+
+  if (warp == C::CW) {  // ---------------- producer: grab, wait for the entry, publish, stream
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      RingPos<C::NS> rp;
+      RingPos<kAI> iq;
+      int exits = 0;
+      int tli = 0;
+      (void)tli;
+      while (exits < C::NE) {
+        AItem it{};
+        if (exits > 0) {
+          it.type = -1;
+        } else {
+          const int g = atomicAdd(ap.ctr, 1);
+          if (g < nconf) {
+            it.type = 0; it.b = g / G; it.slot = 0; it.i = g % G;
+          } else {
+            const int e = g - nconf;
+            for (uint32_t tries = 0;; ++tries) {
+              if (ld_acq(ap.qv_pub + e)) {
+                const int4 q = __ldcg(ap.qv + e);
+                ap.qv_pub[e] = 0;  // leave the workspace re-usable
+                it.type = 1; it.b = q.x; it.slot = q.y; it.i = q.z;
+                it.po = (q.y == 0 && q.z < G);
+                break;
+              }
+              if (ld_acq(ap.ctr + 2) == d.B) {  // every sequence planned: the verify count is final
+                const int nv = ld_acq(ap.ctr + 1);
+                if (e >= nv) {
+                  const int sidx = e - nv;
+                  if (sidx >= d.B) { it.type = -1; break; }
+                  while (!ld_acq(ap.sq_pub + sidx)) __nanosleep(64);
+                  const int b = __ldcg(ap.sq + sidx);
+                  ap.sq_pub[sidx] = 0;
+                  // Eq. 9 / Alg. 1 decision of sequence b (as k_step_tma / k_select_tma)
+                  const SeqInfo in = ldcg_seqinfo(p.info + b);
+                  int ksel = -1, besttok = 0;
+                  float bestkey = 0.f;
+                  for (int k = 0; k < d.K; ++k) {  // A = {k : n_k > s_b} (P239, P540)
+                    if (__ldcg(p.n_acc + (int64_t)b * d.K + k) <= in.s) continue;
+                    const int xk = __ldg(p.tok + ent(d, b, k, in.s));
+                    const float key = (ap.rule == SB_SELECT_ALG1) ? __ldg(p.u + ent(d, b, k, in.s))
+                                                                  : ld_scalar(PL + row_off(d, b, 0, in.s) + xk);
+                    bool better;
+                    if (ksel < 0) better = true;
+                    else if (ap.rule == SB_SELECT_ALG1) better = key > bestkey;
+                    else better = key > bestkey || (key == bestkey && xk < besttok);
+                    if (better) { ksel = k; bestkey = key; besttok = xk; }
+                  }
+                  it.type = 2; it.b = b; it.ksel = ksel;
+                  if (ksel < 0) {
+                    it.npath = min(__ldcg(p.n_acc + (int64_t)b * d.K), in.s);  // rollback (P655)
+                    it.kind = 1; it.i = it.npath; it.slot = 0;
+                  } else {
+                    it.npath = __ldcg(p.n_acc + (int64_t)b * d.K + ksel);
+                    if (it.npath < in.L) { it.kind = 1; it.i = it.npath; it.slot = (it.npath <= in.s) ? 0 : ksel; }
+                    else if (in.s < in.g) { it.kind = 2; it.i = in.g; it.slot = ksel; }  // bonus (P94)
+                    else { it.kind = 0; it.i = 0; it.slot = 0; }                          // (P237)
+                  }
+                  it.rs = (it.kind == 1) ? __ldcg(p.rowstat + ent(d, b, it.slot, it.i)) : make_float4(0.f, 1.f, 0.f, 1.f);
+                  break;
+                }
+              }
+              __nanosleep(64);
+              if (tries > (1u << 26)) __trap();  // watchdog (seconds): a publication never came
+            }
+          }
+        }
+        if (it.type < 0) ++exits;
+#ifdef SB_TRACE
+        if (tli < 60) { SB_TRACE_AT(sb_trace_astep, 1, 2 + tli); sb_trace_astep[blockIdx.x][0][2 + tli] = it.type + 1; }
+        ++tli;
+#endif
+        mbar_wait(&S.iempty[iq.stage], iq.phase ^ 1u);
+        S.item[iq.stage] = it;
+        mbar_arrive(&S.ifull[iq.stage]);
+        iq.advance();
+        if (it.type < 0) continue;
+        const char* prow = reinterpret_cast<const char*>(PL + row_off(d, it.b, it.slot, it.i));
+        const char* qrow = reinterpret_cast<const char*>(QL + row_off(d, it.b, it.slot, it.i));
+        const bool wp = it.type != 0, wq = (it.type == 0) || (it.type == 1 && !it.po) || (it.type == 2 && it.kind == 1);
+        const int passes = (it.type == 2) ? (it.kind == 1 ? 1 : (it.kind == 2 ? 2 : 0)) : 1;
+        for (int pass = 0; pass < passes; ++pass)
+          for (int c = 0; c < nchunks; ++c) {
+            const uint32_t bytes = min((uint32_t)C::CHUNK, row_bytes - (uint32_t)c * C::CHUNK);
+            mbar_wait(&S.empty[rp.stage], rp.phase ^ 1u);
+            mbar_expect_tx(&S.full[rp.stage], ((wp ? 1 : 0) + (wq ? 1 : 0)) * bytes);
+            if (wp) bulk_g2s(S.buf[rp.stage][0], prow + (size_t)c * C::CHUNK, bytes, &S.full[rp.stage], pol);
+            if (wq) bulk_g2s(S.buf[rp.stage][1], qrow + (size_t)c * C::CHUNK, bytes, &S.full[rp.stage], pol);
+            rp.advance();
+          }
+      }
+    }
+  } else if (warp > C::CW) {  // ---------------- epilogue warps: warp e takes items e, e + NE, ...
+    const int e = warp - C::CW - 1;
+    for (int li = e;; li += C::NE) {
+      const int islot = li % kAI;
+      mbar_wait(&S.ifull[islot], (uint32_t)(li / kAI) & 1u);
+      const AItem it = S.item[islot];
+      if (it.type < 0) break;
+      const int ps_slot = li % C::NP;
+      const uint32_t pph = (uint32_t)(li / C::NP) & 1u;
+      if (it.type == 0) {  // ---- confidence row (b, i): statistic, Eq. 6 / 7; the group's last plans b
+        const T* qrow = QL + row_off(d, it.b, 0, it.i);
+        mbar_wait(&S.pfull[ps_slot], pph);
+        RowStat qs = lane < C::CW ? S.part[ps_slot][1][lane] : rowstat_empty();
+        const uint2 cand = lane < C::CW ? S.cand[ps_slot][lane] : make_uint2(0xffffffffu, 0u);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.pempty[ps_slot]);
+        const float qmw = qs.m;
+        qs = warp_reduce_state(qs);
+        qs.idx = resolve_argmax<C, T>(qmw, cand, qs.m, qrow, nvec_last, nchunks);
+        conf_epilogue(ap.c, it.b, it.i, qrow, qs, lane, &S.s_last[e], [] { __syncwarp(); });
+        if (S.s_last[e]) {  // gamma_b = max(1, stop_b) is known: b's verify items (k_plan's layout)
+          __threadfence();
+          const int g = __ldcg(ap.c.gamma_next + it.b);
+          const int s0 = ap.bpos ? __ldg(ap.bpos + it.b) : 0;
+          const SeqInfo in = astep_seqinfo(g, s0, G);
+          const int per = in.Lr - 1 - in.s;
+          const int count = in.Lr + (d.K - 1) * per;
+          int start = 0;
+          if (lane == 0) {
+            const_cast<SeqInfo*>(p.info)[it.b] = in;  // (read-only for the other kernels)
+            start = atomicAdd(ap.ctr + 1, count);
+          }
+          start = __shfl_sync(0xffffffffu, start, 0);
+          for (int j = lane; j < count; j += 32) {
+            int slot, i;
+            if (j < in.Lr) { slot = 0; i = j; }
+            else { const int jj = j - in.Lr; slot = 1 + jj / per; i = in.s + 1 + jj % per; }
+            ap.qv[start + j] = make_int4(it.b, slot, i, 0);
+          }
+          __threadfence();
+          __syncwarp();
+          for (int j = lane; j < count; j += 32) st_rel(ap.qv_pub + start + j, 1);
+          __syncwarp();
+          if (lane == 0) {
+            __threadfence();
+            atomicAdd(ap.ctr + 2, 1);  // after the reservation: ctr[1] is final once this reaches B
+          }
+        }
+      } else if (it.type == 1) {  // ---- verify row pair: token tests, n_k (warp_epilogue)
+        Unit un;
+        un.b = it.b; un.slot = it.slot; un.i = it.i; un.in = ldcg_seqinfo(p.info + it.b);
+        const T* prow = PL + row_off(d, un.b, un.slot, un.i);
+        const T* qrow = QL + row_off(d, un.b, un.slot, un.i);
+        const bool branch_row = (un.slot == 0 && un.i == un.in.s);
+        const int ntok = branch_row ? d.K : 1;
+        int x = 0;
+        float lpx = 0.f, lqx = 0.f, uu = 0.f;
+        int64_t et = 0;
+        if (lane < ntok && un.i < un.in.L) {
+          et = ent(d, un.b, branch_row ? lane : un.slot, un.i);
+          x = __ldg(p.tok + et);
+          uu = __ldg(p.u + et);
+          if (x >= 0 && x < d.V) {
+            lpx = ld_scalar(prow + x);
+            lqx = ld_scalar(qrow + x);
+          } else {
+            lpx = lqx = -CUDART_INF_F;
+          }
+        }
+        RowStat qr;
+        if (it.po) qr = ldcg_rowstat(p.qreuse + (int64_t)un.b * G + un.i);
+        mbar_wait(&S.pfull[ps_slot], pph);
+        RowStat ps = lane < C::CW ? S.part[ps_slot][0][lane] : rowstat_empty();
+        RowStat qs = lane < C::CW ? S.part[ps_slot][1][lane] : rowstat_empty();
+        const uint2 cand = lane < C::CW ? S.cand[ps_slot][lane] : make_uint2(0xffffffffu, 0u);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.pempty[ps_slot]);
+        const float qmw = qs.m;
+        ps = warp_reduce_state(ps);
+        qs = warp_reduce_state(qs);
+        if (it.po) qs = qr;
+        else qs.idx = resolve_argmax<C, T>(qmw, cand, qs.m, qrow, nvec_last, nchunks);
+        warp_epilogue<T>(p, un, ps, qs, qrow, x, lpx, lqx, uu, et);
+      } else {  // ---- sample: locate us * R, rescan one segment, commit (as k_step_tma)
+        const int b = it.b;
+        const SeqInfo in = ldcg_seqinfo(p.info + b);
+        mbar_wait(&S.pfull[ps_slot], pph);
+        int kind = it.kind, y = -1, st = 0;
+        double mass = 0.0;
+        if (kind != 0) {
+          const float4 rs = (kind == 1) ? it.rs : S.brs[ps_slot];
+          const int cls = z_class(rs.y) | z_class(rs.w);
+          if (cls) {
+            kind = 0;
+            st |= cls;
+          } else {
+            const T* prow = PL + row_off(d, b, it.slot, it.i);
+            const T* qrow = QL + row_off(d, b, it.slot, it.i);
+            bool resid = (kind == 1);
+            double R = 0.0;
+            y = sample_segments<T>(prow, qrow, row_bytes, d.V, S.seg[ps_slot], nseg, resid, rs.x, rs.z,
+                                   rs.y / rs.w, __ldg(ap.us + b), st, &R);
+            mass = R / (double)rs.y;  // back to probability mass
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.pempty[ps_slot]);
+        const int ksel = it.ksel, npath = it.npath, kpath = ksel < 0 ? 0 : ksel;  // commit
+        int* out = ap.out_tok + (int64_t)b * (G + 2);
+        for (int qq = lane; qq < G + 2; qq += 32) {
+          int v = -1;
+          if (qq < npath) v = __ldg(p.tok + ent(d, b, (qq < in.s) ? 0 : kpath, qq));
+          else if (qq == npath && kind != 0) v = y;
+          out[qq] = v;
+        }
+        if (lane < d.K) {
+          uint32_t km = 0;
+          for (int qq = 0; qq < npath; ++qq)
+            if (((qq < in.s) ? 0 : kpath) == lane) km |= 1u << qq;
+          ap.keep_mask[(int64_t)b * d.K + lane] = km;
+        }
+        if (lane == 0) {
+          ap.sel_k[b] = ksel;
+          ap.commit_len[b] = npath + (kind != 0);
+          ap.y_tok[b] = (kind != 0) ? y : -1;
+          ap.y_kind[b] = kind;
+          ap.path_rolled[b] = in.L - npath;
+          ap.branch_discarded[b] = (d.K - 1) * (in.L - in.s);
+          if (ap.resid_mass) ap.resid_mass[b] = (kind != 0) ? (float)mass : 0.f;
+          if (st) atomicOr(p.status + b, st);
+        }
+        __syncwarp();
+        int last = 0;
+        if (lane == 0) {
+          __threadfence();
+          last = (atomicAdd(ap.ctr + 5, 1) == d.B - 1);
+        }
+        last = __shfl_sync(0xffffffffu, last, 0);
+        if (last) {
+          __threadfence();
+          warp_offsets(d.B, G, ap.commit_len, ap.out_tok, ap.offsets, ap.packed_tok);
+          if (lane == 0) ap.ctr[5] = 0;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.iempty[islot]);
+      if (lane == 0 && li < 60) SB_TRACE_AT(sb_trace_astep, 2, 2 + li);
+    }
+  } else {  // ---------------- consumers
+    RingPos<C::NS> rp;
+    for (int li = 0;; ++li) {
+      const int islot = li % kAI;
+      mbar_wait(&S.ifull[islot], (uint32_t)(li / kAI) & 1u);
+      const AItem it = S.item[islot];
+      if (it.type < 0) break;
+      const int ps_slot = li % C::NP;
+      const uint32_t pph = (uint32_t)(li / C::NP) & 1u;
+      if (it.type != 2) {
+        LazyAcc<false, 4> pa;
+        LazyAcc<true, 4> qa;
+        pa.init();
+        qa.init();
+        for (int c = 0; c < nchunks; ++c) {
+          const bool full = c < nchunks - 1;
+          const int nvec = full ? C::CHUNK / 16 : nvec_last;
+          StageRegs<C> r;
+          mbar_wait_spin(&S.full[rp.stage], rp.phase);
+#pragma unroll
+          for (int j = 0; j < C::VPT; ++j) {
+            const int v = tid + j * C::CT;
+            const bool have = full || v < nvec;
+            r.p[j] = (it.type == 1 && have) ? lds128(S.buf[rp.stage][0] + v * 16) : neg_inf_vec<T>();
+            r.q[j] = (!it.po && have) ? lds128(S.buf[rp.stage][1] + v * 16) : neg_inf_vec<T>();
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&S.empty[rp.stage]);
+          rp.advance();
+          if (it.type == 0) {  // q row only
+            if (c == 0) {
+              if constexpr (sizeof(T) == 2) acc_vecs_bf16<C::VPT, true, true>(qa, r.q, c);
+              else { float f[C::VPT * E];
+#pragma unroll
+                for (int j = 0; j < C::VPT; ++j) Vec<T>::unpack(r.q[j], f + j * E);
+                qa.template add<C::VPT * E, true>(f, c); }
+            } else {
+              if constexpr (sizeof(T) == 2) acc_vecs_bf16<C::VPT, true, false>(qa, r.q, c);
+              else { float f[C::VPT * E];
+#pragma unroll
+                for (int j = 0; j < C::VPT; ++j) Vec<T>::unpack(r.q[j], f + j * E);
+                qa.template add<C::VPT * E, false>(f, c); }
+            }
+          } else if (it.po) {
+            if (c == 0) compute_stage_p<C, T, true>(r, c, pa);
+            else compute_stage_p<C, T, false>(r, c, pa);
+          } else {
+            if (c == 0) compute_stage<C, T, true>(r, c, pa, qa);
+            else compute_stage<C, T, false>(r, c, pa, qa);
+          }
+        }
+        uint2 cand = make_uint2(0xffffffffu, 0u);
+        const RowStat ps = (it.type == 1) ? warp_part<C, T, false>(pa, nullptr, nvec_last, nchunks) : rowstat_empty();
+        const RowStat qs = it.po ? rowstat_empty() : warp_part_deferred(qa, cand);
+        if (lane == 0) {
+          mbar_wait(&S.pempty[ps_slot], pph ^ 1u);
+          S.part[ps_slot][0][warp] = ps;
+          S.part[ps_slot][1][warp] = qs;
+          S.cand[ps_slot][warp] = cand;
+          mbar_arrive(&S.pfull[ps_slot]);
+        }
+        __syncwarp();
+      } else {  // sample item: one sum per 1 KB segment (bonus rows: their softmax state first)
+        if (lane == 0) mbar_wait(&S.pempty[ps_slot], pph ^ 1u);  // seg slot free
+        __syncwarp();
+        float* seg = S.seg[ps_slot];
+        if (it.kind == 2) {
+          LazyAcc<false, 4> a;
+          a.init();
+          for (int c = 0; c < nchunks; ++c) {
+            const int nvec = (c == nchunks - 1) ? nvec_last : C::CHUNK / 16;
+            mbar_wait(&S.full[rp.stage], rp.phase);
+            uint4 x[C::VPT];
+#pragma unroll
+            for (int j = 0; j < C::VPT; ++j) {
+              const int v = tid + j * C::CT;
+              x[j] = (v < nvec) ? lds128(S.buf[rp.stage][0] + v * 16) : neg_inf_vec<T>();
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&S.empty[rp.stage]);
+            rp.advance();
+            float f[C::VPT * E];
+#pragma unroll
+            for (int j = 0; j < C::VPT; ++j) Vec<T>::unpack(x[j], f + j * E);
+            a.template add<C::VPT * E>(f, c);
+          }
+          RowStat s = fold_lazy(a);
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) s = combine(s, shfl_xor(s, o));
+          if (lane == 0) S.red[warp] = s;
+          consumer_sync(C::CT);
+          RowStat rr = S.red[0];
+#pragma unroll
+          for (int j = 1; j < C::CW; ++j) rr = combine(rr, S.red[j]);
+          const RowOut o = finish(rr);
+          if (tid == 0) S.brs[ps_slot] = make_float4(o.MS, z_store(o), 0.f, 1.f);
+          consumer_sync(C::CT);
+          step_seg_pass<AStepSmem<C>, C, T, false>(S, rp, seg, nchunks, nvec_last, o.finite, o.MS, 0.f, 0.f);
+        } else if (it.kind == 1) {
+          const bool ok = (z_class(it.rs.y) | z_class(it.rs.w)) == 0;
+          step_seg_pass<AStepSmem<C>, C, T, true>(S, rp, seg, nchunks, nvec_last, ok, it.rs.x, it.rs.z,
+                                                  it.rs.y / it.rs.w);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.pfull[ps_slot]);
+      }
+      if (lane == 0) mbar_arrive(&S.iempty[islot]);
+      if (tid == 0 && li < 60) SB_TRACE_AT(sb_trace_astep, 3, 2 + li);
+    }
+  }
+  // ---------------- exit: the last CTA out resets the grab / queue counters
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    if (atomicAdd(ap.ctr + 4, 1) == (int)gridDim.x - 1) {
+      ap.ctr[0] = 0; ap.ctr[1] = 0; ap.ctr[2] = 0; ap.ctr[3] = 0; ap.ctr[4] = 0;
+    }
+  }
+}
+
+template <class C, typename T>
+static sb_status launch_astep(const AStepParams& ap, cudaStream_t s) {
+  const int smem = (int)sizeof(AStepSmem<C>);
+  if (ensure_smem<k_astep<C, T>>(smem) != cudaSuccess) return SB_ERR_CUDA;
+  return cuda_status(launch_pdl(k_astep<C, T>, dim3(num_sms()), dim3(C::ROWS_THREADS), smem, s, ap));
+}
+
+// sb_step_adaptive's single-launch path (called after its argument checks).
+// w / cw: the step and confidence workspaces; outputs as sb_step_adaptive documents.
+// Default: small problems (<= 4096 physical rows per slot set: C2's 64 x 4 x 9), where the
+// three kernels' launch / ramp / drain dominate (C2 step 77.6 -> 71.3 us); on C3 (17408)
+// the three kernels are faster (0.962 vs 0.992 ms).  SB_ASTEP=1 / 0 forces it on / off.
+bool astep_eligible(const sb_dims* dd, const void* PL, const void* QL) {
+  const char* e = getenv("SB_ASTEP");
+  if (e && e[0] == '0') return false;
+  if (tma_disabled() || sharded(dd) || dd->G < 1) return false;
+  if (!vec_ok(dd, PL) || !vec_ok(dd, QL)) return false;
+  const size_t rb = (size_t)dd->V * elem_size(dd);
+  if (rb % 16 || rb > (size_t)kSegMax * kSegBytes) return false;
+  return (e && e[0] == '1') || (size_t)dd->B * dd->K * (dd->G + 1) <= 4096;
+}
+
+using RCA = RC<16, 6, 2, 4, 4>;  // k_astep: 16 consumer warps, 6 x 32 KB stages, 4 epilogue warps
+
+sb_status astep_run(const sb_dims* dd, const Workspace& w, const Workspace& cw, const void* PL, const void* QL,
+                    const int32_t* tok, const float* u, const float* us, const int32_t* branch_pos,
+                    sb_select_rule rule, float eps, int32_t k_max, float* c_top1, int32_t* c_id, float* c_ent,
+                    float* c_stat, int32_t* c_stop, int32_t* c_knext, int32_t* c_gamma, float* lse_p, float* lse_q,
+                    float* p_tok, float* q_tok, uint32_t* acc_mask, int32_t* n_acc, float* top1_q,
+                    int32_t* top1_id_q, float* entropy_q, int32_t* status, int32_t* sel_k, int32_t* commit_len,
+                    int32_t* out_tok, int32_t* y_tok, int32_t* y_kind, int32_t* offsets, int32_t* packed_tok,
+                    int32_t* path_rolled, int32_t* branch_discarded, uint32_t* keep_mask, float* resid_mass,
+                    cudaStream_t s) {
+  const Dims d = to_dims(dd);
+  AStepParams ap{};
+  RowsParams& p = ap.r;
+  p.d = d; p.PL = PL; p.QL = QL; p.tok = tok; p.u = u;
+  p.info = w.info; p.unit_off = w.unit_off; p.seqpk = w.seqpk; p.cnt = w.cnt; p.rowstat = w.rowstat;
+  p.pflag = w.pflag;
+  p.lse_p = lse_p; p.lse_q = lse_q; p.p_tok = p_tok; p.q_tok = q_tok;
+  p.top1_q = top1_q; p.entropy_q = entropy_q; p.top1_id_q = top1_id_q;
+  p.acc_mask = acc_mask; p.n_acc = n_acc; p.status = status;
+  p.qreuse = cw.qrs;
+  p.sq_ctr = w.actr + 3; p.sq = w.asq; p.sq_pub = w.asq_pub;
+  ConfParams& c = ap.c;
+  c.d = d;
+  c.d.K = 1;  // slot-0 view of the draft rows
+  c.QL = QL; c.tok = nullptr; c.mode = SB_CONF_TOP1; c.eps = eps; c.lambda = 1.f; c.k_max = k_max;
+  c.top1_prob = c_top1; c.entropy = c_ent; c.tok_prob = nullptr; c.stat = c_stat; c.top1_id = c_id;
+  c.stop = c_stop; c.k_next = c_knext; c.gamma_next = c_gamma;
+  c.cnt = cw.conf_cnt; c.ws_stat = cw.conf_stat; c.ws_c = cw.conf_c; c.qrs = cw.qrs;
+  ap.us = us; ap.bpos = branch_pos; ap.rule = rule;
+  ap.ctr = w.actr; ap.qv = w.aqv; ap.qv_pub = w.aqv_pub; ap.sq = w.asq; ap.sq_pub = w.asq_pub;
+  ap.sel_k = sel_k; ap.commit_len = commit_len; ap.out_tok = out_tok; ap.y_tok = y_tok; ap.y_kind = y_kind;
+  ap.offsets = offsets; ap.packed_tok = packed_tok; ap.path_rolled = path_rolled;
+  ap.branch_discarded = branch_discarded; ap.keep_mask = keep_mask; ap.resid_mass = resid_mass;
+  return dd->dtype == SB_BF16 ? launch_astep<RCA, __nv_bfloat16>(ap, s) : launch_astep<RCA, float>(ap, s);
 }
 
 // Geometry (SB_ROWS_VARIANT=0 / 2 forces one).  Also measured: 24 consumer warps x 4 x
@@ -1318,17 +1880,6 @@ static sb_status launch_rows_variant(const RowsParams& p, cudaStream_t s) {
 
 using namespace sb;
 
-namespace sb {
-bool flow_eligible(const sb_dims* dd, const void* PL, const void* QL);
-}
-sb_status sb_flow_verify_select(const sb_dims* dd, const void* p_logits, const void* q_logits, const int32_t* tok,
-                                const float* u, const float* us, const int32_t* gamma, const int32_t* branch_pos,
-                                sb_select_rule rule, float* lse_p, float* lse_q, float* p_tok, float* q_tok,
-                                uint32_t* acc_mask, int32_t* n_acc, float* top1_q, int32_t* top1_id_q,
-                                float* entropy_q, int32_t* status, int32_t* sel_k, int32_t* commit_len,
-                                int32_t* out_tok, int32_t* y_tok, int32_t* y_kind, int32_t* offsets,
-                                int32_t* packed_tok, int32_t* path_rolled, int32_t* branch_discarded,
-                                uint32_t* keep_mask, float* resid_mass, void* workspace, cudaStream_t s);
 
 struct sb_comm;
 sb_status sb_shard_verify_nccl(const sb_dims* d, const void* p_logits, const void* q_logits, const int32_t* tok,
@@ -1395,7 +1946,7 @@ static sb_status verify_impl(const sb_dims* dd, const void* p_logits, const void
                  (int*)nullptr, (int*)nullptr, w.seqpk) != cudaSuccess)
     return SB_ERR_CUDA;
 
-  RowsParams p;
+  RowsParams p{};
   p.d = d; p.PL = p_logits; p.QL = q_logits; p.tok = tok; p.u = u;
   p.info = w.info; p.unit_off = w.unit_off; p.seqpk = w.seqpk; p.cnt = w.cnt; p.rowstat = w.rowstat;
   p.pflag = w.pflag;
@@ -1473,11 +2024,6 @@ extern "C" sb_status sb_verify_select(const sb_dims* dd, const void* p_logits, c
   if (workspace_bytes < w.bytes) return SB_ERR_WORKSPACE;
   const bool vok = vec_ok(dd, p_logits) && vec_ok(dd, q_logits);
   const size_t row_bytes = (size_t)dd->V * elem_size(dd);
-  if (flow_eligible(dd, p_logits, q_logits))  // small batches: one launch (sb_flow.cu)
-    return sb_flow_verify_select(dd, p_logits, q_logits, tok, u, us, gamma, branch_pos, rule, lse_p, lse_q, p_tok,
-                                 q_tok, acc_mask, n_acc, top1_q, top1_id_q, entropy_q, status, sel_k, commit_len,
-                                 out_tok, y_tok, y_kind, offsets, packed_tok, path_rolled, branch_discarded,
-                                 keep_mask, resid_mass, workspace, (cudaStream_t)stream);
   // The single-launch fused kernel (k_step_tma) is correct but measured slower than the
   // two launches on B200 (C4: 6.88 vs 6.70 ms), so it is opt-in.
   const char* fz = getenv("SB_FUSED_STEP");
@@ -1509,4 +2055,53 @@ extern "C" sb_status sb_verify_select(const sb_dims* dd, const void* p_logits, c
   sp.offsets = offsets; sp.packed_tok = packed_tok; sp.path_rolled = path_rolled;
   sp.branch_discarded = branch_discarded; sp.keep_mask = keep_mask; sp.resid_mass = resid_mass;
   return dd->dtype == SB_BF16 ? launch_step_tma<RCF, __nv_bfloat16>(sp, s) : launch_step_tma<RCF, float>(sp, s);
+}
+
+extern "C" sb_status sb_step_adaptive(const sb_dims* dd, const void* p_logits, const void* q_logits,
+                                      const int32_t* tok, const float* u, const float* us,
+                                      const int32_t* branch_pos, sb_select_rule rule, float eps, int32_t k_max,
+                                      float* c_top1_prob, int32_t* c_top1_id, float* c_entropy, float* c_stat,
+                                      int32_t* c_stop, int32_t* c_k_next, int32_t* c_gamma_next, float* lse_p,
+                                      float* lse_q, float* p_tok, float* q_tok, uint32_t* acc_mask, int32_t* n_acc,
+                                      float* top1_q, int32_t* top1_id_q, float* entropy_q, int32_t* status,
+                                      int32_t* sel_k, int32_t* commit_len, int32_t* out_tok, int32_t* y_tok,
+                                      int32_t* y_kind, int32_t* offsets, int32_t* packed_tok, int32_t* path_rolled,
+                                      int32_t* branch_discarded, uint32_t* keep_mask, float* resid_mass,
+                                      void* conf_workspace, size_t conf_workspace_bytes, void* workspace,
+                                      size_t workspace_bytes, sb_stream_t stream) {
+  SB_NVTX("sb_step_adaptive");
+  if (!dims_valid(dd) || sharded(dd) || dd->G < 1) return SB_ERR_INVALID_ARG;
+  if (!p_logits || !q_logits || !tok || !u || !us || !c_top1_prob || !c_top1_id || !c_entropy || !c_stat ||
+      !c_stop || !c_k_next || !c_gamma_next || !lse_p || !lse_q || !p_tok || !q_tok || !acc_mask || !n_acc ||
+      !status || !sel_k || !commit_len || !out_tok || !y_tok || !y_kind || !offsets || !path_rolled ||
+      !branch_discarded || !keep_mask || !workspace || !conf_workspace)
+    return SB_ERR_INVALID_ARG;
+  if (rule != SB_SELECT_EQ9 && rule != SB_SELECT_ALG1) return SB_ERR_INVALID_ARG;
+  if (!(eps > 0.f && eps < 1.f) || k_max < 1) return SB_ERR_INVALID_ARG;
+  if ((uintptr_t)workspace % 256 || (uintptr_t)conf_workspace % 256) return SB_ERR_INVALID_ARG;
+  const Workspace w = carve(*dd, workspace);
+  if (workspace_bytes < w.bytes) return SB_ERR_WORKSPACE;
+  sb_dims cd = *dd;  // slot-0 view of the draft rows
+  cd.K = 1;
+  cd.seq_stride = to_dims(dd).ss;
+  if (conf_workspace_bytes < sb_workspace_bytes(&cd)) return SB_ERR_WORKSPACE;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (astep_eligible(dd, p_logits, q_logits))  // one persistent launch (k_astep)
+    return astep_run(dd, w, carve(cd, conf_workspace), p_logits, q_logits, tok, u, us, branch_pos, rule, eps, k_max,
+                     c_top1_prob, c_top1_id, c_entropy, c_stat, c_stop, c_k_next, c_gamma_next, lse_p, lse_q, p_tok,
+                     q_tok, acc_mask, n_acc, top1_q, top1_id_q, entropy_q, status, sel_k, commit_len, out_tok, y_tok,
+                     y_kind, offsets, packed_tok, path_rolled, branch_discarded, keep_mask, resid_mass, s);
+  // SB_ASTEP=0 or unaligned rows: the three streaming kernels (the verify reuses the
+  // confidence pass's slot-0 draft-row states)
+  sb_status st = sb_draft_confidence(&cd, q_logits, nullptr, SB_CONF_TOP1, eps, 1.0f, k_max, c_top1_prob, c_top1_id,
+                                     c_entropy, nullptr, c_stat, c_stop, c_k_next, c_gamma_next, nullptr,
+                                     conf_workspace, conf_workspace_bytes, stream);
+  if (st != SB_OK) return st;
+  st = sb_verify_branches_reuse(dd, p_logits, q_logits, tok, u, c_gamma_next, branch_pos, lse_p, lse_q, p_tok, q_tok,
+                                acc_mask, n_acc, top1_q, top1_id_q, entropy_q, status, conf_workspace, workspace,
+                                workspace_bytes, stream);
+  if (st != SB_OK) return st;
+  return sb_select_branch(dd, p_logits, q_logits, tok, u, us, c_gamma_next, branch_pos, n_acc, rule, sel_k,
+                          commit_len, out_tok, y_tok, y_kind, offsets, packed_tok, path_rolled, branch_discarded,
+                          keep_mask, resid_mass, status, nullptr, workspace, workspace_bytes, stream);
 }

@@ -3,6 +3,7 @@
 // (b) the same TMA bulk ring as k_rows_tma with trivial consumers (XOR of one word).
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o readbw readbw.cu && ./readbw
 #include <cstdio>
+#include <type_traits>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -86,17 +87,31 @@ int main() {
     }
     printf("ldg  %d CTA/SM x 512 thr, 8x16B in flight/thread: %.1f GB/s\n", blocks_per_sm, bytes / (ms * 1e-3) / 1e9);
   }
-  constexpr int NS = 6, CH = 32768;
-  const int smem = 1024 + NS * CH;
-  cudaFuncSetAttribute(k_tma<NS, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  for (int it = 0; it < 3; ++it) {
-    cudaEventRecord(a);
-    k_tma<NS, CH><<<sms, 544, smem>>>(p, bytes, out);
-    cudaEventRecord(b);
-    cudaEventSynchronize(b);
-    cudaEventElapsedTime(&ms, a, b);
+  auto run_tma = [&](auto ns_tag, auto ch_tag, size_t nbytes, int reps) {
+    constexpr int NS_ = decltype(ns_tag)::value, CH_ = decltype(ch_tag)::value;
+    const int smem = 1024 + NS_ * CH_;
+    cudaFuncSetAttribute(k_tma<NS_, CH_>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    float best = 1e30f;
+    for (int it = 0; it < reps; ++it) {
+      cudaEventRecord(a);
+      k_tma<NS_, CH_><<<sms, 544, smem>>>(p + (size_t)(it % 8) * (1ull << 30), nbytes, out);
+      cudaEventRecord(b);
+      cudaEventSynchronize(b);
+      cudaEventElapsedTime(&ms, a, b);
+      best = ms < best ? ms : best;
+    }
+    printf("tma  bulk ring %2d x %2d KB (%3d KB in flight/SM), %7.1f MB: %7.1f GB/s  %8.2f us (%s)\n", NS_, CH_ / 1024,
+           NS_ * CH_ / 1024, nbytes / 1e6, nbytes / (best * 1e-3) / 1e9, best * 1e3, cudaGetErrorString(cudaGetLastError()));
+  };
+  using std::integral_constant;
+  for (size_t nb : {(size_t)4 << 30, (size_t)33554432, (size_t)8388608}) {
+    const int reps = nb > (1u << 30) ? 3 : 20;
+    run_tma(integral_constant<int, 2>{}, integral_constant<int, 16384>{}, nb, reps);
+    run_tma(integral_constant<int, 6>{}, integral_constant<int, 16384>{}, nb, reps);
+    run_tma(integral_constant<int, 12>{}, integral_constant<int, 16384>{}, nb, reps);
+    run_tma(integral_constant<int, 3>{}, integral_constant<int, 32768>{}, nb, reps);
+    run_tma(integral_constant<int, 6>{}, integral_constant<int, 32768>{}, nb, reps);
+    run_tma(integral_constant<int, 24>{}, integral_constant<int, 8192>{}, nb, reps);
   }
-  printf("tma  bulk ring %d x %d KB, 1 CTA/SM: %.1f GB/s (%s)\n", NS, CH / 1024, bytes / (ms * 1e-3) / 1e9,
-         cudaGetErrorString(cudaGetLastError()));
   return 0;
 }

@@ -106,17 +106,14 @@ SMALL = [
 ]
 
 
-@pytest.mark.parametrize("fused", ["flow", "single_launch", "verify_select", "two_calls"])
+@pytest.mark.parametrize("fused", ["single_launch", "verify_select", "two_calls"])
 @pytest.mark.parametrize("name,kw,pad,rule", SMALL, ids=[c[0] for c in SMALL])
 def test_small_parity(name, kw, pad, rule, fused, monkeypatch):
-    """flow: the opt-in one-launch small-batch kernel (SB_FLOW=1, sb_flow.cu);
-    single_launch: the persistent TMA-ring k_step_tma (SB_FUSED_STEP=1); verify_select: the
-    two streaming kernels behind sb_verify_select (the default); two_calls:
+    """single_launch: the persistent TMA-ring k_step_tma (SB_FUSED_STEP=1); verify_select:
+    the two streaming kernels behind sb_verify_select (the default); two_calls:
     sb_verify_branches then sb_select_branch."""
     kw = dict(kw)
     c = cfg(kw.pop("name"), **kw)
-    if fused == "flow":
-        monkeypatch.setenv("SB_FLOW", "1")
     if fused == "single_launch":
         monkeypatch.setenv("SB_FUSED_STEP", "1")  # the persistent k_step_tma kernel
     rep, g = _run(c, row_pad=pad, rule=rule, fused=(fused != "two_calls"))
@@ -136,17 +133,31 @@ def test_register_staged_fallback_parity(monkeypatch, name, kw):
     assert rep["exact_seq"] >= 0.9 * rep["n"], rep
 
 
-@pytest.mark.parametrize("path", ["flow", "three_calls"])
-def test_adaptive_confidence_parity(path, monkeypatch):
-    """The adaptive-gamma step through sb_step_adaptive: the opt-in one-launch kernel
-    (SB_FLOW=1) and the default three streaming kernels (confidence -> verify reusing its
-    rows -> select)."""
-    if path == "flow":
-        monkeypatch.setenv("SB_FLOW", "1")
-    rep, g = _run(cfg("c2", B=64), adaptive=True)
-    assert rep["n"] >= 60
-    rep, g = _run(cfg("c2", V=5000, B=40, K=3, G=12, layout="mixed"), adaptive=True)
-    assert rep["n"] >= 36
+ADAPTIVE = [
+    ("c2_B64", dict(name="c2", B=64), 0, 60),
+    ("bf16_ragged_mixed", dict(name="c2", V=5000, B=40, K=3, G=12, layout="mixed"), 0, 36),
+    ("bf16_K8_G16_alg1", dict(name="c5", V=9000, B=24, K=8, G=16, layout="mixed"), 1, 20),
+    ("f32_mixed", dict(name="c1", V=4000, B=40, K=3, G=8, rounds=1, layout="mixed"), 0, 36),
+    ("f32_unaligned_V3001", dict(name="c1", V=3001, B=24, K=2, G=6, rounds=1, layout="mixed"), 0, 20),
+    ("bf16_B300_more_than_sms", dict(name="c2", V=2048, B=300, K=4, G=8), 0, 280),
+    ("tiny_V8", dict(name="c2", V=8, B=64, K=2, G=4, layout="mixed", delta=2.0, rho_same=0.5), 0, 50),
+    ("gamma_max_31", dict(name="c2", V=4096, B=16, K=2, G=31, layout="mixed"), 0, 14),
+]
+
+
+@pytest.mark.parametrize("path", ["astep", "three_calls"])
+@pytest.mark.parametrize("name,kw,rule,nmin", ADAPTIVE, ids=[a[0] for a in ADAPTIVE])
+def test_adaptive_confidence_parity(name, kw, rule, nmin, path, monkeypatch):
+    """The adaptive-gamma step through sb_step_adaptive: the single persistent launch
+    k_astep (default; confidence -> verify -> select items in one grid) and the three
+    streaming kernels (SB_ASTEP=0: confidence -> verify reusing its rows -> select), on
+    shapes with several items per CTA, more sequences than SMs, ragged / unaligned rows
+    (the latter always take the three kernels), K = 8, gamma_max = 31 and Alg. 1."""
+    monkeypatch.setenv("SB_ASTEP", "0" if path == "three_calls" else "1")
+    kw = dict(kw)
+    rep, g = _run(cfg(kw.pop("name"), **kw), adaptive=True, rule=rule)
+    assert rep["n"] >= nmin, rep
+    assert rep["exact_seq"] >= 0.85 * rep["n"], rep
 
 
 def test_deterministic_run_to_run():
