@@ -73,7 +73,7 @@ __host__ __device__ inline int64_t ent(const Dims& d, int b, int k, int i) {  //
 // global timer at numbered events of the streaming kernels.  Each translation unit
 // defines its own table (SB_TRACE_TABLE) and a C reader.
 #ifdef SB_TRACE
-constexpr int kTrCtas = 160, kTrRoles = 4, kTrEvents = 64;
+constexpr int kTrCtas = 160, kTrRoles = 8, kTrEvents = 64;
 #define SB_TRACE_TABLE(name)                                                              \
   __device__ unsigned long long name[::sb::kTrCtas][::sb::kTrRoles][::sb::kTrEvents];     \
   extern "C" int name##_read(void* host, size_t bytes) {                                  \

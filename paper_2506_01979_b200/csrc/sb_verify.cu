@@ -1397,6 +1397,20 @@ __device__ __forceinline__ SeqInfo astep_seqinfo(int g, int s, int G) {
   return SeqInfo{g, s, L, st, L, {0, 0, 0}};
 }
 
+// One chunk of one row into its accumulator (FIRST: the row's first chunk).
+template <class C, typename T, bool kQ, bool FIRST>
+__device__ __forceinline__ void acc_chunk(LazyAcc<kQ, 4>& a, const uint4* x, int c) {
+  constexpr int E = Vec<T>::E;
+  if constexpr (sizeof(T) == 2) {
+    acc_vecs_bf16<C::VPT, kQ, FIRST>(a, x, c);
+  } else {
+    float f[C::VPT * E];
+#pragma unroll
+    for (int j = 0; j < C::VPT; ++j) Vec<T>::unpack(x[j], f + j * E);
+    a.template add<C::VPT * E, FIRST>(f, c);
+  }
+}
+
 template <class C, typename T>
 __global__ void __launch_bounds__(C::ROWS_THREADS, 1) k_astep(AStepParams ap) {
   constexpr int E = Vec<T>::E;
@@ -1440,12 +1454,16 @@ __global__ void __launch_bounds__(C::ROWS_THREADS, 1) k_astep(AStepParams ap) {
       int exits = 0;
       int tli = 0;
       (void)tli;
+      // one grab kept in flight: the next item's atomicAdd round trip (~1 us when 148
+      // producers contend) overlaps this item's decode and copies
+      int gnext = atomicAdd(ap.ctr, 1);
       while (exits < C::NE) {
         AItem it{};
         if (exits > 0) {
           it.type = -1;
         } else {
-          const int g = atomicAdd(ap.ctr, 1);
+          const int g = gnext;
+          gnext = atomicAdd(ap.ctr, 1);
           if (g < nconf) {
             it.type = 0; it.b = g / G; it.slot = 0; it.i = g % G;
           } else {
@@ -1512,7 +1530,20 @@ __global__ void __launch_bounds__(C::ROWS_THREADS, 1) k_astep(AStepParams ap) {
         if (it.type < 0) continue;
         const char* prow = reinterpret_cast<const char*>(PL + row_off(d, it.b, it.slot, it.i));
         const char* qrow = reinterpret_cast<const char*>(QL + row_off(d, it.b, it.slot, it.i));
-        const bool wp = it.type != 0, wq = (it.type == 0) || (it.type == 1 && !it.po) || (it.type == 2 && it.kind == 1);
+        if (it.type == 0 || (it.type == 1 && it.po)) {  // one row: chunks c, c + 1 in one stage
+          const char* row = it.type == 0 ? qrow : prow;
+          for (int c = 0; c < nchunks; c += 2) {
+            const uint32_t b0 = min((uint32_t)C::CHUNK, row_bytes - (uint32_t)c * C::CHUNK);
+            const uint32_t b1 = c + 1 < nchunks ? min((uint32_t)C::CHUNK, row_bytes - (uint32_t)(c + 1) * C::CHUNK) : 0u;
+            mbar_wait(&S.empty[rp.stage], rp.phase ^ 1u);
+            mbar_expect_tx(&S.full[rp.stage], b0 + b1);
+            bulk_g2s(S.buf[rp.stage][0], row + (size_t)c * C::CHUNK, b0, &S.full[rp.stage], pol);
+            if (b1) bulk_g2s(S.buf[rp.stage][1], row + (size_t)(c + 1) * C::CHUNK, b1, &S.full[rp.stage], pol);
+            rp.advance();
+          }
+          continue;
+        }
+        const bool wp = true, wq = (it.type == 1) || (it.type == 2 && it.kind == 1);
         const int passes = (it.type == 2) ? (it.kind == 1 ? 1 : (it.kind == 2 ? 2 : 0)) : 1;
         for (int pass = 0; pass < passes; ++pass)
           for (int c = 0; c < nchunks; ++c) {
@@ -1687,46 +1718,54 @@ __global__ void __launch_bounds__(C::ROWS_THREADS, 1) k_astep(AStepParams ap) {
         LazyAcc<true, 4> qa;
         pa.init();
         qa.init();
-        for (int c = 0; c < nchunks; ++c) {
-          const bool full = c < nchunks - 1;
-          const int nvec = full ? C::CHUNK / 16 : nvec_last;
-          StageRegs<C> r;
-          mbar_wait_spin(&S.full[rp.stage], rp.phase);
+        if (it.type == 0 || it.po) {  // one row: chunks c and c + 1 share a stage
+          for (int c = 0; c < nchunks; c += 2) {
+            const int n0 = (c < nchunks - 1) ? C::CHUNK / 16 : nvec_last;
+            const bool has1 = c + 1 < nchunks;
+            const int n1 = has1 ? ((c + 1 < nchunks - 1) ? C::CHUNK / 16 : nvec_last) : 0;
+            StageRegs<C> r;
+            mbar_wait_spin(&S.full[rp.stage], rp.phase);
+            if (c == 0 && tid == 0 && li < 60) SB_TRACE_AT(sb_trace_astep, 4, 2 + li);
 #pragma unroll
-          for (int j = 0; j < C::VPT; ++j) {
-            const int v = tid + j * C::CT;
-            const bool have = full || v < nvec;
-            r.p[j] = (it.type == 1 && have) ? lds128(S.buf[rp.stage][0] + v * 16) : neg_inf_vec<T>();
-            r.q[j] = (!it.po && have) ? lds128(S.buf[rp.stage][1] + v * 16) : neg_inf_vec<T>();
-          }
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&S.empty[rp.stage]);
-          rp.advance();
-          if (it.type == 0) {  // q row only
-            if (c == 0) {
-              if constexpr (sizeof(T) == 2) acc_vecs_bf16<C::VPT, true, true>(qa, r.q, c);
-              else { float f[C::VPT * E];
-#pragma unroll
-                for (int j = 0; j < C::VPT; ++j) Vec<T>::unpack(r.q[j], f + j * E);
-                qa.template add<C::VPT * E, true>(f, c); }
-            } else {
-              if constexpr (sizeof(T) == 2) acc_vecs_bf16<C::VPT, true, false>(qa, r.q, c);
-              else { float f[C::VPT * E];
-#pragma unroll
-                for (int j = 0; j < C::VPT; ++j) Vec<T>::unpack(r.q[j], f + j * E);
-                qa.template add<C::VPT * E, false>(f, c); }
+            for (int j = 0; j < C::VPT; ++j) {
+              const int v = tid + j * C::CT;
+              r.p[j] = v < n0 ? lds128(S.buf[rp.stage][0] + v * 16) : neg_inf_vec<T>();
+              r.q[j] = v < n1 ? lds128(S.buf[rp.stage][1] + v * 16) : neg_inf_vec<T>();
             }
-          } else if (it.po) {
-            if (c == 0) compute_stage_p<C, T, true>(r, c, pa);
-            else compute_stage_p<C, T, false>(r, c, pa);
-          } else {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&S.empty[rp.stage]);
+            rp.advance();
+            if (it.type == 0) {
+              if (c == 0) acc_chunk<C, T, true, true>(qa, r.p, c);
+              else acc_chunk<C, T, true, false>(qa, r.p, c);
+              if (has1) acc_chunk<C, T, true, false>(qa, r.q, c + 1);
+            } else {
+              if (c == 0) acc_chunk<C, T, false, true>(pa, r.p, c);
+              else acc_chunk<C, T, false, false>(pa, r.p, c);
+              if (has1) acc_chunk<C, T, false, false>(pa, r.q, c + 1);
+            }
+          }
+        } else {
+          for (int c = 0; c < nchunks; ++c) {
+            const bool full = c < nchunks - 1;
+            const int nvec = full ? C::CHUNK / 16 : nvec_last;
+            StageRegs<C> r;
+            mbar_wait_spin(&S.full[rp.stage], rp.phase);
+            if (c == 0 && tid == 0 && li < 60) SB_TRACE_AT(sb_trace_astep, 4, 2 + li);
+            if (full) load_stage<C, T, true>(S.buf[rp.stage][0], S.buf[rp.stage][1], nvec, r);
+            else load_stage<C, T, false>(S.buf[rp.stage][0], S.buf[rp.stage][1], nvec, r);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&S.empty[rp.stage]);
+            rp.advance();
             if (c == 0) compute_stage<C, T, true>(r, c, pa, qa);
             else compute_stage<C, T, false>(r, c, pa, qa);
           }
         }
+        if (tid == 0 && li < 60) SB_TRACE_AT(sb_trace_astep, 5, 2 + li);
         uint2 cand = make_uint2(0xffffffffu, 0u);
         const RowStat ps = (it.type == 1) ? warp_part<C, T, false>(pa, nullptr, nvec_last, nchunks) : rowstat_empty();
         const RowStat qs = it.po ? rowstat_empty() : warp_part_deferred(qa, cand);
+        if (tid == 0 && li < 60) SB_TRACE_AT(sb_trace_astep, 6, 2 + li);
         if (lane == 0) {
           mbar_wait(&S.pempty[ps_slot], pph ^ 1u);
           S.part[ps_slot][0][warp] = ps;

@@ -22,7 +22,7 @@ for _ in range(5):
 torch.cuda.synchronize()
 fn = _lib.lib().sb_trace_astep_read
 fn.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
-a = np.zeros((160, 4, 64), np.uint64)
+a = np.zeros((160, 8, 64), np.uint64)
 fn(a.ctypes.data, a.nbytes)
 act = a[:, 0, 0] > 0
 t0 = int(a[act, 0, 0].min())
@@ -45,3 +45,22 @@ for typ, code in (("conf", 1), ("verify", 2), ("sample", 3)):
     gs = [us(a[c, 1, 2 + k]) for c in np.where(act)[0] for k in range(60) if a[c, 0, 2 + k] == code]
     if ts:
         print(f"{typ}: {len(ts)} items, grabbed {min(gs):.1f}..{max(gs):.1f} us, consumers done {min(ts):.1f}..{max(ts):.1f} us")
+
+# consumer split per item type: wait for the first chunk / stream+compute / warp reduction / publish
+for typ, code in (("conf", 1), ("verify", 2)):
+    w, c_, r_, pub = [], [], [], []
+    for cta in np.where(act)[0]:
+        prev = None
+        for k in range(60):
+            if a[cta, 0, 2 + k] == 0:
+                break
+            t_first, t_comp, t_red, t_done = (a[cta, 4, 2 + k], a[cta, 5, 2 + k], a[cta, 6, 2 + k], a[cta, 3, 2 + k])
+            if a[cta, 0, 2 + k] == code and t_first and t_comp and t_red and t_done and prev:
+                w.append((int(t_first) - int(prev)) / 1e3)
+                c_.append((int(t_comp) - int(t_first)) / 1e3)
+                r_.append((int(t_red) - int(t_comp)) / 1e3)
+                pub.append((int(t_done) - int(t_red)) / 1e3)
+            prev = t_done if t_done else prev
+    if w:
+        print(f"{typ} items: wait-for-data median {np.median(w):.2f} us, stream+math {np.median(c_):.2f}, "
+              f"warp reductions {np.median(r_):.2f}, publish (pempty wait) {np.median(pub):.2f}")

@@ -29,7 +29,7 @@ tabs = {}
 for t in ("sb_trace_conf", "sb_trace_rows", "sb_trace_select"):
     fn = getattr(L, t + "_read")
     fn.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
-    a = np.zeros((160, 4, 64), np.uint64)
+    a = np.zeros((160, 8, 64), np.uint64)
     fn(a.ctypes.data, a.nbytes)
     tabs[t] = a
 t0 = min(int(a[:, 0, 0][a[:, 0, 0] > 0].min()) for a in tabs.values() if (a[:, 0, 0] > 0).any())
