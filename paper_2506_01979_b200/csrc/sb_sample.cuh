@@ -17,17 +17,27 @@ template <typename T>
 __device__ __forceinline__ void r_scaled(const uint4& vp, const uint4& vq, bool resid, float MSp, float MSq,
                                          float kq, float* r) {
   constexpr int E = Vec<T>::E;
+  static_assert(E % 2 == 0, "element pairs");
   float lp[E], lq[E];
   Vec<T>::unpack(vp, lp);
   if (resid) Vec<T>::unpack(vq, lq);
+  // element pairs through FFMA2 (fma.rn.f32x2: the same IEEE operation per element as
+  // the scalar fmaf, so the consumers' and the epilogue's values stay bit-identical)
+  const float2 c2 = make_float2(kC, kC), np = make_float2(-MSp, -MSp), nq = make_float2(-MSq, -MSq),
+               nk = make_float2(-kq, -kq);
 #pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const float ep = ex2(__fmaf_rn(lp[e], kC, -MSp));
+  for (int e = 0; e < E; e += 2) {
+    const float2 ap = __ffma2_rn(make_float2(lp[e], lp[e + 1]), c2, np);
+    const float2 ep = make_float2(ex2(ap.x), ex2(ap.y));
     if (resid) {
-      const float eq = ex2(__fmaf_rn(lq[e], kC, -MSq));
-      r[e] = fmaxf(__fmaf_rn(-kq, eq, ep), 0.f);
+      const float2 aq = __ffma2_rn(make_float2(lq[e], lq[e + 1]), c2, nq);
+      const float2 eq = make_float2(ex2(aq.x), ex2(aq.y));
+      const float2 d = __ffma2_rn(nk, eq, ep);
+      r[e] = fmaxf(d.x, 0.f);
+      r[e + 1] = fmaxf(d.y, 0.f);
     } else {
-      r[e] = ep;
+      r[e] = ep.x;
+      r[e + 1] = ep.y;
     }
   }
 }

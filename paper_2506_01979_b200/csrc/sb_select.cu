@@ -557,21 +557,25 @@ __global__ void __launch_bounds__(sThreads, 1) k_select_tma(SelParams p) {
       for (int c = 0; c < nchunks; ++c) {
         const int nvec = (c == nchunks - 1) ? nvec_last : sChunk / 16;
         mbar_wait(&S.full[rp.stage], rp.phase);
-        float f[sVPT * E];
+        uint4 x[sVPT];
 #pragma unroll
         for (int j = 0; j < sVPT; ++j) {
           const int v = tid + j * sCT;
-          if (v < nvec) {
-            Vec<T>::unpack(lds128(S.buf[rp.stage][0] + v * 16), f + j * E);
-          } else {
-#pragma unroll
-            for (int e = 0; e < E; ++e) f[j * E + e] = -CUDART_INF_F;
-          }
+          x[j] = (v < nvec) ? lds128(S.buf[rp.stage][0] + v * 16) : neg_inf_vec<T>();
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&S.empty[rp.stage]);
         rp.advance();
-        a.template add<sVPT * E>(f, c);
+        if constexpr (sizeof(T) == 2) {  // packed FFMA2 / FADD2 (the same operations as add())
+          if (c == 0) acc_vecs_bf16<sVPT, false, true>(a, x, c);
+          else acc_vecs_bf16<sVPT, false, false>(a, x, c);
+        } else {
+          float f[sVPT * E];
+#pragma unroll
+          for (int j = 0; j < sVPT; ++j) Vec<T>::unpack(x[j], f + j * E);
+          if (c == 0) a.template add<sVPT * E, true>(f, c);
+          else a.template add<sVPT * E, false>(f, c);
+        }
       }
       RowStat s = fold_lazy(a);
 #pragma unroll
