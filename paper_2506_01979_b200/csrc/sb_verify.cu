@@ -1332,6 +1332,8 @@ struct AStepParams {
   ConfParams c;       // confidence outputs, K = 1 slot-0 view
   const float* us;
   const int* bpos;
+  const int* gamma_in;  // non-adaptive step: gamma_b (NULL -> G)
+  int adaptive;         // 1: confidence items first; 0: plan items (gamma_b from the input)
   int rule;
   int *ctr;           // [0] grab, [1] verify entries reserved, [2] sequences planned, [3] samples queued,
                       // [4] exit count, [5] committed sequences
@@ -1397,6 +1399,39 @@ __device__ __forceinline__ SeqInfo astep_seqinfo(int g, int s, int G) {
   return SeqInfo{g, s, L, st, L, {0, 0, 0}};
 }
 
+// Sequence b's verify items once gamma_b is known (k_plan's clamps and unit layout): its
+// SeqInfo, then one reservation of its entries in the verify queue, published entry by
+// entry; ctr[2] counts planned sequences (after the reservation, so ctr[1] is final once
+// it reaches B).  One warp.
+__device__ __forceinline__ void astep_plan(const AStepParams& ap, int b, int g) {
+  const Dims& d = ap.r.d;
+  const int lane = threadIdx.x & 31;
+  const int s0 = ap.bpos ? __ldg(ap.bpos + b) : 0;
+  const SeqInfo in = astep_seqinfo(g, s0, d.G);
+  const int per = in.Lr - 1 - in.s;
+  const int count = in.Lr + (d.K - 1) * per;
+  int start = 0;
+  if (lane == 0) {
+    const_cast<SeqInfo*>(ap.r.info)[b] = in;  // (read-only for the other kernels)
+    start = atomicAdd(ap.ctr + 1, count);
+  }
+  start = __shfl_sync(0xffffffffu, start, 0);
+  for (int j = lane; j < count; j += 32) {
+    int slot, i;
+    if (j < in.Lr) { slot = 0; i = j; }
+    else { const int jj = j - in.Lr; slot = 1 + jj / per; i = in.s + 1 + jj % per; }
+    ap.qv[start + j] = make_int4(b, slot, i, 0);
+  }
+  __threadfence();
+  __syncwarp();
+  for (int j = lane; j < count; j += 32) st_rel(ap.qv_pub + start + j, 1);
+  __syncwarp();
+  if (lane == 0) {
+    __threadfence();
+    atomicAdd(ap.ctr + 2, 1);
+  }
+}
+
 // One chunk of one row into its accumulator (FIRST: the row's first chunk).
 template <class C, typename T, bool kQ, bool FIRST>
 __device__ __forceinline__ void acc_chunk(LazyAcc<kQ, 4>& a, const uint4* x, int c) {
@@ -1438,7 +1473,7 @@ __global__ void __launch_bounds__(C::ROWS_THREADS, MINB) k_astep(AStepParams ap)
   if (tid == 0) SB_TRACE_AT(sb_trace_astep, 0, 0);
   pdl_wait();
   if (tid == 0) SB_TRACE_AT(sb_trace_astep, 0, 1);
-  const int G = d.G, nconf = d.B * G;
+  const int G = d.G, nconf = ap.adaptive ? d.B * G : d.B;  // confidence or plan items first
   const T* PL = static_cast<const T*>(p.PL);
   const T* QL = static_cast<const T*>(p.QL);
   const uint32_t row_bytes = (uint32_t)d.V * sizeof(T);
@@ -1465,7 +1500,8 @@ __global__ void __launch_bounds__(C::ROWS_THREADS, MINB) k_astep(AStepParams ap)
           const int g = gnext;
           gnext = atomicAdd(ap.ctr, 1);
           if (g < nconf) {
-            it.type = 0; it.b = g / G; it.slot = 0; it.i = g % G;
+            if (ap.adaptive) { it.type = 0; it.b = g / G; it.slot = 0; it.i = g % G; }
+            else { it.type = 3; it.b = g; }
           } else {
             const int e = g - nconf;
             for (uint32_t tries = 0;; ++tries) {
@@ -1473,7 +1509,7 @@ __global__ void __launch_bounds__(C::ROWS_THREADS, MINB) k_astep(AStepParams ap)
                 const int4 q = __ldcg(ap.qv + e);
                 ap.qv_pub[e] = 0;  // leave the workspace re-usable
                 it.type = 1; it.b = q.x; it.slot = q.y; it.i = q.z;
-                it.po = (q.y == 0 && q.z < G);
+                it.po = ap.adaptive && (q.y == 0 && q.z < G);  // q state from the confidence item
                 break;
               }
               if (ld_acq(ap.ctr + 2) == d.B) {  // every sequence planned: the verify count is final
@@ -1527,7 +1563,7 @@ __global__ void __launch_bounds__(C::ROWS_THREADS, MINB) k_astep(AStepParams ap)
         S.item[iq.stage] = it;
         mbar_arrive(&S.ifull[iq.stage]);
         iq.advance();
-        if (it.type < 0) continue;
+        if (it.type < 0 || it.type == 3) continue;  // exit / plan items carry no rows
         const char* prow = reinterpret_cast<const char*>(PL + row_off(d, it.b, it.slot, it.i));
         const char* qrow = reinterpret_cast<const char*>(QL + row_off(d, it.b, it.slot, it.i));
         if (it.type == 0 || (it.type == 1 && it.po)) {  // one row: chunks c, c + 1 in one stage
@@ -1576,34 +1612,15 @@ __global__ void __launch_bounds__(C::ROWS_THREADS, MINB) k_astep(AStepParams ap)
         qs = warp_reduce_state(qs);
         qs.idx = resolve_argmax<C, T>(qmw, cand, qs.m, qrow, nvec_last, nchunks);
         conf_epilogue(ap.c, it.b, it.i, qrow, qs, lane, &S.s_last[e], [] { __syncwarp(); });
-        if (S.s_last[e]) {  // gamma_b = max(1, stop_b) is known: b's verify items (k_plan's layout)
+        if (S.s_last[e]) {  // gamma_b = max(1, stop_b) is known: b's verify items
           __threadfence();
-          const int g = __ldcg(ap.c.gamma_next + it.b);
-          const int s0 = ap.bpos ? __ldg(ap.bpos + it.b) : 0;
-          const SeqInfo in = astep_seqinfo(g, s0, G);
-          const int per = in.Lr - 1 - in.s;
-          const int count = in.Lr + (d.K - 1) * per;
-          int start = 0;
-          if (lane == 0) {
-            const_cast<SeqInfo*>(p.info)[it.b] = in;  // (read-only for the other kernels)
-            start = atomicAdd(ap.ctr + 1, count);
-          }
-          start = __shfl_sync(0xffffffffu, start, 0);
-          for (int j = lane; j < count; j += 32) {
-            int slot, i;
-            if (j < in.Lr) { slot = 0; i = j; }
-            else { const int jj = j - in.Lr; slot = 1 + jj / per; i = in.s + 1 + jj % per; }
-            ap.qv[start + j] = make_int4(it.b, slot, i, 0);
-          }
-          __threadfence();
-          __syncwarp();
-          for (int j = lane; j < count; j += 32) st_rel(ap.qv_pub + start + j, 1);
-          __syncwarp();
-          if (lane == 0) {
-            __threadfence();
-            atomicAdd(ap.ctr + 2, 1);  // after the reservation: ctr[1] is final once this reaches B
-          }
+          astep_plan(ap, it.b, __ldcg(ap.c.gamma_next + it.b));
         }
+      } else if (it.type == 3) {  // ---- plan item (non-adaptive step): gamma_b from the input
+        mbar_wait(&S.pfull[ps_slot], pph);  // (empty partial slot: its phase stays in step)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.pempty[ps_slot]);
+        astep_plan(ap, it.b, ap.gamma_in ? __ldg(ap.gamma_in + it.b) : d.G);
       } else if (it.type == 1) {  // ---- verify row pair: token tests, n_k (warp_epilogue)
         Unit un;
         un.b = it.b; un.slot = it.slot; un.i = it.i; un.in = ldcg_seqinfo(p.info + it.b);
@@ -1713,7 +1730,13 @@ __global__ void __launch_bounds__(C::ROWS_THREADS, MINB) k_astep(AStepParams ap)
       if (it.type < 0) break;
       const int ps_slot = li % C::NP;
       const uint32_t pph = (uint32_t)(li / C::NP) & 1u;
-      if (it.type != 2) {
+      if (it.type == 3) {  // plan item: no rows; keep the partial slot's phase in step
+        if (lane == 0) {
+          mbar_wait(&S.pempty[ps_slot], pph ^ 1u);
+          mbar_arrive(&S.pfull[ps_slot]);
+        }
+        __syncwarp();
+      } else if (it.type != 2) {
         LazyAcc<false, 4> pa;
         LazyAcc<true, 4> qa;
         pa.init();
@@ -1850,7 +1873,7 @@ static sb_status launch_astep(const AStepParams& ap, cudaStream_t s) {
 bool astep_eligible(const sb_dims* dd, const void* PL, const void* QL) {
   const char* e = getenv("SB_ASTEP");
   if (e && e[0] == '0') return false;
-  if (tma_disabled() || sharded(dd) || dd->G < 1) return false;
+  if (tma_disabled() || sharded(dd)) return false;
   if (!vec_ok(dd, PL) || !vec_ok(dd, QL)) return false;
   const size_t rb = (size_t)dd->V * elem_size(dd);
   if (rb % 16 || rb > (size_t)kSegMax * kSegBytes) return false;
@@ -1860,8 +1883,9 @@ bool astep_eligible(const sb_dims* dd, const void* PL, const void* QL) {
 using RCA = RC<16, 6, 2, 4, 4>;  // k_astep: 16 consumer warps, 6 x 32 KB stages, 4 epilogue warps
 // (two CTAs per SM of 8 consumer warps, 5 x 16 KB stages each, measured 72.3 vs 71.6 us on C2)
 
-sb_status astep_run(const sb_dims* dd, const Workspace& w, const Workspace& cw, const void* PL, const void* QL,
-                    const int32_t* tok, const float* u, const float* us, const int32_t* branch_pos,
+sb_status astep_run(const sb_dims* dd, const Workspace& w, const Workspace* cw, const void* PL, const void* QL,
+                    const int32_t* tok, const float* u, const float* us, const int32_t* gamma,
+                    const int32_t* branch_pos,
                     sb_select_rule rule, float eps, int32_t k_max, float* c_top1, int32_t* c_id, float* c_ent,
                     float* c_stat, int32_t* c_stop, int32_t* c_knext, int32_t* c_gamma, float* lse_p, float* lse_q,
                     float* p_tok, float* q_tok, uint32_t* acc_mask, int32_t* n_acc, float* top1_q,
@@ -1878,15 +1902,19 @@ sb_status astep_run(const sb_dims* dd, const Workspace& w, const Workspace& cw, 
   p.lse_p = lse_p; p.lse_q = lse_q; p.p_tok = p_tok; p.q_tok = q_tok;
   p.top1_q = top1_q; p.entropy_q = entropy_q; p.top1_id_q = top1_id_q;
   p.acc_mask = acc_mask; p.n_acc = n_acc; p.status = status;
-  p.qreuse = cw.qrs;
   p.sq_ctr = w.actr + 3; p.sq = w.asq; p.sq_pub = w.asq_pub;
-  ConfParams& c = ap.c;
-  c.d = d;
-  c.d.K = 1;  // slot-0 view of the draft rows
-  c.QL = QL; c.tok = nullptr; c.mode = SB_CONF_TOP1; c.eps = eps; c.lambda = 1.f; c.k_max = k_max;
-  c.top1_prob = c_top1; c.entropy = c_ent; c.tok_prob = nullptr; c.stat = c_stat; c.top1_id = c_id;
-  c.stop = c_stop; c.k_next = c_knext; c.gamma_next = c_gamma;
-  c.cnt = cw.conf_cnt; c.ws_stat = cw.conf_stat; c.ws_c = cw.conf_c; c.qrs = cw.qrs;
+  if (cw) {  // adaptive: confidence items first, their q states reused by slot-0 verify items
+    p.qreuse = cw->qrs;
+    ConfParams& c = ap.c;
+    c.d = d;
+    c.d.K = 1;  // slot-0 view of the draft rows
+    c.QL = QL; c.tok = nullptr; c.mode = SB_CONF_TOP1; c.eps = eps; c.lambda = 1.f; c.k_max = k_max;
+    c.top1_prob = c_top1; c.entropy = c_ent; c.tok_prob = nullptr; c.stat = c_stat; c.top1_id = c_id;
+    c.stop = c_stop; c.k_next = c_knext; c.gamma_next = c_gamma;
+    c.cnt = cw->conf_cnt; c.ws_stat = cw->conf_stat; c.ws_c = cw->conf_c; c.qrs = cw->qrs;
+  }
+  ap.adaptive = cw != nullptr;
+  ap.gamma_in = gamma;
   ap.us = us; ap.bpos = branch_pos; ap.rule = rule;
   ap.ctr = w.actr; ap.qv = w.aqv; ap.qv_pub = w.aqv_pub; ap.sq = w.asq; ap.sq_pub = w.asq_pub;
   ap.sel_k = sel_k; ap.commit_len = commit_len; ap.out_tok = out_tok; ap.y_tok = y_tok; ap.y_kind = y_kind;
@@ -2071,6 +2099,14 @@ extern "C" sb_status sb_verify_select(const sb_dims* dd, const void* p_logits, c
   // two launches on B200 (C4: 6.88 vs 6.70 ms), so it is opt-in.
   const char* fz = getenv("SB_FUSED_STEP");
   const bool fused = fz && fz[0] == '1';
+  // k_astep with plan items instead of confidence items: opt-in (SB_ASTEP=1) — one C1 round
+  // (batch 1) measured 31.8 us against 29.6 us for k_plan + the two streaming kernels
+  const char* ae = getenv("SB_ASTEP");
+  if (!fused && ae && ae[0] == '1' && astep_eligible(dd, p_logits, q_logits))
+    return astep_run(dd, w, nullptr, p_logits, q_logits, tok, u, us, gamma, branch_pos, rule, 0.f, 0, nullptr,
+                     nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, lse_p, lse_q, p_tok, q_tok, acc_mask,
+                     n_acc, top1_q, top1_id_q, entropy_q, status, sel_k, commit_len, out_tok, y_tok, y_kind,
+                     offsets, packed_tok, path_rolled, branch_discarded, keep_mask, resid_mass, (cudaStream_t)stream);
   if (!fused || !vok || row_bytes % 16 || row_bytes > (size_t)kSegMax * kSegBytes || tma_disabled()) {
     // the two calls back to back
     sb_status st = sb_verify_branches(dd, p_logits, q_logits, tok, u, gamma, branch_pos, lse_p, lse_q, p_tok,
@@ -2130,10 +2166,13 @@ extern "C" sb_status sb_step_adaptive(const sb_dims* dd, const void* p_logits, c
   if (conf_workspace_bytes < sb_workspace_bytes(&cd)) return SB_ERR_WORKSPACE;
   cudaStream_t s = (cudaStream_t)stream;
   if (astep_eligible(dd, p_logits, q_logits))  // one persistent launch (k_astep)
-    return astep_run(dd, w, carve(cd, conf_workspace), p_logits, q_logits, tok, u, us, branch_pos, rule, eps, k_max,
+  {
+    const Workspace cw = carve(cd, conf_workspace);
+    return astep_run(dd, w, &cw, p_logits, q_logits, tok, u, us, nullptr, branch_pos, rule, eps, k_max,
                      c_top1_prob, c_top1_id, c_entropy, c_stat, c_stop, c_k_next, c_gamma_next, lse_p, lse_q, p_tok,
                      q_tok, acc_mask, n_acc, top1_q, top1_id_q, entropy_q, status, sel_k, commit_len, out_tok, y_tok,
                      y_kind, offsets, packed_tok, path_rolled, branch_discarded, keep_mask, resid_mass, s);
+  }
   // SB_ASTEP=0 or unaligned rows: the three streaming kernels (the verify reuses the
   // confidence pass's slot-0 draft-row states)
   sb_status st = sb_draft_confidence(&cd, q_logits, nullptr, SB_CONF_TOP1, eps, 1.0f, k_max, c_top1_prob, c_top1_id,

@@ -106,14 +106,16 @@ SMALL = [
 ]
 
 
-@pytest.mark.parametrize("fused", ["single_launch", "verify_select", "two_calls"])
+@pytest.mark.parametrize("fused", ["single_launch", "astep", "verify_select", "two_calls"])
 @pytest.mark.parametrize("name,kw,pad,rule", SMALL, ids=[c[0] for c in SMALL])
 def test_small_parity(name, kw, pad, rule, fused, monkeypatch):
-    """single_launch: the persistent TMA-ring k_step_tma (SB_FUSED_STEP=1); verify_select:
-    the two streaming kernels behind sb_verify_select (the default); two_calls:
-    sb_verify_branches then sb_select_branch."""
+    """single_launch: the persistent TMA-ring k_step_tma (SB_FUSED_STEP=1); astep: the
+    persistent work-queue kernel k_astep with plan items (opt-in for sb_verify_select,
+    SB_ASTEP=1); verify_select: the two streaming kernels behind sb_verify_select (the
+    default); two_calls: sb_verify_branches then sb_select_branch."""
     kw = dict(kw)
     c = cfg(kw.pop("name"), **kw)
+    monkeypatch.setenv("SB_ASTEP", "1" if fused == "astep" else "0")
     if fused == "single_launch":
         monkeypatch.setenv("SB_FUSED_STEP", "1")  # the persistent k_step_tma kernel
     rep, g = _run(c, row_pad=pad, rule=rule, fused=(fused != "two_calls"))
