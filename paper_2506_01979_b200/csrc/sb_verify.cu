@@ -1339,6 +1339,7 @@ struct AStepParams {
                       // [4] exit count, [5] committed sequences
   int4* qv;           // verify entries (b, slot, i)
   int* qv_pub;
+  int qcap;           // capacity of qv / qv_pub (B K (G+1))
   int* sq;            // sample queue: sequences
   int* sq_pub;
   int *sel_k, *commit_len, *out_tok, *y_tok, *y_kind, *offsets, *packed_tok, *path_rolled, *branch_discarded;
@@ -1505,7 +1506,9 @@ __global__ void __launch_bounds__(C::ROWS_THREADS, MINB) k_astep(AStepParams ap)
           } else {
             const int e = g - nconf;
             for (uint32_t tries = 0;; ++tries) {
-              if (ld_acq(ap.qv_pub + e)) {
+              // (an index past the queue's capacity can only be a sample / exit index: never
+              // probe qv_pub there, the words after it belong to the sample queue)
+              if (e < ap.qcap && ld_acq(ap.qv_pub + e)) {
                 const int4 q = __ldcg(ap.qv + e);
                 ap.qv_pub[e] = 0;  // leave the workspace re-usable
                 it.type = 1; it.b = q.x; it.slot = q.y; it.i = q.z;
@@ -1917,6 +1920,7 @@ sb_status astep_run(const sb_dims* dd, const Workspace& w, const Workspace* cw, 
   ap.gamma_in = gamma;
   ap.us = us; ap.bpos = branch_pos; ap.rule = rule;
   ap.ctr = w.actr; ap.qv = w.aqv; ap.qv_pub = w.aqv_pub; ap.sq = w.asq; ap.sq_pub = w.asq_pub;
+  ap.qcap = dd->B * dd->K * (dd->G + 1);
   ap.sel_k = sel_k; ap.commit_len = commit_len; ap.out_tok = out_tok; ap.y_tok = y_tok; ap.y_kind = y_kind;
   ap.offsets = offsets; ap.packed_tok = packed_tok; ap.path_rolled = path_rolled;
   ap.branch_discarded = branch_discarded; ap.keep_mask = keep_mask; ap.resid_mass = resid_mass;
