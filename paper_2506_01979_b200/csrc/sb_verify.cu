@@ -1761,6 +1761,9 @@ __global__ void __launch_bounds__(C::ROWS_THREADS, MINB) k_astep(AStepParams ap)
             __syncwarp();
             if (lane == 0) mbar_arrive(&S.empty[rp.stage]);
             rp.advance();
+#ifdef SB_ASTEP_NOMATH  // experiment: data-rate ceiling of the k_astep structure (wrong results)
+            if (true) { qa.z[0] += __uint_as_float(r.p[0].x & 1u) + __uint_as_float(r.q[0].x & 1u); } else
+#endif
             if (it.type == 0) {
               if (c == 0) acc_chunk<C, T, true, true>(qa, r.p, c);
               else acc_chunk<C, T, true, false>(qa, r.p, c);
@@ -1783,6 +1786,9 @@ __global__ void __launch_bounds__(C::ROWS_THREADS, MINB) k_astep(AStepParams ap)
             __syncwarp();
             if (lane == 0) mbar_arrive(&S.empty[rp.stage]);
             rp.advance();
+#ifdef SB_ASTEP_NOMATH
+            if (true) { pa.z[0] += __uint_as_float(r.p[0].x & 1u) + __uint_as_float(r.q[0].x & 1u); } else
+#endif
             if (c == 0) compute_stage<C, T, true>(r, c, pa, qa);
             else compute_stage<C, T, false>(r, c, pa, qa);
           }
