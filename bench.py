@@ -109,6 +109,17 @@ def bytes_model(gamma, bpos, y_kind, K, V, es, G, conf_rows=0, bonus_rows=False)
     return a1, a4, a6, small, units
 
 
+def launches_per_step(cfg, d, adaptive, vocab, es):
+    """The library's kernel launches in one step: the adaptive step of a small problem is
+    one k_astep launch (sb_step_adaptive's rule: B K (G+1) <= 4096, 16-byte rows, not
+    SB_ASTEP=0); otherwise confidence (adaptive) + k_plan + k_rows_tma + k_select_tma,
+    plus the three shard kernels of the vocabulary-sharded path."""
+    if adaptive and not vocab and os.environ.get("SB_ASTEP") != "0" and (d.V * es) % 16 == 0 \
+            and d.B * d.K * (d.G + 1) <= 4096:
+        return 1
+    return (1 if adaptive else 0) + (6 if vocab else 3)
+
+
 def rank_slice(cfg, rank, world, scaling="strong"):
     """Sequences [b0, b1) a rank owns (global sequence keys; no data-path collective).
     strong (default): the configuration's batch split contiguously, rank g
@@ -341,7 +352,7 @@ def run_ours(args, rank, world, local_rank):
                      "achieved": round(ver_gbs, 1), "peak": peak, "peak_source": peak_src, "unit": "GB/s",
                      "frac": round(ver_gbs / peak, 4), "traffic": traffic_from_profiles(cfg.name),
                      "algorithmic_bytes_per_launch": rf_bytes, "row_pairs_per_launch": units},
-        "gpu_launches": args.steps * ((1 if adaptive else 0) + (6 if vocab else 3)),  # conf; plan + rows + select (+3 shard kernels)
+        "gpu_launches": args.steps * launches_per_step(cfg, d, adaptive, vocab, es),
         "clocks": clk.summary(),
         "generation_s": round(gen_s, 1),
     }
