@@ -1933,6 +1933,206 @@ sb_status astep_run(const sb_dims* dd, const Workspace& w, const Workspace* cw, 
   return dd->dtype == SB_BF16 ? launch_astep<RCA, __nv_bfloat16, 1>(ap, s) : launch_astep<RCA, float, 1>(ap, s);
 }
 
+// ---------------------------------------------------------------- short rows, many units
+// k_rows_warp: one warp per unit (row pair) for rows of <= 64 KB when there are many units
+// (the vocabulary shards of C5 at G >= 4: 32-64 KB rows, ~66 K units per rank).  With
+// k_rows_tma's 16-20 consumer warps per unit a lane sees only 2-4 groups of a 32 KB row,
+// so the per-row costs (first-group freeze, two warp reductions, the cross-warp combine)
+// doubled the instructions per element (shard sweep: 0.51 of the copy peak at V/8).  Here
+// each lane sees a whole row's share (U vectors per row per step), the per-row reduction is
+// one warp tree, there is no cross-warp combine, and the warp runs its own epilogue
+// (warp_epilogue or the shard partial record).  Bytes in flight come from a per-warp
+// cp.async ring in shared memory (each lane copies and later reads only its own vectors:
+// no barrier beyond cp.async.wait_group), NSW steps ahead across unit boundaries; the next
+// unit's geometry is decoded one unit ahead (warp-cooperative probe).
+template <int U>
+using WG = RC<1, 1, U, 1, 1>;  // one warp covers a "chunk" of 32 x U 16-byte vectors per row
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// warp_part for a one-warp unit: fold, warp tree, and (q rows) the exact first argmax by
+// re-reading the U vectors of the step where each max-holding lane first saw it.
+template <int U, typename T, bool kQ>
+__device__ __forceinline__ RowStat warp_part_lane(const LazyAcc<kQ, 4>& a, const T* row, int nvec) {
+  constexpr int E = Vec<T>::E;
+  const int lane = threadIdx.x & 31;
+  RowStat s = fold_lazy(a);
+  float mw = s.m;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mw = fmaxf(mw, __shfl_xor_sync(0xffffffffu, mw, o));
+  uint4 x[U];
+  const bool need = kQ && (a.m == mw) && (mw > -CUDART_INF_F) && (a.tag >= 0);
+  const int base = a.tag * 32 * U;
+  if (need) {
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const int v = base + lane + 32 * j;
+      x[j] = v < nvec ? __ldg(reinterpret_cast<const uint4*>(row) + v) : neg_inf_vec<T>();
+    }
+  }
+  s = warp_reduce_offsets(s);
+  s.m = mw;
+  int cand = 0x7fffffff;
+  if (need) {
+#pragma unroll
+    for (int j = U - 1; j >= 0; --j) {
+      float f[E];
+      Vec<T>::unpack(x[j], f);
+#pragma unroll
+      for (int e = E - 1; e >= 0; --e)
+        if (f[e] == mw) cand = (base + lane + 32 * j) * E + e;
+    }
+  }
+  s.idx = kQ ? (int)__reduce_min_sync(0xffffffffu, (unsigned)cand) : 0;
+  return s;
+}
+
+template <typename T, int U, int NSW, int WPB>
+struct RowsWarpSmem {
+  uint4 buf[WPB][NSW][2][32 * U];  // per warp: NSW steps of (p, q) x 32 lanes x U vectors
+};
+
+template <typename T, int U, int NSW, int WPB>
+__global__ void __launch_bounds__(WPB * 32, 1) k_rows_warp(RowsParams p) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  RowsWarpSmem<T, U, NSW, WPB>& S = *reinterpret_cast<RowsWarpSmem<T, U, NSW, WPB>*>(smem_raw);
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const int gw = blockIdx.x * WPB + wl, nw = gridDim.x * WPB;
+  pdl_wait();
+  const Dims& d = p.d;
+  const int total = __ldg(p.unit_off + d.B);
+  const T* PL = static_cast<const T*>(p.PL);
+  const T* QL = static_cast<const T*>(p.QL);
+  const int nvec = (int)((uint32_t)d.V * sizeof(T) / 16);
+  const int nsteps = (nvec + 32 * U - 1) / (32 * U);
+  if (gw >= total) return;
+  // producer cursor: (unit pu, step pc) with decoded geometry pcur; consumer: (unit, step)
+  int pbase = 0, cbase = 0;
+  int4 pcur = probe_resolve(p, probe_load(p, 0), pbase, gw, total);
+  int pu = gw, pc = 0;
+  auto issue = [&](int slot) {
+    if (pu < total) {
+      const Unit un = unit_from(pcur);
+      const bool po = q_reused(p, un);
+      const uint4* pr = reinterpret_cast<const uint4*>(PL + row_off(d, un.b, un.slot, un.i));
+      const uint4* qr = reinterpret_cast<const uint4*>(QL + row_off(d, un.b, un.slot, un.i));
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const int v = pc * 32 * U + lane + 32 * j;
+        if (v < nvec) {
+          cp_async16(&S.buf[wl][slot][0][lane + 32 * j], pr + v);
+          if (!po) cp_async16(&S.buf[wl][slot][1][lane + 32 * j], qr + v);
+        }
+      }
+    }
+    cp_async_commit();  // (empty groups keep the wait_group count uniform)
+    if (pu < total && ++pc == nsteps) {  // next unit of this warp: one probe round
+      pc = 0;
+      pu += nw;
+      pcur = probe_resolve(p, probe_load(p, pbase), pbase, pu, total);
+    }
+  };
+#pragma unroll
+  for (int s = 0; s < NSW; ++s) issue(s);
+  int slot = 0;
+  int4 ccur = probe_resolve(p, probe_load(p, 0), cbase, gw, total);
+  for (int unit = gw; unit < total; unit += nw) {
+    const Unit un = unit_from(ccur);
+    const T* prow = PL + row_off(d, un.b, un.slot, un.i);
+    const T* qrow = QL + row_off(d, un.b, un.slot, un.i);
+    const bool po = q_reused(p, un);
+    // path tokens through this row, their uniforms and logits (prefetched)
+    const bool branch_row = (un.slot == 0 && un.i == un.in.s);
+    const int ntok = branch_row ? d.K : 1;
+    int x = 0;
+    float lpx = 0.f, lqx = 0.f, uu = 0.f;
+    int64_t et = 0;
+    const bool has_tok = un.i < un.in.L;
+    if (lane < ntok && has_tok) {
+      et = ent(d, un.b, branch_row ? lane : un.slot, un.i);
+      x = __ldg(p.tok + et);
+      uu = __ldg(p.u + et);
+      const int xl = x - p.v_offset;
+      if (xl >= 0 && xl < d.V) {
+        lpx = ld_scalar(prow + xl);
+        lqx = ld_scalar(qrow + xl);
+      } else {
+        lpx = lqx = -CUDART_INF_F;
+      }
+    }
+    RowStat qr;
+    if (po) qr = p.qreuse[(int64_t)un.b * d.G + un.i];
+    LazyAcc<false, 4> pa;
+    LazyAcc<true, 4> qa;
+    pa.init();
+    qa.init();
+    for (int c = 0; c < nsteps; ++c) {
+      cp_async_wait<NSW - 1>();  // this lane's copies of step (unit, c) have landed
+      StageRegs<WG<U>> r;
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const int v = c * 32 * U + lane + 32 * j;
+        const bool have = v < nvec;
+        r.p[j] = have ? S.buf[wl][slot][0][lane + 32 * j] : neg_inf_vec<T>();
+        r.q[j] = (have && !po) ? S.buf[wl][slot][1][lane + 32 * j] : neg_inf_vec<T>();
+      }
+      issue(slot);  // refill this slot NSW steps ahead
+      slot = (slot + 1 == NSW) ? 0 : slot + 1;
+      if (po) {
+        if (c == 0) compute_stage_p<WG<U>, T, true>(r, c, pa);
+        else compute_stage_p<WG<U>, T, false>(r, c, pa);
+      } else {
+        if (c == 0) compute_stage<WG<U>, T, true>(r, c, pa, qa);
+        else compute_stage<WG<U>, T, false>(r, c, pa, qa);
+      }
+    }
+    const Probe pr = probe_load(p, cbase);  // the next unit's geometry, in flight during the epilogue
+    RowStat ps = warp_part_lane<U, T, false>(pa, prow, nvec);
+    RowStat qs = po ? qr : warp_part_lane<U, T, true>(qa, qrow, nvec);
+    if (p.partial) {  // a7: this shard's state (as k_rows_tma's epilogue)
+      if (lane < ntok && has_tok) p.tokpart[et] = make_float2(lpx, lqx);
+      bool fin = qs.m > kMaskedLogit && qs.m < CUDART_INF_F;
+      if (sizeof(T) == 2 && qs.m == kMaskedLogit)
+        fin = row_has_finite_bf16(reinterpret_cast<const __nv_bfloat16*>(qrow), d.V);
+      else if (sizeof(T) == 4)
+        fin = qs.m > -CUDART_INF_F && qs.m < CUDART_INF_F;
+      if (lane == 0) {
+        ShardRow rr;
+        rr.pm = ps.m; rr.pms = ps.ms; rr.pz = ps.z;
+        rr.qm = qs.m; rr.qms = qs.ms; rr.qz = qs.z; rr.qs1 = qs.s1;
+        rr.qidx = (qs.idx == 0x7fffffff) ? qs.idx : qs.idx + p.v_offset;
+        rr.qfin = fin;
+        p.rowpart[ent(d, un.b, un.slot, un.i)] = rr;
+      }
+    } else {
+      warp_epilogue<T>(p, un, ps, qs, qrow, x, lpx, lqx, uu, et);
+    }
+    ccur = probe_resolve(p, pr, cbase, unit + nw, total);
+  }
+  cp_async_wait<0>();
+}
+
+template <typename T, int U, int NSW, int WPB>
+static sb_status launch_rows_warp_g(const RowsParams& p, cudaStream_t s) {
+  using SM = RowsWarpSmem<T, U, NSW, WPB>;
+  const int smem = (int)sizeof(SM);
+  if (ensure_smem<k_rows_warp<T, U, NSW, WPB>>(smem) != cudaSuccess) return SB_ERR_CUDA;
+  return cuda_status(launch_pdl(k_rows_warp<T, U, NSW, WPB>, dim3(num_sms()), dim3(WPB * 32), smem, s, p));
+}
+// 20 warps x 5 steps x (2 + 2) vectors per lane (200 KB of cp.async in flight per SM,
+// 96 registers).  Rank-0 slice of C5 (scripts/shard_sweep.py, one GPU): G = 8 (32 KB rows)
+// 0.75 of the copy peak, G = 4 (64 KB) 0.79, against 0.49 / 0.67 through k_rows_tma;
+// 12 / 16 / 24 warps per SM, 1 or 4 vectors per lane per step measured 0.64-0.74 at G = 8.
+template <typename T>
+static sb_status launch_rows_warp(const RowsParams& p, cudaStream_t s) {
+  return launch_rows_warp_g<T, 2, 5, 20>(p, s);
+}
+
 // Geometry (SB_ROWS_VARIANT=0 / 2 forces one).  Also measured: 24 consumer warps x 4 x
 // 48 KB stages, 1-vector-per-row stages (24 x 8 x 24 KB, 16 x 12 x 16 KB; round 1) and
 // 4 vectors per row per stage (16 x 3 x 64 KB; round 2: C4 verify +10 %, C3 +6 %): none
@@ -1945,6 +2145,10 @@ template <typename T>
 static sb_status launch_rows_variant(const RowsParams& p, cudaStream_t s) {
   const char* e = getenv("SB_ROWS_VARIANT");
   int v = e ? atoi(e) : -1;
+  // many short rows (<= 64 KB, >= 16384 row slots): one warp per unit (k_rows_warp)
+  const size_t rb = (size_t)p.d.V * sizeof(T);
+  if ((v < 0 && rb <= 65536 && (size_t)p.d.B * p.d.K * (p.d.G + 1) >= 16384) || v == 9)
+    return launch_rows_warp<T>(p, s);
   if (v < 0) {
     // default: 20 consumer warps (20 KB chunks), unless the padding of a row's last
     // chunk (lanes that cost instructions, not bytes) wastes > 3 % more of the stages

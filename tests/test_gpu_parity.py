@@ -125,6 +125,23 @@ def test_small_parity(name, kw, pad, rule, fused, monkeypatch):
         assert {1, 2} <= kinds or 0 in kinds, kinds
 
 
+@pytest.mark.parametrize("name,kw,pad,rule", SMALL, ids=[c[0] for c in SMALL])
+def test_rows_warp_kernel_parity(name, kw, pad, rule, monkeypatch):
+    """k_rows_warp (one warp per row pair, per-warp cp.async ring) on every small shape
+    (SB_ROWS_VARIANT=9 forces it; unaligned rows keep the register-staged kernel)."""
+    monkeypatch.setenv("SB_ROWS_VARIANT", "9")
+    kw = dict(kw)
+    rep, _ = _run(cfg(kw.pop("name"), **kw), row_pad=pad, rule=rule, fused=False)
+    assert rep["exact_seq"] >= 0.9 * rep["n"], rep
+
+
+def test_rows_warp_kernel_default_route():
+    """Many short rows take k_rows_warp by default (>= 16384 row slots of <= 64 KB): 512
+    sequences x K = 4 x 9 rows of 16 KB, checked on a sample of 96 sequences."""
+    rep, _ = _run(cfg("c2", V=8192, B=512, K=4, G=8, layout="mixed"), sample=96, fused=False)
+    assert rep["exact_seq"] >= 0.9 * rep["n"], rep
+
+
 @pytest.mark.parametrize("name,kw", [("bf16", dict(name="c2", B=40, layout="mixed")),
                                      ("f32", dict(name="c1", B=40, rounds=1, layout="mixed"))])
 def test_register_staged_fallback_parity(monkeypatch, name, kw):

@@ -36,8 +36,13 @@ CASES = [
 ]
 
 
+@pytest.mark.parametrize("warp_kernel", [False, True], ids=["tma_rows", "warp_rows"])
 @pytest.mark.parametrize("name,kw,granks,rule", CASES, ids=[c[0] for c in CASES])
-def test_sharded_loopback_matches_oracle(name, kw, granks, rule):
+def test_sharded_loopback_matches_oracle(name, kw, granks, rule, warp_kernel, monkeypatch):
+    """warp_rows: the partial pass through k_rows_warp (one warp per row pair; forced with
+    SB_ROWS_VARIANT=9, the default for many rows of <= 64 KB such as C5's shards at G >= 4)."""
+    if warp_kernel:
+        monkeypatch.setenv("SB_ROWS_VARIANT", "9")
     from paper_2506_01979_b200 import api, synth
 
     from parity_util import compare, internal_consistency, oracle_for
