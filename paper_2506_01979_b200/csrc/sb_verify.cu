@@ -1948,12 +1948,6 @@ sb_status astep_run(const sb_dims* dd, const Workspace& w, const Workspace* cw, 
 template <int U>
 using WG = RC<1, 1, U, 1, 1>;  // one warp covers a "chunk" of 32 x U 16-byte vectors per row
 
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 // warp_part for a one-warp unit: fold, warp tree, and (q rows) the exact first argmax by
 // re-reading the U vectors of the step where each max-holding lane first saw it.

@@ -195,6 +195,28 @@ def test_deterministic_run_to_run():
         assert np.array_equal(a[k], b[k], equal_nan=True), k
 
 
+@pytest.mark.parametrize("nranks", [2, 3, 8])
+def test_sequence_shards_bit_identical(nranks):
+    """sequence-sharded output at every G is bit-identical to G = 1.  Each
+    rank's contiguous slice [g B / G, (g+1) B / G) (bench.py rank_slice) generated on its
+    own (the counter-keyed generator gives the same bytes) and run alone must reproduce the
+    full batch's per-sequence outputs exactly."""
+    from paper_2506_01979_b200 import synth
+
+    from parity_util import gpu_run
+
+    c = cfg("c2", V=8000, B=48, layout="mixed")
+    full, _, _ = gpu_run(synth.generate(c, device="cuda"))
+    per = ("lse_p", "lse_q", "p_tok", "q_tok", "acc_mask", "n_acc", "top1_q", "top1_id_q", "entropy_q", "status",
+           "sel_k", "commit_len", "out_tok", "y_tok", "y_kind", "path_rolled", "branch_discarded", "keep_mask",
+           "resid_mass")
+    for g in range(nranks):
+        b0, b1 = g * c.B // nranks, (g + 1) * c.B // nranks
+        part, _, _ = gpu_run(synth.generate(c, device="cuda", b0=b0, b1=b1))
+        for k in per:
+            assert np.array_equal(part[k], full[k][b0:b1], equal_nan=True), (nranks, g, k)
+
+
 def test_workspace_reuse_across_calls():
     """One workspace, three rounds of different inputs: the self-resetting counters
     leave it re-usable (include/specbranch.h workspace contract)."""
