@@ -191,11 +191,11 @@ sb_status sb_select_branch(const sb_dims* d, const void* p_logits, const void* q
 
 /*
  * sb_verify_select — sb_verify_branches followed by sb_select_branch: every output of
- * both calls, with the same meaning, in one call (one workspace, one stream).  Small
- * problems (as sb_step_adaptive) run as one persistent launch with V-split rows
- * (sb_flow.cu); otherwise the two streaming kernels run back to back (with
- * SB_FUSED_STEP=1 in the environment a single persistent TMA-ring launch instead; correct,
- * measured slower on B200).  Unsharded only.
+ * both calls, with the same meaning, in one call (one workspace, one stream).  The two
+ * streaming kernels run back to back (PDL-chained).  Experiment switches (environment):
+ * SB_FUSED_STEP=1 runs the single persistent TMA-ring launch k_step_tma, SB_ASTEP=1 the
+ * persistent work-queue launch k_astep with plan items (both correct, both measured
+ * slower on B200).  Unsharded only.
  */
 sb_status sb_verify_select(const sb_dims* d, const void* p_logits, const void* q_logits,
                            const int32_t* tok, const float* u, const float* us,
@@ -214,10 +214,13 @@ sb_status sb_verify_select(const sb_dims* d, const void* p_logits, const void* q
  * with eps, Eq. 7 k with k_max), gamma_b = max(1, stop_b) (written to c_gamma_next), then
  * sb_verify_branches and sb_select_branch with that gamma and branch_pos.  Every output
  * has the meaning of the corresponding call (c_* arrays [B][G] / [B] as sb_draft_confidence
- * with K = 1).  Small problems (unsharded, 16-byte aligned rows of 16-byte multiples,
- * B <= 1024, <= ~1 GB of rows) run as ONE persistent launch that splits every row into
- * V-segments (sb_flow.cu); larger ones as the three streaming kernels, the verify reusing
- * the confidence pass's row states.  conf_workspace: sb_workspace_bytes of the slot-0
+ * with K = 1).  Small problems (16-byte aligned rows of 16-byte multiples up to 1 MB,
+ * B * K * (G+1) <= 4096) run as ONE persistent launch (k_astep: confidence items, then
+ * each sequence's verify items as soon as its gamma is known, then its sample item as
+ * soon as its n_k is known; SB_ASTEP=0 / 1 forces it off / on); larger ones as the three
+ * streaming kernels, the verify reusing the confidence pass's row states.  All CTAs of
+ * the persistent launch must be co-resident (one per SM; SB_ERR_UNSUPPORTED if the
+ * occupancy check fails).  conf_workspace: sb_workspace_bytes of the slot-0
  * dims (K = 1, seq_stride of d), zero-filled once; workspace: sb_workspace_bytes(d).
  * Errors as the three calls; G must be >= 1.
  */
