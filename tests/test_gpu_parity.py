@@ -255,6 +255,43 @@ def test_identical_p_q_accepts_all_on_gpu():
     assert (g["path_rolled"] == 0).all()
 
 
+@pytest.mark.parametrize("path", ["astep", "three_calls"])
+def test_adaptive_special_values(path, monkeypatch):
+    """The adaptive step (k_astep and the three kernels) on rows that break the usual
+    assumptions: NaN / +inf / all -inf / one-hot / finfo(bf16).min-masked draft rows in
+    slot 0 (the confidence pass and its reused q states), NaN target rows, out-of-range
+    tokens, a clamped branch row; statistics, stop / k / gamma and every verify / select
+    output against the oracle (_check_chunk's adaptive path)."""
+    from paper_2506_01979_b200 import synth
+
+    monkeypatch.setenv("SB_ASTEP", "1" if path == "astep" else "0")
+    c = cfg("c2", V=4096, B=24, K=3, G=6, layout="adaptive")
+    inp = synth.generate(c, device="cuda", seed=13)
+    bmin = torch.finfo(torch.bfloat16).min
+    inp["QL"][0, 0, 0, 100] = float("nan")      # confidence row 0 of b=0 poisoned
+    inp["QL"][1, 0, 2, 7] = float("inf")
+    inp["QL"][2, 0, 1, :] = float("-inf")        # an all -inf draft row
+    inp["QL"][3, 0, 0, :] = float("-inf")
+    inp["QL"][3, 0, 0, 11] = 5.0                 # one-hot: top-1 = 1, H = 0 exactly
+    inp["QL"][4, 0, 3, 1::2] = bmin              # half the row masked with finfo.min
+    inp["PL"][5, 0, 0, 3] = float("nan")         # target row NaN at the first row
+    inp["PL"][6, 1, 2, :] = float("-inf")
+    inp["tok"][7, 0, 0] = 99999                  # out-of-range token
+    inp["branch_pos"][8] = 40                    # clamped branch row
+    rep, g = _run_inp(inp, c, adaptive=True)
+    assert rep["n"] >= 16, rep
+
+
+def _run_inp(inp, c, adaptive=False, rule=0):
+    """_run on given inputs (all sequences, one chunk)."""
+    from parity_util import gpu_run, internal_consistency
+
+    g, d, _ = gpu_run(inp, rule=rule, adaptive=adaptive)
+    internal_consistency(g, c.G)
+    idx = np.arange(inp["PL"].shape[0])
+    return _check_chunk(inp, g, idx, adaptive, rule, 0), g
+
+
 def test_special_values_and_status():
     """NaN / +inf / all -inf rows, out-of-range tokens and clamped layouts are reported
     per sequence in status and match the oracle's handling."""
