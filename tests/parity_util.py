@@ -156,6 +156,30 @@ def compare(g: dict, o: dict, sel=None, strict=True, inp_np=None):
                 fail("out_tok_tie", [b])
         m = o["margin_sample"][t_samp]
         rep["tie_margin_hist"] = np.histogram(np.log10(np.maximum(m, 1e-12)), bins=[-12, -9, -8, -7, -6])[0].tolist()
+        # flagged accept decisions (|u - P/Q| < 1e-6 somewhere on a path): the GPU's
+        # acceptance bits may differ from the oracle's only at rows whose own test is that
+        # close, and its n_k must be the first rejection of its own bits
+        rep["tie_decisions_checked"] = 0
+        G = inp_np["PL"].shape[2] - 1
+        K = inp_np["PL"].shape[1]
+        for b in np.where(t_dec)[0]:
+            rep["tie_decisions_checked"] += 1
+            g_b = int(o["_gamma"][b]) if "_gamma" in o else int(inp_np["gamma"][b])
+            g_b = min(max(g_b, 0), G)
+            s_b = min(max(int(inp_np["branch_pos"][b]), 0), g_b)
+            L = g_b if s_b < g_b else g_b + 1
+            for k in range(K):
+                gm, om = int(gs["acc_mask"][b, k]), int(o["acc_mask"][b, k])
+                rej = [r for r in range(L) if not (gm >> r) & 1]
+                if int(gs["n_acc"][b, k]) != (rej[0] if rej else L):
+                    fail("n_acc_tie_inconsistent", [b])
+                for r in range(L):
+                    if ((gm ^ om) >> r) & 1:
+                        ts = 0 if r < s_b else k
+                        uu = float(inp_np["u"][b, ts, r])
+                        pt, qt = float(gs["p_tok"][b, ts, r]), float(gs["q_tok"][b, ts, r])
+                        if not (qt > 0 and abs(uu - pt / qt) < 2e-6):
+                            fail("acc_tie_invalid", [b])
     same = (gs["y_kind"] == o["y_kind"]) & ~t_dec & ~t_samp
     ok, relerr = _close(gs["resid_mass"][same], o["resid_mass"][same])
     rep["max_rel_resid_mass"] = relerr

@@ -56,10 +56,12 @@ def _check_chunk(inp, g, idx, adaptive, rule, nthreads):
 
 def _merge(reps):
     out = {"n": 0, "ties": {"acc_mask": 0, "decision": 0, "sample": 0}, "exact_seq": 0, "y_compared": 0,
-           "tie_samples_checked": 0, "tie_samples_differ": 0, "tie_margin_hist": [0, 0, 0, 0]}
+           "tie_samples_checked": 0, "tie_samples_differ": 0, "tie_decisions_checked": 0,
+           "tie_margin_hist": [0, 0, 0, 0]}
     for r in reps:
-        for k in ("n", "exact_seq", "y_compared", "tie_samples_checked", "tie_samples_differ"):
-            out[k] += r[k]
+        for k in ("n", "exact_seq", "y_compared", "tie_samples_checked", "tie_samples_differ",
+                  "tie_decisions_checked"):
+            out[k] += r.get(k, 0)
         for k in out["ties"]:
             out["ties"][k] += r["ties"][k]
         out["tie_margin_hist"] = [a + b for a, b in zip(out["tie_margin_hist"], r.get("tie_margin_hist", [0] * 4))]
