@@ -1889,7 +1889,11 @@ bool astep_eligible(const sb_dims* dd, const void* PL, const void* QL) {
   return (e && e[0] == '1') || (size_t)dd->B * dd->K * (dd->G + 1) <= 4096;
 }
 
+#ifndef SB_AG_CW  // (SB_AG_CW / SB_AG_NS: experiment builds)
 using RCA = RC<16, 6, 2, 4, 4>;  // k_astep: 16 consumer warps, 6 x 32 KB stages, 4 epilogue warps
+#else
+using RCA = RC<SB_AG_CW, SB_AG_NS, 2, 4, 4>;
+#endif
 // (two CTAs per SM of 8 consumer warps, 5 x 16 KB stages each, measured 72.3 vs 71.6 us on C2)
 
 sb_status astep_run(const sb_dims* dd, const Workspace& w, const Workspace* cw, const void* PL, const void* QL,
