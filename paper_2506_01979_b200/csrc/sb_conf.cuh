@@ -60,23 +60,27 @@ __device__ __forceinline__ void conf_epilogue(const ConfParams& p, int grp, int 
     *s_last = (atomicAdd(p.cnt + grp, 1) == G - 1);
   }
   sync();
-  if (*s_last && tid == 0) {
+  if (*s_last && tid < 32) {  // the first warp: row r's statistic in lane r (G <= 31), one ballot
     __threadfence();
-    int stop = G;
-    for (int r = 0; r < G; ++r) {
-      const float sv = __ldcg(p.ws_stat + (int64_t)grp * G + r);
-      if ((double)sv <= (double)p.eps) { stop = r; break; }  // Eq. 6: keep q(x) > eps
+    float sv = 0.f, cv = 0.f;
+    if (tid < G) {
+      sv = __ldcg(p.ws_stat + (int64_t)grp * G + tid);
+      cv = __ldcg(p.ws_c + (int64_t)grp * G + tid);
     }
-    int kn = -1;
-    if (stop < G) {
-      const double c = (double)__ldcg(p.ws_c + (int64_t)grp * G + stop);
-      const double kk = floor((double)p.k_max * (1.0 - c));  // Eq. 7
-      kn = kk < 1.0 ? 1 : (int)kk;
+    const unsigned low = __ballot_sync(0xffffffffu, tid < G && (double)sv <= (double)p.eps);  // Eq. 6: keep q(x) > eps
+    const int stop = low ? __ffs(low) - 1 : G;
+    const float cs = __shfl_sync(0xffffffffu, cv, stop < G ? stop : 0);
+    if (tid == 0) {
+      int kn = -1;
+      if (stop < G) {
+        const double kk = floor((double)p.k_max * (1.0 - (double)cs));  // Eq. 7
+        kn = kk < 1.0 ? 1 : (int)kk;
+      }
+      p.stop[grp] = stop;
+      if (p.k_next) p.k_next[grp] = kn;
+      if (p.gamma_next) p.gamma_next[grp] = stop > 1 ? stop : 1;
+      p.cnt[grp] = 0;
     }
-    p.stop[grp] = stop;
-    if (p.k_next) p.k_next[grp] = kn;
-    if (p.gamma_next) p.gamma_next[grp] = stop > 1 ? stop : 1;
-    p.cnt[grp] = 0;
   }
   sync();
 }

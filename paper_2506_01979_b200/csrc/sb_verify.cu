@@ -24,6 +24,7 @@
 #include "sb_sample.cuh"
 #include "sb_conf.cuh"
 #include "sb_stream.cuh"
+#include "sb_rows.cuh"
 
 namespace sb {
 
@@ -34,33 +35,6 @@ SB_TRACE_TABLE(sb_trace_astep)
 namespace sb {
 #endif
 
-struct RowsParams {
-  Dims d;
-  const void* PL;
-  const void* QL;
-  const int* tok;
-  const float* u;
-  const SeqInfo* info;
-  const int* unit_off;
-  const int* seqpk;       // [B] packed layout (k_plan), read by the warp-cooperative decode
-  const RowStat* qreuse;  // [B][G] slot-0 q-row states from sb_draft_confidence, or NULL
-  int* cnt;
-  float4* rowstat;
-  uint8_t* pflag;
-  float *lse_p, *lse_q, *p_tok, *q_tok, *top1_q, *entropy_q;
-  int* top1_id_q;
-  uint32_t* acc_mask;
-  int* n_acc;
-  int* status;
-  int* ready;  // fused step: per-sequence "n_k known" flags (NULL otherwise)
-  // adaptive single-launch step (k_astep): the sequence whose n_k is known is appended to
-  // the sample queue (sq[atomicAdd(sq_ctr)] = b, then sq_pub[slot] released); NULL otherwise
-  int *sq_ctr, *sq, *sq_pub;
-  // vocabulary-shard partial mode (a7): write the shard's row states / token logits
-  int partial, v_offset;
-  ShardRow* rowpart;  // [B][K][G+1] physical rows
-  float2* tokpart;    // [B][K][G+1] token slots: (p logit, q logit) if the token is in this shard
-};
 
 // ---------------------------------------------------------------- plan
 // A unit's sequence, row geometry and the sequence's layout packed in 16 bytes.
@@ -140,10 +114,6 @@ __global__ void __launch_bounds__(1024) k_plan(Dims d, const int* __restrict__ g
 }
 
 // ---------------------------------------------------------------- shared unit logic
-struct Unit {
-  int b, slot, i;
-  SeqInfo in;
-};
 
 // unit -> (sequence, slot, row): upper-bound search over the offsets, then slot 0 rows
 // 0..L-1 followed by rows s+1..L-1 of slots 1..K-1
@@ -475,119 +445,6 @@ __device__ __forceinline__ RowStat warp_part(const LazyAcc<kQ, 4>& a, const T* r
   return s;
 }
 
-// Epilogue of one unit by one warp, with the token data already prefetched.
-template <typename T>
-__device__ __forceinline__ void warp_epilogue(const RowsParams& p, const Unit& un, const RowStat& ps,
-                                              const RowStat& qs, const T* qrow, int x, float lpx, float lqx,
-                                              float uu, int64_t et) {
-  const Dims& d = p.d;
-  const int lane = threadIdx.x & 31;
-  const int b = un.b, slot = un.slot, i = un.i;
-  const SeqInfo& in = un.in;
-  const RowOut po = finish(ps), qo = finish_q<T>(qs, qrow, d.V);
-  const bool branch_row = (slot == 0 && i == in.s);
-  const int ntok = branch_row ? d.K : 1;
-  if (lane < ntok) {
-    uint8_t fl = 0;
-    float pt = CUDART_NAN_F, qt = CUDART_NAN_F;
-    if (!(po.finite && qo.finite)) {
-      fl |= st_flags(po.st | qo.st);
-    } else if (x < 0 || x >= d.V) {
-      fl |= 2;
-    } else {
-      const double Px = tok_prob(lpx, po.MS, po.Z);
-      const double Qx = tok_prob(lqx, qo.MS, qo.Z);
-      pt = (float)Px;
-      qt = (float)Qx;
-      // accept iff r <= p/q (P534, P538), as u*Q[x] <= P[x]; Q[x] = 0 accepts (S127)
-      if ((double)uu * Qx <= Px) fl |= 1;
-    }
-    p.p_tok[et] = pt;
-    p.q_tok[et] = qt;
-    p.pflag[et] = fl;
-  }
-  if (lane == 0) {
-    const int64_t e = ent(d, b, slot, i);
-    const double LN2 = 0.69314718055994530942;
-    p.lse_p[e] = po.finite ? (float)(((double)po.MS + log2((double)po.Z)) * LN2) : CUDART_NAN_F;
-    p.lse_q[e] = qo.finite ? (float)(((double)qo.MS + log2((double)qo.Z)) * LN2) : CUDART_NAN_F;
-    const bool conf_ok = po.finite && qo.finite;  // as the oracle: q stats iff both rows finite
-    if (p.top1_q) p.top1_q[e] = conf_ok ? (float)tok_prob(qs.m, qo.MS, qo.Z) : CUDART_NAN_F;
-    if (p.top1_id_q) p.top1_id_q[e] = conf_ok ? qs.idx : -1;
-    if (p.entropy_q) {
-      const double Z = qo.Z;
-      p.entropy_q[e] = conf_ok ? (float)(LN2 * (log2(Z) - (double)qs.s1 / Z)) : CUDART_NAN_F;
-    }
-    p.rowstat[e] = make_float4(po.MS, z_store(po), qo.MS, z_store(qo));
-  }
-  __syncwarp();
-  int last = 0;
-  if (lane == 0) {
-    __threadfence();
-    // phase-1 row pairs of b (the fused unit list also interleaves sample units)
-    const int units_b = in.Lr + (d.K - 1) * (in.Lr - 1 - in.s);
-    last = (atomicAdd(p.cnt + b, 1) == units_b - 1);
-  }
-  last = __shfl_sync(0xffffffffu, last, 0);
-  if (!last) return;
-  __threadfence();
-  // first rejection per branch: lane r holds row r's flags for every branch (loads
-  // issued back to back), then one ballot per branch
-  uint32_t fw[4] = {0u, 0u, 0u, 0u};  // 4 flag bits per branch, 8 branches per word
-  if (lane < in.L) {
-#pragma unroll 8
-    for (int k = 0; k < d.K; ++k) {
-      const uint32_t f = __ldcg(p.pflag + ent(d, b, (lane < in.s) ? 0 : k, lane));
-      fw[k / 8] |= (f & 15u) << (4 * (k % 8));
-    }
-  }
-  const uint32_t rowmask = in.L >= 32 ? 0xffffffffu : ((1u << in.L) - 1u);
-  uint32_t anyf = 0;
-  for (int k = 0; k < d.K; ++k) {
-    const uint32_t f = (fw[k / 8] >> (4 * (k % 8))) & 15u;
-    const uint32_t mask = __ballot_sync(0xffffffffu, f & 1u) & rowmask;
-    anyf |= f;
-    if (lane == 0) {
-      const uint32_t rej = ~mask & rowmask;
-      p.acc_mask[(int64_t)b * d.K + k] = mask;
-      p.n_acc[(int64_t)b * d.K + k] = rej ? (__ffs(rej) - 1) : in.L;
-    }
-  }
-  anyf = __reduce_or_sync(0xffffffffu, anyf);
-  // sentinels for entries no tested path touches
-  const int R1 = d.G + 1;
-  for (int q = lane; q < d.K * R1; q += 32) {
-    const int k = q / R1, r = q % R1;
-    const int64_t e = ent(d, b, k, r);
-    const bool phys = (k == 0) ? (r < in.L) : (r > in.s && r < in.L);
-    const bool path = (k == 0) ? (r < in.L) : (r >= in.s && r < in.L);
-    if (!phys) {
-      p.lse_p[e] = CUDART_NAN_F;
-      p.lse_q[e] = CUDART_NAN_F;
-      if (p.top1_q) p.top1_q[e] = CUDART_NAN_F;
-      if (p.top1_id_q) p.top1_id_q[e] = -1;
-      if (p.entropy_q) p.entropy_q[e] = CUDART_NAN_F;
-    }
-    if (!path) {
-      p.p_tok[e] = CUDART_NAN_F;
-      p.q_tok[e] = CUDART_NAN_F;
-    }
-  }
-  if (lane == 0) {
-    p.status[b] = in.st | flags_st(anyf);
-    p.cnt[b] = 0;  // leave the workspace re-usable
-    if (p.ready) {  // fused step: the sequence's sample unit may start
-      __threadfence();
-      asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p.ready + b), "r"(1) : "memory");
-    }
-    if (p.sq) {  // adaptive single-launch step: queue the sequence's sample item
-      const int slot = atomicAdd(p.sq_ctr, 1);
-      p.sq[slot] = b;
-      __threadfence();
-      asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p.sq_pub + slot), "r"(1) : "memory");
-    }
-  }
-}
 
 // One ring stage as this thread sees it: VPT 16-byte vectors of the p and q chunks.
 template <class C>
@@ -1342,9 +1199,7 @@ struct AStepParams {
   int qcap;           // capacity of qv / qv_pub (B K (G+1))
   int* sq;            // sample queue: sequences
   int* sq_pub;
-  int *sel_k, *commit_len, *out_tok, *y_tok, *y_kind, *offsets, *packed_tok, *path_rolled, *branch_discarded;
-  uint32_t* keep_mask;
-  float* resid_mass;
+  CommitOut co;
 };
 
 template <class C>
@@ -1362,43 +1217,6 @@ struct AStepSmem {
   alignas(128) uint8_t buf[C::NS][2][C::CHUNK];
 };
 
-// Records written by other CTAs during this launch are read through L2 (ld.global.cg):
-// a line of neighbouring records may sit in this SM's L1 from before they were written.
-__device__ __forceinline__ SeqInfo ldcg_seqinfo(const SeqInfo* src) {
-  static_assert(sizeof(SeqInfo) == 32, "two 16-byte loads");
-  const int4 a = __ldcg(reinterpret_cast<const int4*>(src)), b = __ldcg(reinterpret_cast<const int4*>(src) + 1);
-  SeqInfo r;
-  r.g = a.x; r.s = a.y; r.L = a.z; r.st = a.w; r.Lr = b.x;
-  r.pad_[0] = b.y; r.pad_[1] = b.z; r.pad_[2] = b.w;
-  return r;
-}
-__device__ __forceinline__ RowStat ldcg_rowstat(const RowStat* src) {
-  static_assert(sizeof(RowStat) == 32, "two 16-byte loads");
-  const int4 a = __ldcg(reinterpret_cast<const int4*>(src)), b = __ldcg(reinterpret_cast<const int4*>(src) + 1);
-  RowStat r;
-  int4 w[2] = {a, b};
-  memcpy(&r, w, sizeof(r));
-  return r;
-}
-__device__ __forceinline__ int ld_acq(const int* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_rel(int* p, int v) {
-  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-// Geometry of sequence b once gamma_b is known (k_plan's clamps, unsharded): its SeqInfo.
-__device__ __forceinline__ SeqInfo astep_seqinfo(int g, int s, int G) {
-  int st = 0;
-  if (g > G) { g = G; st |= SB_ST_GAMMA_CLAMPED; }
-  if (g < 0) { g = 0; st |= SB_ST_GAMMA_CLAMPED; }
-  if (s > g) { s = g; st |= SB_ST_BRANCH_CLAMPED; }
-  if (s < 0) { s = 0; st |= SB_ST_BRANCH_CLAMPED; }
-  const int L = (s < g) ? g : g + 1;
-  return SeqInfo{g, s, L, st, L, {0, 0, 0}};
-}
 
 // Sequence b's verify items once gamma_b is known (k_plan's clamps and unit layout): its
 // SeqInfo, then one reservation of its entries in the verify queue, published entry by
@@ -1492,14 +1310,22 @@ __global__ void __launch_bounds__(C::ROWS_THREADS, MINB) k_astep(AStepParams ap)
       (void)tli;
       // one grab kept in flight: the next item's atomicAdd round trip (~1 us when 148
       // producers contend) overlaps this item's decode and copies
-      int gnext = atomicAdd(ap.ctr, 1);
+      // the first-phase items (confidence / plan) are dealt statically, CTA c taking c,
+      // c + grid, ...; the dependent items that follow come from one global counter
+      int kst = 0;
+      auto next_item = [&]() -> int {
+        const int gs = (int)blockIdx.x + kst * (int)gridDim.x;
+        if (gs < nconf) { ++kst; return gs; }
+        return nconf + atomicAdd(ap.ctr, 1);
+      };
+      int gnext = next_item();
       while (exits < C::NE) {
         AItem it{};
         if (exits > 0) {
           it.type = -1;
         } else {
           const int g = gnext;
-          gnext = atomicAdd(ap.ctr, 1);
+          gnext = next_item();
           if (g < nconf) {
             if (ap.adaptive) { it.type = 0; it.b = g / G; it.slot = 0; it.i = g % G; }
             else { it.type = 3; it.b = g; }
@@ -1683,30 +1509,7 @@ __global__ void __launch_bounds__(C::ROWS_THREADS, MINB) k_astep(AStepParams ap)
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&S.pempty[ps_slot]);
-        const int ksel = it.ksel, npath = it.npath, kpath = ksel < 0 ? 0 : ksel;  // commit
-        int* out = ap.out_tok + (int64_t)b * (G + 2);
-        for (int qq = lane; qq < G + 2; qq += 32) {
-          int v = -1;
-          if (qq < npath) v = __ldg(p.tok + ent(d, b, (qq < in.s) ? 0 : kpath, qq));
-          else if (qq == npath && kind != 0) v = y;
-          out[qq] = v;
-        }
-        if (lane < d.K) {
-          uint32_t km = 0;
-          for (int qq = 0; qq < npath; ++qq)
-            if (((qq < in.s) ? 0 : kpath) == lane) km |= 1u << qq;
-          ap.keep_mask[(int64_t)b * d.K + lane] = km;
-        }
-        if (lane == 0) {
-          ap.sel_k[b] = ksel;
-          ap.commit_len[b] = npath + (kind != 0);
-          ap.y_tok[b] = (kind != 0) ? y : -1;
-          ap.y_kind[b] = kind;
-          ap.path_rolled[b] = in.L - npath;
-          ap.branch_discarded[b] = (d.K - 1) * (in.L - in.s);
-          if (ap.resid_mass) ap.resid_mass[b] = (kind != 0) ? (float)mass : 0.f;
-          if (st) atomicOr(p.status + b, st);
-        }
+        commit_seq(p, ap.co, b, in, it.ksel, it.npath, kind, y, mass, st);
         __syncwarp();
         int last = 0;
         if (lane == 0) {
@@ -1716,7 +1519,7 @@ __global__ void __launch_bounds__(C::ROWS_THREADS, MINB) k_astep(AStepParams ap)
         last = __shfl_sync(0xffffffffu, last, 0);
         if (last) {
           __threadfence();
-          warp_offsets(d.B, G, ap.commit_len, ap.out_tok, ap.offsets, ap.packed_tok);
+          warp_offsets(d.B, G, ap.co.commit_len, ap.co.out_tok, ap.co.offsets, ap.co.packed_tok);
           if (lane == 0) ap.ctr[5] = 0;
         }
       }
@@ -1931,9 +1734,8 @@ sb_status astep_run(const sb_dims* dd, const Workspace& w, const Workspace* cw, 
   ap.us = us; ap.bpos = branch_pos; ap.rule = rule;
   ap.ctr = w.actr; ap.qv = w.aqv; ap.qv_pub = w.aqv_pub; ap.sq = w.asq; ap.sq_pub = w.asq_pub;
   ap.qcap = dd->B * dd->K * (dd->G + 1);
-  ap.sel_k = sel_k; ap.commit_len = commit_len; ap.out_tok = out_tok; ap.y_tok = y_tok; ap.y_kind = y_kind;
-  ap.offsets = offsets; ap.packed_tok = packed_tok; ap.path_rolled = path_rolled;
-  ap.branch_discarded = branch_discarded; ap.keep_mask = keep_mask; ap.resid_mass = resid_mass;
+  ap.co = CommitOut{sel_k, commit_len, out_tok, y_tok, y_kind, offsets, packed_tok, path_rolled, branch_discarded,
+                    keep_mask, resid_mass};
   return dd->dtype == SB_BF16 ? launch_astep<RCA, __nv_bfloat16, 1>(ap, s) : launch_astep<RCA, float, 1>(ap, s);
 }
 
@@ -2159,6 +1961,15 @@ static sb_status launch_rows_variant(const RowsParams& p, cudaStream_t s) {
   return v == 2 ? launch_rows_tma<RC2, T>(p, s) : launch_rows_tma<RC0, T>(p, s);
 }
 
+// The small-batch split-vocabulary step (sb_sv.cu).
+bool sv_eligible(const sb_dims* dd, const void* PL, const void* QL);
+sb_status sv_run(const sb_dims* dd, const Workspace& w, const Workspace* cw, const void* PL, const void* QL,
+                 const int32_t* tok, const float* u, const float* us, const int32_t* gamma, const int32_t* branch_pos,
+                 sb_select_rule rule, float eps, int32_t k_max, float* c_top1, int32_t* c_id, float* c_ent,
+                 float* c_stat, int32_t* c_stop, int32_t* c_knext, int32_t* c_gamma, float* lse_p, float* lse_q,
+                 float* p_tok, float* q_tok, uint32_t* acc_mask, int32_t* n_acc, float* top1_q, int32_t* top1_id_q,
+                 float* entropy_q, int32_t* status, const CommitOut& co, cudaStream_t s);
+
 }  // namespace sb
 
 using namespace sb;
@@ -2314,6 +2125,13 @@ extern "C" sb_status sb_verify_select(const sb_dims* dd, const void* p_logits, c
   // k_astep with plan items instead of confidence items: opt-in (SB_ASTEP=1) — one C1 round
   // (batch 1) measured 31.8 us against 29.6 us for k_plan + the two streaming kernels
   const char* ae = getenv("SB_ASTEP");
+  if (!fused && !(ae && ae[0] == '1') && sv_eligible(dd, p_logits, q_logits))
+    return sv_run(dd, w, nullptr, p_logits, q_logits, tok, u, us, gamma, branch_pos, rule, 0.f, 0, nullptr, nullptr,
+                  nullptr, nullptr, nullptr, nullptr, nullptr, lse_p, lse_q, p_tok, q_tok, acc_mask, n_acc, top1_q,
+                  top1_id_q, entropy_q, status,
+                  CommitOut{sel_k, commit_len, out_tok, y_tok, y_kind, offsets, packed_tok, path_rolled,
+                            branch_discarded, keep_mask, resid_mass},
+                  (cudaStream_t)stream);
   if (!fused && ae && ae[0] == '1' && astep_eligible(dd, p_logits, q_logits))
     return astep_run(dd, w, nullptr, p_logits, q_logits, tok, u, us, gamma, branch_pos, rule, 0.f, 0, nullptr,
                      nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, lse_p, lse_q, p_tok, q_tok, acc_mask,
@@ -2377,6 +2195,16 @@ extern "C" sb_status sb_step_adaptive(const sb_dims* dd, const void* p_logits, c
   cd.seq_stride = to_dims(dd).ss;
   if (conf_workspace_bytes < sb_workspace_bytes(&cd)) return SB_ERR_WORKSPACE;
   cudaStream_t s = (cudaStream_t)stream;
+  const char* ae = getenv("SB_ASTEP");
+  if (!(ae && ae[0] == '1') && sv_eligible(dd, p_logits, q_logits)) {  // one split-vocabulary launch (k_sv)
+    const Workspace cw = carve(cd, conf_workspace);
+    return sv_run(dd, w, &cw, p_logits, q_logits, tok, u, us, nullptr, branch_pos, rule, eps, k_max, c_top1_prob,
+                  c_top1_id, c_entropy, c_stat, c_stop, c_k_next, c_gamma_next, lse_p, lse_q, p_tok, q_tok, acc_mask,
+                  n_acc, top1_q, top1_id_q, entropy_q, status,
+                  CommitOut{sel_k, commit_len, out_tok, y_tok, y_kind, offsets, packed_tok, path_rolled,
+                            branch_discarded, keep_mask, resid_mass},
+                  s);
+  }
   if (astep_eligible(dd, p_logits, q_logits))  // one persistent launch (k_astep)
   {
     const Workspace cw = carve(cd, conf_workspace);

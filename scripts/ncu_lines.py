@@ -6,7 +6,7 @@ import subprocess
 import sys
 
 rep = sys.argv[1]
-N = int(sys.argv[2]) if len(sys.argv) > 2 else 40
+N = int(sys.argv[2]) if len(sys.argv) > 2 and sys.argv[2].isdigit() else 40
 txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
 rows, fname, hdr = [], None, None
@@ -30,5 +30,6 @@ for r in csv.reader(io.StringIO(txt)):
 tot_i = sum(x[0] for x in rows) or 1
 tot_s = sum(x[1] for x in rows) or 1
 print(f"total warp instructions {tot_i}, stall samples {tot_s}")
-for inst, stall, f, ln, src in sorted(rows, reverse=True)[:N]:
+key = (lambda x: x[1]) if "--by-stall" in sys.argv else (lambda x: x[0])
+for inst, stall, f, ln, src in sorted(rows, key=key, reverse=True)[:N]:
     print(f"{inst / tot_i:6.3f} {stall / tot_s:6.3f}  {f}:{ln}  {src}")
