@@ -64,20 +64,8 @@ struct Workspace {
   int* aqv_pub;      // [B][K][G+1] entry published
   int* asq;          // [B] sample queue
   int* asq_pub;      // [B]
-  // small-batch split-vocabulary step (k_sv, sb_sv.cu); empty unless B K (G+1) <= 4096
-  RowStat* sv_part_p;  // [kSvPartCap] per-(row, slice) partial states
-  RowStat* sv_part_q;
-  void* sv_desc;       // [B] sample descriptors (48 B)
-  float* sv_seg;       // [B][nseg] 1 KB segment sums
-  float* sv_segm;      // [B][nseg] segment maxima
-  int* sv_ctr;         // [4] grid barrier, exit and commit counters (self-resetting)
   size_t bytes;
 };
-
-// k_sv partial-record capacity (sb_sv.cu: one unit per lane, <= 160 SMs x 16 warps x 32
-// lanes, plus warp padding of its two sub-phases) and its problem-size bound.
-constexpr int kSvPartCap = 160 * 16 * 32 + 64;
-constexpr int kSvPartRowsMax = 4096;
 
 inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
@@ -114,17 +102,6 @@ inline Workspace carve(const sb_dims& d, void* base) {
   w.aqv_pub = (int*)take(sizeof(int) * B * K * R1);
   w.asq = (int*)take(sizeof(int) * B);
   w.asq_pub = (int*)take(sizeof(int) * B);
-  {
-    const bool small = B * K * R1 <= (size_t)kSvPartRowsMax;
-    const size_t cap = small ? (size_t)kSvPartCap : 0;
-    const size_t nseg1k = ((size_t)d.V * (d.dtype == SB_BF16 ? 2 : 4) + 1023) / 1024;
-    w.sv_part_p = (RowStat*)take(sizeof(RowStat) * cap);
-    w.sv_part_q = (RowStat*)take(sizeof(RowStat) * cap);
-    w.sv_desc = (void*)take(small ? 48 * B : 0);
-    w.sv_seg = (float*)take(small ? sizeof(float) * B * nseg1k : 0);
-    w.sv_segm = (float*)take(small ? sizeof(float) * B * nseg1k : 0);
-    w.sv_ctr = (int*)take(sizeof(int) * 4);
-  }
   w.bytes = off;
   return w;
 }

@@ -1,5 +1,5 @@
 // sb_rows.cuh — the row-pair epilogue shared by every verify kernel (k_rows_tma, k_astep,
-// k_rows_warp, k_sv): row outputs, the fp64 acceptance test u*Q[x] <= P[x] (P94, Alg. 1
+// k_rows_warp): row outputs, the fp64 acceptance test u*Q[x] <= P[x] (P94, Alg. 1
 // P534/P538), and in the warp completing a sequence its first rejection per branch
 // n_k; plus the cross-CTA record loads of the persistent kernels.
 #pragma once
@@ -78,12 +78,11 @@ __device__ __forceinline__ SeqInfo astep_seqinfo(int g, int s, int G) {
   return SeqInfo{g, s, L, st, L, {0, 0, 0}};
 }
 
-// Epilogue of one unit by one warp, with the token data already prefetched.  Returns
-// true in the warp that completed the sequence; lane k < K then holds n_k in *nk_lane.
+// Epilogue of one unit by one warp, with the token data already prefetched.
 template <typename T>
-__device__ __forceinline__ bool warp_epilogue(const RowsParams& p, const Unit& un, const RowStat& ps,
+__device__ __forceinline__ void warp_epilogue(const RowsParams& p, const Unit& un, const RowStat& ps,
                                               const RowStat& qs, const T* qrow, int x, float lpx, float lqx,
-                                              float uu, int64_t et, int* nk_lane = nullptr) {
+                                              float uu, int64_t et) {
   const Dims& d = p.d;
   const int lane = threadIdx.x & 31;
   const int b = un.b, slot = un.slot, i = un.i;
@@ -133,7 +132,7 @@ __device__ __forceinline__ bool warp_epilogue(const RowsParams& p, const Unit& u
     last = (atomicAdd(p.cnt + b, 1) == units_b - 1);
   }
   last = __shfl_sync(0xffffffffu, last, 0);
-  if (!last) return false;
+  if (!last) return;
   __threadfence();
   // first rejection per branch: lane r holds row r's flags for every branch (loads
   // issued back to back), then one ballot per branch
@@ -155,10 +154,6 @@ __device__ __forceinline__ bool warp_epilogue(const RowsParams& p, const Unit& u
       const uint32_t rej = ~mask & rowmask;
       p.acc_mask[(int64_t)b * d.K + k] = mask;
       p.n_acc[(int64_t)b * d.K + k] = rej ? (__ffs(rej) - 1) : in.L;
-    }
-    if (nk_lane && lane == k) {
-      const uint32_t rej = ~mask & rowmask;
-      *nk_lane = rej ? (__ffs(rej) - 1) : in.L;
     }
   }
   anyf = __reduce_or_sync(0xffffffffu, anyf);
@@ -195,7 +190,6 @@ __device__ __forceinline__ bool warp_epilogue(const RowsParams& p, const Unit& u
       asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p.sq_pub + slot), "r"(1) : "memory");
     }
   }
-  return true;
 }
 
 // Outputs of sb_select_branch (include/specbranch.h).

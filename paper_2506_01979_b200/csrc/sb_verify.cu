@@ -1961,15 +1961,6 @@ static sb_status launch_rows_variant(const RowsParams& p, cudaStream_t s) {
   return v == 2 ? launch_rows_tma<RC2, T>(p, s) : launch_rows_tma<RC0, T>(p, s);
 }
 
-// The small-batch split-vocabulary step (sb_sv.cu).
-bool sv_eligible(const sb_dims* dd, const void* PL, const void* QL);
-sb_status sv_run(const sb_dims* dd, const Workspace& w, const Workspace* cw, const void* PL, const void* QL,
-                 const int32_t* tok, const float* u, const float* us, const int32_t* gamma, const int32_t* branch_pos,
-                 sb_select_rule rule, float eps, int32_t k_max, float* c_top1, int32_t* c_id, float* c_ent,
-                 float* c_stat, int32_t* c_stop, int32_t* c_knext, int32_t* c_gamma, float* lse_p, float* lse_q,
-                 float* p_tok, float* q_tok, uint32_t* acc_mask, int32_t* n_acc, float* top1_q, int32_t* top1_id_q,
-                 float* entropy_q, int32_t* status, const CommitOut& co, cudaStream_t s);
-
 }  // namespace sb
 
 using namespace sb;
@@ -2125,13 +2116,6 @@ extern "C" sb_status sb_verify_select(const sb_dims* dd, const void* p_logits, c
   // k_astep with plan items instead of confidence items: opt-in (SB_ASTEP=1) — one C1 round
   // (batch 1) measured 31.8 us against 29.6 us for k_plan + the two streaming kernels
   const char* ae = getenv("SB_ASTEP");
-  if (!fused && !(ae && ae[0] == '1') && sv_eligible(dd, p_logits, q_logits))
-    return sv_run(dd, w, nullptr, p_logits, q_logits, tok, u, us, gamma, branch_pos, rule, 0.f, 0, nullptr, nullptr,
-                  nullptr, nullptr, nullptr, nullptr, nullptr, lse_p, lse_q, p_tok, q_tok, acc_mask, n_acc, top1_q,
-                  top1_id_q, entropy_q, status,
-                  CommitOut{sel_k, commit_len, out_tok, y_tok, y_kind, offsets, packed_tok, path_rolled,
-                            branch_discarded, keep_mask, resid_mass},
-                  (cudaStream_t)stream);
   if (!fused && ae && ae[0] == '1' && astep_eligible(dd, p_logits, q_logits))
     return astep_run(dd, w, nullptr, p_logits, q_logits, tok, u, us, gamma, branch_pos, rule, 0.f, 0, nullptr,
                      nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, lse_p, lse_q, p_tok, q_tok, acc_mask,
@@ -2195,16 +2179,6 @@ extern "C" sb_status sb_step_adaptive(const sb_dims* dd, const void* p_logits, c
   cd.seq_stride = to_dims(dd).ss;
   if (conf_workspace_bytes < sb_workspace_bytes(&cd)) return SB_ERR_WORKSPACE;
   cudaStream_t s = (cudaStream_t)stream;
-  const char* ae = getenv("SB_ASTEP");
-  if (!(ae && ae[0] == '1') && sv_eligible(dd, p_logits, q_logits)) {  // one split-vocabulary launch (k_sv)
-    const Workspace cw = carve(cd, conf_workspace);
-    return sv_run(dd, w, &cw, p_logits, q_logits, tok, u, us, nullptr, branch_pos, rule, eps, k_max, c_top1_prob,
-                  c_top1_id, c_entropy, c_stat, c_stop, c_k_next, c_gamma_next, lse_p, lse_q, p_tok, q_tok, acc_mask,
-                  n_acc, top1_q, top1_id_q, entropy_q, status,
-                  CommitOut{sel_k, commit_len, out_tok, y_tok, y_kind, offsets, packed_tok, path_rolled,
-                            branch_discarded, keep_mask, resid_mass},
-                  s);
-  }
   if (astep_eligible(dd, p_logits, q_logits))  // one persistent launch (k_astep)
   {
     const Workspace cw = carve(cd, conf_workspace);

@@ -108,18 +108,16 @@ SMALL = [
 ]
 
 
-@pytest.mark.parametrize("fused", ["sv", "single_launch", "astep", "verify_select", "two_calls"])
+@pytest.mark.parametrize("fused", ["single_launch", "astep", "verify_select", "two_calls"])
 @pytest.mark.parametrize("name,kw,pad,rule", SMALL, ids=[c[0] for c in SMALL])
 def test_small_parity(name, kw, pad, rule, fused, monkeypatch):
-    """sv: the split-vocabulary single launch k_sv (opt-in SB_SV=1: B K (G+1) <= 4096,
-    aligned rows; measured slower than the default); single_launch: the persistent TMA-ring k_step_tma
-    (SB_FUSED_STEP=1); astep: the persistent work-queue kernel k_astep with plan items
-    (SB_ASTEP=1); verify_select: the two streaming kernels behind sb_verify_select
-    (SB_SV=0); two_calls: sb_verify_branches then sb_select_branch."""
+    """single_launch: the persistent TMA-ring k_step_tma (SB_FUSED_STEP=1); astep: the
+    persistent work-queue kernel k_astep with plan items (opt-in for sb_verify_select,
+    SB_ASTEP=1); verify_select: the two streaming kernels behind sb_verify_select (the
+    default); two_calls: sb_verify_branches then sb_select_branch."""
     kw = dict(kw)
     c = cfg(kw.pop("name"), **kw)
     monkeypatch.setenv("SB_ASTEP", "1" if fused == "astep" else "0")
-    monkeypatch.setenv("SB_SV", "1" if fused == "sv" else "0")
     if fused == "single_launch":
         monkeypatch.setenv("SB_FUSED_STEP", "1")  # the persistent k_step_tma kernel
     rep, g = _run(c, row_pad=pad, rule=rule, fused=(fused != "two_calls"))
@@ -168,17 +166,15 @@ ADAPTIVE = [
 ]
 
 
-@pytest.mark.parametrize("path", ["sv", "astep", "three_calls"])
+@pytest.mark.parametrize("path", ["astep", "three_calls"])
 @pytest.mark.parametrize("name,kw,rule,nmin", ADAPTIVE, ids=[a[0] for a in ADAPTIVE])
 def test_adaptive_confidence_parity(name, kw, rule, nmin, path, monkeypatch):
-    """The adaptive-gamma step through sb_step_adaptive: the work-queue launch k_astep
-    (the default for small problems), the split-vocabulary launch k_sv (opt-in SB_SV=1)
-    and the three streaming kernels (SB_ASTEP=0: confidence -> verify reusing its
-    rows -> select), on shapes with several items per CTA, more sequences than SMs,
+    """The adaptive-gamma step through sb_step_adaptive: the single persistent launch
+    k_astep (default; confidence -> verify -> select items in one grid) and the three
+    streaming kernels (SB_ASTEP=0: confidence -> verify reusing its rows -> select), on shapes with several items per CTA, more sequences than SMs,
     ragged / unaligned rows (the latter always take the three kernels), K = 8,
     gamma_max = 31 and Alg. 1."""
     monkeypatch.setenv("SB_ASTEP", "0" if path == "three_calls" else "1")
-    monkeypatch.setenv("SB_SV", "1" if path == "sv" else "0")
     kw = dict(kw)
     rep, g = _run(cfg(kw.pop("name"), **kw), adaptive=True, rule=rule)
     assert rep["n"] >= nmin, rep
@@ -261,9 +257,9 @@ def test_identical_p_q_accepts_all_on_gpu():
     assert (g["path_rolled"] == 0).all()
 
 
-@pytest.mark.parametrize("path", ["sv", "astep", "three_calls"])
+@pytest.mark.parametrize("path", ["astep", "three_calls"])
 def test_adaptive_special_values(path, monkeypatch):
-    """The adaptive step (k_sv, k_astep and the three kernels) on rows that break the usual
+    """The adaptive step (k_astep and the three kernels) on rows that break the usual
     assumptions: NaN / +inf / all -inf / one-hot / finfo(bf16).min-masked draft rows in
     slot 0 (the confidence pass and its reused q states), NaN target rows, out-of-range
     tokens, a clamped branch row; statistics, stop / k / gamma and every verify / select
@@ -271,7 +267,6 @@ def test_adaptive_special_values(path, monkeypatch):
     from paper_2506_01979_b200 import synth
 
     monkeypatch.setenv("SB_ASTEP", "1" if path == "astep" else "0")
-    monkeypatch.setenv("SB_SV", "1" if path == "sv" else "0")
     c = cfg("c2", V=4096, B=24, K=3, G=6, layout="adaptive")
     inp = synth.generate(c, device="cuda", seed=13)
     bmin = torch.finfo(torch.bfloat16).min
