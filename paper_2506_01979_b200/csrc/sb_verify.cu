@@ -1406,6 +1406,9 @@ __global__ void __launch_bounds__(C::ROWS_THREADS, MINB) k_astep(AStepParams ap)
             if (b1) bulk_g2s(S.buf[rp.stage][1], row + (size_t)(c + 1) * C::CHUNK, b1, &S.full[rp.stage], pol);
             rp.advance();
           }
+#ifdef SB_TRACE
+          if (tli - 1 < 60) SB_TRACE_AT(sb_trace_astep, 7, 2 + tli - 1);  // last chunk issued
+#endif
           continue;
         }
         const bool wp = true, wq = (it.type == 1) || (it.type == 2 && it.kind == 1);
@@ -1419,6 +1422,9 @@ __global__ void __launch_bounds__(C::ROWS_THREADS, MINB) k_astep(AStepParams ap)
             if (wq) bulk_g2s(S.buf[rp.stage][1], qrow + (size_t)c * C::CHUNK, bytes, &S.full[rp.stage], pol);
             rp.advance();
           }
+#ifdef SB_TRACE
+        if (tli - 1 < 60) SB_TRACE_AT(sb_trace_astep, 7, 2 + tli - 1);  // last chunk issued
+#endif
       }
     }
   } else if (warp > C::CW) {  // ---------------- epilogue warps: warp e takes items e, e + NE, ...

@@ -64,3 +64,18 @@ for typ, code in (("conf", 1), ("verify", 2)):
     if w:
         print(f"{typ} items: wait-for-data median {np.median(w):.2f} us, stream+math {np.median(c_):.2f}, "
               f"warp reductions {np.median(r_):.2f}, publish (pempty wait) {np.median(pub):.2f}")
+
+# producer side: grab -> last chunk issued, last chunk issued -> consumers done
+for typ, code in (("conf", 1), ("verify", 2), ("sample", 3)):
+    gi, ic = [], []
+    for cta in np.where(act)[0]:
+        for k in range(60):
+            if a[cta, 0, 2 + k] != code:
+                continue
+            g_, i_, c_ = int(a[cta, 1, 2 + k]), int(a[cta, 7, 2 + k]), int(a[cta, 3, 2 + k])
+            if g_ and i_ and c_:
+                gi.append((i_ - g_) / 1e3)
+                ic.append((c_ - i_) / 1e3)
+    if gi:
+        print(f"{typ}: grab -> last chunk issued median {np.median(gi):.2f} us (p90 {np.percentile(gi, 90):.2f}); "
+              f"last issued -> consumers done median {np.median(ic):.2f} us (p90 {np.percentile(ic, 90):.2f})")
