@@ -1314,7 +1314,12 @@ __global__ void __launch_bounds__(C::ROWS_THREADS, MINB) k_astep(AStepParams ap)
       // c + grid, ...; the dependent items that follow come from one global counter
       int kst = 0;
       auto next_item = [&]() -> int {
+#ifdef SB_ASTEP_BLOCKED  // experiment: CTA c takes a contiguous block of the first-phase items
+        const int b0 = (int)((int64_t)blockIdx.x * nconf / gridDim.x), b1 = (int)((int64_t)(blockIdx.x + 1) * nconf / gridDim.x);
+        const int gs = b0 + kst < b1 ? b0 + kst : nconf;
+#else
         const int gs = (int)blockIdx.x + kst * (int)gridDim.x;
+#endif
         if (gs < nconf) { ++kst; return gs; }
         return nconf + atomicAdd(ap.ctr, 1);
       };
