@@ -202,15 +202,15 @@ struct CommitOut {
 // Commit of sequence b (SURVEY §8.0 "Commit"; P94, P237, P541-555, rollback P655): the
 // kept path k*'s tokens for rows 0..npath-1 (slot 0 before the branch row), then y if
 // kind != 0; keep mask per slot, rollback counters (P317 / P734).  One warp.
-__device__ __forceinline__ void commit_seq(const RowsParams& p, const CommitOut& co, int b, const SeqInfo& in,
-                                           int ksel, int npath, int kind, int y, double mass, int st) {
-  const Dims& d = p.d;
+__device__ __forceinline__ void commit_seq(const Dims& d, const int* tok, int* status, const CommitOut& co, int b,
+                                           const SeqInfo& in, int ksel, int npath, int kind, int y, double mass,
+                                           int st) {
   const int lane = threadIdx.x & 31, G = d.G;
   const int kpath = ksel < 0 ? 0 : ksel;
   int* out = co.out_tok + (int64_t)b * (G + 2);
   for (int qq = lane; qq < G + 2; qq += 32) {
     int v = -1;
-    if (qq < npath) v = __ldg(p.tok + ent(d, b, (qq < in.s) ? 0 : kpath, qq));
+    if (qq < npath) v = __ldg(tok + ent(d, b, (qq < in.s) ? 0 : kpath, qq));
     else if (qq == npath && kind != 0) v = y;
     out[qq] = v;
   }
@@ -228,7 +228,7 @@ __device__ __forceinline__ void commit_seq(const RowsParams& p, const CommitOut&
     co.path_rolled[b] = in.L - npath;
     co.branch_discarded[b] = (d.K - 1) * (in.L - in.s);
     if (co.resid_mass) co.resid_mass[b] = (kind != 0) ? (float)mass : 0.f;
-    if (st) atomicOr(p.status + b, st);
+    if (st) atomicOr(status + b, st);
   }
 }
 

@@ -20,6 +20,7 @@
 #include "sb_ring.cuh"
 #include "sb_block_sample.cuh"
 #include "sb_sample.cuh"
+#include "sb_rows.cuh"
 
 #ifdef SB_TRACE
 SB_TRACE_TABLE(sb_trace_select)
@@ -91,8 +92,6 @@ __global__ void __launch_bounds__(NT) k_select(SelParams p, bool vec_ok) {
   __syncthreads();
   const int ksel = sh_ksel, npath = sh_npath;
   int kind = sh_kind;
-  const int kpath = ksel < 0 ? 0 : ksel;
-
   int y = -1;
   double mass = 0.0;
   if (kind != 0) {
@@ -124,32 +123,12 @@ __global__ void __launch_bounds__(NT) k_select(SelParams p, bool vec_ok) {
     }
   }
 
-  // commit: path tokens, y, counters, keep mask (SURVEY §8.0 "Commit")
-  const int R1 = d.G + 1;
-  int* out = p.out_tok + (int64_t)b * (d.G + 2);
-  for (int q = tid; q < d.G + 2; q += NT) {
-    int v = -1;
-    if (q < npath) v = __ldg(p.tok + ent(d, b, (q < in.s) ? 0 : kpath, q));
-    else if (q == npath && kind != 0) v = y;
-    out[q] = v;
-  }
-  if (tid < d.K) {
-    uint32_t km = 0;
-    for (int q = 0; q < npath; ++q)
-      if (((q < in.s) ? 0 : kpath) == tid) km |= 1u << q;
-    p.keep_mask[(int64_t)b * d.K + tid] = km;
-  }
-  (void)R1;
-  if (tid == 0) {
-    p.sel_k[b] = ksel;
-    p.commit_len[b] = npath + (kind != 0);
-    p.y_tok[b] = (kind != 0) ? y : -1;
-    p.y_kind[b] = kind;
-    p.path_rolled[b] = in.L - npath;
-    p.branch_discarded[b] = (d.K - 1) * (in.L - in.s);
-    if (p.resid_mass) p.resid_mass[b] = (kind != 0) ? (float)mass : 0.f;
-    if (sh_st) atomicOr(p.status + b, sh_st);
-  }
+  // commit: path tokens, y, counters, keep mask (SURVEY §8.0 "Commit"), by the first warp
+  if (tid < 32)
+    commit_seq(d, p.tok, p.status,
+               CommitOut{p.sel_k, p.commit_len, p.out_tok, p.y_tok, p.y_kind, p.offsets, p.packed_tok, p.path_rolled,
+                         p.branch_discarded, p.keep_mask, p.resid_mass},
+               b, in, ksel, npath, kind, y, mass, sh_st);
 
   // last CTA: offsets (exclusive scan of commit_len) and the packed commit stream
   __syncthreads();
@@ -415,121 +394,17 @@ __global__ void __launch_bounds__(sThreads, 1) k_select_tma(SelParams p) {
         } else {
           const T* prow = PL + row_off(d, b, D.slot, D.row);
           const T* qrow = QL + row_off(d, b, D.slot, D.row);
-          const float kq = Zp / Zq;
           bool resid = (kind == 1);
-          float* seg = S.seg[q];
-          const int per = (nseg + 31) / 32;
-          double R = 0.0, excl = 0.0, incl = 0.0;
-          for (int attempt = 0; attempt < 2; ++attempt) {
-            double local = 0.0;
-            for (int j = 0; j < per; ++j) {
-              const int sI = lane * per + j;
-              if (sI < nseg) local += (double)seg[sI];
-            }
-            incl = local;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-              const double yv = __shfl_up_sync(0xffffffffu, incl, o);
-              if (lane >= o) incl += yv;
-            }
-            excl = __shfl_up_sync(0xffffffffu, incl, 1);  // lane ranges [excl, incl) tile [0, R)
-            if (lane == 0) excl = 0.0;
-            R = __shfl_sync(0xffffffffu, incl, 31);
-            if (R > 0.0 || !resid) break;
-            resid = false;  // "no residual mass" (S134-140): sample from P
-            st |= SB_ST_ZERO_RESID;
-            warp_segments<T>(prow, qrow, row_bytes, nseg, false, MSp, MSq, kq, seg);
-          }
-          const double t = (double)__ldg(p.us + b) * R;
-          // exactly one lane's [excl, incl) holds t; it rescans its segments in fp64
-          int found = -1, lastpos = -1;
-          double Fprev = 0.0;
-          const bool mine = (excl <= t && incl > t);
-          if (mine) {
-            double F = excl;
-            for (int j = 0; j < per; ++j) {
-              const int sI = lane * per + j;
-              if (sI >= nseg) break;
-              if (seg[sI] > 0.f) lastpos = sI;
-              if (found < 0 && F + (double)seg[sI] > t) { found = sI; Fprev = F; }
-              F += (double)seg[sI];
-            }
-          } else {
-            for (int j = 0; j < per; ++j) {
-              const int sI = lane * per + j;
-              if (sI < nseg && seg[sI] > 0.f) lastpos = sI;
-            }
-          }
-          const unsigned who = __ballot_sync(0xffffffffu, found >= 0);
-          int sStar;
-          double trem;
-          if (who) {
-            const int src = __ffs(who) - 1;
-            sStar = __shfl_sync(0xffffffffu, found, src);
-            trem = t - __shfl_sync(0xffffffffu, Fprev, src);
-          } else {  // rounding: the last segment with mass, and the in-segment fallback
-            const unsigned mw = __ballot_sync(0xffffffffu, mine);
-            const int src = mw ? __ffs(mw) - 1 : -1;
-            const int cand = src >= 0 ? __shfl_sync(0xffffffffu, lastpos, src) : -1;
-            sStar = cand >= 0 ? cand : (int)__reduce_max_sync(0xffffffffu, (unsigned)(lastpos + 1)) - 1;
-            trem = CUDART_INF;
-          }
-          if (sStar >= 0) {
-            // pass B: re-read segment sStar (two 16-byte vectors per lane) from L2
-            float r[2][E], own = 0.f;
-#pragma unroll
-            for (int j = 0; j < 2; ++j) {
-              const uint32_t off = (uint32_t)sStar * kSegBytes + lane * 32 + j * 16;
-              r_scaled<T>(seg_vec(prow, row_bytes, off), resid ? seg_vec(qrow, row_bytes, off) : uint4{}, resid,
-                          MSp, MSq, kq, r[j]);
-              own = seq_sum<E>(r[j], own);
-            }
-            const float incl = warp_scan_rn(own);
-            float F = __shfl_up_sync(0xffffffffu, incl, 1);
-            if (lane == 0) F = 0.f;
-            int cand = 0x7fffffff, lastv = -1;
-            const int vbase = (int)(((uint32_t)sStar * kSegBytes + lane * 32) / sizeof(T));
-#pragma unroll
-            for (int j = 0; j < 2; ++j)
-#pragma unroll
-              for (int e = 0; e < E; ++e) {
-                F = __fadd_rn(F, r[j][e]);
-                const int v = vbase + j * E + e;
-                if (cand == 0x7fffffff && (double)F > trem && r[j][e] > 0.f) cand = v;
-                if (r[j][e] > 0.f) lastv = v;
-              }
-            const int pick = (int)__reduce_min_sync(0xffffffffu, (unsigned)cand);
-            y = (pick != 0x7fffffff) ? pick : (int)__reduce_max_sync(0xffffffffu, (unsigned)(lastv + 1)) - 1;
-            if (y >= d.V) y = -1;
-          }
+          double R = 0.0;
+          y = sample_segments<T>(prow, qrow, row_bytes, d.V, S.seg[q], nseg, resid, MSp, MSq, Zp / Zq,
+                                 __ldg(p.us + b), st, &R);
           mass = R / (double)Zp;  // back to probability mass
         }
       }
-      // commit (SURVEY §8.0 "Commit")
-      const int ksel = D.ksel, npath = D.npath, kpath = ksel < 0 ? 0 : ksel;
-      int* out = p.out_tok + (int64_t)b * (d.G + 2);
-      for (int qq = lane; qq < d.G + 2; qq += 32) {
-        int v = -1;
-        if (qq < npath) v = __ldg(p.tok + ent(d, b, (qq < in.s) ? 0 : kpath, qq));
-        else if (qq == npath && kind != 0) v = y;
-        out[qq] = v;
-      }
-      if (lane < d.K) {
-        uint32_t km = 0;
-        for (int qq = 0; qq < npath; ++qq)
-          if (((qq < in.s) ? 0 : kpath) == lane) km |= 1u << qq;
-        p.keep_mask[(int64_t)b * d.K + lane] = km;
-      }
-      if (lane == 0) {
-        p.sel_k[b] = ksel;
-        p.commit_len[b] = npath + (kind != 0);
-        p.y_tok[b] = (kind != 0) ? y : -1;
-        p.y_kind[b] = kind;
-        p.path_rolled[b] = in.L - npath;
-        p.branch_discarded[b] = (d.K - 1) * (in.L - in.s);
-        if (p.resid_mass) p.resid_mass[b] = (kind != 0) ? (float)mass : 0.f;
-        if (st) atomicOr(p.status + b, st);
-      }
+      commit_seq(d, p.tok, p.status,
+                 CommitOut{p.sel_k, p.commit_len, p.out_tok, p.y_tok, p.y_kind, p.offsets, p.packed_tok,
+                           p.path_rolled, p.branch_discarded, p.keep_mask, p.resid_mass},
+                 b, in, D.ksel, D.npath, kind, y, mass, st);
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.dempty[dq.stage]);
       if (lane == 0) SB_TRACE_AT(sb_trace_select, 2, 2 + (b / gridDim.x));

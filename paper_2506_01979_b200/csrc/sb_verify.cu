@@ -1018,31 +1018,10 @@ __global__ void __launch_bounds__(C::THREADS, 1) k_step_tma(StepParams sp) {
       }
       up.advance();
       dq.advance();
-      // commit (SURVEY §8.0 "Commit")
-      const int ksel = D.ksel, npath = D.npath, kpath = ksel < 0 ? 0 : ksel;
-      int* out = sp.out_tok + (int64_t)b * (d.G + 2);
-      for (int qq = lane; qq < d.G + 2; qq += 32) {
-        int v = -1;
-        if (qq < npath) v = __ldg(p.tok + ent(d, b, (qq < in.s) ? 0 : kpath, qq));
-        else if (qq == npath && kind != 0) v = y;
-        out[qq] = v;
-      }
-      if (lane < d.K) {
-        uint32_t km = 0;
-        for (int qq = 0; qq < npath; ++qq)
-          if (((qq < in.s) ? 0 : kpath) == lane) km |= 1u << qq;
-        sp.keep_mask[(int64_t)b * d.K + lane] = km;
-      }
-      if (lane == 0) {
-        sp.sel_k[b] = ksel;
-        sp.commit_len[b] = npath + (kind != 0);
-        sp.y_tok[b] = (kind != 0) ? y : -1;
-        sp.y_kind[b] = kind;
-        sp.path_rolled[b] = in.L - npath;
-        sp.branch_discarded[b] = (d.K - 1) * (in.L - in.s);
-        if (sp.resid_mass) sp.resid_mass[b] = (kind != 0) ? (float)mass : 0.f;
-        if (st) atomicOr(p.status + b, st);
-      }
+      commit_seq(d, p.tok, p.status,
+                 CommitOut{sp.sel_k, sp.commit_len, sp.out_tok, sp.y_tok, sp.y_kind, sp.offsets, sp.packed_tok,
+                           sp.path_rolled, sp.branch_discarded, sp.keep_mask, sp.resid_mass},
+                 b, in, D.ksel, D.npath, kind, y, mass, st);
       __syncwarp();
       int last = 0;
       if (lane == 0) {
@@ -1520,7 +1499,7 @@ __global__ void __launch_bounds__(C::ROWS_THREADS, MINB) k_astep(AStepParams ap)
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&S.pempty[ps_slot]);
-        commit_seq(p, ap.co, b, in, it.ksel, it.npath, kind, y, mass, st);
+        commit_seq(d, p.tok, p.status, ap.co, b, in, it.ksel, it.npath, kind, y, mass, st);
         __syncwarp();
         int last = 0;
         if (lane == 0) {
