@@ -1588,8 +1588,12 @@ __global__ void __launch_bounds__(C::ROWS_THREADS, MINB) k_astep(AStepParams ap)
         }
         if (tid == 0 && li < 60) SB_TRACE_AT(sb_trace_astep, 5, 2 + li);
         uint2 cand = make_uint2(0xffffffffu, 0u);
+#ifdef SB_ASTEP_NORED  // experiment: the consumers' per-item warp reductions removed (wrong results)
+        RowStat ps = fold_lazy(pa), qs = fold_lazy(qa);
+#else
         const RowStat ps = (it.type == 1) ? warp_part<C, T, false>(pa, nullptr, nvec_last, nchunks) : rowstat_empty();
         const RowStat qs = it.po ? rowstat_empty() : warp_part_deferred(qa, cand);
+#endif
         if (tid == 0 && li < 60) SB_TRACE_AT(sb_trace_astep, 6, 2 + li);
         if (lane == 0) {
           mbar_wait(&S.pempty[ps_slot], pph ^ 1u);

@@ -15,7 +15,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2506_01979_b200 import _lib, api, synth  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "c2"
-cfg = synth.config(name) if name != "c1one" else synth.config("c1", rounds=1)
+cfg = (synth.config("c1", rounds=1) if name == "c1one" else
+       synth.config("c2", layout="fixed") if name == "c2fixed" else synth.config(name))
 adaptive = cfg.layout == "adaptive"
 inp = synth.generate(cfg, device="cuda")
 d = api.dims_for(inp["PL"], V=inp["V"])
