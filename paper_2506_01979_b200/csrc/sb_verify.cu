@@ -680,8 +680,13 @@ __global__ void __launch_bounds__(C::ROWS_THREADS, 1) k_rows_tma(RowsParams p) {
       consume_chunk<C, T, false, false, REUSE>(S, rp, nchunks - 1, nvec_last, pa, qa);
     }
     uint2 cand;
+#ifdef SB_ROWS_NORED  // experiment: the consumers' per-unit warp reductions removed (wrong results)
+    const RowStat ps = fold_lazy(pa), qs = fold_lazy(qa);
+    cand = make_uint2(0xffffffffu, 0u);
+#else
     const RowStat ps = warp_part<C, T, false>(pa, nullptr, nvec_last, nchunks);
     const RowStat qs = warp_part_deferred(qa, cand);
+#endif
     if (lane == 0) {
       mbar_wait(&S.pempty[up.stage], up.phase ^ 1u);
       S.part[up.stage][0][warp] = ps;
