@@ -179,13 +179,22 @@ __global__ void __launch_bounds__(NT) k_select(SelParams p, bool vec_ok) {
 //                        a bonus row first gets a softmax-state pass;
 //   epilogue  (warp 17): fp64 prefix over segment sums, locate us*R, re-read that one
 //                        segment (L2), same arithmetic -> first id past us*R; commit.
-constexpr int sNS = 6;
-constexpr int sCW = 16;
+// 20 consumer warps x 5 stages of 20 KB (same box, C4: select 0.236-0.237 ms against
+// 0.246 ms for 16 x 6 x 16 KB; 12 x 8: 0.28, 24 x 4: 0.240-0.243; SB_SEL_NS / SB_SEL_CW:
+// experiment builds)
+#ifndef SB_SEL_NS
+#define SB_SEL_NS 5
+#endif
+#ifndef SB_SEL_CW
+#define SB_SEL_CW 20
+#endif
+constexpr int sNS = SB_SEL_NS;
+constexpr int sCW = SB_SEL_CW;
 constexpr int sCT = sCW * 32;
 constexpr int sVPT = 2;
-constexpr int sChunk = sCT * sVPT * 16;  // 16 KB per row per stage
+constexpr int sChunk = sCT * sVPT * 16;  // sCW KB per row per stage
 constexpr int sNQ = 4;                   // sequences in flight
-constexpr int sSegMax = 1024;            // 512-byte segments per row (rows <= 512 KB)
+constexpr int sSegMax = 1024;            // 1 KB segments per row (one per consumer warp per chunk)
 constexpr int sThreads = sCT + 96;
 
 struct Dec {
@@ -558,7 +567,8 @@ extern "C" sb_status sb_select_branch(const sb_dims* dd, const void* p_logits, c
   const bool vok = vec_ok(dd, p_logits) && vec_ok(dd, q_logits);
   cudaStream_t s = (cudaStream_t)stream;
   const size_t row_bytes = (size_t)dd->V * elem_size(dd);
-  if (vok && row_bytes % 16 == 0 && row_bytes <= (size_t)sSegMax * kSegBytes && !tma_disabled())
+  // every chunk holds sCW segments: rows up to (sSegMax / sCW) whole chunks (1020 KB)
+  if (vok && row_bytes % 16 == 0 && (row_bytes + sChunk - 1) / sChunk * sCW <= (size_t)sSegMax && !tma_disabled())
     return dd->dtype == SB_BF16 ? launch_select_tma<__nv_bfloat16>(p, s) : launch_select_tma<float>(p, s);
   if (dd->dtype == SB_BF16) {
     if ((dd->V + 256 * 8 - 1) / (256 * 8) > kMaxTiles) return SB_ERR_UNSUPPORTED;
