@@ -41,16 +41,20 @@ __global__ void __launch_bounds__(NT) k_conf(ConfParams p, bool vec_ok) {
   }
 }
 
-// TMA ring version (same warp roles as k_rows_tma): producer warp streams 16 KB chunks
-// of each q row, 16 consumer warps fold them, an epilogue warp finishes each row.
+// TMA ring version (same warp roles as k_rows_tma): the producer warp streams cChunk-byte
+// chunks of each q row, cCW consumer warps fold them, cNE epilogue warps finish the rows.
+// 28 consumer warps x 7 stages of 28 KB, 2 epilogue warps (same box, C3's 4096 draft rows:
+// 0.1995-0.2001 ms against 0.2162-0.2176 ms for 16 x 12 x 16 KB with 4 epilogue warps;
+// 20 x 10: 0.210, 24 x 8: 0.208, 24 x 8 / 2: 0.206, 26 x 7: 0.212, 28 x 7 / 1: 0.204,
+// 30 x 7 / 1: 0.217, 12 x 16: 0.237)
 #ifndef SB_CONF_NS
-#define SB_CONF_NS 12
+#define SB_CONF_NS 7
 #endif
 #ifndef SB_CONF_CW
-#define SB_CONF_CW 16
+#define SB_CONF_CW 28
 #endif
 #ifndef SB_CONF_NE
-#define SB_CONF_NE 4
+#define SB_CONF_NE 2
 #endif
 constexpr int cNS = SB_CONF_NS;  // (macros: A/B experiment builds only)
 constexpr int cCW = SB_CONF_CW;
