@@ -1937,7 +1937,9 @@ static sb_status launch_rows_warp(const RowsParams& p, cudaStream_t s) {
 // 4 vectors per row per stage (16 x 3 x 64 KB; round 2: C4 verify +10 %, C3 +6 %): none
 // beat these two.
 using RC0 = RC<20, 5, 2, 4, 4>;  // 20 consumer warps, 5 x 40 KB stages, 4 epilogue warps
+// (24 x 4 / 4 or 2, 28 x 3 / 2 and 20 x 5 / 2 epilogue warps measured slower on C4, r4_experiments.txt)
 using RC2 = RC<16, 6, 2, 4, 4>;  // 16 consumer warps, 6 x 32 KB stages
+using RC3 = RC<28, 3, 2, 4, 2>;  // 28 consumer warps, 3 x 56 KB stages, 2 epilogue warps (reuse units)
 using RCF = RC<16, 6, 2, 4>;   // the fused step kernel's geometry
 
 template <typename T>
@@ -1957,6 +1959,12 @@ static sb_status launch_rows_variant(const RowsParams& p, cudaStream_t s) {
     auto waste = [&](double chunk) { const double n = std::ceil(rb / chunk); return (n * chunk - rb) / (n * chunk); };
     v = waste(RC0::CHUNK) - waste(RC2::CHUNK) > 0.03 ? 2 : 0;
   }
+  // the adaptive step's verify (q states of the slot-0 draft rows reused, those units
+  // stream p only): 28 consumer warps x 3 stages of 56 KB, 2 epilogue warps (same box, C3:
+  // step 0.895-0.897 vs 0.920 ms with RC0; on C4's pairs RC0 stays faster, 5.35-5.48 vs
+  // 5.48-5.65 ms)
+  if (v == 0 && p.qreuse) return launch_rows_tma_k<RC3, T, true>(p, s);
+  if (v == 3) return launch_rows_tma<RC3, T>(p, s);
   return v == 2 ? launch_rows_tma<RC2, T>(p, s) : launch_rows_tma<RC0, T>(p, s);
 }
 
