@@ -1691,10 +1691,13 @@ bool astep_eligible(const sb_dims* dd, const void* PL, const void* QL) {
   return (e && e[0] == '1') || (size_t)dd->B * dd->K * (dd->G + 1) <= 4096;
 }
 
-#ifndef SB_AG_CW  // (SB_AG_CW / SB_AG_NS: experiment builds)
+#ifndef SB_AG_CW  // (SB_AG_CW / SB_AG_NS / SB_AG_NE: experiment builds)
 using RCA = RC<16, 6, 2, 4, 4>;  // k_astep: 16 consumer warps, 6 x 32 KB stages, 4 epilogue warps
 #else
-using RCA = RC<SB_AG_CW, SB_AG_NS, 2, 4, 4>;
+#ifndef SB_AG_NE
+#define SB_AG_NE 4
+#endif
+using RCA = RC<SB_AG_CW, SB_AG_NS, 2, 4, SB_AG_NE>;
 #endif
 // (two CTAs per SM of 8 consumer warps, 5 x 16 KB stages each, measured 72.3 vs 71.6 us on C2)
 
